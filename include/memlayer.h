@@ -1,0 +1,192 @@
+/* libmemlayer — C ABI of the B200-native (sm_100a) memory-layer hot path of
+ * "Memory Layers at Scale" (arXiv 2412.09764).
+ *
+ * Paper passages (PAPER.md line numbers, "P:n"):
+ *   Eq. 1  I = SelectTopkIndices(Kq), s = Softmax(K_I q), y = s V_I
+ *   §3.1.1     product keys: K1, K2 in R^{sqrt(N) x n/2}; split q into
+ *                      q1, q2; top-k per half; argmax over s1[i1] + s2[i2]
+ *   §3.1.2     values sharded along the embedding dim (
+ *                      the group exchange is driven from Python, NCCL)
+ *   §3.1.4     EmbeddingBag: bandwidth-bound weighted gather-sum; the
+ *                      backward with an inverted token->row map ("reverse_indices")
+ *   Eq. 2      output = (y ⊙ silu(x^T W1))^T W2
+ *
+ * Conventions (all calls):
+ *  - Every data pointer is a DEVICE pointer owned by the caller, pointing to a
+ *    dense row-major array with the stated shape; 16-byte aligned.  The
+ *    library never allocates device memory inside a call and never
+ *    synchronises the host (except under ML_CHECK_INDICES=1, see below).
+ *  - `stream` is a cudaStream_t passed as void*; all work is enqueued on it in
+ *    order.  NULL means the legacy default stream.
+ *  - Scratch comes from a caller workspace `ws` of at least the size returned
+ *    by the matching *_workspace() query for the same shape.
+ *  - Outputs are overwritten unless documented "accumulate".
+ *  - idx are int32, weights / scores / gradients of scores, of keys, of
+ *    queries and of values are fp32 regardless of mlDtype; q, K1, K2, V, x,
+ *    W1, W2, y, g, out, dout, dx are of mlDtype.
+ *  - Errors: every call returns mlStatus and, on failure, leaves a message in
+ *    ml_last_error() (thread-local).  Shape/config validation happens on the
+ *    host before any launch.  No C++ exception crosses this boundary.
+ *  - Indices outside [0, N) are clamped to row 0 with weight 0 (no fault); the
+ *    kernels raise a device flag.  With the environment variable
+ *    ML_CHECK_INDICES=1 each bag call synchronises its stream, reads the flag
+ *    and returns ML_ERR_INDEX if it was raised ("index error").
+ */
+#ifndef MEMLAYER_H_
+#define MEMLAYER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ML_OK = 0,
+  ML_ERR_ARG = 1,          /* null / misaligned pointer, negative size          */
+  ML_ERR_CONFIG = 2,       /* shape rules violated (k > S, odd Dk, N != S^2 ...) */
+  ML_ERR_INDEX = 3,        /* out-of-range index seen (ML_CHECK_INDICES=1)      */
+  ML_ERR_WORKSPACE = 4,    /* workspace smaller than the *_workspace() size     */
+  ML_ERR_CUDA = 5,         /* CUDA runtime / launch error (text in last_error)  */
+  ML_ERR_UNSUPPORTED = 7   /* legal per the paper but not supported by v1       */
+} mlStatus;
+
+typedef enum { ML_F32 = 0, ML_BF16 = 1 } mlDtype;
+
+/* ---------------------------------------------------------------- misc */
+const char* ml_last_error(void);
+int ml_version(void);
+/* Number of kernels this library has launched since load (all calls). */
+uint64_t ml_launch_count(void);
+/* Number of SMs / compute capability of the current device (host query). */
+int ml_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* Optional per-launch timing: when enabled, the library records a CUDA event
+ * on the launch stream after every kernel / GEMM / memset it issues (and a
+ * start marker at each entry point).  ml_timing_report() synchronises on the
+ * recorded events and writes "name count total_ms" lines aggregated per
+ * kernel name into buf (len bytes); returns the bytes needed incl. NUL.
+ * Not thread-safe against concurrent calls on different streams' reports. */
+void ml_timing_enable(int on);
+void ml_timing_reset(void);
+size_t ml_timing_report(char* buf, size_t len);
+
+/* Counter-based synthetic generator (not method arithmetic).
+ * Fills out[r - row0][c] for rows r in [row0, row0 + n_rows), c < n_cols of a
+ * logical [*, n_cols] tensor with
+ *   u = splitmix64(seed*0x9E3779B97F4A7C15 + tag*0xD1B54A32D192ED03 + r*n_cols + c)
+ * cls 0 (continuous): f = ((u>>40) - 2^23) / 2^23;  cls 1 (exact):
+ * f = (((u>>60)&15) - 8)/8;  cls 2 (dyadic): f = ((u>>58)&63)/64;
+ * value = RN_fp32(f * scale) then RNE to `dtype`.  cls 3 (index): int32
+ * (u mod modulus) (out is int32, scale/dtype ignored). */
+mlStatus ml_synth_fill(void* out, int64_t n_rows, int64_t n_cols, int64_t row0,
+                       uint64_t seed, uint32_t tag, float scale, int cls,
+                       mlDtype dtype, int64_t modulus, void* stream);
+
+/* ------------------------------------------------ product-key top-k (a1-a4)
+ * Per token t and head h (reading Q1: H independent heads):
+ *   q1 = q[t,h,0:Dk/2], q2 = q[t,h,Dk/2:Dk]
+ *   s1[a] = q1 . K1[h,a,:], s2[b] = q2 . K2[h,b,:] for a, b < S
+ *   I1, I2 = top-k of s1, s2 (score desc, ties -> lower sub-index)
+ *   keep the k best of the k*k sums s1[i]+s2[j] (score desc, ties -> lower
+ *   flat index a*S+b)
+ *   w = softmax of the k kept scores (fp32, max-subtracted)        (Eq. 1)
+ * Arithmetic: fp32 products/accumulation of the mlDtype inputs.
+ * Shapes: q [T,H,Dk]; K1, K2 [H,S,Dk/2];  outputs idx [T,H,k] (flat a*S+b,
+ * sorted by descending score), w [T,H,k], score [T,H,k] pre-softmax
+ * (nullable).  Rules: 1 <= k <= min(S, 32); Dk even; S*S < 2^31; T >= 0
+ * (T == 0 is a no-op).  Scratch: [T,H,2,S] fp32 scores + half top-k lists. */
+typedef struct { int32_t T, H, S, Dk, k; mlDtype dtype; } mlPkmShape;
+
+mlStatus pkm_topk_workspace(const mlPkmShape* shape, size_t* bytes);
+mlStatus pkm_topk(const mlPkmShape* shape, const void* q, const void* K1, const void* K2,
+                  int32_t* idx, float* w, float* score,
+                  void* ws, size_t ws_bytes, void* stream);
+
+/* Backward of the lookup into the query and the half keys ("keys ...
+ * are trainable"; reading Q8: no gradient through the selection):
+ *   ds = w ⊙ (dw - sum_j w_j dw_j);  with a_j = idx/S, b_j = idx%S:
+ *   dq[t,h,0:Dk/2]  = sum_j ds_j K1[h,a_j,:],   dq[t,h,Dk/2:] = sum_j ds_j K2[h,b_j,:]
+ *   dK1[h,a,:] += sum_{(t,j): a_j = a} ds_j q1[t,h,:]   (likewise dK2)
+ * dw [T,H,k] fp32 (the bag's weight gradient).  dq [T,H,Dk] fp32 overwrite;
+ * dK1, dK2 [H,S,Dk/2] fp32 ACCUMULATE (deterministic: sorted segments, fixed
+ * order, no float atomics). */
+mlStatus pkm_topk_bwd_workspace(const mlPkmShape* shape, size_t* bytes);
+mlStatus pkm_topk_bwd(const mlPkmShape* shape, const void* q, const void* K1, const void* K2,
+                      const int32_t* idx, const float* w, const float* dw,
+                      float* dq, float* dK1, float* dK2,
+                      void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------- EmbeddingBag (a5, a9)
+ * One bag per token of B (index, weight) pairs (B = H*k in the layer):
+ *   y[t,:] = sum_{j<B} w[t,j] * V[idx[t,j],:]            (Eq. 1 y = s V_I)
+ * fp32 accumulation in j order, stored as dtype.  If gate_pre != NULL
+ * (Eq. 2): y_out = y ⊙ silu(gate_pre) and, if y_ungated != NULL, y is
+ * stored there too.  V [N,dv], idx/w [T,B], gate_pre/y/y_ungated [T,dv].
+ * Rules: dv*e a multiple of 16 B; dv/(16/e) a power of two <= 256 or a
+ * multiple of 256; 1 <= B <= 1024. */
+typedef struct { int64_t N; int32_t dv; int32_t T; int32_t B; mlDtype dtype; } mlBagShape;
+
+mlStatus embbag_fwd(const mlBagShape* shape, const void* V, const int32_t* idx, const float* w,
+                    const void* gate_pre, void* y, void* y_ungated, void* stream);
+
+/* Backward, "reverse_indices" strategy: the P = T*B (idx, position)
+ * pairs are stably radix-sorted by idx (the inverted token->row map); each
+ * distinct row r is reduced by one owner in position order:
+ *   dV[r,:] = sum_{p: idx[p]=r} w[p] * dy[t(p),:]   (fp32; V[r] read once per row)
+ *   dw[p]   = <dy[t(p),:], V[idx[p],:]>
+ * Outputs: rows[0..U) ascending distinct indices, dV[0..U) their fp32
+ * gradient rows (compact SparseGrad), *U (device int32), dw [T,B]
+ * fp32.  rows / dV need capacity T*B rows.  Deterministic: bitwise equal
+ * across runs (no float atomics; runs longer than 32 positions are split into
+ * fixed pieces combined in piece order). */
+mlStatus embbag_bwd_workspace(const mlBagShape* shape, size_t* bytes);
+mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, const float* w,
+                    const void* dy, int32_t* rows, float* dV, int32_t* U, float* dw,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* dV_dense[rows[i],:] += dV[i,:] for i < *U (unique rows: no atomics).
+ * dV_dense [N,dv] fp32. */
+mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const float* dV,
+                           const int32_t* U, float* dV_dense, void* stream);
+
+/* ------------------------------------------------ memory layer (a1-a11)
+ * Forward: pkm_topk -> g = x W1 -> z = embbag(V; idx, w) ⊙ silu(g) ->
+ * out = z W2 (Eq. 1 + Eq. 2).  With gated == 0 (vanilla Memory) out = y and
+ * D must equal dv; x, W1, W2, g_saved are unused.
+ * x [T,D], q [T,H,Dk], K1/K2 [H,S,Dk/2], V [N,dv], W1 [D,dv], W2 [dv,D],
+ * out [T,D].  Saved for the backward (caller-owned): idx_saved [T,H,k] i32,
+ * w_saved [T,H,k] f32, g_saved [T,dv] (dtype, gated only), y_saved [T,dv]
+ * (dtype).  N must equal S*S.  W1/W2 products run on cuBLASLt (library GEMM,
+ * fp32 accumulation). */
+typedef struct { mlPkmShape pkm; int64_t N; int32_t dv; int32_t D; int32_t gated; } mlLayerShape;
+
+mlStatus memory_layer_fwd_workspace(const mlLayerShape* shape, size_t* bytes);
+mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* q,
+                          const void* K1, const void* K2, const void* V,
+                          const void* W1, const void* W2, void* out,
+                          int32_t* idx_saved, float* w_saved, void* g_saved, void* y_saved,
+                          void* ws, size_t ws_bytes, void* stream);
+
+/* Backward of memory_layer_fwd given dout [T,D]:
+ *   gate (Eq. 2): dz = dout W2^T, dW2 = z^T dout, dy = dz ⊙ silu(g),
+ *   dg = dz ⊙ y ⊙ silu'(g), dW1 = x^T dg, dx = dg W1^T     (dx: gate path only)
+ *   bag: rows/dV/U compact as embbag_bwd; dw_out [T,H,k] (nullable)
+ *   keys: dq [T,H,Dk] overwrite, dK1/dK2 ACCUMULATE as pkm_topk_bwd.
+ * dW1 [D,dv], dW2 [dv,D] fp32 overwrite; dx [T,D] dtype. */
+mlStatus memory_layer_bwd_workspace(const mlLayerShape* shape, size_t* bytes);
+mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const void* x,
+                          const void* q, const void* K1, const void* K2, const void* V,
+                          const void* W1, const void* W2,
+                          const int32_t* idx_saved, const float* w_saved,
+                          const void* g_saved, const void* y_saved,
+                          void* dx, float* dq, float* dK1, float* dK2,
+                          int32_t* dV_rows, float* dV, int32_t* U,
+                          float* dW1, float* dW2, float* dw_out,
+                          void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEMLAYER_H_ */

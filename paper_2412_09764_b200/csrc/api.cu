@@ -1,0 +1,510 @@
+// C-ABI entry points of libmemlayer (declared and documented in
+// include/memlayer.h): host-side validation, workspace planning, and the
+// stream-ordered composition of the kernels.  No C++ exception crosses the
+// boundary; every failure is an mlStatus plus ml_last_error() text.
+#include "internal.cuh"
+
+#include <atomic>
+#include <cstdio>
+#include <exception>
+
+namespace ml {
+
+static thread_local std::string t_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+mlStatus fail(mlStatus st, const std::string& msg) {
+  t_last_error = msg;
+  return st;
+}
+void count_launch(int n) { g_launches.fetch_add(uint64_t(n), std::memory_order_relaxed); }
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+static int ceil_log2(int64_t n) {
+  int b = 0;
+  while ((int64_t(1) << b) < n) ++b;
+  return b;
+}
+
+// ------------------------------------------------------------ validation
+static mlStatus check_pkm(const mlPkmShape* s) {
+  if (!s) return fail(ML_ERR_ARG, "null shape");
+  if (s->dtype != ML_F32 && s->dtype != ML_BF16) return fail(ML_ERR_ARG, "unknown dtype");
+  if (s->T < 0 || s->H < 1 || s->S < 1 || s->Dk < 2)
+    return fail(ML_ERR_CONFIG, "pkm: need T >= 0, H >= 1, S >= 1, Dk >= 2");
+  if (s->Dk % 2) return fail(ML_ERR_CONFIG, "pkm: odd key dimension Dk (SPEC S:143)");
+  if (s->k < 1 || s->k > s->S) return fail(ML_ERR_CONFIG, "pkm: need 1 <= k <= S (SPEC S:150)");
+  if (s->k > 32) return fail(ML_ERR_UNSUPPORTED, "pkm: k > 32 not supported by the warp select");
+  if (int64_t(s->S) * s->S >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "pkm: N = S^2 must be < 2^31");
+  if (int64_t(s->H) * s->S >= (int64_t(1) << 30)) return fail(ML_ERR_CONFIG, "pkm: H*S too large");
+  ML_TRY(check_cols(s->Dk / 2, s->dtype, "pkm half-key row"));
+  return ML_OK;
+}
+
+static mlStatus check_bag(const mlBagShape* s) {
+  if (!s) return fail(ML_ERR_ARG, "null shape");
+  if (s->dtype != ML_F32 && s->dtype != ML_BF16) return fail(ML_ERR_ARG, "unknown dtype");
+  if (s->N < 1 || s->N >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "bag: need 1 <= N < 2^31");
+  if (s->T < 0) return fail(ML_ERR_CONFIG, "bag: T < 0");
+  if (s->B < 1 || s->B > 1024) return fail(ML_ERR_CONFIG, "bag: need 1 <= B <= 1024");
+  if (int64_t(s->T) * s->B >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "bag: T*B must be < 2^31");
+  ML_TRY(check_cols(s->dv, s->dtype, "value row"));
+  return ML_OK;
+}
+
+static mlStatus check_ptrs(std::initializer_list<const void*> ps) {
+  for (const void* p : ps) {
+    if (!p) return fail(ML_ERR_ARG, "null pointer argument");
+    if (reinterpret_cast<uintptr_t>(p) % 16) return fail(ML_ERR_ARG, "pointer not 16-byte aligned");
+  }
+  return ML_OK;
+}
+
+// ------------------------------------------------------------ plans
+struct PkmFwdBufs { float* scores; int32_t* hI; float* hs; };
+static void pkm_fwd_carve(Carver& c, const mlPkmShape& s, PkmFwdBufs& b) {
+  const int64_t TH = int64_t(s.T) * s.H;
+  b.scores = c.take<float>(TH * 2 * s.S);
+  b.hI = c.take<int32_t>(TH * 2 * s.k);
+  b.hs = c.take<float>(TH * 2 * s.k);
+}
+
+struct PkmBwdBufs {
+  float* ds; int32_t* key1; int32_t* key2;
+  SortBufs sort; RunBufs runs; float* partial; int32_t* counters;
+};
+static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
+  const int64_t P = int64_t(s.T) * s.H * s.k;
+  b.ds = c.take<float>(P);
+  b.key1 = c.take<int32_t>(P);
+  b.key2 = c.take<int32_t>(P);
+  sort_carve(c, P, ceil_log2(int64_t(s.H) * s.S), b.sort);
+  runs_carve(c, P, b.runs);
+  seg_carve(c, P, s.Dk / 2, s.dtype, &b.partial, &b.counters);
+}
+
+struct BagBwdBufs { SortBufs sort; RunBufs runs; float* partial; int32_t* counters; float* dw_part; };
+static void bag_bwd_carve(Carver& c, const mlBagShape& s, BagBwdBufs& b) {
+  const int64_t P = int64_t(s.T) * s.B;
+  sort_carve(c, P, ceil_log2(s.N), b.sort);
+  runs_carve(c, P, b.runs);
+  seg_carve(c, P, s.dv, s.dtype, &b.partial, &b.counters);
+  b.dw_part = c.take<float>(int64_t(seg_slices(s.dv, s.dtype)) * P);
+}
+
+// ------------------------------------------------------------ cores
+static mlStatus pkm_fwd_core(const mlPkmShape& s, const void* q, const void* K1, const void* K2,
+                             int32_t* idx, float* w, float* score, PkmFwdBufs& b, cudaStream_t st) {
+  if (s.T == 0) return ML_OK;
+  ML_TRY(launch_pkm_scores(s, q, K1, K2, b.scores, st));
+  ML_TRY(launch_half_topk(s, b.scores, b.hI, b.hs, st));
+  ML_TRY(launch_combine_softmax(s, b.hI, b.hs, idx, w, score, st));
+  return ML_OK;
+}
+
+static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1, const void* K2,
+                             const int32_t* idx, const float* w, const float* dw_part, int ns,
+                             int64_t sstride, float* dq, float* dK1, float* dK2, PkmBwdBufs& b,
+                             cudaStream_t st) {
+  if (s.T == 0) return ML_OK;
+  const int64_t P = int64_t(s.T) * s.H * s.k;
+  const int Dh = s.Dk / 2;
+  ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, st));
+  const int bits = ceil_log2(int64_t(s.H) * s.S);
+  for (int half = 0; half < 2; ++half) {
+    const void* K = half ? K2 : K1;
+    const int32_t* key = half ? b.key2 : b.key1;
+    // dq_half[t,h] = sum_j ds_j K_half[h, a_j]  (a bag over the [H*S, Dh] table)
+    BagFwdArgs a;
+    a.V = K; a.ldv = Dh; a.N = int64_t(s.H) * s.S;
+    a.idx = key; a.w = b.ds; a.B = s.k; a.nbags = s.T * s.H; a.dv = Dh;
+    a.out = dq; a.ldo = s.Dk; a.out_col0 = half * Dh; a.out_f32 = true; a.dtype = s.dtype;
+    a.name = "pkm_dq_bag";
+    ML_TRY(launch_bag_fwd(a, st));
+    // dK_half[h, a] += sum ds * q_half[t,h]  (sorted segments, dense accumulate)
+    int32_t *skey, *spos;
+    ML_TRY(sort_pairs(key, P, bits, b.sort, &skey, &spos, st));
+    ML_TRY(find_runs(skey, P, b.runs, nullptr, nullptr, st));
+    SegArgs g;
+    g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = b.ds;
+    g.src = q; g.lds = s.Dk; g.src_col0 = half * Dh; g.B = s.k;
+    g.out = half ? dK2 : dK1; g.ldo = Dh; g.dense_accumulate = true;
+    g.partial = b.partial; g.counters = b.counters; g.dv = Dh; g.dtype = s.dtype;
+    g.name = "pkm_dK_segreduce";
+    ML_TRY(launch_segreduce(g, st));
+  }
+  return ML_OK;
+}
+
+static mlStatus bag_bwd_core(const mlBagShape& s, const void* V, const int32_t* idx, const float* w,
+                             const void* dy, int32_t* rows, float* dV, int32_t* U, BagBwdBufs& b,
+                             cudaStream_t st) {
+  const int64_t P = int64_t(s.T) * s.B;
+  if (P == 0) {
+    ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
+    return ML_OK;
+  }
+  int32_t *skey, *spos;
+  ML_TRY(sort_pairs(idx, P, ceil_log2(s.N), b.sort, &skey, &spos, st));
+  ML_TRY(find_runs(skey, P, b.runs, rows, U, st));
+  SegArgs g;
+  g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = w;
+  g.src = dy; g.lds = s.dv; g.src_col0 = 0; g.B = s.B;
+  g.V = V; g.ldv = s.dv; g.v_col0 = 0; g.dw_part = b.dw_part;
+  g.out = dV; g.ldo = s.dv; g.dense_accumulate = false;
+  g.partial = b.partial; g.counters = b.counters; g.dv = s.dv; g.dtype = s.dtype;
+  g.name = "embbag_bwd_segreduce";
+  ML_TRY(launch_segreduce(g, st));
+  return ML_OK;
+}
+
+}  // namespace ml
+
+using namespace ml;
+
+#define ML_API_BEGIN try {
+#define ML_API_END                                                        \
+  }                                                                       \
+  catch (const std::exception& e) {                                       \
+    return fail(ML_ERR_CUDA, std::string("internal exception: ") + e.what()); \
+  }                                                                       \
+  catch (...) {                                                           \
+    return fail(ML_ERR_CUDA, "internal exception");                       \
+  }
+
+static cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
+
+extern "C" {
+
+const char* ml_last_error(void) { return t_last_error.c_str(); }
+int ml_version(void) { return 100; }
+uint64_t ml_launch_count(void) { return g_launches.load(); }
+
+int ml_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (sm_count) cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return 0;
+}
+
+mlStatus ml_synth_fill(void* out, int64_t n_rows, int64_t n_cols, int64_t row0, uint64_t seed,
+                       uint32_t tag, float scale, int cls, mlDtype dtype, int64_t modulus,
+                       void* stream) {
+  ML_API_BEGIN
+  if (!out) return fail(ML_ERR_ARG, "null output");
+  if (n_rows < 0 || n_cols < 0 || row0 < 0) return fail(ML_ERR_ARG, "negative size");
+  timing_mark(nullptr, S(stream));
+  return launch_synth(out, n_rows, n_cols, row0, seed, tag, scale, cls, dtype, modulus, S(stream));
+  ML_API_END
+}
+
+mlStatus pkm_topk_workspace(const mlPkmShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_pkm(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  PkmFwdBufs b;
+  pkm_fwd_carve(c, *shape, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus pkm_topk(const mlPkmShape* shape, const void* q, const void* K1, const void* K2,
+                  int32_t* idx, float* w, float* score, void* ws, size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_pkm(shape));
+  if (shape->T == 0) return ML_OK;
+  ML_TRY(check_ptrs({q, K1, K2, idx, w, ws}));
+  if (score) ML_TRY(check_ptrs({score}));
+  size_t need = 0;
+  ML_TRY(pkm_topk_workspace(shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "pkm_topk: workspace too small");
+  Carver c(ws);
+  PkmFwdBufs b;
+  pkm_fwd_carve(c, *shape, b);
+  timing_mark(nullptr, S(stream));
+  return pkm_fwd_core(*shape, q, K1, K2, idx, w, score, b, S(stream));
+  ML_API_END
+}
+
+mlStatus pkm_topk_bwd_workspace(const mlPkmShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_pkm(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  PkmBwdBufs b;
+  pkm_bwd_carve(c, *shape, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus pkm_topk_bwd(const mlPkmShape* shape, const void* q, const void* K1, const void* K2,
+                      const int32_t* idx, const float* w, const float* dw, float* dq, float* dK1,
+                      float* dK2, void* ws, size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_pkm(shape));
+  if (shape->T == 0) return ML_OK;
+  ML_TRY(check_ptrs({q, K1, K2, idx, w, dw, dq, dK1, dK2, ws}));
+  size_t need = 0;
+  ML_TRY(pkm_topk_bwd_workspace(shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "pkm_topk_bwd: workspace too small");
+  Carver c(ws);
+  PkmBwdBufs b;
+  pkm_bwd_carve(c, *shape, b);
+  const int64_t P = int64_t(shape->T) * shape->H * shape->k;
+  timing_mark(nullptr, S(stream));
+  return pkm_bwd_core(*shape, q, K1, K2, idx, w, dw, 1, P, dq, dK1, dK2, b, S(stream));
+  ML_API_END
+}
+
+mlStatus embbag_fwd(const mlBagShape* shape, const void* V, const int32_t* idx, const float* w,
+                    const void* gate_pre, void* y, void* y_ungated, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (shape->T == 0) return ML_OK;
+  ML_TRY(check_ptrs({V, idx, w, y}));
+  if (gate_pre) ML_TRY(check_ptrs({gate_pre}));
+  if (y_ungated) ML_TRY(check_ptrs({y_ungated}));
+  BagFwdArgs a;
+  a.V = V; a.ldv = shape->dv; a.N = shape->N;
+  a.idx = idx; a.w = w; a.B = shape->B; a.nbags = shape->T; a.dv = shape->dv;
+  a.out = y; a.ldo = shape->dv; a.out_col0 = 0; a.out_f32 = false;
+  a.gate = gate_pre; a.y_ungated = y_ungated; a.dtype = shape->dtype;
+  a.name = gate_pre ? "embbag_fwd_gate" : "embbag_fwd";
+  timing_mark(nullptr, S(stream));
+  ML_TRY(launch_bag_fwd(a, S(stream)));
+  return check_index_flag(S(stream));
+  ML_API_END
+}
+
+mlStatus embbag_bwd_workspace(const mlBagShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  BagBwdBufs b;
+  bag_bwd_carve(c, *shape, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, const float* w,
+                    const void* dy, int32_t* rows, float* dV, int32_t* U, float* dw, void* ws,
+                    size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (!U) return fail(ML_ERR_ARG, "null U");
+  if (shape->T == 0) {
+    ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), S(stream)));
+    return ML_OK;
+  }
+  ML_TRY(check_ptrs({V, idx, w, dy, rows, dV, dw, ws}));
+  size_t need = 0;
+  ML_TRY(embbag_bwd_workspace(shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_bwd: workspace too small");
+  Carver c(ws);
+  BagBwdBufs b;
+  bag_bwd_carve(c, *shape, b);
+  timing_mark(nullptr, S(stream));
+  ML_TRY(bag_bwd_core(*shape, V, idx, w, dy, rows, dV, U, b, S(stream)));
+  const int64_t P = int64_t(shape->T) * shape->B;
+  ML_TRY(launch_sum_slices(b.dw_part, seg_slices(shape->dv, shape->dtype), P, dw, S(stream)));
+  return check_index_flag(S(stream));
+  ML_API_END
+}
+
+mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const float* dV,
+                           const int32_t* U, float* dV_dense, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (shape->T == 0) return ML_OK;
+  ML_TRY(check_ptrs({rows, dV, U, dV_dense}));
+  timing_mark(nullptr, S(stream));
+  return launch_scatter_rows(rows, dV, U, int64_t(shape->T) * shape->B, shape->dv, dV_dense,
+                             S(stream));
+  ML_API_END
+}
+
+// ------------------------------------------------------------ layer
+static mlStatus check_layer(const mlLayerShape* s) {
+  if (!s) return fail(ML_ERR_ARG, "null shape");
+  ML_TRY(check_pkm(&s->pkm));
+  if (s->N != int64_t(s->pkm.S) * s->pkm.S) return fail(ML_ERR_CONFIG, "layer: N must equal S*S");
+  mlBagShape bs{s->N, s->dv, s->pkm.T, s->pkm.H * s->pkm.k, s->pkm.dtype};
+  ML_TRY(check_bag(&bs));
+  if (s->gated) {
+    if (s->D < 1) return fail(ML_ERR_CONFIG, "layer: D < 1");
+    if ((int64_t(s->D) * int64_t(dtype_size(s->pkm.dtype))) % 16)
+      return fail(ML_ERR_CONFIG, "layer: D*e must be a multiple of 16 bytes");
+  } else if (s->D != s->dv) {
+    return fail(ML_ERR_CONFIG, "layer: ungated Memory needs D == dv");
+  }
+  return ML_OK;
+}
+
+static mlBagShape bag_of(const mlLayerShape& s) {
+  return mlBagShape{s.N, s.dv, s.pkm.T, s.pkm.H * s.pkm.k, s.pkm.dtype};
+}
+
+struct LayerFwdBufs { PkmFwdBufs pkm; void* z; void* gemm_ws; };
+static void layer_fwd_carve(Carver& c, const mlLayerShape& s, LayerFwdBufs& b) {
+  pkm_fwd_carve(c, s.pkm, b.pkm);
+  b.z = c.take<char>(int64_t(s.pkm.T) * s.dv * int64_t(dtype_size(s.pkm.dtype)));
+  b.gemm_ws = c.take<char>(kGemmWs);
+}
+
+struct LayerBwdBufs {
+  BagBwdBufs bag; PkmBwdBufs pkm; void *dz, *z, *dy, *dg, *gemm_ws;
+};
+static void layer_bwd_carve(Carver& c, const mlLayerShape& s, LayerBwdBufs& b) {
+  const int64_t act = int64_t(s.pkm.T) * s.dv * int64_t(dtype_size(s.pkm.dtype));
+  bag_bwd_carve(c, bag_of(s), b.bag);
+  pkm_bwd_carve(c, s.pkm, b.pkm);
+  b.dz = c.take<char>(act);
+  b.z = c.take<char>(act);
+  b.dy = c.take<char>(act);
+  b.dg = c.take<char>(act);
+  b.gemm_ws = c.take<char>(kGemmWs);
+}
+
+mlStatus memory_layer_fwd_workspace(const mlLayerShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_layer(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  LayerFwdBufs b;
+  layer_fwd_carve(c, *shape, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* q, const void* K1,
+                          const void* K2, const void* V, const void* W1, const void* W2, void* out,
+                          int32_t* idx_saved, float* w_saved, void* g_saved, void* y_saved,
+                          void* ws, size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_layer(shape));
+  const mlLayerShape& s = *shape;
+  if (s.pkm.T == 0) return ML_OK;
+  ML_TRY(check_ptrs({q, K1, K2, V, out, idx_saved, w_saved, ws}));
+  if (s.gated) ML_TRY(check_ptrs({x, W1, W2, g_saved, y_saved}));
+  size_t need = 0;
+  ML_TRY(memory_layer_fwd_workspace(shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "memory_layer_fwd: workspace too small");
+  Carver c(ws);
+  LayerFwdBufs b;
+  layer_fwd_carve(c, s, b);
+  cudaStream_t st = S(stream);
+  const int T = s.pkm.T;
+  timing_mark(nullptr, st);
+  ML_TRY(pkm_fwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, nullptr, b.pkm, st));
+  BagFwdArgs a;
+  a.V = V; a.ldv = s.dv; a.N = s.N;
+  a.idx = idx_saved; a.w = w_saved; a.B = s.pkm.H * s.pkm.k; a.nbags = T; a.dv = s.dv;
+  a.ldo = s.dv; a.dtype = s.pkm.dtype;
+  a.name = s.gated ? "embbag_fwd_gate" : "embbag_fwd";
+  if (!s.gated) {
+    a.out = out;
+    ML_TRY(launch_bag_fwd(a, st));
+    if (y_saved && y_saved != out)
+      ML_CUDA_TRY(cudaMemcpyAsync(y_saved, out, size_t(T) * s.dv * dtype_size(s.pkm.dtype),
+                                  cudaMemcpyDeviceToDevice, st));
+    return check_index_flag(st);
+  }
+  // g = x W1  [T, dv]
+  ML_TRY(gemm_rm(false, false, T, s.dv, s.D, x, s.D, W1, s.dv, g_saved, s.dv, s.pkm.dtype, false,
+                 b.gemm_ws, kGemmWs, st));
+  // z = (sum_j w_j V[idx_j]) * silu(g); y saved
+  a.out = b.z; a.gate = g_saved; a.y_ungated = y_saved;
+  ML_TRY(launch_bag_fwd(a, st));
+  // out = z W2  [T, D]
+  ML_TRY(gemm_rm(false, false, T, s.D, s.dv, b.z, s.dv, W2, s.D, out, s.D, s.pkm.dtype, false,
+                 b.gemm_ws, kGemmWs, st));
+  return check_index_flag(st);
+  ML_API_END
+}
+
+mlStatus memory_layer_bwd_workspace(const mlLayerShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_layer(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  LayerBwdBufs b;
+  layer_bwd_carve(c, *shape, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const void* x,
+                          const void* q, const void* K1, const void* K2, const void* V,
+                          const void* W1, const void* W2, const int32_t* idx_saved,
+                          const float* w_saved, const void* g_saved, const void* y_saved,
+                          void* dx, float* dq, float* dK1, float* dK2, int32_t* dV_rows,
+                          float* dV, int32_t* U, float* dW1, float* dW2, float* dw_out, void* ws,
+                          size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_layer(shape));
+  const mlLayerShape& s = *shape;
+  if (!U) return fail(ML_ERR_ARG, "null U");
+  cudaStream_t st = S(stream);
+  if (s.pkm.T == 0) {
+    ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
+    return ML_OK;
+  }
+  ML_TRY(check_ptrs({dout, q, K1, K2, V, idx_saved, w_saved, dq, dK1, dK2, dV_rows, dV, ws}));
+  if (s.gated) ML_TRY(check_ptrs({x, W1, W2, g_saved, y_saved, dx, dW1, dW2}));
+  if (dw_out) ML_TRY(check_ptrs({dw_out}));
+  size_t need = 0;
+  ML_TRY(memory_layer_bwd_workspace(shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "memory_layer_bwd: workspace too small");
+  Carver c(ws);
+  LayerBwdBufs b;
+  layer_bwd_carve(c, s, b);
+  const int T = s.pkm.T;
+  const mlDtype dt = s.pkm.dtype;
+  const void* dy = dout;
+  timing_mark(nullptr, st);
+  if (s.gated) {
+    // dz = dout W2^T
+    ML_TRY(gemm_rm(false, true, T, s.dv, s.D, dout, s.D, W2, s.D, b.dz, s.dv, dt, false, b.gemm_ws,
+                   kGemmWs, st));
+    ML_TRY(launch_gate_bwd(b.dz, g_saved, y_saved, b.z, b.dy, b.dg, int64_t(T) * s.dv, dt, st));
+    // dW2 = z^T dout ; dW1 = x^T dg ; dx = dg W1^T
+    ML_TRY(gemm_rm(true, false, s.dv, s.D, T, b.z, s.dv, dout, s.D, dW2, s.D, dt, true, b.gemm_ws,
+                   kGemmWs, st));
+    ML_TRY(gemm_rm(true, false, s.D, s.dv, T, x, s.D, b.dg, s.dv, dW1, s.dv, dt, true, b.gemm_ws,
+                   kGemmWs, st));
+    ML_TRY(gemm_rm(false, true, T, s.D, s.dv, b.dg, s.dv, W1, s.dv, dx, s.D, dt, false, b.gemm_ws,
+                   kGemmWs, st));
+    dy = b.dy;
+  }
+  const mlBagShape bs = bag_of(s);
+  ML_TRY(bag_bwd_core(bs, V, idx_saved, w_saved, dy, dV_rows, dV, U, b.bag, st));
+  const int ns = seg_slices(s.dv, dt);
+  const int64_t P = int64_t(T) * bs.B;
+  ML_TRY(pkm_bwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, b.bag.dw_part, ns, P, dq, dK1, dK2,
+                      b.pkm, st));
+  if (dw_out) ML_TRY(launch_sum_slices(b.bag.dw_part, ns, P, dw_out, st));
+  return check_index_flag(st);
+  ML_API_END
+}
+
+}  // extern "C"

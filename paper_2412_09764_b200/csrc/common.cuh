@@ -1,0 +1,142 @@
+// Shared device/host helpers of libmemlayer (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/memlayer.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libmemlayer is written for sm_100a (B200) only"
+#endif
+
+namespace ml {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+mlStatus fail(mlStatus st, const std::string& msg);
+void count_launch(int n = 1);
+// Records a timing event after an operation on stream s (no-op unless
+// ml_timing_enable(1)); name == nullptr marks a start point.
+void timing_mark(const char* name, cudaStream_t s);
+
+#define ML_CUDA_TRY(expr)                                                        \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess)                                                       \
+      return ::ml::fail(ML_ERR_CUDA, std::string(#expr) + ": " +                 \
+                                         cudaGetErrorString(_e));                \
+  } while (0)
+
+// Every launch site names its stream `s`.
+#define ML_LAUNCH_CHECK(name)                                                    \
+  do {                                                                           \
+    ::ml::count_launch();                                                        \
+    ::ml::timing_mark(name, s);                                                  \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess)                                                       \
+      return ::ml::fail(ML_ERR_CUDA, std::string("launch ") + name + ": " +      \
+                                         cudaGetErrorString(_e));                \
+  } while (0)
+
+#define ML_TRY(expr)                                                             \
+  do {                                                                           \
+    mlStatus _s = (expr);                                                        \
+    if (_s != ML_OK) return _s;                                                  \
+  } while (0)
+
+// ------------------------------------------------------- workspace carving
+// Host-side bump allocator over the caller's workspace.  With base == nullptr
+// it only measures (used by the *_workspace queries).
+struct Carver {
+  char* base;
+  size_t used = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    used = (used + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + used) : nullptr;
+    used += count * sizeof(T);
+    return p;
+  }
+};
+
+// ------------------------------------------------------------ device utils
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ldg_v4(const void* p) {
+  return *reinterpret_cast<const uint4*>(p);
+}
+
+__device__ __forceinline__ void stg_v4(void* p, uint4 v) {
+  *reinterpret_cast<uint4*>(p) = v;
+}
+
+// bf16 pair <-> float2 (exact widening)
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t u) {
+  float2 f;
+  f.x = __uint_as_float(u << 16);
+  f.y = __uint_as_float(u & 0xFFFF0000u);
+  return f;
+}
+__device__ __forceinline__ uint32_t f2_to_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// A 16-byte vector of the storage type, widened to fp32 lanes.
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ __forceinline__ static void load(const uint4& u, float* f) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
+  __device__ __forceinline__ static uint4 pack(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
+                      __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+};
+template <> struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static void load(const uint4& u, float* f) {
+    float2 a = bf2_to_f2(u.x), b = bf2_to_f2(u.y), c = bf2_to_f2(u.z), d = bf2_to_f2(u.w);
+    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+    f[4] = c.x; f[5] = c.y; f[6] = d.x; f[7] = d.y;
+  }
+  __device__ __forceinline__ static uint4 pack(const float* f) {
+    return make_uint4(f2_to_bf2(f[0], f[1]), f2_to_bf2(f[2], f[3]),
+                      f2_to_bf2(f[4], f[5]), f2_to_bf2(f[6], f[7]));
+  }
+};
+
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+// Order-preserving map fp32 -> u32 (larger float <=> larger key); -0 == +0.
+__device__ __forceinline__ uint32_t ord_f32(float f) {
+  uint32_t b = __float_as_uint(f + 0.0f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t o) {
+  uint32_t b = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(b);
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+__device__ __forceinline__ float sigmoid_f(float g) { return 1.0f / (1.0f + expf(-g)); }
+
+// Device int raised by kernels that saw an out-of-range index (defined in
+// bag_fwd.cu; its address is passed to kernels as an argument).
+int* index_flag_ptr();
+
+inline size_t dtype_size(mlDtype d) { return d == ML_BF16 ? 2 : 4; }
+
+}  // namespace ml

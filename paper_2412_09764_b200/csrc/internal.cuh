@@ -1,0 +1,117 @@
+// Internal launchers shared by the C-ABI entry points (not exported).
+#pragma once
+#include "common.cuh"
+
+namespace ml {
+
+// ------------------------------------------------------------ bag forward
+// out[b, out_col0 + c] = sum_{j<B} w[b,j] * V[idx[b,j], c]   for c < dv
+// (optionally gated: out = y * silu(gate[b, c]); y_ungated gets y).
+struct BagFwdArgs {
+  const void* V = nullptr; int64_t ldv = 0; int64_t N = 0;
+  const int32_t* idx = nullptr; const float* w = nullptr;
+  int32_t B = 0; int32_t nbags = 0; int32_t dv = 0;
+  void* out = nullptr; int64_t ldo = 0; int32_t out_col0 = 0; bool out_f32 = false;
+  const void* gate = nullptr; void* y_ungated = nullptr;
+  mlDtype dtype = ML_BF16;
+  const char* name = "bag_fwd";   // timing / profiling label
+};
+mlStatus check_cols(int32_t dv, mlDtype dt, const char* what);
+mlStatus launch_bag_fwd(const BagFwdArgs& a, cudaStream_t s);
+
+// --------------------------------------------------------------- scan
+// Exclusive prefix sum of n int32 values; total (device int, nullable) gets
+// the sum.  tmp needs scan_tmp_elems(n) ints.
+int64_t scan_tmp_elems(int64_t n);
+mlStatus scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* tmp,
+                        int32_t* total, cudaStream_t s);
+
+// --------------------------------------------------------------- sort
+// Stable LSD radix sort of (key, position) pairs, keys < 2^bits.  The
+// values are the original positions 0..n-1.
+struct SortBufs {
+  int32_t* k[2] = {nullptr, nullptr};
+  int32_t* v[2] = {nullptr, nullptr};
+  int32_t* counts = nullptr;
+  int32_t* scan_tmp = nullptr;
+};
+void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b);
+// On return *keys / *vals point at the sorted arrays (inside b).
+mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b,
+                    int32_t** keys, int32_t** vals, cudaStream_t s);
+
+// --------------------------------------------------- runs of sorted keys
+constexpr int kPieceLen = 32;  // positions per reduction piece (L)
+struct RunBufs {
+  int32_t* flags = nullptr;      // [n]
+  int32_t* excl = nullptr;       // [n] run id of each position (exclusive scan of heads)
+  int32_t* run_begin = nullptr;  // [n+1]
+  int32_t* pieces = nullptr;     // [n] npieces at heads
+  int32_t* piece_base = nullptr; // [n] exclusive scan of pieces
+  int32_t* n_slots = nullptr;    // device scalar
+  int32_t* scan_tmp = nullptr;
+};
+void runs_carve(Carver& c, int64_t n, RunBufs& r);
+// rows_out (nullable) [n]: distinct keys ascending; U (device int) count.
+mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out,
+                   int32_t* U, cudaStream_t s);
+
+// ------------------------------------------------ segmented reduction
+// For every run of equal sorted keys (one output row per run):
+//   out[row, c] (=|+=) sum_{p in run} w[pos_p] * src[pos_p / B, src_col0 + c]
+// and, if V != nullptr, dw_part[slice*P + pos_p] = <src row, V[key] slice>.
+struct SegArgs {
+  const int32_t* skey = nullptr; const int32_t* spos = nullptr; int64_t P = 0;
+  const RunBufs* runs = nullptr;
+  const float* w = nullptr;
+  const void* src = nullptr; int64_t lds = 0; int32_t src_col0 = 0; int32_t B = 1;
+  const void* V = nullptr; int64_t ldv = 0; int32_t v_col0 = 0;
+  float* dw_part = nullptr;
+  float* out = nullptr; int64_t ldo = 0; bool dense_accumulate = false;
+  float* partial = nullptr; int32_t* counters = nullptr;
+  int32_t dv = 0; mlDtype dtype = ML_BF16;
+  const char* name = "segreduce";  // timing / profiling label
+};
+int seg_slices(int32_t dv, mlDtype dt);
+void seg_carve(Carver& c, int64_t P, int32_t dv, mlDtype dt, float** partial, int32_t** counters);
+mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s);
+// dw[p] = sum_s dw_part[s*P + p]
+mlStatus launch_sum_slices(const float* part, int nslices, int64_t P, float* dw, cudaStream_t s);
+
+// ------------------------------------------------------ product keys
+mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1,
+                           const void* K2, float* scores, cudaStream_t s);
+mlStatus launch_half_topk(const mlPkmShape& sh, const float* scores, int32_t* hI,
+                          float* hs, cudaStream_t s);
+mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const float* hs,
+                                int32_t* idx, float* w, float* score, cudaStream_t s);
+// ds = w (dw - sum w dw) with dw = sum over nslices partials; also writes the
+// half-key row ids key1 = h*S + idx/S, key2 = h*S + idx%S per position.
+mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
+                            const float* dw_part, int nslices, int64_t slice_stride,
+                            float* ds, int32_t* key1, int32_t* key2, cudaStream_t s);
+
+// ------------------------------------------------------------ gate
+// z = y*silu(g); dy = dz*silu(g); dg = dz*y*silu'(g)   (elementwise, n elems)
+mlStatus launch_gate_bwd(const void* dz, const void* g, const void* y, void* z, void* dy,
+                         void* dg, int64_t n, mlDtype dt, cudaStream_t s);
+mlStatus launch_scatter_rows(const int32_t* rows, const float* dV, const int32_t* U,
+                             int64_t cap, int32_t dv, float* dense, cudaStream_t s);
+
+// Row-major GEMM on cuBLASLt: C[M,N] = op(A) op(B), fp32 accumulation.
+mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K,
+                 const void* A, int64_t lda, const void* B, int64_t ldb,
+                 void* C, int64_t ldc, mlDtype ab, bool c_f32,
+                 void* ws, size_t ws_bytes, cudaStream_t s);
+constexpr size_t kGemmWs = size_t(32) << 20;
+
+// ------------------------------------------------------------ synth
+mlStatus launch_synth(void* out, int64_t n_rows, int64_t n_cols, int64_t row0, uint64_t seed,
+                      uint32_t tag, float scale, int cls, mlDtype dt, int64_t modulus,
+                      cudaStream_t s);
+
+int num_sms();
+bool check_indices_enabled();
+mlStatus check_index_flag(cudaStream_t s);
+
+}  // namespace ml

@@ -1,0 +1,309 @@
+// Product-key top-k (§3.1.1) and its backward.
+//
+//  scores:   S_half[t,h,half,a] = q[t,h,half*Dk/2 : ...] . K_half[h,a,:]   (fp32 FMA)
+//  half top-k: per (t,h,half) the k best of S (score desc, ties -> lower a)
+//  combine:  the k best of the k*k sums s1[i] + s2[j] (ties -> lower flat
+//            index a*S+b), then w = softmax (Eq. 1)
+//  softmax bwd: ds = w (dw - sum_j w_j dw_j)
+//
+// Selection is exact: every candidate gets a unique 64-bit key
+// (ord(score) << 32 | ~id) whose order is the paper's order plus the
+// tie-break; a warp-cooperative MSB radix select (8-bit digits, shared-memory
+// histogram, early exit once the boundary bin is exactly filled) finds the k
+// largest keys, which are then bitonic-sorted across the warp.
+#include "internal.cuh"
+
+namespace ml {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ------------------------------------------------ SIMT fp32 scoring GEMM
+// Tile: 64 tokens x 64 keys, K-chunks of 32; 256 threads, 4x4 per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) pkm_scores_kernel(const T* q, const T* K1, const T* K2,
+                                                         float* scores, int T_, int H, int S,
+                                                         int Dk) {
+  __shared__ float As[32][64 + 4];
+  __shared__ float Bs[32][64 + 4];
+  const int Dh = Dk / 2;
+  const int hh = blockIdx.z;  // h*2 + half
+  const int h = hh >> 1, half = hh & 1;
+  const T* K = half ? K2 : K1;
+  const int t0 = blockIdx.x * 64, a0 = blockIdx.y * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < Dh; k0 += 32) {
+    for (int e = threadIdx.x; e < 64 * 32; e += 256) {
+      const int m = e >> 5, kk = e & 31;
+      const int t = t0 + m, a = a0 + m, kc = k0 + kk;
+      float av = 0.f, bv = 0.f;
+      if (t < T_ && kc < Dh) av = to_f(q[(int64_t(t) * H + h) * Dk + half * Dh + kc]);
+      if (a < S && kc < Dh) bv = to_f(K[(int64_t(h) * S + a) * Dh + kc]);
+      As[kk][m] = av;
+      Bs[kk][m] = bv;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      float ar[4], br[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ar[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) br[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + ty + 16 * i;
+    if (t >= T_) continue;
+    float* row = scores + ((int64_t(t) * H + h) * 2 + half) * S;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int a = a0 + tx + 16 * j;
+      if (a < S) row[a] = acc[i][j];
+    }
+  }
+}
+
+// ------------------------------------------------ warp top-k machinery
+__device__ __forceinline__ uint64_t make_key(float score, uint32_t id) {
+  return (uint64_t(ord_f32(score)) << 32) | uint64_t(0xFFFFFFFFu - id);
+}
+__device__ __forceinline__ uint32_t key_id(uint64_t k) { return 0xFFFFFFFFu - uint32_t(k); }
+__device__ __forceinline__ float key_score(uint64_t k) { return unord_f32(uint32_t(k >> 32)); }
+
+// Bitonic sort of one u64 per lane, descending across lanes 0..31.
+__device__ __forceinline__ uint64_t warp_sort_desc(uint64_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint64_t y = __shfl_xor_sync(FULL, x, stride);
+      const bool up = ((lane & size) == 0);          // this block sorted descending?
+      const bool lower = ((lane & stride) == 0);
+      const bool take_max = (up == lower);
+      x = take_max ? (x > y ? x : y) : (x < y ? x : y);
+    }
+  }
+  return x;
+}
+
+// k largest of n unique keys gen(e), e < n; lane j < k returns the j-th
+// largest (descending); lanes >= k return 0.  hist: 256 u32 of warp-private
+// smem; buf: 32 u64 of warp-private smem.
+template <class Gen>
+__device__ uint64_t warp_topk(const Gen& gen, int n, int k, uint32_t* hist, uint64_t* buf) {
+  const int lane = threadIdx.x & 31;
+  uint64_t prefix = 0;
+  int shift = 64;
+  int need = k;
+  while (shift > 0) {
+    shift -= 8;
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    const int hs = shift + 8;
+    for (int e = lane; e < n; e += 32) {
+      const uint64_t key = gen(e);
+      const bool match = (hs >= 64) || ((key >> hs) == (prefix >> hs));
+      if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t c[8], tot = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = hist[lane * 8 + j];
+      tot += c[j];
+    }
+    uint32_t incl = tot;  // suffix sum over lanes >= lane
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_down_sync(FULL, incl, o);
+      if (lane + o < 32) incl += v;
+    }
+    uint32_t cum = incl - tot;  // keys in bins of higher lanes
+    int found = -1;
+    uint32_t above = 0, cnt = 0;
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+      if (found < 0 && cum < uint32_t(need) && cum + c[j] >= uint32_t(need)) {
+        found = lane * 8 + j;
+        above = cum;
+        cnt = c[j];
+      }
+      cum += c[j];
+    }
+    const unsigned fm = __ballot_sync(FULL, found >= 0);
+    const int srcl = __ffs(fm) - 1;
+    found = __shfl_sync(FULL, found, srcl);
+    above = __shfl_sync(FULL, above, srcl);
+    cnt = __shfl_sync(FULL, cnt, srcl);
+    need -= int(above);
+    prefix |= uint64_t(found) << shift;
+    __syncwarp();
+    if (int(cnt) == need) break;
+  }
+  // selected: (key >> shift) >= (prefix >> shift); exactly k of them
+  const uint64_t thr = prefix >> shift;
+  int base = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int e = e0 + lane;
+    uint64_t key = 0;
+    bool sel = false;
+    if (e < n) {
+      key = gen(e);
+      sel = (key >> shift) >= thr;
+    }
+    const unsigned sm = __ballot_sync(FULL, sel);
+    if (sel) buf[base + __popc(sm & lt)] = key;
+    base += __popc(sm);
+  }
+  __syncwarp();
+  uint64_t x = lane < k ? buf[lane] : 0ull;
+  __syncwarp();
+  return warp_sort_desc(x);
+}
+
+// one warp per (t, h, half) row of S scores
+__global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int64_t rows, int S,
+                                                        int k, int32_t* hI, float* hs) {
+  __shared__ uint32_t s_hist[8][256];
+  __shared__ uint64_t s_buf[8][32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = int64_t(blockIdx.x) * 8 + wid;
+  if (row >= rows) return;
+  const float* sr = scores + row * S;
+  auto gen = [sr](int e) { return make_key(sr[e], uint32_t(e)); };
+  const uint64_t key = warp_topk(gen, S, k, s_hist[wid], s_buf[wid]);
+  if (lane < k) {
+    hI[row * k + lane] = int32_t(key_id(key));
+    hs[row * k + lane] = key_score(key);
+  }
+}
+
+// one warp per (t, h): combine the two half lists, softmax
+__global__ void __launch_bounds__(256) combine_kernel(const int32_t* hI, const float* hs,
+                                                      int64_t TH, int S, int k, int32_t* idx,
+                                                      float* w, float* score) {
+  __shared__ uint32_t s_hist[8][256];
+  __shared__ uint64_t s_buf[8][32];
+  __shared__ float s_s[8][2][32];
+  __shared__ int32_t s_i[8][2][32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t th = int64_t(blockIdx.x) * 8 + wid;
+  if (th >= TH) return;
+  if (lane < k) {
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      s_s[wid][hf][lane] = hs[(th * 2 + hf) * k + lane];
+      s_i[wid][hf][lane] = hI[(th * 2 + hf) * k + lane];
+    }
+  }
+  __syncwarp();
+  const float* s1 = s_s[wid][0];
+  const float* s2 = s_s[wid][1];
+  const int32_t* I1 = s_i[wid][0];
+  const int32_t* I2 = s_i[wid][1];
+  auto gen = [=](int e) {
+    const int i = e / k, j = e - (e / k) * k;
+    const float c = s1[i] + s2[j];
+    return make_key(c, uint32_t(I1[i]) * uint32_t(S) + uint32_t(I2[j]));
+  };
+  const uint64_t key = warp_topk(gen, k * k, k, s_hist[wid], s_buf[wid]);
+  const float sc = key_score(key);
+  const float m = __shfl_sync(FULL, sc, 0);
+  float ex = lane < k ? expf(sc - m) : 0.f;
+  float sum = ex;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+  if (lane < k) {
+    idx[th * k + lane] = int32_t(key_id(key));
+    w[th * k + lane] = ex / sum;
+    if (score) score[th * k + lane] = sc;
+  }
+}
+
+// one warp per (t, h)
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, const float* w,
+                                                          const float* dw_part, int ns,
+                                                          int64_t sstride, int64_t TH, int H,
+                                                          int S, int k, float* ds, int32_t* key1,
+                                                          int32_t* key2) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t th = int64_t(blockIdx.x) * 8 + wid;
+  if (th >= TH) return;
+  const int h = int(th % H);
+  const int64_t o = th * k + lane;
+  float wv = 0.f, dwv = 0.f;
+  int32_t ix = 0;
+  if (lane < k) {
+    wv = w[o];
+    ix = idx[o];
+    for (int s = 0; s < ns; ++s) dwv += dw_part[int64_t(s) * sstride + o];
+  }
+  float dot = wv * dwv;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(FULL, dot, off);
+  if (lane < k) {
+    ds[o] = wv * (dwv - dot);
+    key1[o] = h * S + ix / S;
+    key2[o] = h * S + ix % S;
+  }
+}
+
+}  // namespace
+
+mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
+                           float* scores, cudaStream_t s) {
+  if (sh.T <= 0) return ML_OK;
+  dim3 grid(unsigned((sh.T + 63) / 64), unsigned((sh.S + 63) / 64), unsigned(sh.H * 2));
+  if (sh.dtype == ML_BF16)
+    pkm_scores_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(K1),
+        static_cast<const __nv_bfloat16*>(K2), scores, sh.T, sh.H, sh.S, sh.Dk);
+  else
+    pkm_scores_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(q),
+                                                  static_cast<const float*>(K1),
+                                                  static_cast<const float*>(K2), scores, sh.T,
+                                                  sh.H, sh.S, sh.Dk);
+  ML_LAUNCH_CHECK("pkm_scores");
+  return ML_OK;
+}
+
+mlStatus launch_half_topk(const mlPkmShape& sh, const float* scores, int32_t* hI, float* hs,
+                          cudaStream_t s) {
+  const int64_t rows = int64_t(sh.T) * sh.H * 2;
+  if (rows <= 0) return ML_OK;
+  half_topk_kernel<<<unsigned((rows + 7) / 8), 256, 0, s>>>(scores, rows, sh.S, sh.k, hI, hs);
+  ML_LAUNCH_CHECK("half_topk");
+  return ML_OK;
+}
+
+mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const float* hs,
+                                int32_t* idx, float* w, float* score, cudaStream_t s) {
+  const int64_t TH = int64_t(sh.T) * sh.H;
+  if (TH <= 0) return ML_OK;
+  combine_kernel<<<unsigned((TH + 7) / 8), 256, 0, s>>>(hI, hs, TH, sh.S, sh.k, idx, w, score);
+  ML_LAUNCH_CHECK("combine_softmax");
+  return ML_OK;
+}
+
+mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
+                            const float* dw_part, int nslices, int64_t slice_stride, float* ds,
+                            int32_t* key1, int32_t* key2, cudaStream_t s) {
+  const int64_t TH = int64_t(sh.T) * sh.H;
+  if (TH <= 0) return ML_OK;
+  softmax_bwd_kernel<<<unsigned((TH + 7) / 8), 256, 0, s>>>(
+      idx, w, dw_part, nslices, slice_stride, TH, sh.H, sh.S, sh.k, ds, key1, key2);
+  ML_LAUNCH_CHECK("softmax_bwd");
+  return ML_OK;
+}
+
+}  // namespace ml

@@ -1,0 +1,339 @@
+// Device-wide scan, stable LSD radix sort of (key, position) pairs and run
+// detection: the "preprocessing to inverse the token_id to embedding_id
+// mapping, so that each row in the embedding gradient can know which token
+// will contribute to it" of the "reverse_indices" backward (§3.1.4,
+// P:176).  Stability keeps positions ascending inside each run, which fixes
+// the summation order of every gradient row (determinism).
+//
+// Sort design: 4096 keys per CTA (8 warps x 16 rounds x 32); each warp ranks
+// its 512 keys with __match_any_sync and warp-private digit counters, the
+// CTA combines warps in order, a device-wide exclusive scan over the
+// digit-major [digit][block] count matrix gives every (digit, block) its
+// output offset.  Digits are <= 8 bits; passes = ceil(bits / 8).
+#include "internal.cuh"
+
+namespace ml {
+namespace {
+
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    int t = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) s_warp[lane] = t;
+  }
+  __syncthreads();
+  const int warp_off = wid ? s_warp[wid - 1] : 0;
+  *total = s_warp[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return warp_off + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int32_t* in, int64_t n,
+                                                                   int32_t* tmp) {
+  __shared__ int s_warp[32];
+  const int64_t base = int64_t(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  int sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) sum += in[base + i];
+  int total;
+  block_excl_scan(sum, s_warp, &total);
+  if (threadIdx.x == 0) tmp[blockIdx.x] = total;
+}
+
+// Single CTA: exclusive scan of the nb block sums, in place; total -> *total.
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(int32_t* tmp, int64_t nb,
+                                                           int32_t* total) {
+  __shared__ int s_warp[32];
+  int carry = 0;
+  for (int64_t c0 = 0; c0 < nb; c0 += 1024 * 4) {
+    const int64_t base = c0 + threadIdx.x * 4;
+    int v[4], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = (base + i < nb) ? tmp[base + i] : 0;
+      sum += v[i];
+    }
+    int tot;
+    int ex = block_excl_scan(sum, s_warp, &tot) + carry;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (base + i < nb) tmp[base + i] = ex;
+      ex += v[i];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const int32_t* in, int32_t* out,
+                                                                 int64_t n, const int32_t* tmp) {
+  __shared__ int s_warp[32];
+  const int64_t base = int64_t(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  int v[kScanItems], sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < n) ? in[base + i] : 0;
+    sum += v[i];
+  }
+  int total;
+  int ex = block_excl_scan(sum, s_warp, &total) + tmp[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = ex;
+    ex += v[i];
+  }
+}
+
+// ------------------------------------------------------------ radix sort
+constexpr int kSortWarps = 8;
+constexpr int kSortRounds = 16;
+constexpr int kSortTile = kSortWarps * kSortRounds * 32;  // 4096
+
+struct SortPassParams {
+  const int32_t* kin; const int32_t* vin;  // vin == nullptr -> value = position
+  int32_t* kout; int32_t* vout;
+  int64_t n; int nblocks; int shift; int dbits; uint32_t key_limit;
+  int32_t* counts;  // [nbins][nblocks]; scanned in place between the kernels
+  int* flag;
+};
+
+__device__ __forceinline__ int32_t load_key(const SortPassParams& p, int64_t i, bool first) {
+  int32_t k = p.kin[i];
+  if (first && static_cast<uint32_t>(k) >= p.key_limit) {
+    atomicExch(p.flag, 1);
+    k = 0;
+  }
+  return k;
+}
+
+__global__ void __launch_bounds__(256) sort_hist_kernel(SortPassParams p, bool first) {
+  __shared__ int s_cnt[kSortWarps][256];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nbins = 1 << p.dbits;
+  for (int d = lane; d < 256; d += 32) s_cnt[wid][d] = 0;
+  __syncwarp();
+  const int64_t wbase = int64_t(blockIdx.x) * kSortTile + int64_t(wid) * kSortRounds * 32;
+  const uint32_t mask = uint32_t(nbins - 1);
+  for (int r = 0; r < kSortRounds; ++r) {
+    const int64_t i = wbase + r * 32 + lane;
+    const bool valid = i < p.n;
+    const uint32_t dig = valid ? ((uint32_t(load_key(p, i, first)) >> p.shift) & mask) : 0x10000u;
+    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    if (valid && lane == __ffs(peers) - 1) s_cnt[wid][dig] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < nbins; d += 256) {
+    int t = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) t += s_cnt[w][d];
+    p.counts[int64_t(d) * p.nblocks + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, bool first) {
+  __shared__ int s_cnt[kSortWarps][256];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nbins = 1 << p.dbits;
+  const uint32_t mask = uint32_t(nbins - 1);
+  for (int d = lane; d < 256; d += 32) s_cnt[wid][d] = 0;
+  __syncwarp();
+  const int64_t wbase = int64_t(blockIdx.x) * kSortTile + int64_t(wid) * kSortRounds * 32;
+  int32_t key[kSortRounds];
+  uint32_t dig[kSortRounds];
+  unsigned peers[kSortRounds];
+#pragma unroll
+  for (int r = 0; r < kSortRounds; ++r) {
+    const int64_t i = wbase + r * 32 + lane;
+    const bool valid = i < p.n;
+    key[r] = valid ? load_key(p, i, first) : 0;
+    dig[r] = valid ? ((uint32_t(key[r]) >> p.shift) & mask) : 0x10000u;
+    peers[r] = __match_any_sync(0xffffffffu, dig[r]);
+    if (valid && lane == __ffs(peers[r]) - 1) s_cnt[wid][dig[r]] += __popc(peers[r]);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per (warp, digit) base offsets: global offset of (digit, block) + earlier warps
+  for (int d = threadIdx.x; d < nbins; d += 256) {
+    int run = p.counts[int64_t(d) * p.nblocks + blockIdx.x];
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      const int c = s_cnt[w][d];
+      s_cnt[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < kSortRounds; ++r) {
+    const int64_t i = wbase + r * 32 + lane;
+    const bool valid = i < p.n;
+    int dst = 0;
+    if (valid) dst = s_cnt[wid][dig[r]] + __popc(peers[r] & lt);
+    __syncwarp();
+    if (valid && lane == __ffs(peers[r]) - 1) s_cnt[wid][dig[r]] += __popc(peers[r]);
+    __syncwarp();
+    if (valid) {
+      p.kout[dst] = key[r];
+      p.vout[dst] = p.vin ? p.vin[i] : int32_t(i);
+    }
+  }
+}
+
+// ------------------------------------------------------------ runs
+__global__ void run_flags_kernel(const int32_t* skey, int64_t n, int32_t* flags) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = (i == 0 || skey[i] != skey[i - 1]) ? 1 : 0;
+}
+
+__global__ void run_fill_kernel(const int32_t* skey, int64_t n, const int32_t* flags,
+                                const int32_t* excl, int32_t* run_begin, int32_t* rows_out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (flags[i]) {
+    const int32_t r = excl[i];
+    run_begin[r] = int32_t(i);
+    if (rows_out) rows_out[r] = skey[i];
+  }
+  if (i == n - 1) run_begin[excl[i] + flags[i]] = int32_t(n);
+}
+
+__global__ void run_pieces_kernel(int64_t n, const int32_t* flags, const int32_t* excl,
+                                  const int32_t* run_begin, int32_t* pieces) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int np = 0;
+  if (flags[i]) {
+    const int32_t len = run_begin[excl[i] + 1] - int32_t(i);
+    np = len > kPieceLen ? (len + kPieceLen - 1) / kPieceLen : 0;
+  }
+  pieces[i] = np;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ host side
+int64_t scan_tmp_elems(int64_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+mlStatus scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* tmp, int32_t* total,
+                        cudaStream_t s) {
+  if (n <= 0) {
+    if (total) ML_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(int32_t), s));
+    return ML_OK;
+  }
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  scan_reduce_kernel<<<unsigned(nb), kScanThreads, 0, s>>>(in, n, tmp);
+  ML_LAUNCH_CHECK("scan_reduce");
+  scan_blocks_kernel<<<1, 1024, 0, s>>>(tmp, nb, total);
+  ML_LAUNCH_CHECK("scan_blocks");
+  scan_down_kernel<<<unsigned(nb), kScanThreads, 0, s>>>(in, out, n, tmp);
+  ML_LAUNCH_CHECK("scan_down");
+  return ML_OK;
+}
+
+static int sort_nblocks(int64_t n) { return int((n + kSortTile - 1) / kSortTile); }
+
+void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b) {
+  (void)bits;
+  const int nb = sort_nblocks(n);
+  b.k[0] = c.take<int32_t>(n);
+  b.v[0] = c.take<int32_t>(n);
+  b.k[1] = c.take<int32_t>(n);
+  b.v[1] = c.take<int32_t>(n);
+  b.counts = c.take<int32_t>(int64_t(256) * nb);
+  b.scan_tmp = c.take<int32_t>(scan_tmp_elems(int64_t(256) * nb));
+}
+
+mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, int32_t** keys,
+                    int32_t** vals, cudaStream_t s) {
+  if (n <= 0) {
+    *keys = b.k[0];
+    *vals = b.v[0];
+    return ML_OK;
+  }
+  if (bits < 1) bits = 1;
+  if (bits > 31) return fail(ML_ERR_CONFIG, "sort: keys must fit in 31 bits");
+  const int passes = (bits + 7) / 8;
+  const int dbits = (bits + passes - 1) / passes;
+  const int nb = sort_nblocks(n);
+  SortPassParams p;
+  p.n = n;
+  p.nblocks = nb;
+  p.dbits = dbits;
+  p.key_limit = uint32_t(1) << bits;
+  p.counts = b.counts;
+  p.flag = index_flag_ptr();
+  const int64_t ncounts = int64_t(nb) << dbits;
+  const int32_t* kin = keys_in;
+  const int32_t* vin = nullptr;
+  int cur = 0;
+  for (int pass = 0; pass < passes; ++pass) {
+    p.kin = kin;
+    p.vin = vin;
+    p.kout = b.k[cur];
+    p.vout = b.v[cur];
+    p.shift = pass * dbits;
+    const bool first = pass == 0;
+    sort_hist_kernel<<<nb, 256, 0, s>>>(p, first);
+    ML_LAUNCH_CHECK("sort_hist");
+    ML_TRY(scan_exclusive(b.counts, b.counts, ncounts, b.scan_tmp, nullptr, s));
+    sort_scatter_kernel<<<nb, 256, 0, s>>>(p, first);
+    ML_LAUNCH_CHECK("sort_scatter");
+    kin = b.k[cur];
+    vin = b.v[cur];
+    cur ^= 1;
+  }
+  *keys = const_cast<int32_t*>(kin);
+  *vals = const_cast<int32_t*>(vin);
+  return ML_OK;
+}
+
+void runs_carve(Carver& c, int64_t n, RunBufs& r) {
+  r.flags = c.take<int32_t>(n);
+  r.excl = c.take<int32_t>(n);
+  r.run_begin = c.take<int32_t>(n + 1);
+  r.pieces = c.take<int32_t>(n);
+  r.piece_base = c.take<int32_t>(n);
+  r.n_slots = c.take<int32_t>(1);
+  r.scan_tmp = c.take<int32_t>(scan_tmp_elems(n));
+}
+
+mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out, int32_t* U,
+                   cudaStream_t s) {
+  if (n <= 0) {
+    if (U) ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), s));
+    return ML_OK;
+  }
+  const unsigned g = unsigned((n + 255) / 256);
+  run_flags_kernel<<<g, 256, 0, s>>>(skey, n, r.flags);
+  ML_LAUNCH_CHECK("run_flags");
+  ML_TRY(scan_exclusive(r.flags, r.excl, n, r.scan_tmp, U, s));
+  run_fill_kernel<<<g, 256, 0, s>>>(skey, n, r.flags, r.excl, r.run_begin, rows_out);
+  ML_LAUNCH_CHECK("run_fill");
+  run_pieces_kernel<<<g, 256, 0, s>>>(n, r.flags, r.excl, r.run_begin, r.pieces);
+  ML_LAUNCH_CHECK("run_pieces");
+  ML_TRY(scan_exclusive(r.pieces, r.piece_base, n, r.scan_tmp, r.n_slots, s));
+  return ML_OK;
+}
+
+}  // namespace ml

@@ -1,0 +1,242 @@
+"""Torch-facing binding of libmemlayer: argument marshalling only.
+
+Every function checks dtype/device/contiguity, allocates outputs with torch
+(device memory is PyTorch's job here), and calls the C ABI on the current
+CUDA stream.  No arithmetic of the method happens in Python.  Names follow
+include/memlayer.h.
+"""
+import ctypes as C
+
+import torch
+
+from . import _lib
+from ._lib import PkmShape, BagShape, LayerShape, check, lib
+
+_DT = {torch.bfloat16: _lib.ML_BF16, torch.float32: _lib.ML_F32}
+_WS = {}
+
+
+def _dt(t):
+    if t.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+    return _DT[t.dtype]
+
+
+def _p(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("tensor must be on a CUDA device")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def workspace(nbytes, device=None, tag="default"):
+    """A cached uint8 device buffer of at least nbytes (grown on demand)."""
+    device = torch.device(device or torch.cuda.current_device())
+    key = (device.index, tag)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _WS.pop(key, None)
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+def release_workspaces():
+    _WS.clear()
+
+
+def launch_count():
+    """Kernels launched by libmemlayer since it was loaded."""
+    return int(lib().ml_launch_count())
+
+
+def timing_enable(on=True):
+    lib().ml_timing_enable(1 if on else 0)
+
+
+def timing_reset():
+    lib().ml_timing_reset()
+
+
+def timing_report():
+    """{kernel name: (launches, total_ms)} from the library's CUDA events."""
+    n = lib().ml_timing_report(None, 0)
+    buf = C.create_string_buffer(int(n))
+    lib().ml_timing_report(buf, n)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.rsplit(" ", 2)
+        out[name] = (int(cnt), float(ms))
+    return out
+
+
+def _size(fn, shape):
+    n = C.c_size_t(0)
+    check(fn(C.byref(shape), C.byref(n)))
+    return n.value
+
+
+# ------------------------------------------------------------------ synth
+def synth_fill(out, seed, tag, scale=1.0, cls=0, row0=0, modulus=0):
+    """Counter-based generator (synthetic/gen.py semantics) into `out`
+    ([rows, cols] view of a contiguous tensor; int32 for cls=3)."""
+    cols = out.shape[-1] if out.dim() else 1
+    rows = out.numel() // max(cols, 1)
+    dt = _lib.ML_BF16 if out.dtype == torch.bfloat16 else _lib.ML_F32
+    check(lib().ml_synth_fill(_p(out), rows, cols, row0, seed & (2**64 - 1), tag, scale, cls, dt,
+                              modulus, _stream()))
+    return out
+
+
+# ------------------------------------------------------------- product keys
+def pkm_shape(q, K1, k):
+    T, H, Dk = q.shape
+    return PkmShape(T, H, K1.shape[1], Dk, k, _dt(q))
+
+
+def pkm_topk(q, K1, K2, k, with_score=False):
+    """Product-key top-k + softmax (Eq. 1).  q [T,H,Dk], K1/K2 [H,S,Dk/2].
+    Returns idx [T,H,k] int32, w [T,H,k] fp32 (and pre-softmax scores)."""
+    sh = pkm_shape(q, K1, k)
+    T, H = q.shape[0], q.shape[1]
+    idx = torch.empty((T, H, k), dtype=torch.int32, device=q.device)
+    w = torch.empty((T, H, k), dtype=torch.float32, device=q.device)
+    score = torch.empty_like(w) if with_score else None
+    n = _size(lib().pkm_topk_workspace, sh)
+    ws = workspace(n, q.device)
+    check(lib().pkm_topk(C.byref(sh), _p(q), _p(K1), _p(K2), _p(idx), _p(w), _p(score),
+                         _p(ws), n, _stream()))
+    return (idx, w, score) if with_score else (idx, w)
+
+
+def pkm_topk_bwd(q, K1, K2, idx, w, dw, dK1=None, dK2=None):
+    """dq (overwrite) and dK1/dK2 (accumulate; zero-initialised if None)."""
+    k = idx.shape[-1]
+    sh = pkm_shape(q, K1, k)
+    dq = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    if dK1 is None:
+        dK1 = torch.zeros(K1.shape, dtype=torch.float32, device=q.device)
+    if dK2 is None:
+        dK2 = torch.zeros(K2.shape, dtype=torch.float32, device=q.device)
+    n = _size(lib().pkm_topk_bwd_workspace, sh)
+    ws = workspace(n, q.device)
+    check(lib().pkm_topk_bwd(C.byref(sh), _p(q), _p(K1), _p(K2), _p(idx), _p(w), _p(dw),
+                             _p(dq), _p(dK1), _p(dK2), _p(ws), n, _stream()))
+    return dq, dK1, dK2
+
+
+# ------------------------------------------------------------- EmbeddingBag
+def bag_shape(V, idx):
+    return BagShape(V.shape[0], V.shape[1], idx.shape[0], idx.shape[1], _dt(V))
+
+
+def embbag_fwd(V, idx, w, gate_pre=None, return_ungated=False):
+    """y[t] = sum_j w[t,j] V[idx[t,j]] (Eq. 1); with gate_pre: y * silu(gate_pre)."""
+    sh = bag_shape(V, idx)
+    y = torch.empty((idx.shape[0], V.shape[1]), dtype=V.dtype, device=V.device)
+    yu = torch.empty_like(y) if (gate_pre is not None and return_ungated) else None
+    check(lib().embbag_fwd(C.byref(sh), _p(V), _p(idx), _p(w), _p(gate_pre), _p(y), _p(yu),
+                           _stream()))
+    return (y, yu) if return_ungated else y
+
+
+def embbag_bwd(V, idx, w, dy, sync=True):
+    """"reverse_indices" backward.  Returns rows [U] int32 (ascending),
+    dV [U, dv] fp32, dw [T,B] fp32 (sync=True trims to U on the host);
+    with sync=False returns the capacity-sized buffers and the device U."""
+    sh = bag_shape(V, idx)
+    P = idx.numel()
+    rows = torch.empty(P, dtype=torch.int32, device=V.device)
+    dV = torch.empty((P, V.shape[1]), dtype=torch.float32, device=V.device)
+    U = torch.empty(1, dtype=torch.int32, device=V.device)
+    dw = torch.empty(idx.shape, dtype=torch.float32, device=V.device)
+    n = _size(lib().embbag_bwd_workspace, sh)
+    ws = workspace(n, V.device)
+    check(lib().embbag_bwd(C.byref(sh), _p(V), _p(idx), _p(w), _p(dy), _p(rows), _p(dV), _p(U),
+                           _p(dw), _p(ws), n, _stream()))
+    if not sync:
+        return rows, dV, U, dw
+    u = int(U.item())
+    return rows[:u], dV[:u], dw
+
+
+def embbag_grad_apply(V, idx, rows, dV, U, dV_dense):
+    sh = bag_shape(V, idx)
+    check(lib().embbag_grad_apply(C.byref(sh), _p(rows), _p(dV), _p(U), _p(dV_dense), _stream()))
+    return dV_dense
+
+
+# ------------------------------------------------------------ memory layer
+def layer_shape(x, q, K1, V, k, gated):
+    T, H, Dk = q.shape
+    D = x.shape[1] if (gated and x is not None) else V.shape[1]
+    return LayerShape(PkmShape(T, H, K1.shape[1], Dk, k, _dt(q)), V.shape[0], V.shape[1], D,
+                      1 if gated else 0)
+
+
+def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True):
+    """Eq. 1 + Eq. 2 forward.  Returns out [T,D] and the saved tensors."""
+    sh = layer_shape(x, q, K1, V, k, gated)
+    T, H = q.shape[0], q.shape[1]
+    dev = q.device
+    out = torch.empty((T, sh.D), dtype=V.dtype, device=dev)
+    idx = torch.empty((T, H, k), dtype=torch.int32, device=dev)
+    w = torch.empty((T, H, k), dtype=torch.float32, device=dev)
+    g = torch.empty((T, V.shape[1]), dtype=V.dtype, device=dev) if gated else None
+    y = torch.empty((T, V.shape[1]), dtype=V.dtype, device=dev) if gated else None
+    n = _size(lib().memory_layer_fwd_workspace, sh)
+    ws = workspace(n, dev)
+    check(lib().memory_layer_fwd(C.byref(sh), _p(x if gated else None), _p(q), _p(K1), _p(K2),
+                                 _p(V), _p(W1 if gated else None), _p(W2 if gated else None),
+                                 _p(out), _p(idx), _p(w), _p(g), _p(y), _p(ws), n, _stream()))
+    return out, dict(idx=idx, w=w, g=g, y=y, k=k, gated=gated)
+
+
+class LayerGrads(dict):
+    __getattr__ = dict.__getitem__
+
+
+def memory_layer_bwd(dout, x, q, K1, K2, V, W1, W2, saved, dK1=None, dK2=None, want_dw=False,
+                     bufs=None):
+    """Backward of memory_layer_fwd.  dK1/dK2 accumulate (zeros if None).
+    dV is compact: rows[:U], dV[:U] (capacity-sized buffers + device U)."""
+    k, gated = saved["k"], saved["gated"]
+    sh = layer_shape(x, q, K1, V, k, gated)
+    T, H = q.shape[0], q.shape[1]
+    dev = q.device
+    P = T * H * k
+    b = bufs if bufs is not None else {}
+    def buf(name, shape, dtype):
+        t = b.get(name)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            t = torch.empty(shape, dtype=dtype, device=dev)
+            b[name] = t
+        return t
+    dq = buf("dq", q.shape, torch.float32)
+    if dK1 is None:
+        dK1 = torch.zeros(K1.shape, dtype=torch.float32, device=dev)
+    if dK2 is None:
+        dK2 = torch.zeros(K2.shape, dtype=torch.float32, device=dev)
+    rows = buf("rows", (P,), torch.int32)
+    dV = buf("dV", (P, V.shape[1]), torch.float32)
+    U = buf("U", (1,), torch.int32)
+    dx = buf("dx", x.shape, V.dtype) if gated else None
+    dW1 = buf("dW1", W1.shape, torch.float32) if gated else None
+    dW2 = buf("dW2", W2.shape, torch.float32) if gated else None
+    dw = buf("dw", (T, H, k), torch.float32) if want_dw else None
+    n = _size(lib().memory_layer_bwd_workspace, sh)
+    ws = workspace(n, dev, tag="bwd")
+    check(lib().memory_layer_bwd(
+        C.byref(sh), _p(dout), _p(x if gated else None), _p(q), _p(K1), _p(K2), _p(V),
+        _p(W1 if gated else None), _p(W2 if gated else None), _p(saved["idx"]), _p(saved["w"]),
+        _p(saved["g"]), _p(saved["y"]), _p(dx), _p(dq), _p(dK1), _p(dK2), _p(rows), _p(dV),
+        _p(U), _p(dW1), _p(dW2), _p(dw), _p(ws), n, _stream()))
+    return LayerGrads(dq=dq, dK1=dK1, dK2=dK2, rows=rows, dV=dV, U=U, dx=dx, dW1=dW1, dW2=dW2,
+                      dw=dw)

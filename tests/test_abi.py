@@ -1,0 +1,95 @@
+"""The C-ABI library builds/loads and exports every symbol include/memlayer.h
+declares; host-side validation works without a GPU (no compute calls)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2412_09764_b200 import _lib
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "memlayer.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_header_parsed():
+    names = declared_functions()
+    for n in ("pkm_topk", "pkm_topk_bwd", "embbag_fwd", "embbag_bwd", "memory_layer_fwd",
+              "memory_layer_bwd", "ml_last_error", "ml_synth_fill"):
+        assert n in names
+
+
+def test_every_declared_symbol_exported():
+    lib = _lib.lib()
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    # and the binding declares a signature for each of them
+    assert set(declared_functions()) <= set(_lib.SIGNATURES)
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                       capture_output=True, text=True)
+    archs = set(re.findall(r"sm_(\d+a?)", r.stdout))
+    assert archs == {"100a"}, archs
+
+
+def _pkm(T=16, H=2, S=32, Dk=32, k=4, dt=_lib.ML_F32):
+    return _lib.PkmShape(T, H, S, Dk, k, dt)
+
+
+def _size(fn, shape):
+    n = C.c_size_t(0)
+    st = fn(C.byref(shape), C.byref(n))
+    return st, n.value
+
+
+def test_workspace_queries_on_host():
+    lib = _lib.lib()
+    st, n = _size(lib.pkm_topk_workspace, _pkm())
+    assert st == _lib.ML_OK and n >= 16 * 2 * 2 * 32 * 4
+    st, n = _size(lib.embbag_bwd_workspace, _lib.BagShape(1024, 64, 16, 8, _lib.ML_F32))
+    assert st == _lib.ML_OK and n > 0
+    sh = _lib.LayerShape(_pkm(), 1024, 64, 64, 1)
+    for fn in (lib.memory_layer_fwd_workspace, lib.memory_layer_bwd_workspace):
+        st, n = _size(fn, sh)
+        assert st == _lib.ML_OK and n > 0
+
+
+@pytest.mark.parametrize("shape,status", [
+    (_pkm(k=33, S=64), _lib.ML_ERR_UNSUPPORTED),   # k > 32 (warp select)
+    (_pkm(k=5, S=4), _lib.ML_ERR_CONFIG),          # k > S
+    (_pkm(Dk=31), _lib.ML_ERR_CONFIG),             # odd Dk
+    (_pkm(Dk=6), _lib.ML_ERR_CONFIG),              # half row of 12 B: not 16-B vectors
+    (_pkm(S=1 << 16), _lib.ML_ERR_CONFIG),         # N = S^2 >= 2^31
+])
+def test_pkm_validation(shape, status):
+    st, _ = _size(_lib.lib().pkm_topk_workspace, shape)
+    assert st == status
+    assert _lib.lib().ml_last_error()
+
+
+def test_bag_and_layer_validation():
+    lib = _lib.lib()
+    st, _ = _size(lib.embbag_bwd_workspace, _lib.BagShape(1024, 3, 16, 8, _lib.ML_F32))
+    assert st == _lib.ML_ERR_CONFIG          # 12-byte rows
+    st, _ = _size(lib.embbag_bwd_workspace, _lib.BagShape(1024, 64, 16, 0, _lib.ML_F32))
+    assert st == _lib.ML_ERR_CONFIG          # empty bag size
+    st, _ = _size(lib.memory_layer_fwd_workspace, _lib.LayerShape(_pkm(), 1000, 64, 64, 1))
+    assert st == _lib.ML_ERR_CONFIG          # N != S^2
+    st, _ = _size(lib.memory_layer_fwd_workspace, _lib.LayerShape(_pkm(), 1024, 64, 32, 0))
+    assert st == _lib.ML_ERR_CONFIG          # ungated needs D == dv
+
+
+def test_null_pointer_rejected_before_any_launch():
+    lib = _lib.lib()
+    sh = _lib.BagShape(1024, 64, 16, 8, _lib.ML_F32)
+    st = lib.embbag_fwd(C.byref(sh), None, None, None, None, None, None, None)
+    assert st == _lib.ML_ERR_ARG

@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element
+by element on the same seeded inputs, at sizes spanning several tiles with
+ragged tails.  Bit-exact for indices / row sets and for the exact input
+classes; otherwise within the north_star tolerances (tests/gpu_util.TOL)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import bag as obag, layer as olayer, pkm as opkm
+from synthetic import gen, streams
+from tests.gpu_util import TOL, assert_close, compare_topk, dev, host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_09764_b200 import ops  # noqa: F401  (fails loudly without the .so)
+    yield
+
+
+def ops():
+    from paper_2412_09764_b200 import ops as o
+    return o
+
+
+# ------------------------------------------------------------------ synth
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("cls", [gen.CLS_CONTINUOUS, gen.CLS_EXACT, gen.CLS_DYADIC])
+def test_synth_generator_matches_numpy(dtype, cls):
+    scale = gen.scale_for("K1", Dk=1024) if cls == gen.CLS_CONTINUOUS else 0.5
+    rows, cols, row0 = 37, 48, 1000
+    t = torch.empty((rows, cols), dtype=torch.bfloat16 if dtype == "bf16" else torch.float32,
+                    device="cuda")
+    ops().synth_fill(t, seed=11, tag=gen.TAGS["K1"], scale=scale, cls=cls, row0=row0)
+    ref = gen.rows(11, "K1", np.arange(row0, row0 + rows), cols, scale=scale, dtype=dtype, cls=cls)
+    assert np.array_equal(t.float().cpu().numpy(), ref)
+
+
+def test_synth_indices_match_numpy():
+    t = torch.empty((64, 128), dtype=torch.int32, device="cuda")
+    ops().synth_fill(t, seed=3, tag=gen.TAGS["idx"], cls=3, modulus=1 << 20)
+    assert np.array_equal(t.cpu().numpy(), streams.uniform_indices(3, 64, 128, 1 << 20))
+
+
+# ------------------------------------------------------------ bag forward
+BAG_CASES = [  # (dtype, N, dv, T, B)
+    ("f32", 1024, 64, 37, 4),
+    ("f32", 4096, 128, 129, 16),
+    ("bf16", 4096, 256, 67, 128),
+    ("bf16", 8192, 2048, 45, 128),
+    ("bf16", 2048, 4096, 19, 40),     # two column slices
+    ("bf16", 1024, 512, 300, 8),
+]
+
+
+@pytest.mark.parametrize("dtype,N,dv,T,B", BAG_CASES)
+def test_embbag_fwd_exact_class_bit_exact(dtype, N, dv, T, B):
+    V = gen.tensor(1, "V", (N, dv), dtype=dtype, cls=gen.CLS_EXACT)
+    idx = streams.uniform_indices(1, T, B, N)
+    w = streams.softmax_free_weights(1, T, B, cls=gen.CLS_DYADIC)
+    y = ops().embbag_fwd(dev(V, dtype), dev(idx), dev(w))
+    ref = obag.embbag_fwd(V, idx, w)
+    # dyadic * exact values: every partial sum is exact in fp32 while
+    # |partial| < 2^24/64; the bf16 output rounding is the only error
+    want = gen.round_bf16(ref.astype(np.float32)) if dtype == "bf16" else ref
+    assert np.array_equal(host(y), want)
+
+
+@pytest.mark.parametrize("dtype,N,dv,T,B", BAG_CASES)
+def test_embbag_fwd_continuous_and_gate(dtype, N, dv, T, B):
+    V = gen.tensor(2, "V", (N, dv), dtype=dtype)
+    idx = streams.zipf_indices(2, T, B, N, 1.1)
+    w = streams.softmax_free_weights(2, T, B)
+    g = gen.tensor(2, "x", (T, dv), dtype=dtype) * 3
+    g = gen.round_bf16(g) if dtype == "bf16" else g
+    z, y = ops().embbag_fwd(dev(V, dtype), dev(idx), dev(w), gate_pre=dev(g, dtype),
+                            return_ungated=True)
+    ref = obag.embbag_fwd(V, idx, w)
+    from oracle.gate import silu
+    assert_close(host(y), ref, TOL[dtype], "y")
+    assert_close(host(z), ref * silu(g.astype(np.float64)), TOL[dtype], "y*silu(g)")
+
+
+def test_embbag_fwd_edge_cases():
+    o = ops()
+    V = gen.tensor(3, "V", (64, 32), dtype="f32")
+    # k=1, w=1 -> row copy; w=0 -> 0
+    idx = np.array([[5], [63], [0]], np.int32)
+    y = o.embbag_fwd(dev(V), dev(idx), dev(np.ones((3, 1), np.float32)))
+    assert np.array_equal(host(y), V[[5, 63, 0]])
+    y0 = o.embbag_fwd(dev(V), dev(idx), dev(np.zeros((3, 1), np.float32)))
+    assert np.all(host(y0) == 0)
+    # empty batch is a no-op
+    ye = o.embbag_fwd(dev(V), dev(np.zeros((0, 4), np.int32)), dev(np.zeros((0, 4), np.float32)))
+    assert ye.shape == (0, 32)
+
+
+# ----------------------------------------------------------- bag backward
+@pytest.mark.parametrize("profile", ["u", "c0", "c50", "c100", "zipf"])
+@pytest.mark.parametrize("dtype,dv", [("f32", 64), ("bf16", 2048)])
+def test_embbag_bwd_profiles(profile, dtype, dv):
+    N, T, B = 1 << 14, 40, 32
+    if profile == "u":
+        idx = streams.uniform_indices(4, T, B, N)
+    elif profile == "zipf":
+        idx = streams.zipf_indices(4, T, B, N, 1.1)
+    else:
+        idx = streams.collision_indices(4, T, B, N, int(profile[1:]))
+    V = gen.tensor(4, "V", (N, dv), dtype=dtype, cls=gen.CLS_EXACT)
+    w = streams.softmax_free_weights(4, T, B, cls=gen.CLS_DYADIC)
+    dy = gen.tensor(4, "dout", (T, dv), dtype=dtype, cls=gen.CLS_EXACT)
+    rows, dV, dw = ops().embbag_bwd(dev(V, dtype), dev(idx), dev(w), dev(dy, dtype))
+    rr, rdV, rdw = obag.embbag_bwd(V, idx, w, dy)
+    assert np.array_equal(host(rows), rr)              # rows = distinct indices
+    assert np.array_equal(host(dV), rdV)               # exact class: bit-exact
+    assert np.array_equal(host(dw), rdw)
+
+
+@pytest.mark.parametrize("dtype,dv", [("f32", 64), ("bf16", 256), ("bf16", 4096)])
+def test_embbag_bwd_continuous_and_deterministic(dtype, dv):
+    N, T, B = 1 << 12, 97, 48
+    idx = streams.zipf_indices(5, T, B, N, 0.8)
+    V = gen.tensor(5, "V", (N, dv), dtype=dtype)
+    w = streams.softmax_free_weights(5, T, B)
+    dy = gen.tensor(5, "dout", (T, dv), dtype=dtype)
+    a = ops().embbag_bwd(dev(V, dtype), dev(idx), dev(w), dev(dy, dtype))
+    b = ops().embbag_bwd(dev(V, dtype), dev(idx), dev(w), dev(dy, dtype))
+    for x, y in zip(a, b):                              # determinism
+        assert torch.equal(x, y)
+    rr, rdV, rdw = obag.embbag_bwd(V, idx, w, dy)
+    assert np.array_equal(host(a[0]), rr)
+    assert_close(host(a[1]), rdV, TOL["f32"], "dV")     # fp32 accumulation of dtype inputs
+    assert_close(host(a[2]), rdw, TOL["f32"], "dw")
+
+
+def test_embbag_bwd_long_runs_and_grad_apply():
+    """A hot row hit by 3000 positions: split into 32-position pieces and
+    combined in piece order; dense apply equals A^T dy."""
+    o = ops()
+    N, dv, T, B = 256, 64, 300, 10
+    idx = np.full((T, B), 7, np.int32)
+    idx.flat[::7] = (np.arange(0, T * B, 7) * 13) % N
+    V = gen.tensor(6, "V", (N, dv), dtype="f32")
+    w = streams.softmax_free_weights(6, T, B)
+    dy = gen.tensor(6, "dout", (T, dv), dtype="f32")
+    rows, dV, U, dw = o.embbag_bwd(dev(V), dev(idx), dev(w), dev(dy), sync=False)
+    rr, rdV, rdw = obag.embbag_bwd(V, idx, w, dy)
+    u = int(U.item())
+    assert np.array_equal(host(rows[:u]), rr)
+    assert_close(host(dV[:u]), rdV, TOL["f32"], "dV")
+    dense = torch.zeros((N, dv), dtype=torch.float32, device="cuda")
+    o.embbag_grad_apply(dev(V), dev(idx), rows, dV, U, dense)
+    A = obag.dense_selection_matrix(idx, w, N)
+    assert_close(host(dense), A.T @ dy, TOL["f32"], "dense dV")
+
+
+# ------------------------------------------------------------ product keys
+def _pkm_inputs(seed, T, H, S, Dk, dtype, cls):
+    sc = gen.scale_for("K1", Dk=Dk) if cls == gen.CLS_CONTINUOUS else 1.0
+    q = gen.tensor(seed, "q", (T, H, Dk), dtype=dtype, cls=cls)
+    K1 = gen.tensor(seed, "K1", (H, S, Dk // 2), scale=sc, dtype=dtype, cls=cls)
+    K2 = gen.tensor(seed, "K2", (H, S, Dk // 2), scale=sc, dtype=dtype, cls=cls)
+    return q, K1, K2
+
+
+PKM_CASES = [  # (dtype, T, H, S, Dk, k)
+    ("f32", 256, 1, 32, 32, 4),        # C1 (tiny PKM)
+    ("f32", 77, 2, 32, 64, 4),
+    ("bf16", 130, 4, 64, 128, 8),
+    ("bf16", 70, 4, 128, 256, 32),
+    ("bf16", 33, 2, 1024, 1024, 32),   # C2 per-head shapes, few tokens
+]
+
+
+@pytest.mark.parametrize("dtype,T,H,S,Dk,k", PKM_CASES)
+def test_pkm_topk_exact_class(dtype, T, H, S, Dk, k):
+    """Exact class: scores exact in fp32, so indices AND scores bit-exact with
+    the plain definition (brute force over all N = S^2 keys), including the
+    many exact ties (tie-break)."""
+    q, K1, K2 = _pkm_inputs(8, T, H, S, Dk, dtype, gen.CLS_EXACT)
+    idx, w, score = ops().pkm_topk(dev(q, dtype), dev(K1, dtype), dev(K2, dtype), k, with_score=True)
+    method = "full" if S * S <= 1 << 14 else "two_stage"
+    ridx, rscore, rw = opkm.pkm_lookup(q.astype(np.float64), K1.astype(np.float64),
+                                       K2.astype(np.float64), k, method=method)
+    assert np.array_equal(host(idx), ridx)
+    assert np.array_equal(host(score), rscore)
+    assert_close(host(w), rw, 1e-6, "w")
+    np.testing.assert_allclose(host(w).sum(-1), 1.0, atol=1e-6)
+
+
+@pytest.mark.parametrize("dtype,T,H,S,Dk,k", PKM_CASES)
+def test_pkm_topk_continuous(dtype, T, H, S, Dk, k):
+    q, K1, K2 = _pkm_inputs(9, T, H, S, Dk, dtype, gen.CLS_CONTINUOUS)
+    idx, w, score = ops().pkm_topk(dev(q, dtype), dev(K1, dtype), dev(K2, dtype), k, with_score=True)
+    q64, K164, K264 = (a.astype(np.float64) for a in (q, K1, K2))
+    ridx, rscore, rw = opkm.pkm_lookup(q64, K164, K264, k)
+    near = compare_topk(host(idx), ridx, q64, K164, K264)
+    ok = np.ones(ridx.shape[:2], bool)
+    for t, h, _ in near:
+        ok[t, h] = False
+    assert_close(host(score)[ok], rscore[ok], 1e-5, "score")
+    assert_close(host(w)[ok], rw[ok], TOL["f32"], "w")
+    np.testing.assert_allclose(host(w).sum(-1), 1.0, atol=1e-5)
+
+
+def test_pkm_topk_degenerate_queries():
+    """q = 0 -> flat indices 0..k-1, w = 1/k; k = 1 -> w = 1."""
+    T, H, S, Dk, k = 5, 2, 32, 32, 6
+    _, K1, K2 = _pkm_inputs(10, T, H, S, Dk, "f32", gen.CLS_CONTINUOUS)
+    idx, w = ops().pkm_topk(dev(np.zeros((T, H, Dk), np.float32)), dev(K1), dev(K2), k)
+    assert np.array_equal(host(idx), np.broadcast_to(np.arange(k), (T, H, k)))
+    np.testing.assert_allclose(host(w), 1.0 / k, rtol=1e-6)
+    q, _, _ = _pkm_inputs(10, T, H, S, Dk, "f32", gen.CLS_CONTINUOUS)
+    idx1, w1 = ops().pkm_topk(dev(q), dev(K1), dev(K2), 1)
+    assert np.all(host(w1) == 1.0)
+
+
+@pytest.mark.parametrize("dtype,T,H,S,Dk,k", PKM_CASES[:4])
+def test_pkm_topk_bwd(dtype, T, H, S, Dk, k):
+    q, K1, K2 = _pkm_inputs(11, T, H, S, Dk, dtype, gen.CLS_CONTINUOUS)
+    q64, K164, K264 = (a.astype(np.float64) for a in (q, K1, K2))
+    ridx, rscore, rw = opkm.pkm_lookup(q64, K164, K264, k)
+    dw = gen.tensor(11, "dout", (T, H, k), dtype="f32")
+    # the backward takes the selection as an input: feed the oracle's
+    rdq, rdK1, rdK2, _ = opkm.pkm_bwd(q64, K164, K264, ridx, rw, dw)
+    dq, dK1, dK2 = ops().pkm_topk_bwd(dev(q, dtype), dev(K1, dtype), dev(K2, dtype),
+                                      dev(ridx.astype(np.int32)), dev(rw.astype(np.float32)), dev(dw))
+    tol = TOL["f32"]
+    assert_close(host(dq), rdq, tol, "dq")
+    assert_close(host(dK1), rdK1, tol, "dK1")
+    assert_close(host(dK2), rdK2, tol, "dK2")
+
+
+# ------------------------------------------------------------ memory layer
+LAYER_CASES = [  # (dtype, T, H, S, Dk, k, dv, D, gated)
+    ("f32", 256, 1, 32, 32, 4, 64, 64, True),      # C1
+    ("f32", 256, 1, 32, 64, 4, 64, 64, False),     # C1, Dk = 64, vanilla Memory
+    ("f32", 99, 2, 32, 32, 4, 128, 64, True),
+    ("bf16", 150, 4, 64, 128, 8, 256, 256, True),
+    ("bf16", 64, 4, 128, 512, 32, 1024, 512, True),
+]
+
+
+@pytest.mark.parametrize("dtype,T,H,S,Dk,k,dv,D,gated", LAYER_CASES)
+def test_memory_layer_fwd_bwd(dtype, T, H, S, Dk, k, dv, D, gated):
+    seed = 12
+    f = lambda tag, shape, sc=1.0: gen.tensor(seed, tag, shape, scale=sc, dtype=dtype)
+    h = dict(x=f("x", (T, D)), q=f("q", (T, H, Dk)),
+             K1=f("K1", (H, S, Dk // 2), gen.scale_for("K1", Dk=Dk)),
+             K2=f("K2", (H, S, Dk // 2), gen.scale_for("K2", Dk=Dk)),
+             V=f("V", (S * S, dv)), W1=f("W1", (D, dv), gen.scale_for("W1", D=D)),
+             W2=f("W2", (dv, D), gen.scale_for("W2", dv=dv)),
+             dout=f("dout", (T, D if gated else dv)))
+    t = {n: dev(a, dtype) for n, a in h.items()}
+    o = ops()
+    out, saved = o.memory_layer_fwd(t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"],
+                                    k, gated=gated)
+    g = o.memory_layer_bwd(t["dout"], t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"],
+                           saved, want_dw=True)
+    h64 = {n: a.astype(np.float64) for n, a in h.items()}
+    rout, rs = olayer.memory_layer_fwd(h64["x"], h64["q"], h64["K1"], h64["K2"], h64["V"],
+                                       h64["W1"], h64["W2"], k, gated=gated)
+    near = compare_topk(host(saved["idx"]), rs["idx"], h64["q"], h64["K1"], h64["K2"])
+    assert not near, f"near ties in a small case: {near}"
+    r = olayer.memory_layer_bwd(h64["dout"], h64["x"], h64["q"], h64["K1"], h64["K2"], h64["V"],
+                                h64["W1"], h64["W2"], rs, gated=gated)
+    tol = TOL[dtype]
+    assert_close(host(out), rout, tol, "out")
+    U = int(g["U"].item())
+    assert np.array_equal(host(g["rows"][:U]), r["rows"])
+    assert_close(host(g["dV"][:U]), r["dV"], tol, "dV")
+    assert_close(host(g["dw"]), r["dw"], tol, "dw")
+    assert_close(host(g["dq"]), r["dq"], tol, "dq")
+    assert_close(host(g["dK1"]), r["dK1"], tol, "dK1")
+    assert_close(host(g["dK2"]), r["dK2"], tol, "dK2")
+    if gated:
+        assert_close(host(g["dx"]), r["dx"], tol, "dx")
+        assert_close(host(g["dW1"]), r["dW1"], tol, "dW1")
+        assert_close(host(g["dW2"]), r["dW2"], tol, "dW2")
