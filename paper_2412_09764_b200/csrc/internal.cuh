@@ -81,6 +81,10 @@ mlStatus launch_sum_slices(const float* part, int nslices, int64_t P, float* dw,
 // ------------------------------------------------------ product keys
 mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1,
                            const void* K2, float* scores, cudaStream_t s);
+// tcgen05 path (bf16, Dk/2 % 64 == 0, S = 32..256 power of two or multiple of 256)
+bool pkm_scores_tc_eligible(const mlPkmShape& sh);
+mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
+                              float* scores, cudaStream_t s);
 mlStatus launch_half_topk(const mlPkmShape& sh, const float* scores, int32_t* hI,
                           float* hs, cudaStream_t s);
 mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const float* hs,

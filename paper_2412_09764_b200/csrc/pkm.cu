@@ -263,7 +263,8 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
 mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
                            float* scores, cudaStream_t s) {
   if (sh.T <= 0) return ML_OK;
-  dim3 grid(unsigned((sh.T + 63) / 64), unsigned((sh.S + 63) / 64), unsigned(sh.H * 2));
+  if (pkm_scores_tc_eligible(sh)) return launch_pkm_scores_tc(sh, q, K1, K2, scores, s);
+  dim3 grid{unsigned((sh.T + 63) / 64), unsigned((sh.S + 63) / 64), unsigned(sh.H * 2)};
   if (sh.dtype == ML_BF16)
     pkm_scores_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(K1),
@@ -273,7 +274,7 @@ mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1, 
                                                   static_cast<const float*>(K1),
                                                   static_cast<const float*>(K2), scores, sh.T,
                                                   sh.H, sh.S, sh.Dk);
-  ML_LAUNCH_CHECK("pkm_scores");
+  ML_LAUNCH_CHECK("pkm_scores_simt");
   return ML_OK;
 }
 

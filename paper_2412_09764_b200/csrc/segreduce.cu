@@ -11,8 +11,10 @@
 // Whole runs are written directly (rows are unique: no atomics); pieces of
 // long runs go to a partial buffer and the last piece to arrive (counter)
 // sums all pieces of its run in piece order -> bitwise deterministic.
-// Columns: lane l owns 16-byte vectors l, l+32, ... (CPL of them) of a
+// Columns: lane l owns 16-byte vectors l, l+32 (CPL <= 2 of them) of a
 // 32*CPL-vector column slice (blockIdx.y); loads are coalesced 512 B rows.
+// Per chunk the warp loads all position metadata in one round (lane <->
+// position), so each piece costs one memory round trip (V row + dy rows).
 #include "internal.cuh"
 
 namespace ml {
@@ -52,10 +54,37 @@ __device__ __forceinline__ void write_row(const SegParams& p, int64_t row, const
   }
 }
 
+// Butterfly "transpose" reduction of N per-lane values across the warp:
+// after it, lane l holds in a[0] the warp total of value index
+// (l >> (5 - log2 N)) & (N - 1).  N - 1 + 5 - log2 N shuffles instead of 5 N.
+template <int N, int O>
+struct TransposeReduce {
+  __device__ __forceinline__ static void run(float* a, int lane) {
+    const bool up = (lane & O) != 0;
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      const float lo = a[i], hi = a[i + N / 2];
+      const float keep = up ? hi : lo;
+      const float send = up ? lo : hi;
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    TransposeReduce<N / 2, O / 2>::run(a, lane);
+  }
+};
+template <int O>
+struct TransposeReduce<1, O> {
+  __device__ __forceinline__ static void run(float* a, int) {
+#pragma unroll
+    for (int o = O; o > 0; o >>= 1) a[0] += __shfl_xor_sync(0xffffffffu, a[0], o);
+  }
+};
+template <int N> struct Log2 { static constexpr int v = 1 + Log2<N / 2>::v; };
+template <> struct Log2<1> { static constexpr int v = 0; };
+
 template <typename T, int CPL, bool DW>
-__global__ void __launch_bounds__(256) seg_kernel(SegParams p) {
+__global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
   constexpr int VEC = Vec<T>::N;
-  constexpr int NB = CPL >= 4 ? 4 : 8;     // positions per batch of loads
+  constexpr int NB = 8 / CPL;             // positions per batch of loads
   constexpr int L = kPieceLen;
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -65,37 +94,56 @@ __global__ void __launch_bounds__(256) seg_kernel(SegParams p) {
   if (c0 >= p.P) return;
   const int64_t c1 = min(c0 + 32, p.P);
 
+  // ---- per-lane metadata of position c0 + lane (one round of loads)
+  const int64_t iA = c0 + lane;
+  int posA = 0, keyA = 0, rA = 0, rbA = 0, reA = 0;
+  float wA = 0.f;
+  bool stA = false;
+  if (iA < c1) {
+    posA = p.spos[iA];
+    keyA = p.skey[iA];
+    rA = p.excl[iA] - 1 + p.flags[iA];
+    wA = p.w[posA];
+    rbA = p.run_begin[rA];
+    reA = p.run_begin[rA + 1];
+    stA = ((int32_t(iA) - rbA) % L) == 0;
+  }
+  unsigned starts = __ballot_sync(FULL, stA);
+  if (!starts) return;  // the whole chunk continues a piece begun earlier
+  // the last piece may run up to 31 positions past the chunk: prefetch those
+  const int last = 31 - __clz(starts);
+  const int32_t e_last = min(__shfl_sync(FULL, reA, last), int32_t(c0) + last + L);
+  int posB = 0;
+  float wB = 0.f;
+  if (e_last > c1) {
+    const int64_t iB = c1 + lane;
+    if (iB < e_last) {
+      posB = p.spos[iB];
+      wB = p.w[posB];
+    }
+  }
+
   bool act[CPL];
-  int64_t colb[CPL];  // byte offset of this lane's vectors inside a row slice
+  int64_t colb[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int u = slice * 32 * CPL + c * 32 + lane;
     act[c] = u < p.vec_units;
     colb[c] = int64_t(u) * 16;
   }
-  const int64_t slice_w = int64_t(32) * CPL * VEC;  // floats per slice row
+  const int64_t slice_w = int64_t(32) * CPL * VEC;
+  const int64_t src_off = int64_t(p.src_col0) * int64_t(sizeof(T));
 
-  // which positions of this chunk start a piece?
-  const int64_t i = c0 + lane;
-  bool st = false;
-  int r = 0, rb = 0;
-  if (i < c1) {
-    const int f = p.flags[i];
-    r = p.excl[i] - 1 + f;
-    rb = p.run_begin[r];
-    st = ((int32_t(i) - rb) % L) == 0;
-  }
-  unsigned m = __ballot_sync(FULL, st);
-  while (m) {
-    const int b = __ffs(m) - 1;
-    m &= m - 1;
+  while (starts) {
+    const int b = __ffs(starts) - 1;
+    starts &= starts - 1;
     const int32_t s = int32_t(c0) + b;
-    const int32_t rr = __shfl_sync(FULL, r, b);
-    const int32_t rbb = __shfl_sync(FULL, rb, b);
-    const int32_t re = p.run_begin[rr + 1];
+    const int32_t rr = __shfl_sync(FULL, rA, b);
+    const int32_t rbb = __shfl_sync(FULL, rbA, b);
+    const int32_t re = __shfl_sync(FULL, reA, b);
+    const int32_t key = __shfl_sync(FULL, keyA, b);
     const int32_t e = min(re, s + L);
     const bool lng = (re - rbb) > L;
-    const int32_t key = p.skey[s];
 
     uint4 vv[CPL];
     if constexpr (DW) {
@@ -110,19 +158,21 @@ __global__ void __launch_bounds__(256) seg_kernel(SegParams p) {
 
     for (int32_t pb = s; pb < e; pb += NB) {
       const int n = min(NB, e - pb);
-      int pj = 0;
-      float wj = 0.f;
-      if (lane < n) {
-        pj = p.spos[pb + lane];
-        wj = p.w[pj];
-      }
+      int posb[NB];
+      float wb[NB];
       uint4 d[NB][CPL];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const int pos = __shfl_sync(FULL, pj, j);
+        const int off = pb + j - int32_t(c0);  // 0..62
+        const int src = off & 31;
+        const int pa = __shfl_sync(FULL, posA, src);
+        const float wa = __shfl_sync(FULL, wA, src);
+        const int pbv = __shfl_sync(FULL, posB, src);
+        const float wbv = __shfl_sync(FULL, wB, src);
+        posb[j] = off < 32 ? pa : pbv;
+        wb[j] = off < 32 ? wa : wbv;
         if (j < n) {
-          const char* row = p.src + int64_t(pos / p.B) * p.lds_bytes +
-                            int64_t(p.src_col0) * int64_t(sizeof(T));
+          const char* row = p.src + int64_t(posb[j] / p.B) * p.lds_bytes + src_off;
 #pragma unroll
           for (int c = 0; c < CPL; ++c)
             if (act[c]) d[j][c] = ldg_v4(row + colb[c]);
@@ -131,7 +181,6 @@ __global__ void __launch_bounds__(256) seg_kernel(SegParams p) {
       float part[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const float wv = __shfl_sync(FULL, wj, j);
         part[j] = 0.f;
         if (j < n) {
 #pragma unroll
@@ -146,18 +195,20 @@ __global__ void __launch_bounds__(256) seg_kernel(SegParams p) {
               for (int v = 0; v < VEC; ++v) part[j] = fmaf(f[v], g[v], part[j]);
             }
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[c * VEC + v] = fmaf(wv, f[v], acc[c * VEC + v]);
+            for (int v = 0; v < VEC; ++v) acc[c * VEC + v] = fmaf(wb[j], f[v], acc[c * VEC + v]);
           }
         }
       }
       if constexpr (DW) {
+        TransposeReduce<NB, 16>::run(part, lane);
+        constexpr int SH = 5 - Log2<NB>::v;
+        const int jj = (lane >> SH) & (NB - 1);
+        int pos_mine = posb[0];
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          float t = part[j];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
-          if (lane == j && j < n) p.dw_part[int64_t(slice) * p.P + pj] = t;
-        }
+        for (int j = 1; j < NB; ++j)
+          if (jj == j) pos_mine = posb[j];
+        if ((lane & ((1 << SH) - 1)) == 0 && jj < n)
+          p.dw_part[int64_t(slice) * p.P + pos_mine] = part[0];
       }
     }
 
@@ -215,16 +266,16 @@ __global__ void sum_slices_kernel(const float* part, int ns, int64_t P, float* d
   dw[i] = t;
 }
 
-int cpl_for(int64_t vu) { return vu <= 32 ? 1 : (vu <= 64 ? 2 : 4); }
+int cpl_for(int64_t vu) { return vu <= 32 ? 1 : 2; }
 
 template <typename T>
 mlStatus dispatch_seg(int cpl, bool dw, dim3 grid, const SegParams& p, cudaStream_t s,
                       const char* name) {
 #define ML_SEG(C, D) seg_kernel<T, C, D><<<grid, 256, 0, s>>>(p)
   if (dw) {
-    if (cpl == 1) ML_SEG(1, true); else if (cpl == 2) ML_SEG(2, true); else ML_SEG(4, true);
+    if (cpl == 1) ML_SEG(1, true); else ML_SEG(2, true);
   } else {
-    if (cpl == 1) ML_SEG(1, false); else if (cpl == 2) ML_SEG(2, false); else ML_SEG(4, false);
+    if (cpl == 1) ML_SEG(1, false); else ML_SEG(2, false);
   }
 #undef ML_SEG
   ML_LAUNCH_CHECK(name);
@@ -235,7 +286,7 @@ mlStatus dispatch_seg(int cpl, bool dw, dim3 grid, const SegParams& p, cudaStrea
 
 int seg_slices(int32_t dv, mlDtype dt) {
   const int64_t vu = int64_t(dv) * int64_t(dtype_size(dt)) / 16;
-  return vu <= 128 ? 1 : int(vu / 128);
+  return vu <= 64 ? 1 : int(vu / 64);
 }
 
 static int64_t nslots_cap(int64_t P) { return 2 * (P / kPieceLen) + 2; }
@@ -255,7 +306,7 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   const int64_t vu = int64_t(a.dv) * int64_t(dtype_size(a.dtype)) / 16;
   const int cpl = cpl_for(vu);
   const int ns = seg_slices(a.dv, a.dtype);
-  if (vu > 128 && vu % 128) return fail(ML_ERR_CONFIG, "segreduce: row vectors must divide into slices of 128");
+  if (vu > 64 && vu % 64) return fail(ML_ERR_CONFIG, "segreduce: row vectors must divide into slices of 64");
   SegParams p;
   p.skey = a.skey; p.spos = a.spos; p.P = a.P;
   p.flags = a.runs->flags; p.excl = a.runs->excl; p.run_begin = a.runs->run_begin;
