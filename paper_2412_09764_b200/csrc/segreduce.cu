@@ -5,14 +5,23 @@
 // The same kernel (without dw, dense-accumulating) produces the half-key
 // gradients dK[h, a] = sum ds * q_half (pkm backward).
 //
-// Work split (load balance under skew, determinism): one warp per chunk of
-// 32 sorted positions; it reduces every "piece" that STARTS in its chunk.  A
-// piece is a whole run, or a 32-position piece of a run longer than 32.
-// Whole runs are written directly (rows are unique: no atomics); pieces of
-// long runs go to a partial buffer and the last piece to arrive (counter)
+// Work split (load balance under skew, determinism): one CTA ("team") per
+// chunk of 64 sorted positions; it reduces every "piece" that STARTS in its
+// chunk.  A piece is a whole run, or a 32-position piece of a run longer than
+// 32.  Whole runs are written directly (rows are unique: no atomics); pieces
+// of long runs go to a partial buffer and the last piece to arrive (counter)
 // sums all pieces of its run in piece order -> bitwise deterministic.
-// Columns: lane l owns 16-byte vectors l, l+32 (CPL <= 2 of them) of a
-// 32*CPL-vector column slice (blockIdx.y); loads are coalesced 512 B rows.
+// The team's threads each own one 16-byte vector of the row (blockDim =
+// row vectors, up to 256 = 2048 bf16 columns; wider rows use column slices,
+// blockIdx.y).  Per-position metadata is decoded once into shared memory and
+// read as broadcasts; the position range is walked in full batches of NB
+// positions regardless of piece boundaries: all source-row and value-row
+// loads of a batch are issued at once (value rows repeat inside a piece and
+// hit L1), then the batch is accumulated, flushing each piece at its end.
+// The fused dw dot products are reduced per batch: warp butterfly, then one
+// shared-memory exchange and one barrier per batch.
+// Columns: lane l owns 16-byte vector l of a 32-vector (512 B) column slice
+// (blockIdx.y); every load is a coalesced 512 B row segment.
 // Per chunk the warp loads all position metadata in one round (lane <->
 // position), so each piece costs one memory round trip (V row + dy rows).
 #include "internal.cuh"
@@ -32,27 +41,8 @@ struct SegParams {
   int32_t vec_units;  // 16-byte vectors per row (whole dv)
 };
 
-template <typename T, int CPL>
-__device__ __forceinline__ void write_row(const SegParams& p, int64_t row, const float* acc,
-                                          int slice, int lane, const bool* act) {
-  constexpr int VEC = Vec<T>::N;
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    if (!act[c]) continue;
-    const int64_t col = (int64_t(slice) * 32 * CPL + c * 32 + lane) * VEC;
-    float* o = p.out + row * p.ldo + col;
-#pragma unroll
-    for (int v = 0; v < VEC; v += 4) {
-      float4 a = make_float4(acc[c * VEC + v], acc[c * VEC + v + 1], acc[c * VEC + v + 2],
-                             acc[c * VEC + v + 3]);
-      if (p.dense) {
-        float4 b = *reinterpret_cast<float4*>(o + v);
-        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-      }
-      *reinterpret_cast<float4*>(o + v) = a;
-    }
-  }
-}
+constexpr int kChunk = 64;                   // positions whose pieces a team owns
+constexpr int kMeta = kChunk + kPieceLen;    // positions a team may touch
 
 // Butterfly "transpose" reduction of N per-lane values across the warp:
 // after it, lane l holds in a[0] the warp total of value index
@@ -78,182 +68,189 @@ struct TransposeReduce<1, O> {
     for (int o = O; o > 0; o >>= 1) a[0] += __shfl_xor_sync(0xffffffffu, a[0], o);
   }
 };
-template <int N> struct Log2 { static constexpr int v = 1 + Log2<N / 2>::v; };
-template <> struct Log2<1> { static constexpr int v = 0; };
 
-template <typename T, int CPL, bool DW>
+template <int VEC>
+__device__ __forceinline__ void store_vec(float* o, const float* acc, bool dense) {
+#pragma unroll
+  for (int v = 0; v < VEC; v += 4) {
+    float4 a = make_float4(acc[v], acc[v + 1], acc[v + 2], acc[v + 3]);
+    if (dense) {
+      const float4 b = *reinterpret_cast<const float4*>(o + v);
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      *reinterpret_cast<float4*>(o + v) = a;
+    } else {
+      __stcs(reinterpret_cast<float4*>(o + v), a);  // streaming: keep dy in L2
+    }
+  }
+}
+
+// Piece of a run longer than kPieceLen: park the partial, the last piece to
+// arrive combines all pieces of the run in piece order (deterministic).
+template <int VEC>
+struct FVec { float v[VEC]; };
+
+template <int VEC>
+__device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VEC> accv, bool act,
+                                               int64_t col, int slice, int32_t row, int32_t rbb,
+                                               int32_t re, int32_t ps, int* s_flag) {
+  const float* acc = accv.v;
+  constexpr int L = kPieceLen;
+  const int64_t slice_w = int64_t(blockDim.x) * VEC;
+  const int32_t base = p.piece_base[rbb];
+  const int32_t slot = base + (ps - rbb) / L;
+  const int32_t npieces = (re - rbb + L - 1) / L;
+  float* pp = p.partial + (int64_t(slice) * p.nslots_cap + slot) * slice_w + threadIdx.x * VEC;
+  if (act) {
+#pragma unroll
+    for (int v = 0; v < VEC; v += 4)
+      __stcg(reinterpret_cast<float4*>(pp + v), make_float4(acc[v], acc[v + 1], acc[v + 2], acc[v + 3]));
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    *s_flag = atomicAdd(p.counters + int64_t(slice) * p.nslots_cap + base, 1) == npieces - 1;
+  __syncthreads();
+  if (*s_flag) {
+    __threadfence();
+    float tot[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) tot[v] = 0.f;
+    for (int32_t q = 0; q < npieces; ++q) {
+      const float* srcp = p.partial + (int64_t(slice) * p.nslots_cap + base + q) * slice_w + threadIdx.x * VEC;
+      if (act) {
+#pragma unroll
+        for (int v = 0; v < VEC; v += 4) {
+          const float4 a = __ldcg(reinterpret_cast<const float4*>(srcp + v));
+          tot[v] += a.x; tot[v + 1] += a.y; tot[v + 2] += a.z; tot[v + 3] += a.w;
+        }
+      }
+    }
+    if (act) store_vec<VEC>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
+  }
+  __syncthreads();
+}
+
+// blockDim.x = row vectors of one column slice (32..256); one CTA per chunk.
+template <typename T, bool DW>
 __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
   constexpr int VEC = Vec<T>::N;
-  constexpr int NB = 8 / CPL;             // positions per batch of loads
+  constexpr int NB = 8;                  // positions per batch
   constexpr int L = kPieceLen;
-  constexpr unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int64_t chunk = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  __shared__ int s_t[kMeta], s_key[kMeta], s_fl[kMeta], s_pos[kMeta];
+  __shared__ float s_w[kMeta];
+  __shared__ int s_rr[kMeta], s_rb[kMeta], s_re[kMeta];
+  __shared__ int s_range[2];
+  __shared__ int s_flag;
+  __shared__ float s_red[2][8][NB];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int slice = blockIdx.y;
-  const int64_t c0 = chunk * 32;
-  if (c0 >= p.P) return;
-  const int64_t c1 = min(c0 + 32, p.P);
-
-  // ---- per-lane metadata of position c0 + lane (one round of loads)
-  const int64_t iA = c0 + lane;
-  int posA = 0, keyA = 0, rA = 0, rbA = 0, reA = 0;
-  float wA = 0.f;
-  bool stA = false;
-  if (iA < c1) {
-    posA = p.spos[iA];
-    keyA = p.skey[iA];
-    rA = p.excl[iA] - 1 + p.flags[iA];
-    wA = p.w[posA];
-    rbA = p.run_begin[rA];
-    reA = p.run_begin[rA + 1];
-    stA = ((int32_t(iA) - rbA) % L) == 0;
+  const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+  if (tid == 0) {
+    s_range[0] = 0x7fffffff;
+    s_range[1] = -1;
   }
-  unsigned starts = __ballot_sync(FULL, stA);
-  if (!starts) return;  // the whole chunk continues a piece begun earlier
-  // the last piece may run up to 31 positions past the chunk: prefetch those
-  const int last = 31 - __clz(starts);
-  const int32_t e_last = min(__shfl_sync(FULL, reA, last), int32_t(c0) + last + L);
-  int posB = 0;
-  float wB = 0.f;
-  if (e_last > c1) {
-    const int64_t iB = c1 + lane;
-    if (iB < e_last) {
-      posB = p.spos[iB];
-      wB = p.w[posB];
-    }
-  }
-
-  bool act[CPL];
-  int64_t colb[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    const int u = slice * 32 * CPL + c * 32 + lane;
-    act[c] = u < p.vec_units;
-    colb[c] = int64_t(u) * 16;
-  }
-  const int64_t slice_w = int64_t(32) * CPL * VEC;
-  const int64_t src_off = int64_t(p.src_col0) * int64_t(sizeof(T));
-
-  while (starts) {
-    const int b = __ffs(starts) - 1;
-    starts &= starts - 1;
-    const int32_t s = int32_t(c0) + b;
-    const int32_t rr = __shfl_sync(FULL, rA, b);
-    const int32_t rbb = __shfl_sync(FULL, rbA, b);
-    const int32_t re = __shfl_sync(FULL, reA, b);
-    const int32_t key = __shfl_sync(FULL, keyA, b);
-    const int32_t e = min(re, s + L);
-    const bool lng = (re - rbb) > L;
-
-    uint4 vv[CPL];
-    if constexpr (DW) {
-#pragma unroll
-      for (int c = 0; c < CPL; ++c)
-        if (act[c]) vv[c] = ldg_nc_v4(p.V + int64_t(key) * p.ldv_bytes +
-                                      int64_t(p.v_col0) * int64_t(sizeof(T)) + colb[c]);
-    }
-    float acc[CPL * VEC];
-#pragma unroll
-    for (int v = 0; v < CPL * VEC; ++v) acc[v] = 0.f;
-
-    for (int32_t pb = s; pb < e; pb += NB) {
-      const int n = min(NB, e - pb);
-      int posb[NB];
-      float wb[NB];
-      uint4 d[NB][CPL];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const int off = pb + j - int32_t(c0);  // 0..62
-        const int src = off & 31;
-        const int pa = __shfl_sync(FULL, posA, src);
-        const float wa = __shfl_sync(FULL, wA, src);
-        const int pbv = __shfl_sync(FULL, posB, src);
-        const float wbv = __shfl_sync(FULL, wB, src);
-        posb[j] = off < 32 ? pa : pbv;
-        wb[j] = off < 32 ? wa : wbv;
-        if (j < n) {
-          const char* row = p.src + int64_t(posb[j] / p.B) * p.lds_bytes + src_off;
-#pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            if (act[c]) d[j][c] = ldg_v4(row + colb[c]);
-        }
+  __syncthreads();
+  // ---- decode the metadata of positions [c0, c0 + kMeta) once
+  for (int k = tid; k < kMeta; k += blockDim.x) {
+    const int64_t i = c0 + k;
+    int fl = 0, t = 0, key = 0, pos = 0, r = 0, rb = 0, re = 0;
+    float w = 0.f;
+    if (i < p.P) {
+      pos = p.spos[i];
+      key = p.skey[i];
+      r = p.excl[i] - 1 + p.flags[i];
+      w = p.w[pos];
+      t = pos / p.B;
+      rb = p.run_begin[r];
+      re = p.run_begin[r + 1];
+      const int32_t ps = rb + ((int32_t(i) - rb) / L) * L;
+      const int32_t pe = min(re, ps + L);
+      fl = (int32_t(i) == ps ? 1 : 0) | (int32_t(i) == pe - 1 ? 2 : 0);
+      if ((fl & 1) && k < kChunk) {   // a piece starting in this chunk
+        atomicMin(&s_range[0], k);
+        atomicMax(&s_range[1], int(pe - c0));
       }
-      float part[NB];
+    }
+    s_t[k] = t; s_key[k] = key; s_fl[k] = fl; s_pos[k] = pos; s_w[k] = w;
+    s_rr[k] = r; s_rb[k] = rb; s_re[k] = re;
+  }
+  __syncthreads();
+  const int k_first = s_range[0], k_end = s_range[1];
+  if (k_end < 0) return;  // the whole chunk continues a piece begun earlier
+
+  const int u = slice * blockDim.x + tid;
+  const bool act = u < p.vec_units;
+  const int64_t col = int64_t(u) * VEC;
+  const char* srcb = p.src + (int64_t(p.src_col0) + col) * int64_t(sizeof(T));
+  const char* vb = DW ? p.V + (int64_t(p.v_col0) + col) * int64_t(sizeof(T)) : nullptr;
+  const uint32_t lds = uint32_t(p.lds_bytes);
+  const uint64_t ldv = uint64_t(p.ldv_bytes);
+
+  float acc[VEC];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        part[j] = 0.f;
-        if (j < n) {
+  for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+  int buf = 0;
+
+  for (int kb = k_first; kb < k_end; kb += NB) {
+    uint4 d[NB];
+    uint4 vr[DW ? NB : 1];
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            if (!act[c]) continue;
-            float f[VEC];
-            Vec<T>::load(d[j][c], f);
-            if constexpr (DW) {
-              float g[VEC];
-              Vec<T>::load(vv[c], g);
+    for (int j = 0; j < NB; ++j) {  // all loads of the batch first (clamped past the end)
+      const int k = min(kb + j, k_end - 1);
+      d[j] = act ? __ldg(reinterpret_cast<const uint4*>(srcb + uint64_t(uint32_t(s_t[k])) * lds))
+                 : make_uint4(0, 0, 0, 0);
+      if constexpr (DW)
+        vr[j] = act ? __ldg(reinterpret_cast<const uint4*>(vb + uint64_t(uint32_t(s_key[k])) * ldv))
+                    : make_uint4(0, 0, 0, 0);
+    }
+    float part[NB];
 #pragma unroll
-              for (int v = 0; v < VEC; ++v) part[j] = fmaf(f[v], g[v], part[j]);
-            }
+    for (int j = 0; j < NB; ++j) {
+      part[j] = 0.f;
+      const int k = kb + j;
+      if (k >= k_end) continue;              // uniform across the team
+      const int fl = s_fl[k];
+      if (fl & 1) {
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[c * VEC + v] = fmaf(wb[j], f[v], acc[c * VEC + v]);
-          }
-        }
+        for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
       }
+      float f[VEC];
+      Vec<T>::load(d[j], f);
+      const float wv = s_w[k];
       if constexpr (DW) {
-        TransposeReduce<NB, 16>::run(part, lane);
-        constexpr int SH = 5 - Log2<NB>::v;
-        const int jj = (lane >> SH) & (NB - 1);
-        int pos_mine = posb[0];
+        float g[VEC];
+        Vec<T>::load(vr[j], g);
 #pragma unroll
-        for (int j = 1; j < NB; ++j)
-          if (jj == j) pos_mine = posb[j];
-        if ((lane & ((1 << SH) - 1)) == 0 && jj < n)
-          p.dw_part[int64_t(slice) * p.P + pos_mine] = part[0];
+        for (int v = 0; v < VEC; ++v) part[j] = fmaf(f[v], g[v], part[j]);
+      }
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[v] = fmaf(wv, f[v], acc[v]);
+      if (fl & 2) {                          // last position of a piece
+        const int32_t rr = s_rr[k], rb = s_rb[k], re = s_re[k];
+        const int32_t row = p.dense ? s_key[k] : rr;
+        if (re - rb <= L) {
+          if (act) store_vec<VEC>(p.out + int64_t(row) * p.ldo + col, acc, p.dense != 0);
+        } else {
+          const int32_t i = int32_t(c0) + k;
+          const int32_t ps = rb + ((i - rb) / L) * L;
+          FVec<VEC> av;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) av.v[v] = acc[v];
+          finish_long_piece<VEC>(p, av, act, col, slice, row, rb, re, ps, &s_flag);
+        }
       }
     }
-
-    if (!lng) {
-      write_row<T, CPL>(p, p.dense ? int64_t(key) : int64_t(rr), acc, slice, lane, act);
-    } else {
-      const int32_t base = p.piece_base[rbb];
-      const int32_t slot = base + (s - rbb) / L;
-      const int32_t npieces = (re - rbb + L - 1) / L;
-      float* pp = p.partial + (int64_t(slice) * p.nslots_cap + slot) * slice_w;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        if (!act[c]) continue;
-#pragma unroll
-        for (int v = 0; v < VEC; v += 4)
-          __stcg(reinterpret_cast<float4*>(pp + (c * 32 + lane) * VEC + v),
-                 make_float4(acc[c * VEC + v], acc[c * VEC + v + 1], acc[c * VEC + v + 2],
-                             acc[c * VEC + v + 3]));
+    if constexpr (DW) {
+      TransposeReduce<NB, 16>::run(part, lane);   // lane l: warp sum of slot (l >> 2) & 7
+      if ((lane & 3) == 0) s_red[buf][warp][lane >> 2] = part[0];
+      __syncthreads();
+      if (tid < NB && kb + tid < k_end) {
+        float t = 0.f;
+        for (int w2 = 0; w2 < nwarps; ++w2) t += s_red[buf][w2][tid];
+        p.dw_part[int64_t(slice) * p.P + s_pos[kb + tid]] = t;
       }
-      __threadfence();
-      __syncwarp();
-      int old = 0;
-      if (lane == 0) old = atomicAdd(p.counters + int64_t(slice) * p.nslots_cap + base, 1);
-      old = __shfl_sync(FULL, old, 0);
-      if (old == npieces - 1) {  // last piece of this run: combine in piece order
-        __threadfence();
-#pragma unroll
-        for (int v = 0; v < CPL * VEC; ++v) acc[v] = 0.f;
-        for (int32_t q = 0; q < npieces; ++q) {
-          const float* src = p.partial + (int64_t(slice) * p.nslots_cap + base + q) * slice_w;
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            if (!act[c]) continue;
-#pragma unroll
-            for (int v = 0; v < VEC; v += 4) {
-              const float4 a = __ldcg(reinterpret_cast<const float4*>(src + (c * 32 + lane) * VEC + v));
-              acc[c * VEC + v] += a.x;
-              acc[c * VEC + v + 1] += a.y;
-              acc[c * VEC + v + 2] += a.z;
-              acc[c * VEC + v + 3] += a.w;
-            }
-          }
-        }
-        write_row<T, CPL>(p, p.dense ? int64_t(key) : int64_t(rr), acc, slice, lane, act);
-      }
+      buf ^= 1;
     }
   }
 }
@@ -266,18 +263,14 @@ __global__ void sum_slices_kernel(const float* part, int ns, int64_t P, float* d
   dw[i] = t;
 }
 
-int cpl_for(int64_t vu) { return vu <= 32 ? 1 : 2; }
+// team size: one thread per 16-byte row vector, 32..256 threads
+int team_threads(int64_t vu) { return vu <= 32 ? 32 : (vu >= 256 ? 256 : int(vu)); }
 
 template <typename T>
-mlStatus dispatch_seg(int cpl, bool dw, dim3 grid, const SegParams& p, cudaStream_t s,
+mlStatus dispatch_seg(int threads, bool dw, dim3 grid, const SegParams& p, cudaStream_t s,
                       const char* name) {
-#define ML_SEG(C, D) seg_kernel<T, C, D><<<grid, 256, 0, s>>>(p)
-  if (dw) {
-    if (cpl == 1) ML_SEG(1, true); else ML_SEG(2, true);
-  } else {
-    if (cpl == 1) ML_SEG(1, false); else ML_SEG(2, false);
-  }
-#undef ML_SEG
+  if (dw) seg_kernel<T, true><<<grid, threads, 0, s>>>(p);
+  else seg_kernel<T, false><<<grid, threads, 0, s>>>(p);
   ML_LAUNCH_CHECK(name);
   return ML_OK;
 }
@@ -286,16 +279,15 @@ mlStatus dispatch_seg(int cpl, bool dw, dim3 grid, const SegParams& p, cudaStrea
 
 int seg_slices(int32_t dv, mlDtype dt) {
   const int64_t vu = int64_t(dv) * int64_t(dtype_size(dt)) / 16;
-  return vu <= 64 ? 1 : int(vu / 64);
+  return vu <= 256 ? 1 : int(vu / 256);
 }
 
 static int64_t nslots_cap(int64_t P) { return 2 * (P / kPieceLen) + 2; }
 
 void seg_carve(Carver& c, int64_t P, int32_t dv, mlDtype dt, float** partial, int32_t** counters) {
   const int64_t vu = int64_t(dv) * int64_t(dtype_size(dt)) / 16;
-  const int cpl = cpl_for(vu);
   const int ns = seg_slices(dv, dt);
-  const int64_t slice_w = int64_t(32) * cpl * (16 / int64_t(dtype_size(dt)));
+  const int64_t slice_w = int64_t(team_threads(vu)) * (16 / int64_t(dtype_size(dt)));
   *partial = c.take<float>(ns * nslots_cap(P) * slice_w);
   *counters = c.take<int32_t>(ns * nslots_cap(P));
 }
@@ -304,9 +296,12 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   if (a.P <= 0) return ML_OK;
   ML_TRY(check_cols(a.dv, a.dtype, "segreduce"));
   const int64_t vu = int64_t(a.dv) * int64_t(dtype_size(a.dtype)) / 16;
-  const int cpl = cpl_for(vu);
+  const int threads = team_threads(vu);
   const int ns = seg_slices(a.dv, a.dtype);
-  if (vu > 64 && vu % 64) return fail(ML_ERR_CONFIG, "segreduce: row vectors must divide into slices of 64");
+  if (vu > 256 && vu % 256) return fail(ML_ERR_CONFIG, "segreduce: row vectors must divide into slices of 256");
+  if (a.P >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "segreduce: too many positions");
+  if (a.lds * int64_t(dtype_size(a.dtype)) >= (int64_t(1) << 32))
+    return fail(ML_ERR_UNSUPPORTED, "segreduce: source row pitch too large");
   SegParams p;
   p.skey = a.skey; p.spos = a.spos; p.P = a.P;
   p.flags = a.runs->flags; p.excl = a.runs->excl; p.run_begin = a.runs->run_begin;
@@ -322,11 +317,11 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   timing_mark(nullptr, s);
   ML_CUDA_TRY(cudaMemsetAsync(a.counters, 0, sizeof(int32_t) * size_t(ns) * size_t(p.nslots_cap), s));
   timing_mark("memset", s);
-  const int64_t nchunks = (a.P + 31) / 32;
-  dim3 grid(unsigned((nchunks + 7) / 8), unsigned(ns));
+  const int64_t nchunks = (a.P + kChunk - 1) / kChunk;
+  dim3 grid{unsigned(nchunks), unsigned(ns), 1u};
   const bool dw = a.V != nullptr;
-  if (a.dtype == ML_BF16) return dispatch_seg<__nv_bfloat16>(cpl, dw, grid, p, s, a.name);
-  return dispatch_seg<float>(cpl, dw, grid, p, s, a.name);
+  if (a.dtype == ML_BF16) return dispatch_seg<__nv_bfloat16>(threads, dw, grid, p, s, a.name);
+  return dispatch_seg<float>(threads, dw, grid, p, s, a.name);
 }
 
 mlStatus launch_sum_slices(const float* part, int nslices, int64_t P, float* dw, cudaStream_t s) {
