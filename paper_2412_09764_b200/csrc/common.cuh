@@ -85,6 +85,22 @@ __device__ __forceinline__ uint4 ldg_nc_v4_hint(const void* p, uint64_t pol) {
   return r;
 }
 
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Packed fp32x2 FMA (sm_100: FFMA2), IEEE round-to-nearest per lane.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
+        "l"(*reinterpret_cast<const uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
 __device__ __forceinline__ uint4 ldg_v4(const void* p) {
   return *reinterpret_cast<const uint4*>(p);
 }

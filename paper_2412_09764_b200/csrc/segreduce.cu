@@ -187,22 +187,32 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
   const uint32_t lds = uint32_t(p.lds_bytes);
   const uint64_t ldv = uint64_t(p.ldv_bytes);
 
-  float acc[VEC];
+  constexpr int V2 = VEC / 2;
+  // dy (bag backward) is re-read ~B times: keep it in L2; the query rows of the
+  // key backward are not (default policy)
+  const uint64_t pol_keep = DW ? l2_evict_last_policy() : 0;
+  const uint64_t pol_stream = l2_evict_first_policy();  // V: read once per piece
+  float2 acc[V2], g[V2];
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+  for (int v = 0; v < V2; ++v) acc[v] = g[v] = make_float2(0.f, 0.f);
   int buf = 0;
 
   for (int kb = k_first; kb < k_end; kb += NB) {
     uint4 d[NB];
     uint4 vr[DW ? NB : 1];
+    int fl[NB];
 #pragma unroll
     for (int j = 0; j < NB; ++j) {  // all loads of the batch first (clamped past the end)
       const int k = min(kb + j, k_end - 1);
-      d[j] = act ? __ldg(reinterpret_cast<const uint4*>(srcb + uint64_t(uint32_t(s_t[k])) * lds))
-                 : make_uint4(0, 0, 0, 0);
-      if constexpr (DW)
-        vr[j] = act ? __ldg(reinterpret_cast<const uint4*>(vb + uint64_t(uint32_t(s_key[k])) * ldv))
-                    : make_uint4(0, 0, 0, 0);
+      fl[j] = s_fl[k];
+      const char* sp = srcb + uint64_t(uint32_t(s_t[k])) * lds;
+      d[j] = make_uint4(0, 0, 0, 0);
+      if (act) d[j] = DW ? ldg_nc_v4_hint(sp, pol_keep) : __ldg(reinterpret_cast<const uint4*>(sp));
+      if constexpr (DW) {
+        vr[j] = make_uint4(0, 0, 0, 0);
+        if (act && (fl[j] & 1))     // value row: only at piece starts
+          vr[j] = ldg_nc_v4_hint(vb + uint64_t(uint32_t(s_key[k])) * ldv, pol_stream);
+      }
     }
     float part[NB];
 #pragma unroll
@@ -210,33 +220,35 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
       part[j] = 0.f;
       const int k = kb + j;
       if (k >= k_end) continue;              // uniform across the team
-      const int fl = s_fl[k];
-      if (fl & 1) {
+      if (fl[j] & 1) {                       // piece start: reset, unpack its value row
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+        for (int v = 0; v < V2; ++v) acc[v] = make_float2(0.f, 0.f);
+        if constexpr (DW) Vec<T>::load(vr[j], reinterpret_cast<float*>(g));
       }
-      float f[VEC];
-      Vec<T>::load(d[j], f);
+      float2 f[V2];
+      Vec<T>::load(d[j], reinterpret_cast<float*>(f));
       const float wv = s_w[k];
+      const float2 w2 = make_float2(wv, wv);
       if constexpr (DW) {
-        float g[VEC];
-        Vec<T>::load(vr[j], g);
+        float2 pr = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) part[j] = fmaf(f[v], g[v], part[j]);
+        for (int v = 0; v < V2; ++v) pr = ffma2(f[v], g[v], pr);
+        part[j] = pr.x + pr.y;
       }
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[v] = fmaf(wv, f[v], acc[v]);
-      if (fl & 2) {                          // last position of a piece
+      for (int v = 0; v < V2; ++v) acc[v] = ffma2(w2, f[v], acc[v]);
+      if (fl[j] & 2) {                       // last position of a piece
         const int32_t rr = s_rr[k], rb = s_rb[k], re = s_re[k];
         const int32_t row = p.dense ? s_key[k] : rr;
+        const float* accf = reinterpret_cast<const float*>(acc);
         if (re - rb <= L) {
-          if (act) store_vec<VEC>(p.out + int64_t(row) * p.ldo + col, acc, p.dense != 0);
+          if (act) store_vec<VEC>(p.out + int64_t(row) * p.ldo + col, accf, p.dense != 0);
         } else {
           const int32_t i = int32_t(c0) + k;
           const int32_t ps = rb + ((i - rb) / L) * L;
           FVec<VEC> av;
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) av.v[v] = acc[v];
+          for (int v = 0; v < VEC; ++v) av.v[v] = accf[v];
           finish_long_piece<VEC>(p, av, act, col, slice, row, rb, re, ps, &s_flag);
         }
       }
