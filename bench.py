@@ -107,7 +107,21 @@ def dist_env():
 
 
 # ------------------------------------------------------------- our arm
-def make_inputs(cfg, dev, G, rank, ops, torch):
+def synth_value_shard(N, dv, G, rank, dt, dev, ops, torch):
+    """This rank's [N, dv/G] column shard of the synthetic value table,
+    regenerated from the same counters as the full table (i = r*dv + c)."""
+    from synthetic import gen
+    lo, hi = rank * dv // G, (rank + 1) * dv // G
+    out = torch.empty((N, hi - lo), dtype=dt, device=dev)
+    buf = torch.empty((1 << 16, dv), dtype=dt, device=dev)
+    for r0 in range(0, N, buf.shape[0]):
+        n = min(buf.shape[0], N - r0)
+        ops.synth_fill(buf[:n], SEED, gen.TAGS["V"], row0=r0)
+        out[r0:r0 + n].copy_(buf[:n, lo:hi])
+    return out
+
+
+def make_inputs(cfg, dev, G, rank, ops, torch, force_group=False):
     from synthetic import gen
     S, dv, D, Dk, H, k, T = (cfg[n] for n in ("S", "dv", "D", "Dk", "H", "k", "T"))
     dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
@@ -127,13 +141,12 @@ def make_inputs(cfg, dev, G, rank, ops, torch):
     fill("K2", (H, S, Dk // 2), "K2", gen.scale_for("K2", Dk=Dk))
     fill("W1", (D, dv), "W1", gen.scale_for("W1", D=D))
     fill("W2", (dv, D), "W2", gen.scale_for("W2", dv=dv))
-    if G == 1:
+    if G == 1 and not force_group:
         fill("V", (N, dv), "V")
     else:
         # this rank's column shard [N, dv/G] of V (regenerated from the same
         # counters as the full table, columns [rank*dv/G, (rank+1)*dv/G))
-        from paper_2412_09764_b200 import group
-        t["V"] = group.synth_value_shard(N, dv, G, rank, SEED, dt, dev)
+        t["V"] = synth_value_shard(N, dv, G, rank, dt, dev, ops, torch)
     return t
 
 
@@ -144,16 +157,17 @@ def run_ours(args, cfg, world, rank, local):
     torch.cuda.set_device(dev)
     G = world
     pg = None
-    if world > 1:
+    use_group = world > 1 or args.force_group
+    if use_group:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
-    t = make_inputs(cfg, dev, G, rank, ops, torch)
+    t = make_inputs(cfg, dev, G, rank, ops, torch, use_group)
     k = cfg["k"]
     dK1 = torch.zeros(t["K1"].shape, dtype=torch.float32, device=dev)
     dK2 = torch.zeros(t["K2"].shape, dtype=torch.float32, device=dev)
     bufs = {}
-    if G > 1:
+    if use_group:
         from paper_2412_09764_b200 import group
         layer = group.GroupMemoryLayer(pg, k=k, mode=args.mode)
 
@@ -387,6 +401,8 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=128)
     ap.add_argument("--ref-tokens", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-group", action="store_true",
+                    help="run the memory-group (NCCL) path even at N=1 (torchrun)")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.warmup < 3:
@@ -419,7 +435,8 @@ def main():
                    "global_tokens": res["tokens_per_step"], "N_values": cfg["S"] ** 2,
                    "value_dim": cfg["dv"], "heads": cfg["H"], "k": cfg["k"],
                    "key_dim": cfg["Dk"], "gated": True,
-                   "parallelism": f"memory-group dim-shard G={G} ({args.mode})" if G > 1 else "single GPU",
+                   "parallelism": (f"memory-group dim-shard G={G} ({args.mode})"
+                                   if (G > 1 or args.force_group) else "single GPU"),
                    "l2": "inputs_larger_than_L2 (value table >= 4 GiB vs 126 MB L2; no flush)",
                    "unique_rows_per_position": round(res["U"] / P, 4), "seed": SEED},
         "roofline": roof,

@@ -186,6 +186,35 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
                           float* dW1, float* dW2, float* dw_out,
                           void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------- memory group pieces (a7, a12)
+ * Parallel memory (§3.1.2, Fig. 2): the value table is
+ * sharded along the embedding dim over the G ranks of a memory group; the
+ * exchange (all-gather of (idx, w), all-to-all of the partial embeddings,
+ * reverse all-to-all of dy, reduce-scatter of the partial dw) is issued by
+ * the caller (paper_2412_09764_b200/group.py, NCCL).  These calls do the
+ * on-device layout work around it:
+ *   ml_group_unpack: recv [G][T_loc][dv/G] (rank g's slice of this rank's
+ *     tokens) -> y [T_loc][dv], y[t][g*dv/G + c] = recv[g][t][c]; if gate !=
+ *     NULL also z = y ⊙ silu(gate) (Eq. 2) into z [T_loc][dv] (y nullable then).
+ *   ml_group_pack: src [T_loc][dv] -> dst [G][T_loc][dv/G] (the reverse).
+ * Rules: G | dv, (dv/G)*e a multiple of 16 bytes (SPEC S:401 config error). */
+mlStatus ml_group_unpack(const void* recv, int32_t G, int32_t T_loc, int32_t dv, const void* gate,
+                         void* y, void* z, mlDtype dtype, void* stream);
+mlStatus ml_group_pack(const void* src, int32_t G, int32_t T_loc, int32_t dv, void* dst,
+                       mlDtype dtype, void* stream);
+
+/* Eq. 2 backward, elementwise over n elements (n*e a multiple of 16 B):
+ * z = y ⊙ silu(g), dy = dz ⊙ silu(g), dg = dz ⊙ y ⊙ sigmoid(g)(1 + g(1 - sigmoid(g))). */
+mlStatus ml_gate_bwd(const void* dz, const void* g, const void* y, void* z, void* dy, void* dg,
+                     int64_t n, mlDtype dtype, void* stream);
+
+/* Library GEMM (cuBLASLt, fp32 accumulation) for the dense gate projections:
+ * row-major C[M,N] = op(A)[M,K] op(B)[K,N], op = transpose if trans*; A/B of
+ * dtype `ab`, C fp32 if c_f32 else `ab`.  ws: >= 32 MiB device scratch. */
+mlStatus ml_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                 const void* B, int64_t ldb, void* C, int64_t ldc, mlDtype ab, int c_f32, void* ws,
+                 size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,10 @@ SIGNATURES = {
     "memory_layer_fwd": [C.POINTER(LayerShape)] + [P] * 13 + [SZ, P],
     "memory_layer_bwd_workspace": [C.POINTER(LayerShape), C.POINTER(SZ)],
     "memory_layer_bwd": [C.POINTER(LayerShape)] + [P] * 23 + [SZ, P],
+    "ml_group_unpack": [P, C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int, P],
+    "ml_group_pack": [P, C.c_int32, C.c_int32, C.c_int32, P, C.c_int, P],
+    "ml_gate_bwd": [P, P, P, P, P, P, I64, C.c_int, P],
+    "ml_gemm": [C.c_int, C.c_int, I64, I64, I64, P, I64, P, I64, P, I64, C.c_int, C.c_int, P, SZ, P],
 }
 _RESTYPES = {"ml_last_error": C.c_char_p, "ml_version": C.c_int, "ml_launch_count": C.c_uint64,
              "ml_device_info": C.c_int, "ml_timing_enable": None, "ml_timing_reset": None,

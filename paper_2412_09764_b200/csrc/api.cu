@@ -507,4 +507,63 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
   ML_API_END
 }
 
+// ------------------------------------------------------------ group pieces
+static mlStatus check_group(int32_t G, int32_t T_loc, int32_t dv, mlDtype dt) {
+  if (G < 1 || T_loc < 0 || dv < 1) return fail(ML_ERR_CONFIG, "group: need G >= 1, T_loc >= 0, dv >= 1");
+  if (dv % G) return fail(ML_ERR_CONFIG, "group: G must divide dv (SPEC S:401)");
+  if ((int64_t(dv / G) * int64_t(dtype_size(dt))) % 16)
+    return fail(ML_ERR_CONFIG, "group: (dv/G)*e must be a multiple of 16 bytes");
+  return ML_OK;
+}
+
+mlStatus ml_group_unpack(const void* recv, int32_t G, int32_t T_loc, int32_t dv, const void* gate,
+                         void* y, void* z, mlDtype dtype, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_group(G, T_loc, dv, dtype));
+  if (T_loc == 0) return ML_OK;
+  ML_TRY(check_ptrs({recv}));
+  if (gate) ML_TRY(check_ptrs({gate, z}));
+  if (y) ML_TRY(check_ptrs({y}));
+  if (!y && !gate) return fail(ML_ERR_ARG, "group_unpack: nothing to write");
+  timing_mark(nullptr, S(stream));
+  return launch_group_unpack(recv, G, T_loc, dv / G, gate, y, z, dtype, S(stream));
+  ML_API_END
+}
+
+mlStatus ml_group_pack(const void* src, int32_t G, int32_t T_loc, int32_t dv, void* dst,
+                       mlDtype dtype, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_group(G, T_loc, dv, dtype));
+  if (T_loc == 0) return ML_OK;
+  ML_TRY(check_ptrs({src, dst}));
+  timing_mark(nullptr, S(stream));
+  return launch_group_pack(src, G, T_loc, dv / G, dst, dtype, S(stream));
+  ML_API_END
+}
+
+mlStatus ml_gate_bwd(const void* dz, const void* g, const void* y, void* z, void* dy, void* dg,
+                     int64_t n, mlDtype dtype, void* stream) {
+  ML_API_BEGIN
+  if (n < 0) return fail(ML_ERR_ARG, "gate_bwd: n < 0");
+  if (n == 0) return ML_OK;
+  if ((n * int64_t(dtype_size(dtype))) % 16) return fail(ML_ERR_CONFIG, "gate_bwd: n*e must be a multiple of 16");
+  ML_TRY(check_ptrs({dz, g, y, z, dy, dg}));
+  timing_mark(nullptr, S(stream));
+  return launch_gate_bwd(dz, g, y, z, dy, dg, n, dtype, S(stream));
+  ML_API_END
+}
+
+mlStatus ml_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                 const void* B, int64_t ldb, void* C, int64_t ldc, mlDtype ab, int c_f32, void* ws,
+                 size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  if (M < 0 || N < 0 || K < 1) return fail(ML_ERR_ARG, "gemm: bad sizes");
+  if (M == 0 || N == 0) return ML_OK;
+  ML_TRY(check_ptrs({A, B, C}));
+  timing_mark(nullptr, S(stream));
+  return gemm_rm(transA != 0, transB != 0, M, N, K, A, lda, B, ldb, C, ldc, ab, c_f32 != 0, ws, ws_bytes,
+                 S(stream));
+  ML_API_END
+}
+
 }  // extern "C"

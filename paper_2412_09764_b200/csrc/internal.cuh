@@ -109,6 +109,12 @@ mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K,
                  void* ws, size_t ws_bytes, cudaStream_t s);
 constexpr size_t kGemmWs = size_t(32) << 20;
 
+// ------------------------------------------------------------ group layout
+mlStatus launch_group_unpack(const void* recv, int G, int64_t T_loc, int32_t dv_slice,
+                             const void* gate, void* y, void* z, mlDtype dt, cudaStream_t s);
+mlStatus launch_group_pack(const void* src, int G, int64_t T_loc, int32_t dv_slice, void* dst,
+                           mlDtype dt, cudaStream_t s);
+
 // ------------------------------------------------------------ synth
 mlStatus launch_synth(void* out, int64_t n_rows, int64_t n_cols, int64_t row0, uint64_t seed,
                       uint32_t tag, float scale, int cls, mlDtype dt, int64_t modulus,

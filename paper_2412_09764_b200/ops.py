@@ -37,9 +37,10 @@ def _stream():
 
 
 def workspace(nbytes, device=None, tag="default"):
-    """A cached uint8 device buffer of at least nbytes (grown on demand)."""
+    """A cached uint8 device buffer of at least nbytes (grown on demand), one
+    per (device, tag, current stream) so concurrent streams never share it."""
     device = torch.device(device or torch.cuda.current_device())
-    key = (device.index, tag)
+    key = (device.index, tag, torch.cuda.current_stream(device).cuda_stream)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         _WS.pop(key, None)
@@ -240,3 +241,42 @@ def memory_layer_bwd(dout, x, q, K1, K2, V, W1, W2, saved, dK1=None, dK2=None, w
         _p(U), _p(dW1), _p(dW2), _p(dw), _p(ws), n, _stream()))
     return LayerGrads(dq=dq, dK1=dK1, dK2=dK2, rows=rows, dV=dV, U=U, dx=dx, dW1=dW1, dW2=dW2,
                       dw=dw)
+
+
+# ------------------------------------------------------- group / gate pieces
+def group_unpack(recv, G, T_loc, dv, gate=None, want_y=True):
+    """recv [G, T_loc, dv/G] -> y [T_loc, dv] (and z = y*silu(gate) if gate)."""
+    dt = _dt(recv)
+    y = torch.empty((T_loc, dv), dtype=recv.dtype, device=recv.device) if want_y else None
+    z = torch.empty((T_loc, dv), dtype=recv.dtype, device=recv.device) if gate is not None else None
+    check(lib().ml_group_unpack(_p(recv), G, T_loc, dv, _p(gate), _p(y), _p(z), dt, _stream()))
+    return y, z
+
+
+def group_pack(src, G):
+    """src [T_loc, dv] -> [G, T_loc, dv/G] (slice g of every token row)."""
+    T_loc, dv = src.shape
+    dst = torch.empty((G, T_loc, dv // G), dtype=src.dtype, device=src.device)
+    check(lib().ml_group_pack(_p(src), G, T_loc, dv, _p(dst), _dt(src), _stream()))
+    return dst
+
+
+def gate_bwd(dz, g, y):
+    """Eq. 2 elementwise backward: returns z = y*silu(g), dy, dg."""
+    z, dy, dg = torch.empty_like(y), torch.empty_like(y), torch.empty_like(y)
+    check(lib().ml_gate_bwd(_p(dz), _p(g), _p(y), _p(z), _p(dy), _p(dg), y.numel(), _dt(y),
+                            _stream()))
+    return z, dy, dg
+
+
+def gemm(A, B, transA=False, transB=False, out_f32=False):
+    """Row-major C = op(A) op(B) on cuBLASLt (library GEMM)."""
+    M = A.shape[1] if transA else A.shape[0]
+    K = A.shape[0] if transA else A.shape[1]
+    N = B.shape[0] if transB else B.shape[1]
+    C_ = torch.empty((M, N), dtype=torch.float32 if out_f32 else A.dtype, device=A.device)
+    ws = workspace(32 << 20, A.device, tag="gemm")
+    check(lib().ml_gemm(1 if transA else 0, 1 if transB else 0, M, N, K, _p(A), A.shape[1], _p(B),
+                        B.shape[1], _p(C_), N, _dt(A), 1 if out_f32 else 0, _p(ws), ws.numel(),
+                        _stream()))
+    return C_
