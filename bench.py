@@ -314,40 +314,44 @@ def roofline(res, cfg, G, peaks):
 
 
 # ------------------------------------------------------------- oracle arm
-def oracle_sample(cfg, T_o, seed=SEED):
-    """Times the CPU oracle (oracle/) on T_o tokens of the workload: full-size
-    tables, rows regenerated on demand OUTSIDE the timed parts.  Returns
-    (seconds, tokens)."""
+def oracle_sample(cfg, T_o, seed=SEED, chunk=256, t0=0):
+    """Times the CPU oracle (oracle/) on T_o tokens of the workload (tokens
+    t0.., in chunks of `chunk`): full-size tables, value rows and inputs
+    regenerated on demand OUTSIDE the timed parts.  Returns (seconds, tokens)."""
     import numpy as np
     from oracle import bag as obag, gate as ogate, pkm as opkm
     from synthetic import gen
     S, dv, D, Dk, H, k = (cfg[n] for n in ("S", "dv", "D", "Dk", "H", "k"))
     dt = cfg["dtype"]
     f64 = lambda a: a.astype(np.float64)
-    q = f64(gen.rows(seed, "q", np.arange(T_o * H), Dk, dtype=dt)).reshape(T_o, H, Dk)
-    x = f64(gen.rows(seed, "x", np.arange(T_o), D, dtype=dt))
-    dout = f64(gen.rows(seed, "dout", np.arange(T_o), D, dtype=dt))
     K1 = f64(gen.tensor(seed, "K1", (H, S, Dk // 2), scale=gen.scale_for("K1", Dk=Dk), dtype=dt))
     K2 = f64(gen.tensor(seed, "K2", (H, S, Dk // 2), scale=gen.scale_for("K2", Dk=Dk), dtype=dt))
     W1 = f64(gen.tensor(seed, "W1", (D, dv), scale=gen.scale_for("W1", D=D), dtype=dt))
     W2 = f64(gen.tensor(seed, "W2", (dv, D), scale=gen.scale_for("W2", dv=dv), dtype=dt))
-    el = 0.0
-    t0 = time.perf_counter()
-    idx, score, w = opkm.pkm_lookup(q, K1, K2, k)
-    el += time.perf_counter() - t0
-    bidx = idx.reshape(T_o, H * k)
-    bw = w.reshape(T_o, H * k)
-    uniq = np.unique(bidx)
-    Vrows = f64(gen.rows(seed, "V", uniq, dv, dtype=dt))        # untimed: input synthesis
-    pos = {int(r): i for i, r in enumerate(uniq)}
-    lidx = np.vectorize(pos.get)(bidx)
-    t0 = time.perf_counter()
-    y = obag.embbag_fwd(Vrows, lidx, bw)
-    out, g, z = ogate.gate_fwd(x, y, W1, W2)
-    gb = ogate.gate_bwd(dout, x, y, g, W1, W2)
-    rows, dV, dw = obag.embbag_bwd(Vrows, lidx, bw, gb["dy"])
-    dq, dK1, dK2, _ = opkm.pkm_bwd(q, K1, K2, idx, w, dw.reshape(T_o, H, k))
-    el += time.perf_counter() - t0
+    el, done = 0.0, 0
+    while done < T_o:
+        n = min(chunk, T_o - done)
+        toks = np.arange(t0 + done, t0 + done + n)
+        rows = (toks[:, None] * H + np.arange(H)[None, :]).reshape(-1)
+        q = f64(gen.rows(seed, "q", rows, Dk, dtype=dt)).reshape(n, H, Dk)
+        x = f64(gen.rows(seed, "x", toks, D, dtype=dt))
+        dout = f64(gen.rows(seed, "dout", toks, D, dtype=dt))
+        t_0 = time.perf_counter()
+        idx, score, w = opkm.pkm_lookup(q, K1, K2, k)
+        el += time.perf_counter() - t_0
+        bidx = idx.reshape(n, H * k)
+        bw = w.reshape(n, H * k)
+        uniq, lidx = np.unique(bidx, return_inverse=True)
+        Vrows = f64(gen.rows(seed, "V", uniq, dv, dtype=dt))      # untimed: input synthesis
+        lidx = lidx.reshape(n, H * k)
+        t_0 = time.perf_counter()
+        y = obag.embbag_fwd(Vrows, lidx, bw)
+        out, g, z = ogate.gate_fwd(x, y, W1, W2)
+        gb = ogate.gate_bwd(dout, x, y, g, W1, W2)
+        rows_, dV, dw = obag.embbag_bwd(Vrows, lidx, bw, gb["dy"])
+        dq, dK1, dK2, _ = opkm.pkm_bwd(q, K1, K2, idx, w, dw.reshape(n, H, k))
+        el += time.perf_counter() - t_0
+        done += n
     return el, T_o
 
 
@@ -362,8 +366,9 @@ def blas_threads():
 def cpu_baseline(cfg, T_o):
     el, n = oracle_sample(cfg, T_o)
     return {"value": n / el, "unit": "tok/s", "cores": blas_threads(), "kind": "oracle",
-            "sample": f"{n} tokens of {cfg['desc']} (full-size tables, rows regenerated on demand "
-                      f"outside the timed parts); numpy fp64, BLAS threads in matmuls only",
+            "sample": f"{n} tokens (chunks of 256) of {cfg['desc']}: full-size tables, rows "
+                      f"regenerated on demand outside the timed parts; numpy fp64, BLAS threads "
+                      f"in matmuls only",
             "seconds": round(el, 3)}
 
 
@@ -398,8 +403,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None)
     ap.add_argument("--mode", default="alltoall", choices=["alltoall", "allgather"])
-    ap.add_argument("--cpu-tokens", type=int, default=128)
-    ap.add_argument("--ref-tokens", type=int, default=32)
+    ap.add_argument("--cpu-tokens", type=int, default=2048)
+    ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-group", action="store_true",
                     help="run the memory-group (NCCL) path even at N=1 (torchrun)")
