@@ -5,6 +5,7 @@
 #include "internal.cuh"
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <exception>
 
@@ -80,15 +81,40 @@ static void pkm_fwd_carve(Carver& c, const mlPkmShape& s, PkmFwdBufs& b) {
   b.hs = c.take<float>(TH * 2 * s.k);
 }
 
+// Key/query backward strategy.  dense: the k selected score gradients per
+// (t, h, half) are scattered into a bf16 [T*H, 2, S] matrix and dq = ds K,
+// dK += ds^T q run as tensor-core GEMMs (cuBLASLt) -- cheaper than the sparse
+// gathers while S / k is small (the dense FLOPs grow with S).  sparse: dq as a
+// k-row bag over the half-key table, dK by the sorted segmented reduction
+// (fp32 end to end; used for fp32 inputs and large S).
+static bool pkm_bwd_dense(const mlPkmShape& s) {
+  static int force_sparse = -1;
+  if (force_sparse < 0) {
+    const char* e = std::getenv("ML_PKM_BWD_SPARSE");
+    force_sparse = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !force_sparse && s.dtype == ML_BF16 && s.S <= 2048 && (s.S % 8) == 0 &&
+         ((s.Dk / 2) % 8) == 0;
+}
+
 struct PkmBwdBufs {
   float* ds; int32_t* key1; int32_t* key2;
   SortBufs sort; RunBufs runs; float* partial; int32_t* counters;
+  __nv_bfloat16* ds_dense; void* gemm_ws;
 };
 static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
   const int64_t P = int64_t(s.T) * s.H * s.k;
   b.ds = c.take<float>(P);
   b.key1 = c.take<int32_t>(P);
   b.key2 = c.take<int32_t>(P);
+  b.ds_dense = nullptr;
+  b.gemm_ws = nullptr;
+  if (pkm_bwd_dense(s)) {
+    b.ds_dense = c.take<__nv_bfloat16>(int64_t(s.T) * s.H * 2 * s.S);
+    b.gemm_ws = c.take<char>(kGemmWs);
+    if (!c.base) b.ds_dense = reinterpret_cast<__nv_bfloat16*>(1);  // measuring: mark dense
+    return;
+  }
   sort_carve(c, P, ceil_log2(int64_t(s.H) * s.S), b.sort);
   runs_carve(c, P, b.runs);
   seg_carve(c, P, s.Dk / 2, s.dtype, &b.partial, &b.counters);
@@ -120,7 +146,30 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
   if (s.T == 0) return ML_OK;
   const int64_t P = int64_t(s.T) * s.H * s.k;
   const int Dh = s.Dk / 2;
-  ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, st));
+  if (b.ds_dense) {
+    timing_mark(nullptr, st);
+    ML_CUDA_TRY(cudaMemsetAsync(b.ds_dense, 0, sizeof(__nv_bfloat16) * size_t(s.T) * s.H * 2 * s.S, st));
+    timing_mark("memset", st);
+    ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, b.ds_dense, st));
+    const int64_t lds = int64_t(s.H) * 2 * s.S;  // row pitch of ds_dense per token
+    for (int h = 0; h < s.H; ++h) {
+      for (int half = 0; half < 2; ++half) {
+        const __nv_bfloat16* A = b.ds_dense + (int64_t(h) * 2 + half) * s.S;
+        const char* Kh = static_cast<const char*>(half ? K2 : K1) + int64_t(h) * s.S * Dh * 2;
+        const char* qh = static_cast<const char*>(q) + (int64_t(h) * s.Dk + int64_t(half) * Dh) * 2;
+        float* dKh = (half ? dK2 : dK1) + int64_t(h) * s.S * Dh;
+        // dq[t, h, half] = ds[t, h, half, :] K_half[h]          [T, Dh]
+        ML_TRY(gemm_rm(false, false, s.T, Dh, s.S, A, lds, Kh, Dh,
+                       dq + int64_t(h) * s.Dk + int64_t(half) * Dh, int64_t(s.H) * s.Dk, ML_BF16,
+                       true, b.gemm_ws, kGemmWs, st));
+        // dK_half[h] += ds[:, h, half, :]^T q_half[:, h]        [S, Dh]
+        ML_TRY(gemm_rm(true, false, s.S, Dh, s.T, A, lds, qh, int64_t(s.H) * s.Dk, dKh, Dh, ML_BF16,
+                       true, b.gemm_ws, kGemmWs, st, 1.f));
+      }
+    }
+    return ML_OK;
+  }
+  ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, nullptr, st));
   const int bits = ceil_log2(int64_t(s.H) * s.S);
   for (int half = 0; half < 2; ++half) {
     const void* K = half ? K2 : K1;

@@ -87,7 +87,7 @@ mlStatus launch_scatter_rows(const int32_t* rows, const float* dV, const int32_t
 
 mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const void* A,
                  int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, mlDtype ab,
-                 bool c_f32, void* ws, size_t ws_bytes, cudaStream_t s) {
+                 bool c_f32, void* ws, size_t ws_bytes, cudaStream_t s, float beta) {
   if (M <= 0 || N <= 0) return ML_OK;
   cublasLtHandle_t h = lt_handle();
   if (!h) return fail(ML_ERR_CUDA, "cublasLtCreate failed");
@@ -121,11 +121,31 @@ mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, cons
     uint64_t wsb = ws_bytes;
     ck(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb,
                                             sizeof(wsb)), "pref ws");
-    ck(cublasLtMatmulAlgoGetHeuristic(h, desc, l1, l2, lc, lc, pref, 1, &heur, &nres), "heuristic");
-    if (st == ML_OK && nres == 0) st = fail(ML_ERR_CUDA, "cublasLt: no algorithm");
+    // heuristic results cached per problem signature (the query costs tens of us)
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, size_t, int>,
+                    cublasLtMatmulHeuristicResult_t> cache;
+    const auto key = std::make_tuple(int(transA), int(transB), M, N, K, lda, ldb, ldc, int(ab),
+                                     int(c_f32), ws_bytes, int(beta != 0.f));
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = cache.find(key);
+      if (it != cache.end()) {
+        heur = it->second;
+        nres = 1;
+      }
+    }
+    if (!nres) {
+      ck(cublasLtMatmulAlgoGetHeuristic(h, desc, l1, l2, lc, lc, pref, 1, &heur, &nres), "heuristic");
+      if (st == ML_OK && nres == 0) st = fail(ML_ERR_CUDA, "cublasLt: no algorithm");
+      if (st == ML_OK) {
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = heur;
+      }
+    }
   }
   if (st == ML_OK) {
-    const float alpha = 1.f, beta = 0.f;
+    const float alpha = 1.f;
     timing_mark(nullptr, s);
     ck(cublasLtMatmul(h, desc, &alpha, B, l1, A, l2, &beta, C, lc, C, lc, &heur.algo, ws, ws_bytes,
                       s), "matmul");

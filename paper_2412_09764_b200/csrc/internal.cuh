@@ -91,9 +91,13 @@ mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const f
                                 int32_t* idx, float* w, float* score, cudaStream_t s);
 // ds = w (dw - sum w dw) with dw = sum over nslices partials; also writes the
 // half-key row ids key1 = h*S + idx/S, key2 = h*S + idx%S per position.
+// If ds_dense != nullptr (bf16 [T*H, 2, S], pre-zeroed) the selected
+// half-key score gradients are also scattered densely (duplicates of one
+// (t,h) summed in lane order): ds_dense[th][0][a_j] += ds_j, [1][b_j] += ds_j.
 mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
                             const float* dw_part, int nslices, int64_t slice_stride,
-                            float* ds, int32_t* key1, int32_t* key2, cudaStream_t s);
+                            float* ds, int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,
+                            cudaStream_t s);
 
 // ------------------------------------------------------------ gate
 // z = y*silu(g); dy = dz*silu(g); dg = dz*y*silu'(g)   (elementwise, n elems)
@@ -106,7 +110,7 @@ mlStatus launch_scatter_rows(const int32_t* rows, const float* dV, const int32_t
 mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K,
                  const void* A, int64_t lda, const void* B, int64_t ldb,
                  void* C, int64_t ldc, mlDtype ab, bool c_f32,
-                 void* ws, size_t ws_bytes, cudaStream_t s);
+                 void* ws, size_t ws_bytes, cudaStream_t s, float beta = 0.f);
 constexpr size_t kGemmWs = size_t(32) << 20;
 
 // ------------------------------------------------------------ group layout

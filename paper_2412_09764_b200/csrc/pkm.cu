@@ -171,52 +171,159 @@ __device__ uint64_t warp_topk(const Gen& gen, int n, int k, uint32_t* hist, uint
   return warp_sort_desc(x);
 }
 
+// ---- fast exact top-k: threshold filter + exact select on the survivors.
+// theta = k-th largest of the union of every lane's 4 largest keys is a lower
+// bound of the true k-th largest key (the union is a subset of all keys), so
+// {keys >= theta} contains the top-k; it is typically ~k + a few elements.
+
+__device__ __forceinline__ void insert4(uint64_t key, uint64_t& t0, uint64_t& t1, uint64_t& t2,
+                                        uint64_t& t3) {
+  if (key > t3) {
+    if (key > t1) {
+      t3 = t2;
+      t2 = t1;
+      if (key > t0) { t1 = t0; t0 = key; } else { t1 = key; }
+    } else {
+      if (key > t2) { t3 = t2; t2 = key; } else { t3 = key; }
+    }
+  }
+}
+
+constexpr int kCandCap = 256;
+
+struct TopkSmem {           // per warp
+  uint32_t hist[256];
+  uint64_t sel[32];
+  uint64_t u128[128];
+  uint64_t cand[kCandCap];
+};
+
+// theta from the per-lane top-4 lists (t0 >= t1 >= t2 >= t3; 0 = empty)
+__device__ __forceinline__ uint64_t warp_theta(uint64_t t0, uint64_t t1, uint64_t t2, uint64_t t3,
+                                               int k, TopkSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  sm.u128[lane * 4 + 0] = t0;
+  sm.u128[lane * 4 + 1] = t1;
+  sm.u128[lane * 4 + 2] = t2;
+  sm.u128[lane * 4 + 3] = t3;
+  __syncwarp();
+  const uint64_t* u = sm.u128;
+  auto gen = [u](int e) { return u[e]; };
+  const uint64_t top = warp_topk(gen, 128, k, sm.hist, sm.sel);
+  return __shfl_sync(FULL, top, k - 1);
+}
+
+// append the keys >= theta of this round (one candidate per lane) to sm.cand
+__device__ __forceinline__ void append_cand(uint64_t key, bool sel, int& count, TopkSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(FULL, sel);
+  const int pos = count + __popc(m & ((1u << lane) - 1u));
+  if (sel && pos < kCandCap) sm.cand[pos] = key;
+  count += __popc(m);
+}
+
+__device__ __forceinline__ uint64_t select_cand(int count, int k, TopkSmem& sm) {
+  __syncwarp();
+  const uint64_t* c = sm.cand;
+  auto gen = [c](int e) { return c[e]; };
+  return warp_topk(gen, count, k, sm.hist, sm.sel);
+}
+
+// theta from every lane's maximum: the k largest lane maxima are k distinct
+// keys, so the k-th largest of them bounds the true k-th largest from below.
+__device__ __forceinline__ uint64_t warp_theta_max(uint64_t lane_max, int k) {
+  const uint64_t sorted = warp_sort_desc(lane_max);
+  return __shfl_sync(FULL, sorted, k - 1);
+}
+
 // one warp per (t, h, half) row of S scores
 __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int64_t rows, int S,
                                                         int k, int32_t* hI, float* hs) {
-  __shared__ uint32_t s_hist[8][256];
-  __shared__ uint64_t s_buf[8][32];
+  __shared__ TopkSmem s_sm[8];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = int64_t(blockIdx.x) * 8 + wid;
   if (row >= rows) return;
+  TopkSmem& sm = s_sm[wid];
   const float* sr = scores + row * S;
-  auto gen = [sr](int e) { return make_key(sr[e], uint32_t(e)); };
-  const uint64_t key = warp_topk(gen, S, k, s_hist[wid], s_buf[wid]);
+  uint64_t mx = 0;
+  for (int e = lane; e < S; e += 32) {
+    const uint64_t key = make_key(sr[e], uint32_t(e));
+    mx = key > mx ? key : mx;
+  }
+  const uint64_t theta = warp_theta_max(mx, k);
+  int count = 0;
+  for (int e0 = 0; e0 < S; e0 += 32) {
+    const int e = e0 + lane;
+    uint64_t key = 0;
+    if (e < S) key = make_key(sr[e], uint32_t(e));
+    append_cand(key, e < S && key >= theta, count, sm);
+  }
+  uint64_t key;
+  if (count <= kCandCap) {
+    key = select_cand(count, k, sm);
+  } else {  // pathological ties: exact select over the whole row
+    auto gen = [sr](int e) { return make_key(sr[e], uint32_t(e)); };
+    key = warp_topk(gen, S, k, sm.hist, sm.sel);
+  }
   if (lane < k) {
     hI[row * k + lane] = int32_t(key_id(key));
     hs[row * k + lane] = key_score(key);
   }
 }
 
-// one warp per (t, h): combine the two half lists, softmax
+// one warp per (t, h): combine the two half lists (k*k Cartesian sums), softmax
 __global__ void __launch_bounds__(256) combine_kernel(const int32_t* hI, const float* hs,
                                                       int64_t TH, int S, int k, int32_t* idx,
                                                       float* w, float* score) {
-  __shared__ uint32_t s_hist[8][256];
-  __shared__ uint64_t s_buf[8][32];
-  __shared__ float s_s[8][2][32];
-  __shared__ int32_t s_i[8][2][32];
+  __shared__ TopkSmem s_sm[8];
+  __shared__ float s_s1[8][32];
+  __shared__ int32_t s_i1[8][32];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t th = int64_t(blockIdx.x) * 8 + wid;
   if (th >= TH) return;
+  TopkSmem& sm = s_sm[wid];
+  float s2 = 0.f;
+  uint32_t i2 = 0;
   if (lane < k) {
-#pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      s_s[wid][hf][lane] = hs[(th * 2 + hf) * k + lane];
-      s_i[wid][hf][lane] = hI[(th * 2 + hf) * k + lane];
-    }
+    s_s1[wid][lane] = hs[(th * 2 + 0) * k + lane];
+    s_i1[wid][lane] = hI[(th * 2 + 0) * k + lane];
+    s2 = hs[(th * 2 + 1) * k + lane];
+    i2 = uint32_t(hI[(th * 2 + 1) * k + lane]);
   }
   __syncwarp();
-  const float* s1 = s_s[wid][0];
-  const float* s2 = s_s[wid][1];
-  const int32_t* I1 = s_i[wid][0];
-  const int32_t* I2 = s_i[wid][1];
-  auto gen = [=](int e) {
-    const int i = e / k, j = e - (e / k) * k;
-    const float c = s1[i] + s2[j];
-    return make_key(c, uint32_t(I1[i]) * uint32_t(S) + uint32_t(I2[j]));
+  // lane j owns column j of the k x k grid: c[i][j] = s1[i] + s2[j]
+  auto key_of = [&](int i) {
+    return make_key(s_s1[wid][i] + s2, uint32_t(s_i1[wid][i]) * uint32_t(S) + i2);
   };
-  const uint64_t key = warp_topk(gen, k * k, k, s_hist[wid], s_buf[wid]);
+  uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  if (lane < k)
+    for (int i = 0; i < k; ++i) insert4(key_of(i), t0, t1, t2, t3);
+  const uint64_t theta = warp_theta(t0, t1, t2, t3, k, sm);
+  int count = 0;
+  for (int i = 0; i < k; ++i) {
+    uint64_t key = 0;
+    if (lane < k) key = key_of(i);
+    append_cand(key, lane < k && key >= theta, count, sm);
+  }
+  uint64_t key;
+  if (count <= kCandCap) {
+    key = select_cand(count, k, sm);
+  } else {
+    const float* s1p = s_s1[wid];
+    const int32_t* i1p = s_i1[wid];
+    __shared__ float s_s2[8][32];
+    __shared__ int32_t s_i2[8][32];
+    s_s2[wid][lane] = s2;
+    s_i2[wid][lane] = int32_t(i2);
+    __syncwarp();
+    const float* s2p = s_s2[wid];
+    const int32_t* i2p = s_i2[wid];
+    auto gen = [=](int e) {
+      const int i = e / k, j = e - (e / k) * k;
+      return make_key(s1p[i] + s2p[j], uint32_t(i1p[i]) * uint32_t(S) + uint32_t(i2p[j]));
+    };
+    key = warp_topk(gen, k * k, k, sm.hist, sm.sel);
+  }
   const float sc = key_score(key);
   const float m = __shfl_sync(FULL, sc, 0);
   float ex = lane < k ? expf(sc - m) : 0.f;
@@ -235,7 +342,9 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
                                                           const float* dw_part, int ns,
                                                           int64_t sstride, int64_t TH, int H,
                                                           int S, int k, float* ds, int32_t* key1,
-                                                          int32_t* key2) {
+                                                          int32_t* key2, __nv_bfloat16* ds_dense) {
+  __shared__ int s_sub[8][2][32];
+  __shared__ float s_ds[8][32];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t th = int64_t(blockIdx.x) * 8 + wid;
   if (th >= TH) return;
@@ -251,10 +360,32 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
   float dot = wv * dwv;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(FULL, dot, off);
+  const float dsv = wv * (dwv - dot);
   if (lane < k) {
-    ds[o] = wv * (dwv - dot);
+    ds[o] = dsv;
     key1[o] = h * S + ix / S;
     key2[o] = h * S + ix % S;
+  }
+  if (ds_dense) {
+    // dense half-key gradients of this (t, h); a sub-key selected by several
+    // of the k pairs is summed in lane order (deterministic, no atomics)
+    s_sub[wid][0][lane] = lane < k ? ix / S : -1;
+    s_sub[wid][1][lane] = lane < k ? ix % S : -1;
+    s_ds[wid][lane] = dsv;
+    __syncwarp();
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int a = s_sub[wid][half][lane];
+      bool leader = lane < k;
+      float sum = 0.f;
+      for (int l = 0; l < k; ++l) {
+        if (s_sub[wid][half][l] == a) {
+          if (l < lane) leader = false;
+          sum += s_ds[wid][l];
+        }
+      }
+      if (leader) ds_dense[(th * 2 + half) * S + a] = __float2bfloat16_rn(sum);
+    }
   }
 }
 
@@ -298,11 +429,11 @@ mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const f
 
 mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
                             const float* dw_part, int nslices, int64_t slice_stride, float* ds,
-                            int32_t* key1, int32_t* key2, cudaStream_t s) {
+                            int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense, cudaStream_t s) {
   const int64_t TH = int64_t(sh.T) * sh.H;
   if (TH <= 0) return ML_OK;
   softmax_bwd_kernel<<<unsigned((TH + 7) / 8), 256, 0, s>>>(
-      idx, w, dw_part, nslices, slice_stride, TH, sh.H, sh.S, sh.k, ds, key1, key2);
+      idx, w, dw_part, nslices, slice_stride, TH, sh.H, sh.S, sh.k, ds, key1, key2, ds_dense);
   ML_LAUNCH_CHECK("softmax_bwd");
   return ML_OK;
 }

@@ -228,7 +228,9 @@ def test_pkm_topk_bwd(dtype, T, H, S, Dk, k):
     rdq, rdK1, rdK2, _ = opkm.pkm_bwd(q64, K164, K264, ridx, rw, dw)
     dq, dK1, dK2 = ops().pkm_topk_bwd(dev(q, dtype), dev(K1, dtype), dev(K2, dtype),
                                       dev(ridx.astype(np.int32)), dev(rw.astype(np.float32)), dev(dw))
-    tol = TOL["f32"]
+    # bf16: the dense path rounds the selected score gradients to bf16 before
+    # the tensor-core products; fp32 inputs stay fp32 end to end
+    tol = TOL[dtype]
     assert_close(host(dq), rdq, tol, "dq")
     assert_close(host(dK1), rdK1, tol, "dK1")
     assert_close(host(dK2), rdK2, tol, "dK2")
