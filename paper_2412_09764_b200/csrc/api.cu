@@ -152,20 +152,19 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
     timing_mark("memset", st);
     ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, b.ds_dense, st));
     const int64_t lds = int64_t(s.H) * 2 * s.S;  // row pitch of ds_dense per token
-    for (int h = 0; h < s.H; ++h) {
-      for (int half = 0; half < 2; ++half) {
-        const __nv_bfloat16* A = b.ds_dense + (int64_t(h) * 2 + half) * s.S;
-        const char* Kh = static_cast<const char*>(half ? K2 : K1) + int64_t(h) * s.S * Dh * 2;
-        const char* qh = static_cast<const char*>(q) + (int64_t(h) * s.Dk + int64_t(half) * Dh) * 2;
-        float* dKh = (half ? dK2 : dK1) + int64_t(h) * s.S * Dh;
-        // dq[t, h, half] = ds[t, h, half, :] K_half[h]          [T, Dh]
-        ML_TRY(gemm_rm(false, false, s.T, Dh, s.S, A, lds, Kh, Dh,
-                       dq + int64_t(h) * s.Dk + int64_t(half) * Dh, int64_t(s.H) * s.Dk, ML_BF16,
-                       true, b.gemm_ws, kGemmWs, st));
-        // dK_half[h] += ds[:, h, half, :]^T q_half[:, h]        [S, Dh]
-        ML_TRY(gemm_rm(true, false, s.S, Dh, s.T, A, lds, qh, int64_t(s.H) * s.Dk, dKh, Dh, ML_BF16,
-                       true, b.gemm_ws, kGemmWs, st, 1.f));
-      }
+    for (int half = 0; half < 2; ++half) {        // one strided-batched GEMM over heads each
+      const __nv_bfloat16* A = b.ds_dense + int64_t(half) * s.S;
+      const void* Kh = half ? K2 : K1;
+      const char* qh = static_cast<const char*>(q) + int64_t(half) * Dh * 2;
+      float* dKh = half ? dK2 : dK1;
+      // dq[t, h, half] = ds[t, h, half, :] K_half[h]          [T, Dh] per head
+      ML_TRY(gemm_rm_batched(false, false, s.T, Dh, s.S, A, lds, 2 * int64_t(s.S), Kh, Dh,
+                             int64_t(s.S) * Dh, dq + int64_t(half) * Dh, int64_t(s.H) * s.Dk, s.Dk,
+                             s.H, ML_BF16, true, b.gemm_ws, kGemmWs, st));
+      // dK_half[h] += ds[:, h, half, :]^T q_half[:, h]        [S, Dh] per head
+      ML_TRY(gemm_rm_batched(true, false, s.S, Dh, s.T, A, lds, 2 * int64_t(s.S), qh,
+                             int64_t(s.H) * s.Dk, s.Dk, dKh, Dh, int64_t(s.S) * Dh, s.H, ML_BF16,
+                             true, b.gemm_ws, kGemmWs, st, 1.f));
     }
     return ML_OK;
   }

@@ -88,6 +88,14 @@ mlStatus launch_scatter_rows(const int32_t* rows, const float* dV, const int32_t
 mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const void* A,
                  int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, mlDtype ab,
                  bool c_f32, void* ws, size_t ws_bytes, cudaStream_t s, float beta) {
+  return gemm_rm_batched(transA, transB, M, N, K, A, lda, 0, B, ldb, 0, C, ldc, 0, 1, ab, c_f32, ws,
+                         ws_bytes, s, beta);
+}
+
+mlStatus gemm_rm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const void* A,
+                         int64_t lda, int64_t strideA, const void* B, int64_t ldb, int64_t strideB,
+                         void* C, int64_t ldc, int64_t strideC, int batch, mlDtype ab, bool c_f32,
+                         void* ws, size_t ws_bytes, cudaStream_t s, float beta) {
   if (M <= 0 || N <= 0) return ML_OK;
   cublasLtHandle_t h = lt_handle();
   if (!h) return fail(ML_ERR_CUDA, "cublasLtCreate failed");
@@ -112,6 +120,18 @@ mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, cons
     ck(cublasLtMatrixLayoutCreate(&l1, tab, transB ? K : N, transB ? N : K, ldb), "l1");
     ck(cublasLtMatrixLayoutCreate(&l2, tab, transA ? M : K, transA ? K : M, lda), "l2");
     ck(cublasLtMatrixLayoutCreate(&lc, tc, N, M, ldc), "lc");
+    if (batch > 1 && st == ML_OK) {
+      const int32_t bc = batch;
+      ck(cublasLtMatrixLayoutSetAttribute(l1, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc)), "b1");
+      ck(cublasLtMatrixLayoutSetAttribute(l2, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc)), "b2");
+      ck(cublasLtMatrixLayoutSetAttribute(lc, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc)), "bc");
+      ck(cublasLtMatrixLayoutSetAttribute(l1, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &strideB,
+                                          sizeof(strideB)), "s1");
+      ck(cublasLtMatrixLayoutSetAttribute(l2, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &strideA,
+                                          sizeof(strideA)), "s2");
+      ck(cublasLtMatrixLayoutSetAttribute(lc, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &strideC,
+                                          sizeof(strideC)), "sc");
+    }
   }
   cublasLtMatmulPreference_t pref = nullptr;
   cublasLtMatmulHeuristicResult_t heur = {};
@@ -123,10 +143,10 @@ mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, cons
                                             sizeof(wsb)), "pref ws");
     // heuristic results cached per problem signature (the query costs tens of us)
     static std::mutex mu;
-    static std::map<std::tuple<int, int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, size_t, int>,
+    static std::map<std::tuple<int, int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, size_t, int, int>,
                     cublasLtMatmulHeuristicResult_t> cache;
     const auto key = std::make_tuple(int(transA), int(transB), M, N, K, lda, ldb, ldc, int(ab),
-                                     int(c_f32), ws_bytes, int(beta != 0.f));
+                                     int(c_f32), ws_bytes, int(beta != 0.f), batch);
     {
       std::lock_guard<std::mutex> lk(mu);
       auto it = cache.find(key);

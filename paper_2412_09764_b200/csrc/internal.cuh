@@ -111,6 +111,12 @@ mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K,
                  const void* A, int64_t lda, const void* B, int64_t ldb,
                  void* C, int64_t ldc, mlDtype ab, bool c_f32,
                  void* ws, size_t ws_bytes, cudaStream_t s, float beta = 0.f);
+// Strided-batched variant (element strides between consecutive batch items).
+mlStatus gemm_rm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t K,
+                         const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                         int64_t strideB, void* C, int64_t ldc, int64_t strideC, int batch,
+                         mlDtype ab, bool c_f32, void* ws, size_t ws_bytes, cudaStream_t s,
+                         float beta = 0.f);
 constexpr size_t kGemmWs = size_t(32) << 20;
 
 // ------------------------------------------------------------ group layout
