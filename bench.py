@@ -171,19 +171,19 @@ def run_ours(args, cfg, world, rank, local):
         from paper_2412_09764_b200 import group
         layer = group.GroupMemoryLayer(pg, k=k, mode=args.mode)
 
-        def step():
+        def step(inp=t):
             dK1.zero_()
             dK2.zero_()
-            out, saved = layer.forward(t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"])
-            g = layer.backward(t["dout"], saved, dK1, dK2)
+            out, saved = layer.forward(inp["x"], inp["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"])
+            g = layer.backward(inp["dout"], saved, dK1, dK2)
             return out, g
     else:
-        def step():
+        def step(inp=t):
             dK1.zero_()
             dK2.zero_()
-            out, saved = ops.memory_layer_fwd(t["x"], t["q"], t["K1"], t["K2"], t["V"],
+            out, saved = ops.memory_layer_fwd(inp["x"], inp["q"], t["K1"], t["K2"], t["V"],
                                               t["W1"], t["W2"], k)
-            g = ops.memory_layer_bwd(t["dout"], t["x"], t["q"], t["K1"], t["K2"], t["V"],
+            g = ops.memory_layer_bwd(inp["dout"], inp["x"], inp["q"], t["K1"], t["K2"], t["V"],
                                      t["W1"], t["W2"], saved, dK1=dK1, dK2=dK2, bufs=bufs)
             return out, g
 
@@ -233,24 +233,48 @@ def run_ours(args, cfg, world, rank, local):
 
 
 def run_e2e(args, t, step, stream, torch, cfg, G, world):
+    """End to end through the public API with HOST buffers: every step copies
+    its inputs (q, x, dout) from pinned host memory and copies the result
+    `out` back.  The copies run on a copy stream, double-buffered, so step
+    i+1's upload overlaps step i's compute (the intended way to feed the
+    layer); all of it is inside the timed region."""
     names = ("q", "x", "dout")
     hostbufs = {n: t[n].cpu().pin_memory() for n in names}
-    out_host = None
     h2d = sum(hostbufs[n].numel() * hostbufs[n].element_size() for n in names)
+    dbuf = [{n: torch.empty_like(t[n]) for n in names} for _ in range(2)]
+    copy = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_done:
+        e.record(stream)
+    out_host = None
     torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n = max(3, args.steps // 2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(n):
-        for nm in names:
-            t[nm].copy_(hostbufs[nm], non_blocking=True)
-        out, g = step()
+    copy.wait_event(e0)
+    for i in range(n):
+        b = i % 2
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev_done[b])             # buffer b no longer read by step i-2
+            for nm in names:
+                dbuf[b][nm].copy_(hostbufs[nm], non_blocking=True)
+            ev_in[b].record(copy)
+        stream.wait_event(ev_in[b])
+        out, g = step({**t, **dbuf[b]})
+        ev_done[b].record(stream)
         if out_host is None:
             out_host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-        out_host.copy_(out, non_blocking=True)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev_done[b])
+            out.record_stream(copy)
+            out_host.copy_(out, non_blocking=True)
+    ev_last = torch.cuda.Event()
+    ev_last.record(copy)
+    stream.wait_event(ev_last)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
@@ -261,7 +285,8 @@ def run_e2e(args, t, step, stream, torch, cfg, G, world):
         ms = float(m.item())
     d2h = out_host.numel() * out_host.element_size()
     return {"value": cfg["T"] * G / (ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "note": "pinned host inputs uploaded on a copy stream, double-buffered against compute"}
 
 
 # ------------------------------------------------- roofline accounting
