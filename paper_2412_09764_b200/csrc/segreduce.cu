@@ -69,17 +69,36 @@ struct TransposeReduce<1, O> {
   }
 };
 
-template <int VEC>
+__device__ __forceinline__ void st_v8(float* o, const float* a) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o),
+               "r"(__float_as_uint(a[0])), "r"(__float_as_uint(a[1])), "r"(__float_as_uint(a[2])),
+               "r"(__float_as_uint(a[3])), "r"(__float_as_uint(a[4])), "r"(__float_as_uint(a[5])),
+               "r"(__float_as_uint(a[6])), "r"(__float_as_uint(a[7]))
+               : "memory");
+}
+// Write (or add into) this thread's VEC fp32 outputs; with bf16 sources each
+// thread owns 32 contiguous bytes: one 256-bit store (full sectors).
+template <int VEC, bool WIDE = true>
 __device__ __forceinline__ void store_vec(float* o, const float* acc, bool dense) {
-#pragma unroll
-  for (int v = 0; v < VEC; v += 4) {
-    float4 a = make_float4(acc[v], acc[v + 1], acc[v + 2], acc[v + 3]);
+  if constexpr (VEC == 8 && WIDE) {
     if (dense) {
-      const float4 b = *reinterpret_cast<const float4*>(o + v);
-      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-      *reinterpret_cast<float4*>(o + v) = a;
+      const float4 b0 = *reinterpret_cast<const float4*>(o);
+      const float4 b1 = *reinterpret_cast<const float4*>(o + 4);
+      float c[8] = {acc[0] + b0.x, acc[1] + b0.y, acc[2] + b0.z, acc[3] + b0.w,
+                    acc[4] + b1.x, acc[5] + b1.y, acc[6] + b1.z, acc[7] + b1.w};
+      st_v8(o, c);
     } else {
-      __stcs(reinterpret_cast<float4*>(o + v), a);  // streaming: keep dy in L2
+      st_v8(o, acc);
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < VEC; v += 4) {
+      float4 a = make_float4(acc[v], acc[v + 1], acc[v + 2], acc[v + 3]);
+      if (dense) {
+        const float4 b = *reinterpret_cast<const float4*>(o + v);
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      *reinterpret_cast<float4*>(o + v) = a;
     }
   }
 }
@@ -125,7 +144,7 @@ __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VE
         }
       }
     }
-    if (act) store_vec<VEC>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
+    if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
   }
   __syncthreads();
 }
