@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && echo plain_ok && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"seg_kernel|bag_fwd_kernel|pkm_scores_tc|half_topk|combine|sort_scatter|sort_hist" -s 20 -c 20 -o gpurun_out/prof_r01 $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu_exit=$?
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"seg_kernel" -s 3 -c 1 -o gpurun_out/prof_r01b $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu_exit=$?
 tail -2 gpurun_out/ncu_full.log
