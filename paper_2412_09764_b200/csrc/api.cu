@@ -5,6 +5,8 @@
 #include "internal.cuh"
 
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cstdio>
 #include <exception>
@@ -30,6 +32,39 @@ int num_sms() {
       n = 148;
   }
   return n;
+}
+
+// ---- auxiliary streams: independent parts of a layer call (the value-row
+// sort, the gate weight-gradient GEMMs, the gate projection) run on
+// library-owned streams forked from / joined into the caller's stream with
+// events, so tensor-core GEMMs overlap the HBM-bound bag kernels.  One set
+// per caller stream (calls on different streams never share them).
+struct Aux {
+  cudaStream_t s[2];
+  cudaEvent_t ev[8];
+};
+static mlStatus aux_for(cudaStream_t caller, Aux** out) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, Aux*> m;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = m.find(caller);
+  if (it != m.end()) {
+    *out = it->second;
+    return ML_OK;
+  }
+  Aux* a = new Aux();
+  for (auto& x : a->s) ML_CUDA_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  for (auto& e : a->ev) ML_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  m[caller] = a;
+  *out = a;
+  return ML_OK;
+}
+// make `to` wait for all work enqueued so far on `from`
+static mlStatus stream_dep(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
+  ML_CUDA_TRY(cudaEventRecord(ev, from));
+  ML_CUDA_TRY(cudaStreamWaitEvent(to, ev, 0));
+  timing_mark(nullptr, to);
+  return ML_OK;
 }
 
 static int ceil_log2(int64_t n) {
@@ -195,17 +230,24 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
   return ML_OK;
 }
 
-static mlStatus bag_bwd_core(const mlBagShape& s, const void* V, const int32_t* idx, const float* w,
-                             const void* dy, int32_t* rows, float* dV, int32_t* U, BagBwdBufs& b,
-                             cudaStream_t st) {
+// the "inverse token_id -> embedding_id map": sort + runs (needs idx only)
+static mlStatus bag_bwd_prepare(const mlBagShape& s, const int32_t* idx, int32_t* rows, int32_t* U,
+                                BagBwdBufs& b, int32_t** skey, int32_t** spos, cudaStream_t st) {
   const int64_t P = int64_t(s.T) * s.B;
   if (P == 0) {
     ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
     return ML_OK;
   }
-  int32_t *skey, *spos;
-  ML_TRY(sort_pairs(idx, P, ceil_log2(s.N), b.sort, &skey, &spos, st));
-  ML_TRY(find_runs(skey, P, b.runs, rows, U, st));
+  ML_TRY(sort_pairs(idx, P, ceil_log2(s.N), b.sort, skey, spos, st));
+  ML_TRY(find_runs(*skey, P, b.runs, rows, U, st));
+  return ML_OK;
+}
+
+static mlStatus bag_bwd_reduce(const mlBagShape& s, const void* V, const float* w, const void* dy,
+                               float* dV, BagBwdBufs& b, int32_t* skey, int32_t* spos,
+                               cudaStream_t st) {
+  const int64_t P = int64_t(s.T) * s.B;
+  if (P == 0) return ML_OK;
   SegArgs g;
   g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = w;
   g.src = dy; g.lds = s.dv; g.src_col0 = 0; g.B = s.B;
@@ -215,6 +257,14 @@ static mlStatus bag_bwd_core(const mlBagShape& s, const void* V, const int32_t* 
   g.name = "embbag_bwd_segreduce";
   ML_TRY(launch_segreduce(g, st));
   return ML_OK;
+}
+
+static mlStatus bag_bwd_core(const mlBagShape& s, const void* V, const int32_t* idx, const float* w,
+                             const void* dy, int32_t* rows, float* dV, int32_t* U, BagBwdBufs& b,
+                             cudaStream_t st) {
+  int32_t *skey = nullptr, *spos = nullptr;
+  ML_TRY(bag_bwd_prepare(s, idx, rows, U, b, &skey, &spos, st));
+  return bag_bwd_reduce(s, V, w, dy, dV, b, skey, spos, st);
 }
 
 }  // namespace ml
@@ -418,7 +468,7 @@ static void layer_fwd_carve(Carver& c, const mlLayerShape& s, LayerFwdBufs& b) {
 }
 
 struct LayerBwdBufs {
-  BagBwdBufs bag; PkmBwdBufs pkm; void *dz, *z, *dy, *dg, *gemm_ws;
+  BagBwdBufs bag; PkmBwdBufs pkm; void *dz, *z, *dy, *dg, *gemm_ws, *gemm_ws2;
 };
 static void layer_bwd_carve(Carver& c, const mlLayerShape& s, LayerBwdBufs& b) {
   const int64_t act = int64_t(s.pkm.T) * s.dv * int64_t(dtype_size(s.pkm.dtype));
@@ -429,6 +479,7 @@ static void layer_bwd_carve(Carver& c, const mlLayerShape& s, LayerBwdBufs& b) {
   b.dy = c.take<char>(act);
   b.dg = c.take<char>(act);
   b.gemm_ws = c.take<char>(kGemmWs);
+  b.gemm_ws2 = c.take<char>(kGemmWs);
 }
 
 mlStatus memory_layer_fwd_workspace(const mlLayerShape* shape, size_t* bytes) {
@@ -462,6 +513,14 @@ mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* 
   cudaStream_t st = S(stream);
   const int T = s.pkm.T;
   timing_mark(nullptr, st);
+  Aux* aux = nullptr;
+  if (s.gated) {
+    // g = x W1 [T, dv] on an auxiliary stream, concurrent with the lookup
+    ML_TRY(aux_for(st, &aux));
+    ML_TRY(stream_dep(st, aux->s[0], aux->ev[0]));
+    ML_TRY(gemm_rm(false, false, T, s.dv, s.D, x, s.D, W1, s.dv, g_saved, s.dv, s.pkm.dtype, false,
+                   b.gemm_ws, kGemmWs, aux->s[0]));
+  }
   ML_TRY(pkm_fwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, nullptr, b.pkm, st));
   BagFwdArgs a;
   a.V = V; a.ldv = s.dv; a.N = s.N;
@@ -476,9 +535,7 @@ mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* 
                                   cudaMemcpyDeviceToDevice, st));
     return check_index_flag(st);
   }
-  // g = x W1  [T, dv]
-  ML_TRY(gemm_rm(false, false, T, s.dv, s.D, x, s.D, W1, s.dv, g_saved, s.dv, s.pkm.dtype, false,
-                 b.gemm_ws, kGemmWs, st));
+  ML_TRY(stream_dep(aux->s[0], st, aux->ev[1]));   // join: g ready
   // z = (sum_j w_j V[idx_j]) * silu(g); y saved
   a.out = b.z; a.gate = g_saved; a.y_ungated = y_saved;
   ML_TRY(launch_bag_fwd(a, st));
@@ -529,27 +586,36 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
   const int T = s.pkm.T;
   const mlDtype dt = s.pkm.dtype;
   const void* dy = dout;
+  const mlBagShape bs = bag_of(s);
   timing_mark(nullptr, st);
+  Aux* aux = nullptr;
+  ML_TRY(aux_for(st, &aux));
+  // aux 0: the value-row sort + runs need only the saved indices
+  ML_TRY(stream_dep(st, aux->s[0], aux->ev[0]));
+  int32_t *skey = nullptr, *spos = nullptr;
+  ML_TRY(bag_bwd_prepare(bs, idx_saved, dV_rows, U, b.bag, &skey, &spos, aux->s[0]));
   if (s.gated) {
-    // dz = dout W2^T
+    // dz = dout W2^T ; elementwise gate backward -> z, dy, dg
     ML_TRY(gemm_rm(false, true, T, s.dv, s.D, dout, s.D, W2, s.D, b.dz, s.dv, dt, false, b.gemm_ws,
                    kGemmWs, st));
     ML_TRY(launch_gate_bwd(b.dz, g_saved, y_saved, b.z, b.dy, b.dg, int64_t(T) * s.dv, dt, st));
-    // dW2 = z^T dout ; dW1 = x^T dg ; dx = dg W1^T
-    ML_TRY(gemm_rm(true, false, s.dv, s.D, T, b.z, s.dv, dout, s.D, dW2, s.D, dt, true, b.gemm_ws,
-                   kGemmWs, st));
-    ML_TRY(gemm_rm(true, false, s.D, s.dv, T, x, s.D, b.dg, s.dv, dW1, s.dv, dt, true, b.gemm_ws,
-                   kGemmWs, st));
-    ML_TRY(gemm_rm(false, true, T, s.D, s.dv, b.dg, s.dv, W1, s.dv, dx, s.D, dt, false, b.gemm_ws,
-                   kGemmWs, st));
+    // aux 1: dW2 = z^T dout ; dW1 = x^T dg ; dx = dg W1^T  (overlap the bag backward)
+    ML_TRY(stream_dep(st, aux->s[1], aux->ev[1]));
+    ML_TRY(gemm_rm(true, false, s.dv, s.D, T, b.z, s.dv, dout, s.D, dW2, s.D, dt, true, b.gemm_ws2,
+                   kGemmWs, aux->s[1]));
+    ML_TRY(gemm_rm(true, false, s.D, s.dv, T, x, s.D, b.dg, s.dv, dW1, s.dv, dt, true, b.gemm_ws2,
+                   kGemmWs, aux->s[1]));
+    ML_TRY(gemm_rm(false, true, T, s.D, s.dv, b.dg, s.dv, W1, s.dv, dx, s.D, dt, false, b.gemm_ws2,
+                   kGemmWs, aux->s[1]));
     dy = b.dy;
   }
-  const mlBagShape bs = bag_of(s);
-  ML_TRY(bag_bwd_core(bs, V, idx_saved, w_saved, dy, dV_rows, dV, U, b.bag, st));
+  ML_TRY(stream_dep(aux->s[0], st, aux->ev[2]));     // sorted runs ready
+  ML_TRY(bag_bwd_reduce(bs, V, w_saved, dy, dV, b.bag, skey, spos, st));
   const int ns = seg_slices(s.dv, dt);
   const int64_t P = int64_t(T) * bs.B;
   ML_TRY(pkm_bwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, b.bag.dw_part, ns, P, dq, dK1, dK2,
                       b.pkm, st));
+  if (s.gated) ML_TRY(stream_dep(aux->s[1], st, aux->ev[3]));   // join the gate GEMMs
   if (dw_out) ML_TRY(launch_sum_slices(b.bag.dw_part, ns, P, dw_out, st));
   return check_index_flag(st);
   ML_API_END
