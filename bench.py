@@ -242,7 +242,9 @@ def run_e2e(args, t, step, stream, torch, cfg, G, world):
     hostbufs = {n: t[n].cpu().pin_memory() for n in names}
     h2d = sum(hostbufs[n].numel() * hostbufs[n].element_size() for n in names)
     dbuf = [{n: torch.empty_like(t[n]) for n in names} for _ in range(2)]
-    copy = torch.cuda.Stream()
+    copy = torch.cuda.Stream()      # uploads
+    down = torch.cuda.Stream()      # result downloads (separate: a queued download must not
+                                    # hold back the next upload)
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(2)]
     for e in ev_done:
@@ -268,12 +270,12 @@ def run_e2e(args, t, step, stream, torch, cfg, G, world):
         ev_done[b].record(stream)
         if out_host is None:
             out_host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-        with torch.cuda.stream(copy):
-            copy.wait_event(ev_done[b])
-            out.record_stream(copy)
+        with torch.cuda.stream(down):
+            down.wait_event(ev_done[b])
+            out.record_stream(down)
             out_host.copy_(out, non_blocking=True)
     ev_last = torch.cuda.Event()
-    ev_last.record(copy)
+    ev_last.record(down)
     stream.wait_event(ev_last)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -286,7 +288,8 @@ def run_e2e(args, t, step, stream, torch, cfg, G, world):
     d2h = out_host.numel() * out_host.element_size()
     return {"value": cfg["T"] * G / (ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "note": "pinned host inputs uploaded on a copy stream, double-buffered against compute"}
+            "note": "pinned host inputs uploaded on a copy stream, double-buffered against compute; "
+                    "results downloaded on a second copy stream"}
 
 
 # ------------------------------------------------- roofline accounting
