@@ -282,3 +282,58 @@ def test_memory_layer_fwd_bwd(dtype, T, H, S, Dk, k, dv, D, gated):
         assert_close(host(g["dx"]), r["dx"], tol, "dx")
         assert_close(host(g["dW1"]), r["dW1"], tol, "dW1")
         assert_close(host(g["dW2"]), r["dW2"], tol, "dW2")
+
+
+# ------------------------------------------------------------ edge cases
+def test_out_of_range_index_reported_under_check_mode():
+    """S:233 index error: with ML_CHECK_INDICES=1 an index >= N is reported
+    as ML_ERR_INDEX (clamped to row 0 / weight 0 on the device, no fault)."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import numpy as np, torch
+        from paper_2412_09764_b200 import ops, MemlayerError
+        V = torch.ones((64, 32), device="cuda")
+        idx = torch.tensor([[1, 2], [3, 64]], dtype=torch.int32, device="cuda")
+        w = torch.ones((2, 2), device="cuda")
+        try:
+            ops.embbag_fwd(V, idx, w)
+            print("NO_ERROR")
+        except MemlayerError as e:
+            print("STATUS", e.status)
+        idx[1, 1] = 5
+        y = ops.embbag_fwd(V, idx, w)
+        print("OK_AFTER", float(y.sum()))
+    """)
+    env = dict(__import__("os").environ, ML_CHECK_INDICES="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert "STATUS 3" in r.stdout, r.stdout + r.stderr
+    assert "OK_AFTER 128.0" in r.stdout, r.stdout + r.stderr
+
+
+def test_empty_batches():
+    o = ops()
+    V = torch.ones((64, 32), device="cuda")
+    idx = torch.zeros((0, 4), dtype=torch.int32, device="cuda")
+    w = torch.zeros((0, 4), device="cuda")
+    rows, dV, U, dw = o.embbag_bwd(V, idx, w, torch.zeros((0, 32), device="cuda"), sync=False)
+    assert int(U.item()) == 0 and dw.shape == (0, 4)
+    q = torch.zeros((0, 1, 32), device="cuda")
+    K = torch.zeros((1, 32, 16), device="cuda")
+    i2, w2 = o.pkm_topk(q, K, K, 4)
+    assert i2.shape == (0, 1, 4)
+
+
+def test_k_equals_S_and_k1_layer_corner():
+    """k = S (every half key selected) and k = 1 (w = 1, dq = dK = 0)."""
+    o = ops()
+    T, H, S, Dk = 40, 2, 32, 32
+    q, K1, K2 = _pkm_inputs(13, T, H, S, Dk, "f32", gen.CLS_CONTINUOUS)
+    q64, K164, K264 = (a.astype(np.float64) for a in (q, K1, K2))
+    idx, w = o.pkm_topk(dev(q), dev(K1), dev(K2), 32)
+    ridx, _, rw = opkm.pkm_lookup(q64, K164, K264, 32)
+    compare_topk(host(idx), ridx, q64, K164, K264)
+    idx1, w1 = o.pkm_topk(dev(q), dev(K1), dev(K2), 1)
+    dq, dK1, dK2 = o.pkm_topk_bwd(dev(q), dev(K1), dev(K2), idx1, w1,
+                                  dev(gen.tensor(13, "dout", (T, H, 1))))
+    assert torch.all(dq == 0) and torch.all(dK1 == 0) and torch.all(dK2 == 0)
