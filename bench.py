@@ -327,7 +327,7 @@ def roofline(res, cfg, G, peaks):
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if dom and os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(dom)
+            traffic = json.load(open(tf)).get(cfg.get("name", ""), {}).get(dom)
         except Exception:
             traffic = None
     if dom in per:
@@ -441,7 +441,7 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     cfg_name = args.config or "c2"
-    cfg = CONFIGS[cfg_name]
+    cfg = dict(CONFIGS[cfg_name], name=cfg_name)
 
     if args.impl == "reference":
         line = run_reference(args, cfg, world, rank)
