@@ -146,6 +146,25 @@ mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, 
                     const void* dy, int32_t* rows, float* dV, int32_t* U, float* dw,
                     void* ws, size_t ws_bytes, void* stream);
 
+/* With V == NULL and dw == NULL only the value gradient is computed (rows /
+ * dV / U), as in the strategy comparison below. */
+
+/* Controls: the other two backward strategies of PAPER.md §3.1.4,
+ * for the strategy benchmark.  Both ACCUMULATE
+ * dV_dense[idx[p],:] += w[p] * dy[t(p),:] into a dense fp32 [N,dv] table the
+ * caller zeroed; neither is bitwise deterministic (order of the adds).
+ *   embbag_bwd_atomics: "accumulation via atomic additions" (vector float
+ *     atomics, one team of threads per token).
+ *   embbag_bwd_lock: "row-level atomic lock where we amortize the cost of
+ *     memory lock over the embedding dimension": one CTA per token acquires a
+ *     spin lock on each destination row, adds the whole row, releases.
+ *     locks: int32 [embbag_bwd_lock_count(shape)] zero-initialised; left zero. */
+mlStatus embbag_bwd_atomics(const mlBagShape* shape, const int32_t* idx, const float* w,
+                            const void* dy, float* dV_dense, void* stream);
+mlStatus embbag_bwd_lock(const mlBagShape* shape, const int32_t* idx, const float* w, const void* dy,
+                         float* dV_dense, int32_t* locks, void* stream);
+int64_t embbag_bwd_lock_count(const mlBagShape* shape);
+
 /* dV_dense[rows[i],:] += dV[i,:] for i < *U (unique rows: no atomics).
  * dV_dense [N,dv] fp32. */
 mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const float* dV,

@@ -60,6 +60,9 @@ SIGNATURES = {
     "embbag_bwd_workspace": [C.POINTER(BagShape), C.POINTER(SZ)],
     "embbag_bwd": [C.POINTER(BagShape), P, P, P, P, P, P, P, P, P, SZ, P],
     "embbag_grad_apply": [C.POINTER(BagShape), P, P, P, P, P],
+    "embbag_bwd_atomics": [C.POINTER(BagShape), P, P, P, P, P],
+    "embbag_bwd_lock": [C.POINTER(BagShape), P, P, P, P, P, P],
+    "embbag_bwd_lock_count": [C.POINTER(BagShape)],
     "memory_layer_fwd_workspace": [C.POINTER(LayerShape), C.POINTER(SZ)],
     "memory_layer_fwd": [C.POINTER(LayerShape)] + [P] * 13 + [SZ, P],
     "memory_layer_bwd_workspace": [C.POINTER(LayerShape), C.POINTER(SZ)],
@@ -71,7 +74,7 @@ SIGNATURES = {
 }
 _RESTYPES = {"ml_last_error": C.c_char_p, "ml_version": C.c_int, "ml_launch_count": C.c_uint64,
              "ml_device_info": C.c_int, "ml_timing_enable": None, "ml_timing_reset": None,
-             "ml_timing_report": C.c_size_t}
+             "ml_timing_report": C.c_size_t, "embbag_bwd_lock_count": C.c_int64}
 
 _lib = None
 

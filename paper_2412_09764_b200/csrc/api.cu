@@ -412,7 +412,9 @@ mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, 
     ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), S(stream)));
     return ML_OK;
   }
-  ML_TRY(check_ptrs({V, idx, w, dy, rows, dV, dw, ws}));
+  ML_TRY(check_ptrs({idx, w, dy, rows, dV, ws}));
+  if ((V == nullptr) != (dw == nullptr)) return fail(ML_ERR_ARG, "embbag_bwd: V and dw are both set or both NULL");
+  if (V) ML_TRY(check_ptrs({V, dw}));
   size_t need = 0;
   ML_TRY(embbag_bwd_workspace(shape, &need));
   if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_bwd: workspace too small");
@@ -422,7 +424,37 @@ mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, 
   timing_mark(nullptr, S(stream));
   ML_TRY(bag_bwd_core(*shape, V, idx, w, dy, rows, dV, U, b, S(stream)));
   const int64_t P = int64_t(shape->T) * shape->B;
-  ML_TRY(launch_sum_slices(b.dw_part, seg_slices(shape->dv, shape->dtype), P, dw, S(stream)));
+  if (dw) ML_TRY(launch_sum_slices(b.dw_part, seg_slices(shape->dv, shape->dtype), P, dw, S(stream)));
+  return check_index_flag(S(stream));
+  ML_API_END
+}
+
+mlStatus embbag_bwd_atomics(const mlBagShape* shape, const int32_t* idx, const float* w,
+                            const void* dy, float* dV_dense, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (shape->T == 0) return ML_OK;
+  ML_TRY(check_ptrs({idx, w, dy, dV_dense}));
+  timing_mark(nullptr, S(stream));
+  ML_TRY(launch_bag_bwd_ctrl(0, *shape, idx, w, dy, dV_dense, nullptr, S(stream)));
+  return check_index_flag(S(stream));
+  ML_API_END
+}
+
+int64_t embbag_bwd_lock_count(const mlBagShape* shape) {
+  if (!shape || shape->N < 1) return -1;
+  const int64_t vu = int64_t(shape->dv) * int64_t(dtype_size(shape->dtype)) / 16;
+  return (vu > 256 ? vu / 256 : 1) * shape->N;
+}
+
+mlStatus embbag_bwd_lock(const mlBagShape* shape, const int32_t* idx, const float* w, const void* dy,
+                         float* dV_dense, int32_t* locks, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (shape->T == 0) return ML_OK;
+  ML_TRY(check_ptrs({idx, w, dy, dV_dense, locks}));
+  timing_mark(nullptr, S(stream));
+  ML_TRY(launch_bag_bwd_ctrl(1, *shape, idx, w, dy, dV_dense, locks, S(stream)));
   return check_index_flag(S(stream));
   ML_API_END
 }

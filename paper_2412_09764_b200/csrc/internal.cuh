@@ -119,6 +119,11 @@ mlStatus gemm_rm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t
                          float beta = 0.f);
 constexpr size_t kGemmWs = size_t(32) << 20;
 
+// ------------------------------------------------ backward controls (f3)
+// strategy 0 = "atomics", 1 = "lock" (§3.1.4); dense fp32 dV, accumulate
+mlStatus launch_bag_bwd_ctrl(int strategy, const mlBagShape& sh, const int32_t* idx, const float* w,
+                             const void* dy, float* dV, int* locks, cudaStream_t s);
+
 // ------------------------------------------------------------ group layout
 mlStatus launch_group_unpack(const void* recv, int G, int64_t T_loc, int32_t dv_slice,
                              const void* gate, void* y, void* z, mlDtype dt, cudaStream_t s);

@@ -105,22 +105,50 @@ __device__ __forceinline__ void store_vec(float* o, const float* acc, bool dense
   }
 }
 
-// Piece of a run longer than kPieceLen: park the partial, the last piece to
-// arrive combines all pieces of the run in piece order (deterministic).
+// Piece of a run longer than kPieceLen: park the partial; pieces are combined
+// in two fixed-order levels so a hot row (e.g. 50 % of all positions) is not
+// summed by one CTA: the last piece to arrive in each group of 32 pieces sums
+// the group, the last group to finish sums the group partials.  Fixed order ->
+// bitwise deterministic.  counters: [2][nslots_cap] per slice, zeroed.
 template <int VEC>
 struct FVec { float v[VEC]; };
+
+template <int VEC>
+__device__ __forceinline__ void sum_slots(const SegParams& p, int slice, int64_t slice_w,
+                                          int32_t first, int32_t count, int32_t stride,
+                                          bool act, float* tot) {
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) tot[v] = 0.f;
+  if (!act) return;
+  for (int32_t q = 0; q < count; ++q) {
+    const float* srcp = p.partial + (int64_t(slice) * p.nslots_cap + first + q * stride) * slice_w +
+                        threadIdx.x * VEC;
+#pragma unroll
+    for (int v = 0; v < VEC; v += 4) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(srcp + v));
+      tot[v] += a.x; tot[v + 1] += a.y; tot[v + 2] += a.z; tot[v + 3] += a.w;
+    }
+  }
+}
 
 template <int VEC>
 __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VEC> accv, bool act,
                                                int64_t col, int slice, int32_t row, int32_t rbb,
                                                int32_t re, int32_t ps, int* s_flag) {
-  const float* acc = accv.v;
   constexpr int L = kPieceLen;
+  constexpr int GRP = 32;
+  const float* acc = accv.v;
   const int64_t slice_w = int64_t(blockDim.x) * VEC;
   const int32_t base = p.piece_base[rbb];
-  const int32_t slot = base + (ps - rbb) / L;
+  const int32_t piece = (ps - rbb) / L;
   const int32_t npieces = (re - rbb + L - 1) / L;
-  float* pp = p.partial + (int64_t(slice) * p.nslots_cap + slot) * slice_w + threadIdx.x * VEC;
+  const int32_t ngroups = (npieces + GRP - 1) / GRP;
+  const int32_t grp = piece / GRP;
+  const int32_t g0 = grp * GRP;
+  const int32_t gn = min(GRP, npieces - g0);
+  int32_t* cnt1 = p.counters + int64_t(slice) * 2 * p.nslots_cap;
+  int32_t* cnt2 = cnt1 + p.nslots_cap;
+  float* pp = p.partial + (int64_t(slice) * p.nslots_cap + base + piece) * slice_w + threadIdx.x * VEC;
   if (act) {
 #pragma unroll
     for (int v = 0; v < VEC; v += 4)
@@ -128,25 +156,32 @@ __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VE
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0)
-    *s_flag = atomicAdd(p.counters + int64_t(slice) * p.nslots_cap + base, 1) == npieces - 1;
+  if (threadIdx.x == 0) *s_flag = atomicAdd(cnt1 + base + g0, 1) == gn - 1;
   __syncthreads();
-  if (*s_flag) {
+  if (*s_flag) {                       // last piece of its group: sum the group
     __threadfence();
     float tot[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) tot[v] = 0.f;
-    for (int32_t q = 0; q < npieces; ++q) {
-      const float* srcp = p.partial + (int64_t(slice) * p.nslots_cap + base + q) * slice_w + threadIdx.x * VEC;
+    sum_slots<VEC>(p, slice, slice_w, base + g0, gn, 1, act, tot);
+    if (ngroups == 1) {
+      if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
+    } else {
+      __syncthreads();                 // every thread has read the group's slots
+      float* gp = p.partial + (int64_t(slice) * p.nslots_cap + base + g0) * slice_w + threadIdx.x * VEC;
       if (act) {
 #pragma unroll
-        for (int v = 0; v < VEC; v += 4) {
-          const float4 a = __ldcg(reinterpret_cast<const float4*>(srcp + v));
-          tot[v] += a.x; tot[v + 1] += a.y; tot[v + 2] += a.z; tot[v + 3] += a.w;
-        }
+        for (int v = 0; v < VEC; v += 4)
+          __stcg(reinterpret_cast<float4*>(gp + v), make_float4(tot[v], tot[v + 1], tot[v + 2], tot[v + 3]));
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) *s_flag = atomicAdd(cnt2 + base, 1) == ngroups - 1;
+      __syncthreads();
+      if (*s_flag) {                   // last group: sum the group partials in order
+        __threadfence();
+        sum_slots<VEC>(p, slice, slice_w, base, ngroups, GRP, act, tot);
+        if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
       }
     }
-    if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
   }
   __syncthreads();
 }
@@ -322,7 +357,7 @@ void seg_carve(Carver& c, int64_t P, int32_t dv, mlDtype dt, float** partial, in
   const int ns = seg_slices(dv, dt);
   const int64_t slice_w = int64_t(team_threads(vu)) * (16 / int64_t(dtype_size(dt)));
   *partial = c.take<float>(ns * nslots_cap(P) * slice_w);
-  *counters = c.take<int32_t>(ns * nslots_cap(P));
+  *counters = c.take<int32_t>(ns * 2 * nslots_cap(P));
 }
 
 mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
@@ -348,7 +383,7 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   p.partial = a.partial; p.counters = a.counters; p.nslots_cap = nslots_cap(a.P);
   p.vec_units = int32_t(vu);
   timing_mark(nullptr, s);
-  ML_CUDA_TRY(cudaMemsetAsync(a.counters, 0, sizeof(int32_t) * size_t(ns) * size_t(p.nslots_cap), s));
+  ML_CUDA_TRY(cudaMemsetAsync(a.counters, 0, sizeof(int32_t) * 2 * size_t(ns) * size_t(p.nslots_cap), s));
   timing_mark("memset", s);
   const int64_t nchunks = (a.P + kChunk - 1) / kChunk;
   dim3 grid{unsigned(nchunks), unsigned(ns), 1u};

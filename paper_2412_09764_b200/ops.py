@@ -168,6 +168,45 @@ def embbag_bwd(V, idx, w, dy, sync=True):
     return rows[:u], dV[:u], dw
 
 
+def embbag_bwd_dv_only(N, idx, w, dy, sync=True):
+    """"reverse_indices" value gradient only (no V, no dw): rows, dV (compact)."""
+    sh = BagShape(N, dy.shape[1], idx.shape[0], idx.shape[1], _dt(dy))
+    P = idx.numel()
+    rows = torch.empty(P, dtype=torch.int32, device=dy.device)
+    dV = torch.empty((P, dy.shape[1]), dtype=torch.float32, device=dy.device)
+    U = torch.empty(1, dtype=torch.int32, device=dy.device)
+    n = _size(lib().embbag_bwd_workspace, sh)
+    ws = workspace(n, dy.device)
+    check(lib().embbag_bwd(C.byref(sh), None, _p(idx), _p(w), _p(dy), _p(rows), _p(dV), _p(U),
+                           None, _p(ws), n, _stream()))
+    if not sync:
+        return rows, dV, U
+    u = int(U.item())
+    return rows[:u], dV[:u]
+
+
+def embbag_bwd_atomics(N, idx, w, dy, dV_dense=None):
+    """Control strategy "atomics": dense fp32 dV, accumulate."""
+    sh = BagShape(N, dy.shape[1], idx.shape[0], idx.shape[1], _dt(dy))
+    if dV_dense is None:
+        dV_dense = torch.zeros((N, dy.shape[1]), dtype=torch.float32, device=dy.device)
+    check(lib().embbag_bwd_atomics(C.byref(sh), _p(idx), _p(w), _p(dy), _p(dV_dense), _stream()))
+    return dV_dense
+
+
+def embbag_bwd_lock(N, idx, w, dy, dV_dense=None, locks=None):
+    """Control strategy "lock": dense fp32 dV, accumulate."""
+    sh = BagShape(N, dy.shape[1], idx.shape[0], idx.shape[1], _dt(dy))
+    if dV_dense is None:
+        dV_dense = torch.zeros((N, dy.shape[1]), dtype=torch.float32, device=dy.device)
+    if locks is None:
+        locks = torch.zeros(int(lib().embbag_bwd_lock_count(C.byref(sh))), dtype=torch.int32,
+                            device=dy.device)
+    check(lib().embbag_bwd_lock(C.byref(sh), _p(idx), _p(w), _p(dy), _p(dV_dense), _p(locks),
+                                _stream()))
+    return dV_dense
+
+
 def embbag_grad_apply(V, idx, rows, dV, U, dV_dense):
     sh = bag_shape(V, idx)
     check(lib().embbag_grad_apply(C.byref(sh), _p(rows), _p(dV), _p(U), _p(dV_dense), _stream()))

@@ -337,3 +337,33 @@ def test_k_equals_S_and_k1_layer_corner():
     dq, dK1, dK2 = o.pkm_topk_bwd(dev(q), dev(K1), dev(K2), idx1, w1,
                                   dev(gen.tensor(13, "dout", (T, H, 1))))
     assert torch.all(dq == 0) and torch.all(dK1 == 0) and torch.all(dK2 == 0)
+
+
+# ------------------------------------------ backward strategy controls (f3)
+@pytest.mark.parametrize("profile", ["u", "c50", "zipf"])
+@pytest.mark.parametrize("dtype,dv", [("f32", 64), ("bf16", 256), ("bf16", 2048), ("bf16", 4096)])
+def test_backward_strategies_agree(profile, dtype, dv):
+    """"atomics" and "lock" agree with the sequential scatter-add
+    oracle within fp32 reordering (rel 1e-5 of the row scale); the sorted
+    "reverse_indices" value gradient equals it on the exact class bit for bit."""
+    o = ops()
+    N, T, B = 1 << 12, 64, 32
+    idx = {"u": streams.uniform_indices(7, T, B, N), "zipf": streams.zipf_indices(7, T, B, N, 1.1),
+           "c50": streams.collision_indices(7, T, B, N, 50)}[profile]
+    w = streams.softmax_free_weights(7, T, B)
+    dy = gen.tensor(7, "dout", (T, dv), dtype=dtype)
+    A = obag.dense_selection_matrix(idx, w, N)
+    ref = A.T @ dy.astype(np.float64)
+    # rigorous fp32 summation bound of an arbitrary-order sum of n terms:
+    # |err| <= (n - 1) 2^-24 sum|terms| (+ one rounding per product)
+    n_r = np.bincount(idx.reshape(-1), minlength=N)[:, None]
+    bound = (n_r + 1) * 2.0 ** -24 * (np.abs(A).T @ np.abs(dy.astype(np.float64)))
+    da = o.embbag_bwd_atomics(N, dev(idx), dev(w), dev(dy, dtype))
+    dl = o.embbag_bwd_lock(N, dev(idx), dev(w), dev(dy, dtype))
+    for name, got in (("atomics", host(da)), ("lock", host(dl))):
+        err = np.abs(got - ref)
+        assert np.all(err <= bound + 1e-12), (name, float((err - bound).max()))
+        assert err.max() <= 1e-5 * np.abs(ref).max(), name
+    rows, dV = o.embbag_bwd_dv_only(N, dev(idx), dev(w), dev(dy, dtype))
+    assert np.array_equal(host(rows), np.unique(idx))
+    assert_close(host(dV), ref[np.unique(idx)], 1e-5, "reverse_indices")
