@@ -170,6 +170,21 @@ int64_t embbag_bwd_lock_count(const mlBagShape* shape);
 mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const float* dV,
                            const int32_t* U, float* dV_dense, void* stream);
 
+/* Sparse (lazy, row-wise) Adam(W) for the memory values (SPEC.md
+ * S:506-514; "associated optimizer states"): consumes the
+ * compact (rows, dV, *U) of embbag_bwd / memory_layer_bwd directly.  For
+ * i < *U, r = rows[i], g = dV[i] (rows distinct):
+ *   c = ++steps[r]; m[r] = b1 m[r] + (1-b1) g; v[r] = b2 v[r] + (1-b2) g^2
+ *   V[r] -= lr * ( m[r]/(1-b1^c) / (sqrt(v[r]/(1-b2^c)) + eps) + wd * V[r] )
+ * Untouched rows (and their moments / counters) are unchanged.  V [N,dv] of
+ * shape->dtype; V_master [N,dv] fp32 (nullable: if given, the update is done
+ * on it and V receives its rounding); m, v [N,dv] fp32; steps [N] int32.
+ * shape->T * shape->B = capacity of rows / dV. */
+typedef struct { float lr, beta1, beta2, eps, weight_decay; } mlAdamParams;
+mlStatus ml_sparse_adam(const mlBagShape* shape, const int32_t* rows, const float* dV,
+                        const int32_t* U, void* V, float* V_master, float* m, float* v,
+                        int32_t* steps, const mlAdamParams* hp, void* stream);
+
 /* ------------------------------------------------ memory layer (a1-a11)
  * Forward: pkm_topk -> g = x W1 -> z = embbag(V; idx, w) ⊙ silu(g) ->
  * out = z W2 (Eq. 1 + Eq. 2).  With gated == 0 (vanilla Memory) out = y and

@@ -32,6 +32,11 @@ class LayerShape(C.Structure):
                 ("gated", C.c_int32)]
 
 
+class AdamParams(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float)]
+
+
 class MemlayerError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
@@ -63,6 +68,7 @@ SIGNATURES = {
     "embbag_bwd_atomics": [C.POINTER(BagShape), P, P, P, P, P],
     "embbag_bwd_lock": [C.POINTER(BagShape), P, P, P, P, P, P],
     "embbag_bwd_lock_count": [C.POINTER(BagShape)],
+    "ml_sparse_adam": [C.POINTER(BagShape), P, P, P, P, P, P, P, P, C.POINTER(AdamParams), P],
     "memory_layer_fwd_workspace": [C.POINTER(LayerShape), C.POINTER(SZ)],
     "memory_layer_fwd": [C.POINTER(LayerShape)] + [P] * 13 + [SZ, P],
     "memory_layer_bwd_workspace": [C.POINTER(LayerShape), C.POINTER(SZ)],

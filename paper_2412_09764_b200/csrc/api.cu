@@ -459,6 +459,21 @@ mlStatus embbag_bwd_lock(const mlBagShape* shape, const int32_t* idx, const floa
   ML_API_END
 }
 
+mlStatus ml_sparse_adam(const mlBagShape* shape, const int32_t* rows, const float* dV,
+                        const int32_t* U, void* V, float* V_master, float* m, float* v,
+                        int32_t* steps, const mlAdamParams* hp, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (!hp) return fail(ML_ERR_ARG, "sparse_adam: null hyper-parameters");
+  if (shape->T == 0) return ML_OK;
+  ML_TRY(check_ptrs({rows, dV, U, V, m, v, steps}));
+  if (V_master) ML_TRY(check_ptrs({V_master}));
+  timing_mark(nullptr, S(stream));
+  return launch_sparse_adam(rows, dV, U, int64_t(shape->T) * shape->B, shape->dv, V, shape->dtype,
+                            V_master, m, v, steps, *hp, S(stream));
+  ML_API_END
+}
+
 mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const float* dV,
                            const int32_t* U, float* dV_dense, void* stream) {
   ML_API_BEGIN

@@ -124,6 +124,11 @@ constexpr size_t kGemmWs = size_t(32) << 20;
 mlStatus launch_bag_bwd_ctrl(int strategy, const mlBagShape& sh, const int32_t* idx, const float* w,
                              const void* dy, float* dV, int* locks, cudaStream_t s);
 
+// ------------------------------------------------ sparse optimizer (f1)
+mlStatus launch_sparse_adam(const int32_t* rows, const float* dV, const int32_t* U, int64_t cap,
+                            int32_t dv, void* V, mlDtype dt, float* Vm, float* m, float* v,
+                            int32_t* steps, const mlAdamParams& hp, cudaStream_t s);
+
 // ------------------------------------------------------------ group layout
 mlStatus launch_group_unpack(const void* recv, int G, int64_t T_loc, int32_t dv_slice,
                              const void* gate, void* y, void* z, mlDtype dt, cudaStream_t s);

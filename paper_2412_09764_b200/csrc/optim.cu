@@ -1,0 +1,84 @@
+// Sparse (lazy, row-wise) Adam(W) on the touched memory-value rows (SURVEY
+// f1): consumes the compact value gradient of
+// the "reverse_indices" backward directly -- no dense gradient, no memset.
+//   c = ++steps[r]; m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+//   V[r] -= lr * ( m/(1-b1^c) / (sqrt(v/(1-b2^c)) + eps) + wd * V[r] )
+// Rows are distinct, so every row is owned by one CTA (no atomics).
+#include "internal.cuh"
+
+namespace ml {
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) sparse_adam_kernel(const int32_t* rows, const float* dV,
+                                                          const int32_t* Uptr, int32_t dv, T* V,
+                                                          float* Vm, float* m, float* v,
+                                                          int32_t* steps, mlAdamParams hp) {
+  __shared__ float s_bc1, s_bc2;
+  const int32_t U = *Uptr;
+  for (int32_t i = blockIdx.x; i < U; i += gridDim.x) {
+    const int64_t r = rows[i];
+    if (threadIdx.x == 0) {
+      const int c = ++steps[r];
+      s_bc1 = 1.f - powf(hp.beta1, float(c));
+      s_bc2 = 1.f - powf(hp.beta2, float(c));
+    }
+    __syncthreads();
+    const float bc1 = s_bc1, bc2 = s_bc2;
+    for (int c0 = threadIdx.x * 4; c0 < dv; c0 += blockDim.x * 4) {
+      const float4 g = *reinterpret_cast<const float4*>(dV + int64_t(i) * dv + c0);
+      float4* mp = reinterpret_cast<float4*>(m + r * dv + c0);
+      float4* vp = reinterpret_cast<float4*>(v + r * dv + c0);
+      float4 mm = *mp, vv = *vp;
+      float w4[4];
+      if (Vm) {
+        const float4 t = *reinterpret_cast<const float4*>(Vm + r * dv + c0);
+        w4[0] = t.x; w4[1] = t.y; w4[2] = t.z; w4[3] = t.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) w4[e] = to_f(V[r * dv + c0 + e]);
+      }
+      const float gs[4] = {g.x, g.y, g.z, g.w};
+      float ms[4] = {mm.x, mm.y, mm.z, mm.w}, vs[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        ms[e] = hp.beta1 * ms[e] + (1.f - hp.beta1) * gs[e];
+        vs[e] = hp.beta2 * vs[e] + (1.f - hp.beta2) * gs[e] * gs[e];
+        const float upd = (ms[e] / bc1) / (sqrtf(vs[e] / bc2) + hp.eps) + hp.weight_decay * w4[e];
+        w4[e] = w4[e] - hp.lr * upd;
+      }
+      *mp = make_float4(ms[0], ms[1], ms[2], ms[3]);
+      *vp = make_float4(vs[0], vs[1], vs[2], vs[3]);
+      if (Vm) *reinterpret_cast<float4*>(Vm + r * dv + c0) = make_float4(w4[0], w4[1], w4[2], w4[3]);
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(V) + r * dv + c0) =
+            make_float4(w4[0], w4[1], w4[2], w4[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) V[r * dv + c0 + e] = __float2bfloat16_rn(w4[e]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+mlStatus launch_sparse_adam(const int32_t* rows, const float* dV, const int32_t* U, int64_t cap,
+                            int32_t dv, void* V, mlDtype dt, float* Vm, float* m, float* v,
+                            int32_t* steps, const mlAdamParams& hp, cudaStream_t s) {
+  if (cap <= 0) return ML_OK;
+  if (dv % 4) return fail(ML_ERR_CONFIG, "sparse_adam: dv must be a multiple of 4");
+  const unsigned grid = unsigned(std::min<int64_t>(cap, int64_t(num_sms()) * 8));
+  if (dt == ML_BF16)
+    sparse_adam_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(rows, dV, U, dv,
+                                                           static_cast<__nv_bfloat16*>(V), Vm, m, v,
+                                                           steps, hp);
+  else
+    sparse_adam_kernel<float><<<grid, 256, 0, s>>>(rows, dV, U, dv, static_cast<float*>(V), Vm, m,
+                                                   v, steps, hp);
+  ML_LAUNCH_CHECK("sparse_adam");
+  return ML_OK;
+}
+
+}  // namespace ml

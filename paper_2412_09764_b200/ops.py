@@ -207,6 +207,17 @@ def embbag_bwd_lock(N, idx, w, dy, dV_dense=None, locks=None):
     return dV_dense
 
 
+def sparse_adam(V, rows, dV, U, m, v, steps, lr, beta1=0.9, beta2=0.999, eps=1e-8,
+                weight_decay=0.0, V_master=None):
+    """Lazy row-wise Adam(W) on the touched value rows (in place); rows/dV/U
+    as returned by embbag_bwd(sync=False) or memory_layer_bwd."""
+    sh = BagShape(V.shape[0], V.shape[1], rows.shape[0], 1, _dt(V))
+    hp = _lib.AdamParams(lr, beta1, beta2, eps, weight_decay)
+    check(lib().ml_sparse_adam(C.byref(sh), _p(rows), _p(dV), _p(U), _p(V), _p(V_master), _p(m),
+                               _p(v), _p(steps), C.byref(hp), _stream()))
+    return V
+
+
 def embbag_grad_apply(V, idx, rows, dV, U, dV_dense):
     sh = bag_shape(V, idx)
     check(lib().embbag_grad_apply(C.byref(sh), _p(rows), _p(dV), _p(U), _p(dV_dense), _stream()))
@@ -319,3 +330,16 @@ def gemm(A, B, transA=False, transB=False, out_f32=False):
                         B.shape[1], _p(C_), N, _dt(A), 1 if out_f32 else 0, _p(ws), ws.numel(),
                         _stream()))
     return C_
+
+
+def embbag_bwd_pool(V, idx_list, w_list, dy_list):
+    """Shared memory pool (P:171-172: one (K, V) pool for all memory layers;
+    SURVEY f1): the value gradient of L layers in ONE sort and ONE segmented
+    pass.  The layers' positions are concatenated (token-major), so a row hit
+    by several layers is reduced once; returns rows, dV, U (capacity-sized,
+    device U) and the per-layer dw."""
+    idx = torch.cat(idx_list, 0)
+    w = torch.cat(w_list, 0)
+    dy = torch.cat(dy_list, 0)
+    rows, dV, U, dw = embbag_bwd(V, idx, w, dy, sync=False)
+    return rows, dV, U, list(torch.split(dw, [i.shape[0] for i in idx_list], 0))
