@@ -9,13 +9,13 @@ import numpy as np
 from . import pkm, bag, gate
 
 
-def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, method="two_stage"):
+def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, method="two_stage", qk_norm=False):
     T, H, _ = q.shape
-    idx, score, w = pkm.pkm_lookup(q, K1, K2, k, method=method)
+    idx, score, w = pkm.pkm_lookup(q, K1, K2, k, method=method, qk_norm=qk_norm)
     bidx = idx.reshape(T, H * k)
     bw = w.reshape(T, H * k)
     y = bag.embbag_fwd(V, bidx, bw)
-    saved = dict(idx=idx, score=score, w=w, y=y)
+    saved = dict(idx=idx, score=score, w=w, y=y, qk_norm=qk_norm)
     if not gated:
         return y, saved
     out, g, z = gate.gate_fwd(x, y, W1, W2)
@@ -36,7 +36,7 @@ def memory_layer_bwd(dout, x, q, K1, K2, V, W1, W2, saved, gated=True):
     bw = saved["w"].reshape(T, H * k)
     rows, dV, dw = bag.embbag_bwd(V, bidx, bw, dy)
     dq, dK1, dK2, ds = pkm.pkm_bwd(q, K1, K2, saved["idx"], saved["w"],
-                                  dw.reshape(T, H, k))
+                                  dw.reshape(T, H, k), qk_norm=saved.get("qk_norm", False))
     grads.update(dy=dy, rows=rows, dV=dV, dw=dw.reshape(T, H, k), dq=dq,
                  dK1=dK1, dK2=dK2)
     return grads

@@ -13,6 +13,36 @@ All arithmetic is float64.
 import numpy as np
 
 
+QK_EPS = 1e-6
+
+
+def l2_normalize(x, eps=QK_EPS):
+    """qk-normalization (P:191 "We use qk-normalization when needed"; form
+    unspecified -- reading Q12 / SPEC S:193: L2 normalisation of each query
+    half and each half-key row at score time, non-learned):
+    x / max(||x||_2, eps) over the last axis."""
+    x = np.asarray(x, np.float64)
+    n = np.sqrt((x * x).sum(axis=-1, keepdims=True))
+    return x / np.maximum(n, eps)
+
+
+def l2_normalize_bwd(x, g, eps=QK_EPS):
+    """Gradient of l2_normalize at x given dL/dy = g:
+    (g - y (y.g)) / ||x|| when ||x|| > eps, else g / eps."""
+    x = np.asarray(x, np.float64)
+    g = np.asarray(g, np.float64)
+    n = np.sqrt((x * x).sum(axis=-1, keepdims=True))
+    y = x / np.maximum(n, eps)
+    proj = (g - y * (y * g).sum(axis=-1, keepdims=True)) / np.maximum(n, eps)
+    return np.where(n > eps, proj, g / eps)
+
+
+def _qk(q, K1, K2):
+    """Per-half normalised query [.., Dk] and half-key tables."""
+    q1, q2 = split_query(q)
+    return np.concatenate([l2_normalize(q1), l2_normalize(q2)], axis=-1), l2_normalize(K1), l2_normalize(K2)
+
+
 def split_query(q):
     """P:157 "we first split the query as q1, q2 in R^{n/2}": first half,
     second half."""
@@ -98,12 +128,15 @@ def softmax(s):
     return e / e.sum(axis=-1, keepdims=True)
 
 
-def pkm_lookup(q, K1, K2, k, method="two_stage"):
+def pkm_lookup(q, K1, K2, k, method="two_stage", qk_norm=False):
     """Eq. 1 lookup for every token and head.
 
     q: [T, H, Dk]; K1, K2: [H, S, Dk/2].  Returns idx [T,H,k] (int64 flat
     index a*S+b), score [T,H,k] (pre-softmax, = K_I q) and w [T,H,k]
-    (softmax per head)."""
+    (softmax per head).  qk_norm: the query halves and half-key rows are
+    L2-normalised first (l2_normalize)."""
+    if qk_norm:
+        q, K1, K2 = _qk(q, K1, K2)
     T, H, _ = q.shape
     f = {"two_stage": topk_two_stage, "full": topk_full,
          "materialized": topk_materialized}[method]
@@ -126,7 +159,7 @@ def dense_eq1(q, K1h, K2h, V, k):
     return I, s, s @ np.asarray(V, np.float64)[I]
 
 
-def pkm_bwd(q, K1, K2, idx, w, dw):
+def pkm_bwd(q, K1, K2, idx, w, dw, qk_norm=False):
     """Backward of the lookup into the query and the half keys ("the
     keys and values ... are trainable parameters").
 
@@ -134,7 +167,15 @@ def pkm_bwd(q, K1, K2, idx, w, dw):
     score is s_j = q1.K1[h, a_j] + q2.K2[h, b_j] with a_j = idx // S,
     b_j = idx % S, hence dq1 = sum_j ds_j K1[h, a_j], dK1[h, a_j] += ds_j q1
     (and the same for half 2).  No gradient through the selection (Q8).
-    Returns dq [T,H,Dk], dK1, dK2 [H,S,Dk/2]."""
+    Returns dq [T,H,Dk], dK1, dK2 [H,S,Dk/2].  With qk_norm the same is done
+    for the normalised operands and chained through l2_normalize_bwd."""
+    if qk_norm:
+        qn, K1n, K2n = _qk(q, K1, K2)
+        dqn, dK1n, dK2n, ds = pkm_bwd(qn, K1n, K2n, idx, w, dw)
+        Dh = q.shape[-1] // 2
+        dq = np.concatenate([l2_normalize_bwd(q[..., :Dh], dqn[..., :Dh]),
+                             l2_normalize_bwd(q[..., Dh:], dqn[..., Dh:])], axis=-1)
+        return dq, l2_normalize_bwd(K1, dK1n), l2_normalize_bwd(K2, dK2n), ds
     T, H, Dk = q.shape
     S = K1.shape[1]
     Dh = Dk // 2

@@ -37,21 +37,22 @@ def test_zero_input_zero_gated_output():
     assert np.all(out == 0)
 
 
-def _loss(p, k, gated):
+def _loss(p, k, gated, qk_norm=False):
     out, saved = layer.memory_layer_fwd(p["x"], p["q"], p["K1"], p["K2"], p["V"],
-                                        p["W1"], p["W2"], k, gated=gated)
+                                        p["W1"], p["W2"], k, gated=gated, qk_norm=qk_norm)
     return float((out * p["dout"]).sum()), saved
 
 
-@pytest.mark.parametrize("gated", [True, False])
+@pytest.mark.parametrize("gated,qk_norm", [(True, False), (False, False), (True, True)])
 @pytest.mark.parametrize("seed", [0, 1, 2])
-def test_finite_differences_all_gradients(gated, seed):
-    """n=8, sqrt(N)=4, k=2: rel. err < 1e-4 for every parameter."""
+def test_finite_differences_all_gradients(gated, qk_norm, seed):
+    """n=8, sqrt(N)=4, k=2: rel. err < 1e-4 for every parameter
+    (also with qk-normalisation)."""
     k = 2
     p = _inputs(seed)
     if not gated:   # ungated Memory: out = y, so dout is [T, dv]
         p["dout"] = gen.tensor(seed, "dout", (p["x"].shape[0], p["V"].shape[1])).astype(np.float64)
-    _, saved = _loss(p, k, gated)
+    _, saved = _loss(p, k, gated, qk_norm)
     g = layer.memory_layer_bwd(p["dout"], p["x"], p["q"], p["K1"], p["K2"], p["V"],
                                p["W1"], p["W2"], saved, gated=gated)
     N, dv = p["V"].shape
@@ -68,9 +69,9 @@ def test_finite_differences_all_gradients(gated, seed):
             i = it.multi_index
             old = p[name][i]
             p[name][i] = old + h
-            lp, sp = _loss(p, k, gated)
+            lp, sp = _loss(p, k, gated, qk_norm)
             p[name][i] = old - h
-            lm, sm = _loss(p, k, gated)
+            lm, sm = _loss(p, k, gated, qk_norm)
             p[name][i] = old
             # the selection must not flip inside the stencil (Q8)
             assert np.array_equal(sp["idx"], saved["idx"]) and np.array_equal(sm["idx"], saved["idx"])

@@ -147,3 +147,45 @@ def test_heads_are_independent():
         i1, s1, w1 = pkm.pkm_lookup(q[:, h:h + 1], K1[h:h + 1], K2[h:h + 1], k)
         assert np.array_equal(i1[:, 0], idx[:, h])
         np.testing.assert_array_equal(w1[:, 0], w[:, h])
+
+
+# ------------------------------------------------------------ qk-norm (f2)
+def test_qk_norm_scores_bounded_and_parallel_closed_form():
+    """with qk_norm every half score lies in [-1, 1]; a query half
+    parallel to a key row scores exactly 1 (closed form)."""
+    S, Dk, k = 16, 8, 4
+    q, K1, K2 = _tables(4, S, Dk, gen.CLS_CONTINUOUS)
+    qn, K1n, K2n = pkm._qk(q, K1, K2)
+    s1 = K1n @ qn[:Dk // 2]
+    assert np.all(np.abs(s1) <= 1 + 1e-12)
+    K1p = K1.copy()
+    K1p[3] = 2.5 * q[:Dk // 2]
+    idx, score, w = pkm.pkm_lookup(q[None, None], K1p[None], K2[None], k, qk_norm=True)
+    qn, K1n, K2n = pkm._qk(q, K1p, K2)
+    assert abs(K1n[3] @ qn[:Dk // 2] - 1.0) < 1e-12
+    assert idx[0, 0, 0] // S == 3          # the parallel key wins half 1
+
+
+def test_qk_norm_two_stage_equals_brute_force_on_normalised_keys():
+    S, Dk, k = 16, 8, 4
+    for seed in range(20):
+        q, K1, K2 = _tables(seed, S, Dk, gen.CLS_CONTINUOUS)
+        idx, score, w = pkm.pkm_lookup(q[None, None], K1[None], K2[None], k, qk_norm=True)
+        qn, K1n, K2n = pkm._qk(q, K1, K2)
+        Ib, sb = pkm.topk_materialized(qn, K1n, K2n, k)
+        assert idx[0, 0].tolist() == Ib.tolist()
+        np.testing.assert_allclose(score[0, 0], sb, atol=1e-13)
+
+
+def test_l2_normalize_bwd_finite_differences():
+    x = gen.tensor(5, "q", (3, 6)).astype(np.float64)
+    g = gen.tensor(5, "dout", (3, 6)).astype(np.float64)
+    an = pkm.l2_normalize_bwd(x, g)
+    h = 1e-6
+    fd = np.zeros_like(x)
+    for i in np.ndindex(x.shape):
+        xp, xm = x.copy(), x.copy()
+        xp[i] += h
+        xm[i] -= h
+        fd[i] = ((pkm.l2_normalize(xp) - pkm.l2_normalize(xm)) * g).sum() / (2 * h)
+    np.testing.assert_allclose(an, fd, rtol=1e-6, atol=1e-9)
