@@ -182,7 +182,7 @@ def run_ours(args, cfg, world, rank, local):
             dK1.zero_()
             dK2.zero_()
             out, saved = ops.memory_layer_fwd(inp["x"], inp["q"], t["K1"], t["K2"], t["V"],
-                                              t["W1"], t["W2"], k)
+                                              t["W1"], t["W2"], k, qk_norm=args.qk_norm)
             g = ops.memory_layer_bwd(inp["dout"], inp["x"], inp["q"], t["K1"], t["K2"], t["V"],
                                      t["W1"], t["W2"], saved, dK1=dK1, dK2=dK2, bufs=bufs)
             return out, g
@@ -434,6 +434,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=2048)
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--qk-norm", action="store_true", help="qk-normalisation (SURVEY f2)")
     ap.add_argument("--force-group", action="store_true",
                     help="run the memory-group (NCCL) path even at N=1 (torchrun)")
     args = ap.parse_args()
@@ -467,7 +468,7 @@ def main():
         "config": {"workload": cfg["desc"], "config": cfg_name, "tokens_per_rank": cfg["T"],
                    "global_tokens": res["tokens_per_step"], "N_values": cfg["S"] ** 2,
                    "value_dim": cfg["dv"], "heads": cfg["H"], "k": cfg["k"],
-                   "key_dim": cfg["Dk"], "gated": True,
+                   "key_dim": cfg["Dk"], "gated": True, "qk_norm": bool(args.qk_norm),
                    "parallelism": (f"memory-group dim-shard G={G} ({args.mode})"
                                    if (G > 1 or args.force_group) else "single GPU"),
                    "l2": "inputs_larger_than_L2 (value table >= 4 GiB vs 126 MB L2; no flush)",

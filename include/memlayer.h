@@ -96,8 +96,12 @@ mlStatus ml_synth_fill(void* out, int64_t n_rows, int64_t n_cols, int64_t row0,
  * Shapes: q [T,H,Dk]; K1, K2 [H,S,Dk/2];  outputs idx [T,H,k] (flat a*S+b,
  * sorted by descending score), w [T,H,k], score [T,H,k] pre-softmax
  * (nullable).  Rules: 1 <= k <= min(S, 32); Dk even; S*S < 2^31; T >= 0
- * (T == 0 is a no-op).  Scratch: [T,H,2,S] fp32 scores + half top-k lists. */
-typedef struct { int32_t T, H, S, Dk, k; mlDtype dtype; } mlPkmShape;
+ * (T == 0 is a no-op).  Scratch: [T,H,2,S] fp32 scores + half top-k lists.
+ * qk_norm != 0: qk-normalisation ("We use qk-normalization when
+ * needed"; reading Q12): every query half and half-key row is L2-normalised,
+ * x / max(||x||_2, 1e-6), before scoring (applied as fp32 scale factors of
+ * the raw products; the backward chains through the normalisation). */
+typedef struct { int32_t T, H, S, Dk, k; mlDtype dtype; int32_t qk_norm; } mlPkmShape;
 
 mlStatus pkm_topk_workspace(const mlPkmShape* shape, size_t* bytes);
 mlStatus pkm_topk(const mlPkmShape* shape, const void* q, const void* K1, const void* K2,

@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "ML_OK", 1: "ML_ERR_ARG", 2: "ML_ERR_CONFIG", 3: "ML_ERR_INDE
 
 class PkmShape(C.Structure):
     _fields_ = [("T", C.c_int32), ("H", C.c_int32), ("S", C.c_int32), ("Dk", C.c_int32),
-                ("k", C.c_int32), ("dtype", C.c_int)]
+                ("k", C.c_int32), ("dtype", C.c_int), ("qk_norm", C.c_int32)]
 
 
 class BagShape(C.Structure):

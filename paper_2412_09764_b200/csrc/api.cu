@@ -82,6 +82,7 @@ static mlStatus check_pkm(const mlPkmShape* s) {
   if (s->Dk % 2) return fail(ML_ERR_CONFIG, "pkm: odd key dimension Dk (SPEC S:143)");
   if (s->k < 1 || s->k > s->S) return fail(ML_ERR_CONFIG, "pkm: need 1 <= k <= S (SPEC S:150)");
   if (s->k > 32) return fail(ML_ERR_UNSUPPORTED, "pkm: k > 32 not supported by the warp select");
+  if (s->qk_norm != 0 && s->qk_norm != 1) return fail(ML_ERR_ARG, "pkm: qk_norm must be 0 or 1");
   if (int64_t(s->S) * s->S >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "pkm: N = S^2 must be < 2^31");
   if (int64_t(s->H) * s->S >= (int64_t(1) << 30)) return fail(ML_ERR_CONFIG, "pkm: H*S too large");
   ML_TRY(check_cols(s->Dk / 2, s->dtype, "pkm half-key row"));
@@ -108,12 +109,36 @@ static mlStatus check_ptrs(std::initializer_list<const void*> ps) {
 }
 
 // ------------------------------------------------------------ plans
-struct PkmFwdBufs { float* scores; int32_t* hI; float* hs; };
+// qk-normalisation scale factors (shape.qk_norm): 1/max(||x||, eps) per query
+// half [T*H*2] and per half-key row [2][H*S]
+struct QkBufs { float* qinv = nullptr; float* kinv = nullptr; };
+static void qk_carve(Carver& c, const mlPkmShape& s, QkBufs& b) {
+  if (!s.qk_norm) return;
+  b.qinv = c.take<float>(int64_t(s.T) * s.H * 2);
+  b.kinv = c.take<float>(int64_t(2) * s.H * s.S);
+}
+static mlStatus qk_compute(const mlPkmShape& s, const void* q, const void* K1, const void* K2,
+                           QkBufs& b, QkNorm* qn, cudaStream_t st) {
+  *qn = QkNorm{};
+  if (!s.qk_norm) return ML_OK;
+  const int Dh = s.Dk / 2;
+  const int64_t HS = int64_t(s.H) * s.S;
+  ML_TRY(launch_row_inv_norm(q, int64_t(s.T) * s.H * 2, Dh, s.dtype, b.qinv, st));
+  ML_TRY(launch_row_inv_norm(K1, HS, Dh, s.dtype, b.kinv, st));
+  ML_TRY(launch_row_inv_norm(K2, HS, Dh, s.dtype, b.kinv + HS, st));
+  qn->qinv = b.qinv;
+  qn->kinv1 = b.kinv;
+  qn->kinv2 = b.kinv + HS;
+  return ML_OK;
+}
+
+struct PkmFwdBufs { float* scores; int32_t* hI; float* hs; QkBufs qk; };
 static void pkm_fwd_carve(Carver& c, const mlPkmShape& s, PkmFwdBufs& b) {
   const int64_t TH = int64_t(s.T) * s.H;
   b.scores = c.take<float>(TH * 2 * s.S);
   b.hI = c.take<int32_t>(TH * 2 * s.k);
   b.hs = c.take<float>(TH * 2 * s.k);
+  qk_carve(c, s, b.qk);
 }
 
 // Key/query backward strategy.  dense: the k selected score gradients per
@@ -136,6 +161,7 @@ struct PkmBwdBufs {
   float* ds; int32_t* key1; int32_t* key2;
   SortBufs sort; RunBufs runs; float* partial; int32_t* counters;
   __nv_bfloat16* ds_dense; void* gemm_ws;
+  QkBufs qk; float* dK_tmp; float* ds1w; float* ds2w;
 };
 static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
   const int64_t P = int64_t(s.T) * s.H * s.k;
@@ -144,11 +170,18 @@ static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
   b.key2 = c.take<int32_t>(P);
   b.ds_dense = nullptr;
   b.gemm_ws = nullptr;
+  b.dK_tmp = b.ds1w = b.ds2w = nullptr;
+  qk_carve(c, s, b.qk);
+  if (s.qk_norm) b.dK_tmp = c.take<float>(int64_t(2) * s.H * s.S * (s.Dk / 2));
   if (pkm_bwd_dense(s)) {
     b.ds_dense = c.take<__nv_bfloat16>(int64_t(s.T) * s.H * 2 * s.S);
     b.gemm_ws = c.take<char>(kGemmWs);
     if (!c.base) b.ds_dense = reinterpret_cast<__nv_bfloat16*>(1);  // measuring: mark dense
     return;
+  }
+  if (s.qk_norm) {
+    b.ds1w = c.take<float>(P);
+    b.ds2w = c.take<float>(P);
   }
   sort_carve(c, P, ceil_log2(int64_t(s.H) * s.S), b.sort);
   runs_carve(c, P, b.runs);
@@ -168,8 +201,10 @@ static void bag_bwd_carve(Carver& c, const mlBagShape& s, BagBwdBufs& b) {
 static mlStatus pkm_fwd_core(const mlPkmShape& s, const void* q, const void* K1, const void* K2,
                              int32_t* idx, float* w, float* score, PkmFwdBufs& b, cudaStream_t st) {
   if (s.T == 0) return ML_OK;
+  QkNorm qn;
+  ML_TRY(qk_compute(s, q, K1, K2, b.qk, &qn, st));
   ML_TRY(launch_pkm_scores(s, q, K1, K2, b.scores, st));
-  ML_TRY(launch_half_topk(s, b.scores, b.hI, b.hs, st));
+  ML_TRY(launch_half_topk(s, b.scores, b.hI, b.hs, qn, st));
   ML_TRY(launch_combine_softmax(s, b.hI, b.hs, idx, w, score, st));
   return ML_OK;
 }
@@ -181,17 +216,30 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
   if (s.T == 0) return ML_OK;
   const int64_t P = int64_t(s.T) * s.H * s.k;
   const int Dh = s.Dk / 2;
+  const int64_t HS = int64_t(s.H) * s.S;
+  QkNorm qn;
+  ML_TRY(qk_compute(s, q, K1, K2, b.qk, &qn, st));
+  // with qk-norm the products below give G = inv * d(x_hat); the half-key
+  // part goes to a temporary and is projected into dK (accumulate)
+  float* dKo1 = s.qk_norm ? b.dK_tmp : dK1;
+  float* dKo2 = s.qk_norm ? b.dK_tmp + HS * Dh : dK2;
+  if (s.qk_norm) {
+    timing_mark(nullptr, st);
+    ML_CUDA_TRY(cudaMemsetAsync(b.dK_tmp, 0, sizeof(float) * size_t(2 * HS * Dh), st));
+    timing_mark("memset", st);
+  }
   if (b.ds_dense) {
     timing_mark(nullptr, st);
     ML_CUDA_TRY(cudaMemsetAsync(b.ds_dense, 0, sizeof(__nv_bfloat16) * size_t(s.T) * s.H * 2 * s.S, st));
     timing_mark("memset", st);
-    ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, b.ds_dense, st));
+    ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, b.ds_dense, qn,
+                              nullptr, nullptr, st));
     const int64_t lds = int64_t(s.H) * 2 * s.S;  // row pitch of ds_dense per token
     for (int half = 0; half < 2; ++half) {        // one strided-batched GEMM over heads each
       const __nv_bfloat16* A = b.ds_dense + int64_t(half) * s.S;
       const void* Kh = half ? K2 : K1;
       const char* qh = static_cast<const char*>(q) + int64_t(half) * Dh * 2;
-      float* dKh = half ? dK2 : dK1;
+      float* dKh = half ? dKo2 : dKo1;
       // dq[t, h, half] = ds[t, h, half, :] K_half[h]          [T, Dh] per head
       ML_TRY(gemm_rm_batched(false, false, s.T, Dh, s.S, A, lds, 2 * int64_t(s.S), Kh, Dh,
                              int64_t(s.S) * Dh, dq + int64_t(half) * Dh, int64_t(s.H) * s.Dk, s.Dk,
@@ -201,31 +249,38 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
                              int64_t(s.H) * s.Dk, s.Dk, dKh, Dh, int64_t(s.S) * Dh, s.H, ML_BF16,
                              true, b.gemm_ws, kGemmWs, st, 1.f));
     }
-    return ML_OK;
+  } else {
+    ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, nullptr, qn,
+                              b.ds1w, b.ds2w, st));
+    const int bits = ceil_log2(HS);
+    for (int half = 0; half < 2; ++half) {
+      const void* K = half ? K2 : K1;
+      const int32_t* key = half ? b.key2 : b.key1;
+      const float* wts = s.qk_norm ? (half ? b.ds2w : b.ds1w) : b.ds;
+      // dq_half[t,h] = sum_j ds_j K_half[h, a_j]  (a bag over the [H*S, Dh] table)
+      BagFwdArgs a;
+      a.V = K; a.ldv = Dh; a.N = HS;
+      a.idx = key; a.w = wts; a.B = s.k; a.nbags = s.T * s.H; a.dv = Dh;
+      a.out = dq; a.ldo = s.Dk; a.out_col0 = half * Dh; a.out_f32 = true; a.dtype = s.dtype;
+      a.name = "pkm_dq_bag";
+      ML_TRY(launch_bag_fwd(a, st));
+      // dK_half[h, a] += sum ds * q_half[t,h]  (sorted segments, dense accumulate)
+      int32_t *skey, *spos;
+      ML_TRY(sort_pairs(key, P, bits, b.sort, &skey, &spos, st));
+      ML_TRY(find_runs(skey, P, b.runs, nullptr, nullptr, st));
+      SegArgs g;
+      g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = wts;
+      g.src = q; g.lds = s.Dk; g.src_col0 = half * Dh; g.B = s.k;
+      g.out = half ? dKo2 : dKo1; g.ldo = Dh; g.dense_accumulate = true;
+      g.partial = b.partial; g.counters = b.counters; g.dv = Dh; g.dtype = s.dtype;
+      g.name = "pkm_dK_segreduce";
+      ML_TRY(launch_segreduce(g, st));
+    }
   }
-  ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, nullptr, st));
-  const int bits = ceil_log2(int64_t(s.H) * s.S);
-  for (int half = 0; half < 2; ++half) {
-    const void* K = half ? K2 : K1;
-    const int32_t* key = half ? b.key2 : b.key1;
-    // dq_half[t,h] = sum_j ds_j K_half[h, a_j]  (a bag over the [H*S, Dh] table)
-    BagFwdArgs a;
-    a.V = K; a.ldv = Dh; a.N = int64_t(s.H) * s.S;
-    a.idx = key; a.w = b.ds; a.B = s.k; a.nbags = s.T * s.H; a.dv = Dh;
-    a.out = dq; a.ldo = s.Dk; a.out_col0 = half * Dh; a.out_f32 = true; a.dtype = s.dtype;
-    a.name = "pkm_dq_bag";
-    ML_TRY(launch_bag_fwd(a, st));
-    // dK_half[h, a] += sum ds * q_half[t,h]  (sorted segments, dense accumulate)
-    int32_t *skey, *spos;
-    ML_TRY(sort_pairs(key, P, bits, b.sort, &skey, &spos, st));
-    ML_TRY(find_runs(skey, P, b.runs, nullptr, nullptr, st));
-    SegArgs g;
-    g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = b.ds;
-    g.src = q; g.lds = s.Dk; g.src_col0 = half * Dh; g.B = s.k;
-    g.out = half ? dK2 : dK1; g.ldo = Dh; g.dense_accumulate = true;
-    g.partial = b.partial; g.counters = b.counters; g.dv = Dh; g.dtype = s.dtype;
-    g.name = "pkm_dK_segreduce";
-    ML_TRY(launch_segreduce(g, st));
+  if (s.qk_norm) {  // chain through x_hat = x / max(||x||, eps)
+    ML_TRY(launch_qk_proj(q, int64_t(s.T) * s.H * 2, Dh, s.dtype, dq, dq, false, st));
+    ML_TRY(launch_qk_proj(K1, HS, Dh, s.dtype, b.dK_tmp, dK1, true, st));
+    ML_TRY(launch_qk_proj(K2, HS, Dh, s.dtype, b.dK_tmp + HS * Dh, dK2, true, st));
   }
   return ML_OK;
 }

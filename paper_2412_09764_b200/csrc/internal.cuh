@@ -79,6 +79,14 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s);
 mlStatus launch_sum_slices(const float* part, int nslices, int64_t P, float* dw, cudaStream_t s);
 
 // ------------------------------------------------------ product keys
+// qk-normalisation factors (all null when off): qinv [T*H*2] per query half,
+// kinv1 / kinv2 [H*S] per half-key row, each 1 / max(||x||, 1e-6)
+struct QkNorm { const float* qinv = nullptr; const float* kinv1 = nullptr; const float* kinv2 = nullptr; };
+mlStatus launch_row_inv_norm(const void* x, int64_t rows, int Dh, mlDtype dt, float* inv,
+                             cudaStream_t s);
+// out (=|+=) G - x_hat (x_hat . G) per row (or G where ||x|| <= eps)
+mlStatus launch_qk_proj(const void* x, int64_t rows, int Dh, mlDtype dt, const float* G, float* out,
+                        bool accumulate, cudaStream_t s);
 mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1,
                            const void* K2, float* scores, cudaStream_t s);
 // tcgen05 path (bf16, Dk/2 % 64 == 0, S = 32..256 power of two or multiple of 256)
@@ -86,7 +94,7 @@ bool pkm_scores_tc_eligible(const mlPkmShape& sh);
 mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
                               float* scores, cudaStream_t s);
 mlStatus launch_half_topk(const mlPkmShape& sh, const float* scores, int32_t* hI,
-                          float* hs, cudaStream_t s);
+                          float* hs, const QkNorm& qn, cudaStream_t s);
 mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const float* hs,
                                 int32_t* idx, float* w, float* score, cudaStream_t s);
 // ds = w (dw - sum w dw) with dw = sum over nslices partials; also writes the
@@ -97,7 +105,7 @@ mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const f
 mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
                             const float* dw_part, int nslices, int64_t slice_stride,
                             float* ds, int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,
-                            cudaStream_t s);
+                            const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s);
 
 // ------------------------------------------------------------ gate
 // z = y*silu(g); dy = dz*silu(g); dg = dz*y*silu'(g)   (elementwise, n elems)

@@ -238,16 +238,21 @@ __device__ __forceinline__ uint64_t warp_theta_max(uint64_t lane_max, int k) {
 
 // one warp per (t, h, half) row of S scores
 __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int64_t rows, int S,
-                                                        int k, int32_t* hI, float* hs) {
+                                                        int k, int32_t* hI, float* hs, QkNorm qn,
+                                                        int H) {
   __shared__ TopkSmem s_sm[8];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = int64_t(blockIdx.x) * 8 + wid;
   if (row >= rows) return;
   TopkSmem& sm = s_sm[wid];
   const float* sr = scores + row * S;
+  // qk-norm: s = (q.k) * inv|q| * inv|k| (scores stay raw tensor-core products)
+  const float qi = qn.qinv ? qn.qinv[row] : 1.f;
+  const float* ki = qn.qinv ? ((row & 1) ? qn.kinv2 : qn.kinv1) + int64_t((row >> 1) % H) * S : nullptr;
+  auto score_at = [=](int e) { return ki ? (sr[e] * qi) * ki[e] : sr[e]; };
   uint64_t mx = 0;
   for (int e = lane; e < S; e += 32) {
-    const uint64_t key = make_key(sr[e], uint32_t(e));
+    const uint64_t key = make_key(score_at(e), uint32_t(e));
     mx = key > mx ? key : mx;
   }
   const uint64_t theta = warp_theta_max(mx, k);
@@ -255,14 +260,14 @@ __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int
   for (int e0 = 0; e0 < S; e0 += 32) {
     const int e = e0 + lane;
     uint64_t key = 0;
-    if (e < S) key = make_key(sr[e], uint32_t(e));
+    if (e < S) key = make_key(score_at(e), uint32_t(e));
     append_cand(key, e < S && key >= theta, count, sm);
   }
   uint64_t key;
   if (count <= kCandCap) {
     key = select_cand(count, k, sm);
   } else {  // pathological ties: exact select over the whole row
-    auto gen = [sr](int e) { return make_key(sr[e], uint32_t(e)); };
+    auto gen = [=](int e) { return make_key(score_at(e), uint32_t(e)); };
     key = warp_topk(gen, S, k, sm.hist, sm.sel);
   }
   if (lane < k) {
@@ -342,9 +347,11 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
                                                           const float* dw_part, int ns,
                                                           int64_t sstride, int64_t TH, int H,
                                                           int S, int k, float* ds, int32_t* key1,
-                                                          int32_t* key2, __nv_bfloat16* ds_dense) {
+                                                          int32_t* key2, __nv_bfloat16* ds_dense,
+                                                          QkNorm qn, float* ds1w, float* ds2w) {
   __shared__ int s_sub[8][2][32];
   __shared__ float s_ds[8][32];
+  __shared__ float s_sc[8][2][32];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t th = int64_t(blockIdx.x) * 8 + wid;
   if (th >= TH) return;
@@ -361,10 +368,21 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(FULL, dot, off);
   const float dsv = wv * (dwv - dot);
+  // qk-norm: the half scores were (q_half.k) * inv_q * inv_k, so the raw
+  // products receive ds * inv_q * inv_k (projection done after the GEMMs)
+  float sc1 = 1.f, sc2 = 1.f;
+  if (qn.qinv && lane < k) {
+    sc1 = qn.qinv[th * 2 + 0] * qn.kinv1[int64_t(h) * S + ix / S];
+    sc2 = qn.qinv[th * 2 + 1] * qn.kinv2[int64_t(h) * S + ix % S];
+  }
   if (lane < k) {
     ds[o] = dsv;
     key1[o] = h * S + ix / S;
     key2[o] = h * S + ix % S;
+    if (ds1w) {
+      ds1w[o] = dsv * sc1;
+      ds2w[o] = dsv * sc2;
+    }
   }
   if (ds_dense) {
     // dense half-key gradients of this (t, h); a sub-key selected by several
@@ -372,6 +390,8 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
     s_sub[wid][0][lane] = lane < k ? ix / S : -1;
     s_sub[wid][1][lane] = lane < k ? ix % S : -1;
     s_ds[wid][lane] = dsv;
+    s_sc[wid][0][lane] = sc1;
+    s_sc[wid][1][lane] = sc2;
     __syncwarp();
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -381,7 +401,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
       for (int l = 0; l < k; ++l) {
         if (s_sub[wid][half][l] == a) {
           if (l < lane) leader = false;
-          sum += s_ds[wid][l];
+          sum += s_ds[wid][l] * s_sc[wid][half][l];
         }
       }
       if (leader) ds_dense[(th * 2 + half) * S + a] = __float2bfloat16_rn(sum);
@@ -410,10 +430,11 @@ mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1, 
 }
 
 mlStatus launch_half_topk(const mlPkmShape& sh, const float* scores, int32_t* hI, float* hs,
-                          cudaStream_t s) {
+                          const QkNorm& qn, cudaStream_t s) {
   const int64_t rows = int64_t(sh.T) * sh.H * 2;
   if (rows <= 0) return ML_OK;
-  half_topk_kernel<<<unsigned((rows + 7) / 8), 256, 0, s>>>(scores, rows, sh.S, sh.k, hI, hs);
+  half_topk_kernel<<<unsigned((rows + 7) / 8), 256, 0, s>>>(scores, rows, sh.S, sh.k, hI, hs, qn,
+                                                            sh.H);
   ML_LAUNCH_CHECK("half_topk");
   return ML_OK;
 }
@@ -429,11 +450,13 @@ mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const f
 
 mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
                             const float* dw_part, int nslices, int64_t slice_stride, float* ds,
-                            int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense, cudaStream_t s) {
+                            int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,
+                            const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s) {
   const int64_t TH = int64_t(sh.T) * sh.H;
   if (TH <= 0) return ML_OK;
   softmax_bwd_kernel<<<unsigned((TH + 7) / 8), 256, 0, s>>>(
-      idx, w, dw_part, nslices, slice_stride, TH, sh.H, sh.S, sh.k, ds, key1, key2, ds_dense);
+      idx, w, dw_part, nslices, slice_stride, TH, sh.H, sh.S, sh.k, ds, key1, key2, ds_dense, qn,
+      ds1w, ds2w);
   ML_LAUNCH_CHECK("softmax_bwd");
   return ML_OK;
 }

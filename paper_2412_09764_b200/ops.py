@@ -97,15 +97,15 @@ def synth_fill(out, seed, tag, scale=1.0, cls=0, row0=0, modulus=0):
 
 
 # ------------------------------------------------------------- product keys
-def pkm_shape(q, K1, k):
+def pkm_shape(q, K1, k, qk_norm=False):
     T, H, Dk = q.shape
-    return PkmShape(T, H, K1.shape[1], Dk, k, _dt(q))
+    return PkmShape(T, H, K1.shape[1], Dk, k, _dt(q), 1 if qk_norm else 0)
 
 
-def pkm_topk(q, K1, K2, k, with_score=False):
+def pkm_topk(q, K1, K2, k, with_score=False, qk_norm=False):
     """Product-key top-k + softmax (Eq. 1).  q [T,H,Dk], K1/K2 [H,S,Dk/2].
     Returns idx [T,H,k] int32, w [T,H,k] fp32 (and pre-softmax scores)."""
-    sh = pkm_shape(q, K1, k)
+    sh = pkm_shape(q, K1, k, qk_norm)
     T, H = q.shape[0], q.shape[1]
     idx = torch.empty((T, H, k), dtype=torch.int32, device=q.device)
     w = torch.empty((T, H, k), dtype=torch.float32, device=q.device)
@@ -117,10 +117,10 @@ def pkm_topk(q, K1, K2, k, with_score=False):
     return (idx, w, score) if with_score else (idx, w)
 
 
-def pkm_topk_bwd(q, K1, K2, idx, w, dw, dK1=None, dK2=None):
+def pkm_topk_bwd(q, K1, K2, idx, w, dw, dK1=None, dK2=None, qk_norm=False):
     """dq (overwrite) and dK1/dK2 (accumulate; zero-initialised if None)."""
     k = idx.shape[-1]
-    sh = pkm_shape(q, K1, k)
+    sh = pkm_shape(q, K1, k, qk_norm)
     dq = torch.empty(q.shape, dtype=torch.float32, device=q.device)
     if dK1 is None:
         dK1 = torch.zeros(K1.shape, dtype=torch.float32, device=q.device)
@@ -225,16 +225,16 @@ def embbag_grad_apply(V, idx, rows, dV, U, dV_dense):
 
 
 # ------------------------------------------------------------ memory layer
-def layer_shape(x, q, K1, V, k, gated):
+def layer_shape(x, q, K1, V, k, gated, qk_norm=False):
     T, H, Dk = q.shape
     D = x.shape[1] if (gated and x is not None) else V.shape[1]
-    return LayerShape(PkmShape(T, H, K1.shape[1], Dk, k, _dt(q)), V.shape[0], V.shape[1], D,
-                      1 if gated else 0)
+    return LayerShape(PkmShape(T, H, K1.shape[1], Dk, k, _dt(q), 1 if qk_norm else 0), V.shape[0],
+                      V.shape[1], D, 1 if gated else 0)
 
 
-def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True):
+def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, qk_norm=False):
     """Eq. 1 + Eq. 2 forward.  Returns out [T,D] and the saved tensors."""
-    sh = layer_shape(x, q, K1, V, k, gated)
+    sh = layer_shape(x, q, K1, V, k, gated, qk_norm)
     T, H = q.shape[0], q.shape[1]
     dev = q.device
     out = torch.empty((T, sh.D), dtype=V.dtype, device=dev)
@@ -247,7 +247,7 @@ def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True):
     check(lib().memory_layer_fwd(C.byref(sh), _p(x if gated else None), _p(q), _p(K1), _p(K2),
                                  _p(V), _p(W1 if gated else None), _p(W2 if gated else None),
                                  _p(out), _p(idx), _p(w), _p(g), _p(y), _p(ws), n, _stream()))
-    return out, dict(idx=idx, w=w, g=g, y=y, k=k, gated=gated)
+    return out, dict(idx=idx, w=w, g=g, y=y, k=k, gated=gated, qk_norm=qk_norm)
 
 
 class LayerGrads(dict):
@@ -259,7 +259,7 @@ def memory_layer_bwd(dout, x, q, K1, K2, V, W1, W2, saved, dK1=None, dK2=None, w
     """Backward of memory_layer_fwd.  dK1/dK2 accumulate (zeros if None).
     dV is compact: rows[:U], dV[:U] (capacity-sized buffers + device U)."""
     k, gated = saved["k"], saved["gated"]
-    sh = layer_shape(x, q, K1, V, k, gated)
+    sh = layer_shape(x, q, K1, V, k, gated, saved.get("qk_norm", False))
     T, H = q.shape[0], q.shape[1]
     dev = q.device
     P = T * H * k

@@ -367,3 +367,57 @@ def test_backward_strategies_agree(profile, dtype, dv):
     rows, dV = o.embbag_bwd_dv_only(N, dev(idx), dev(w), dev(dy, dtype))
     assert np.array_equal(host(rows), np.unique(idx))
     assert_close(host(dV), ref[np.unique(idx)], 1e-5, "reverse_indices")
+
+
+# ------------------------------------------------------------ qk-norm (f2)
+@pytest.mark.parametrize("dtype,T,H,S,Dk,k", [("f32", 77, 2, 32, 64, 4), ("bf16", 70, 4, 128, 256, 32)])
+def test_pkm_topk_qk_norm(dtype, T, H, S, Dk, k):
+    q, K1, K2 = _pkm_inputs(14, T, H, S, Dk, dtype, gen.CLS_CONTINUOUS)
+    q64, K164, K264 = (a.astype(np.float64) for a in (q, K1, K2))
+    idx, w, score = ops().pkm_topk(dev(q, dtype), dev(K1, dtype), dev(K2, dtype), k,
+                                   with_score=True, qk_norm=True)
+    ridx, rscore, rw = opkm.pkm_lookup(q64, K164, K264, k, qk_norm=True)
+    qn, K1n, K2n = opkm._qk(q64, K164, K264)
+    near = compare_topk(host(idx), ridx, qn, K1n, K2n)
+    ok = np.ones(ridx.shape[:2], bool)
+    for t, h, _ in near:
+        ok[t, h] = False
+    assert np.abs(host(score)).max() <= 2.0 + 1e-5            # two normalised halves
+    assert_close(host(score)[ok], rscore[ok], 1e-5, "score")
+    assert_close(host(w)[ok], rw[ok], TOL["f32"], "w")
+    dw = gen.tensor(14, "dout", (T, H, k), dtype="f32")
+    rdq, rdK1, rdK2, _ = opkm.pkm_bwd(q64, K164, K264, ridx, rw, dw, qk_norm=True)
+    dq, dK1, dK2 = ops().pkm_topk_bwd(dev(q, dtype), dev(K1, dtype), dev(K2, dtype),
+                                      dev(ridx.astype(np.int32)), dev(rw.astype(np.float32)),
+                                      dev(dw), qk_norm=True)
+    assert_close(host(dq), rdq, TOL[dtype], "dq")
+    assert_close(host(dK1), rdK1, TOL[dtype], "dK1")
+    assert_close(host(dK2), rdK2, TOL[dtype], "dK2")
+
+
+@pytest.mark.parametrize("dtype,T,H,S,Dk,k,dv,D", [("f32", 128, 1, 32, 32, 4, 64, 64),
+                                                  ("bf16", 96, 4, 64, 128, 8, 256, 256)])
+def test_memory_layer_qk_norm(dtype, T, H, S, Dk, k, dv, D):
+    seed = 15
+    f = lambda tag, shape, sc=1.0: gen.tensor(seed, tag, shape, scale=sc, dtype=dtype)
+    h = dict(x=f("x", (T, D)), q=f("q", (T, H, Dk)), K1=f("K1", (H, S, Dk // 2)),
+             K2=f("K2", (H, S, Dk // 2)), V=f("V", (S * S, dv)),
+             W1=f("W1", (D, dv), gen.scale_for("W1", D=D)), W2=f("W2", (dv, D), gen.scale_for("W2", dv=dv)),
+             dout=f("dout", (T, D)))
+    t = {n: dev(a, dtype) for n, a in h.items()}
+    o = ops()
+    out, saved = o.memory_layer_fwd(t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"], k,
+                                    qk_norm=True)
+    g = o.memory_layer_bwd(t["dout"], t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"], saved)
+    h64 = {n: a.astype(np.float64) for n, a in h.items()}
+    rout, rs = olayer.memory_layer_fwd(h64["x"], h64["q"], h64["K1"], h64["K2"], h64["V"], h64["W1"],
+                                       h64["W2"], k, qk_norm=True)
+    qn, K1n, K2n = opkm._qk(h64["q"], h64["K1"], h64["K2"])
+    assert not compare_topk(host(saved["idx"]), rs["idx"], qn, K1n, K2n)
+    r = olayer.memory_layer_bwd(h64["dout"], h64["x"], h64["q"], h64["K1"], h64["K2"], h64["V"],
+                                h64["W1"], h64["W2"], rs)
+    tol = TOL[dtype]
+    assert_close(host(out), rout, tol, "out")
+    assert_close(host(g["dq"]), r["dq"], tol, "dq")
+    assert_close(host(g["dK1"]), r["dK1"], tol, "dK1")
+    assert_close(host(g["dK2"]), r["dK2"], tol, "dK2")
