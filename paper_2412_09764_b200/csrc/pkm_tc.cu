@@ -8,11 +8,12 @@
 // keys, K = 16 per instruction) with the accumulator in TMEM.  Warp roles in a
 // persistent 256-thread CTA (one per SM):
 //   warp 0   TMA producer: 128x64 query tile + BNx64 key tile per stage
-//            (128-byte swizzle, mbarrier complete_tx), 4-stage ring
+//            (128-byte swizzle, mbarrier complete_tx), 3-stage ring
 //   warp 1   MMA issuer (one elected thread), commits free smem stages and
 //            signals a double-buffered TMEM accumulator
 //   warp 2   TMEM allocator
-//   warps 4-7 epilogue: tcgen05.ld 32x32b (thread = token row) -> fp32 scores
+//   warps 4-7 epilogue: tcgen05.ld 32x32b (thread = token row) -> shared-memory
+//            transpose -> row-contiguous fp32 score stores
 // The selection (half top-k) consumes the scores in pkm.cu.
 #include "internal.cuh"
 
@@ -26,7 +27,8 @@ namespace {
 
 constexpr int kBM = 128;     // tokens per tile (UMMA_M)
 constexpr int kBK = 64;      // K elements per stage = one 128-byte swizzle atom of bf16
-constexpr int kStages = 4;
+constexpr int kStages = 3;
+constexpr int kStageLd = 36;  // epilogue staging row pitch (floats): 16-B aligned, conflict-free
 constexpr int kThreads = 256;
 constexpr uint32_t kSpinLimit = 1u << 28;  // bounded waits: trap instead of hanging
 
@@ -132,6 +134,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // epilogue staging: one [32 rows][kStageLd] fp32 tile per epilogue warp
+  float* stage_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -224,21 +228,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
       const int mt = t % p.m_tiles, hh = t / p.m_tiles;
       const int h = hh >> 1, half = hh & 1;
-      const int row = mt * kBM + q4 * 32 + lane;
-      float* out = p.scores + ((int64_t(row) * p.H + h) * 2 + half) * int64_t(p.S);
+      const int row0 = mt * kBM + q4 * 32;   // this warp's 32 token rows
+      float* stg = stage_all + (warp - 4) * 32 * kStageLd;
+      const int64_t row_pitch = int64_t(p.H) * 2 * p.S;   // floats between consecutive tokens
+      float* out0 = p.scores + (int64_t(row0) * p.H * 2 + h * 2 + half) * int64_t(p.S);
       for (int n = 0; n < p.n_sub; ++n) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         for (int c0 = 0; c0 < p.BN; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
-          if (row < p.T) {
-            float4* o = reinterpret_cast<float4*>(out + n * p.BN + c0);
+          // transpose through shared memory so global stores are row-contiguous:
+          // lane = token row on the TMEM side, 8 lanes x 16 B = one 128-B row segment
+          // on the store side (4 rows per store instruction instead of 32)
 #pragma unroll
-            for (int v = 0; v < 8; ++v)
-              o[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                 __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+          for (int v = 0; v < 8; ++v)
+            *reinterpret_cast<uint4*>(stg + lane * kStageLd + 4 * v) =
+                make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + (lane >> 3), cv = (lane & 7) * 4;
+            if (row0 + rr < p.T)
+              *reinterpret_cast<float4*>(out0 + rr * row_pitch + n * p.BN + c0 + cv) =
+                  *reinterpret_cast<const float4*>(stg + rr * kStageLd + cv);
           }
+          __syncwarp();
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
@@ -331,7 +346,8 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
   ML_TRY(make_map(&mq, q, uint64_t(sh.H) * sh.Dk, uint64_t(sh.T), uint64_t(sh.H) * sh.Dk * 2, kBK, kBM));
   ML_TRY(make_map(&mk1, K1, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN));
   ML_TRY(make_map(&mk2, K2, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN));
-  const size_t smem = 1024 + size_t(kStages) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 256;
+  const size_t smem = 1024 + size_t(kStages) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 256 +
+                      size_t(4) * 32 * kStageLd * sizeof(float);
   static size_t configured = 0;
   if (smem > configured) {
     ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
