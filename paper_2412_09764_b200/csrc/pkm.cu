@@ -250,18 +250,50 @@ __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int
   const float qi = qn.qinv ? qn.qinv[row] : 1.f;
   const float* ki = qn.qinv ? ((row & 1) ? qn.kinv2 : qn.kinv1) + int64_t((row >> 1) % H) * S : nullptr;
   auto score_at = [=](int e) { return ki ? (sr[e] * qi) * ki[e] : sr[e]; };
-  uint64_t mx = 0;
-  for (int e = lane; e < S; e += 32) {
-    const uint64_t key = make_key(score_at(e), uint32_t(e));
-    mx = key > mx ? key : mx;
+  // phase 1: each lane's maximum (float compares; the first index of a tied
+  // maximum is kept, which is the larger 64-bit key)
+  float ms = -INFINITY;
+  int mi = 0x7fffffff;
+  const bool vec4 = (S % 128) == 0 && ki == nullptr;
+  if (vec4) {     // lane owns 4 consecutive scores per 512-B round
+    for (int e0 = lane * 4; e0 < S; e0 += 128) {
+      const float4 v = *reinterpret_cast<const float4*>(sr + e0);
+      if (v.x > ms) { ms = v.x; mi = e0; }
+      if (v.y > ms) { ms = v.y; mi = e0 + 1; }
+      if (v.z > ms) { ms = v.z; mi = e0 + 2; }
+      if (v.w > ms) { ms = v.w; mi = e0 + 3; }
+    }
+  } else {
+    for (int e = lane; e < S; e += 32) {
+      const float v = score_at(e);
+      if (v > ms) { ms = v; mi = e; }
+    }
   }
-  const uint64_t theta = warp_theta_max(mx, k);
+  const uint64_t lane_key = mi == 0x7fffffff ? 0ull : make_key(ms, uint32_t(mi));
+  const uint64_t theta = warp_theta_max(lane_key, k);
+  const float ts = key_score(theta);
+  const int ti = int(key_id(theta));
+  // phase 3: survivors key >= theta <=> s > ts or (s == ts and e <= ti)
   int count = 0;
-  for (int e0 = 0; e0 < S; e0 += 32) {
-    const int e = e0 + lane;
-    uint64_t key = 0;
-    if (e < S) key = make_key(score_at(e), uint32_t(e));
-    append_cand(key, e < S && key >= theta, count, sm);
+  if (vec4) {
+    for (int e0 = 0; e0 < S; e0 += 128) {
+      const int eb = e0 + lane * 4;
+      const float4 v = *reinterpret_cast<const float4*>(sr + eb);
+      const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = eb + c;
+        const bool sel = vs[c] > ts || (vs[c] == ts && e <= ti);
+        append_cand(sel ? make_key(vs[c], uint32_t(e)) : 0ull, sel, count, sm);
+      }
+    }
+  } else {
+    for (int e0 = 0; e0 < S; e0 += 32) {
+      const int e = e0 + lane;
+      const float v = e < S ? score_at(e) : -INFINITY;
+      const bool sel = e < S && (v > ts || (v == ts && e <= ti));
+      append_cand(sel ? make_key(v, uint32_t(e)) : 0ull, sel, count, sm);
+    }
   }
   uint64_t key;
   if (count <= kCandCap) {
