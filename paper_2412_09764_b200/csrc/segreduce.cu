@@ -26,6 +26,9 @@
 // position), so each piece costs one memory round trip (V row + dy rows).
 #include "internal.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace ml {
 namespace {
 
@@ -131,14 +134,22 @@ __device__ __forceinline__ void sum_slots(const SegParams& p, int slice, int64_t
   }
 }
 
-template <int VEC>
+// Barrier over the reducing threads: the whole CTA, or (pipelined kernel) the
+// consumer warps only (named barrier 1; the producer warp never joins).
+template <bool NAMED>
+__device__ __forceinline__ void team_sync(int team) {
+  if constexpr (NAMED) asm volatile("bar.sync 1, %0;" ::"r"(team) : "memory");
+  else __syncthreads();
+}
+
+template <int VEC, bool NAMED = false>
 __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VEC> accv, bool act,
                                                int64_t col, int slice, int32_t row, int32_t rbb,
-                                               int32_t re, int32_t ps, int* s_flag) {
+                                               int32_t re, int32_t ps, int* s_flag, int team) {
   constexpr int L = kPieceLen;
   constexpr int GRP = 32;
   const float* acc = accv.v;
-  const int64_t slice_w = int64_t(blockDim.x) * VEC;
+  const int64_t slice_w = int64_t(team) * VEC;
   const int32_t base = p.piece_base[rbb];
   const int32_t piece = (ps - rbb) / L;
   const int32_t npieces = (re - rbb + L - 1) / L;
@@ -155,9 +166,9 @@ __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VE
       __stcg(reinterpret_cast<float4*>(pp + v), make_float4(acc[v], acc[v + 1], acc[v + 2], acc[v + 3]));
   }
   __threadfence();
-  __syncthreads();
+  team_sync<NAMED>(team);
   if (threadIdx.x == 0) *s_flag = atomicAdd(cnt1 + base + g0, 1) == gn - 1;
-  __syncthreads();
+  team_sync<NAMED>(team);
   if (*s_flag) {                       // last piece of its group: sum the group
     __threadfence();
     float tot[VEC];
@@ -165,7 +176,7 @@ __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VE
     if (ngroups == 1) {
       if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
     } else {
-      __syncthreads();                 // every thread has read the group's slots
+      team_sync<NAMED>(team);                 // every thread has read the group's slots
       float* gp = p.partial + (int64_t(slice) * p.nslots_cap + base + g0) * slice_w + threadIdx.x * VEC;
       if (act) {
 #pragma unroll
@@ -173,9 +184,9 @@ __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VE
           __stcg(reinterpret_cast<float4*>(gp + v), make_float4(tot[v], tot[v + 1], tot[v + 2], tot[v + 3]));
       }
       __threadfence();
-      __syncthreads();
+      team_sync<NAMED>(team);
       if (threadIdx.x == 0) *s_flag = atomicAdd(cnt2 + base, 1) == ngroups - 1;
-      __syncthreads();
+      team_sync<NAMED>(team);
       if (*s_flag) {                   // last group: sum the group partials in order
         __threadfence();
         sum_slots<VEC>(p, slice, slice_w, base, ngroups, GRP, act, tot);
@@ -183,7 +194,7 @@ __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VE
       }
     }
   }
-  __syncthreads();
+  team_sync<NAMED>(team);
 }
 
 // blockDim.x = row vectors of one column slice (32..256); one CTA per chunk.
@@ -305,7 +316,7 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
           FVec<VEC> av;
 #pragma unroll
           for (int v = 0; v < VEC; ++v) av.v[v] = accf[v];
-          finish_long_piece<VEC>(p, av, act, col, slice, row, rb, re, ps, &s_flag);
+          finish_long_piece<VEC>(p, av, act, col, slice, row, rb, re, ps, &s_flag, blockDim.x);
         }
       }
     }
@@ -323,6 +334,278 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined variant (bag backward, dense_accumulate == false): a persistent CTA
+// per SM walks work items (slice-major: all chunks of column slice 0, then
+// slice 1, ... so the GPU-wide working set of dy stays one slice wide).  One
+// producer warp decodes each chunk's metadata into a 2-stage shared ring and
+// issues one bulk copy (cp.async.bulk, 1-D TMA) per position for the dy row
+// slice, plus the value row slice at piece starts, into a ring of nslots
+// shared-memory row slots completed by mbarrier transaction counts.  The
+// consumer warps (one 16-byte vector per thread, as in seg_kernel) read rows
+// from shared memory: the copies of the next ~nslots positions are in flight
+// while a batch is reduced, instead of one register batch per round trip.
+constexpr uint32_t kSegSpin = 1u << 28;   // bounded waits: trap instead of hanging
+constexpr int kMetaStages = 4;
+
+struct SegMeta { int t, key, fl, pos, rr, rb, re; float w; };
+
+__device__ __forceinline__ uint32_t sm_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = sm_addr(b);
+  uint32_t ok = 0, n = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (++n > kSegSpin) __trap();
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(sm_addr(dst)),
+      "l"(src), "r"(bytes), "r"(sm_addr(b)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(sm_addr(p)));
+  return r;
+}
+
+// dynamic smem: [2*nslots] mbarriers (full, empty), pad to 128, nslots x (dy, V) row slots
+template <typename T, bool DW>
+__global__ void __launch_bounds__(320, 1) seg_pipe_kernel(SegParams p, int nslots, int64_t nchunks,
+                                                          int nslices) {
+  constexpr int VEC = Vec<T>::N;
+  constexpr int NB = 8;
+  constexpr int L = kPieceLen;
+  constexpr int MS = kMetaStages;
+  __shared__ SegMeta s_meta[MS][kMeta];
+  __shared__ int s_rng[MS][2];
+  __shared__ uint64_t s_mfull[MS], s_mempty[MS];
+  __shared__ float s_red[2][8][NB];
+  __shared__ int s_flag;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+  uint64_t* empty = full + nslots;
+  const int team = blockDim.x - 64;             // consumer threads (+ issue warp + metadata warp)
+  const int cwarps = team >> 5;
+  const int slice_units = min(team, p.vec_units);
+  const uint32_t RB = uint32_t(slice_units) * 16u;   // bytes of one row slice
+  // nslots = stages of NB positions: [NB dy row slices][NB value row slices]
+  unsigned char* rows = dsm + ((2 * nslots * 8 + 127) / 128) * 128;
+  auto slot_dy = [&](int sl, int j) { return rows + (size_t(sl) * 2 * NB + j) * RB; };
+  auto slot_v = [&](int sl, int j) { return rows + (size_t(sl) * 2 * NB + NB + j) * RB; };
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < nslots; ++i) { bar_init(&full[i], 1); bar_init(&empty[i], cwarps); }
+    for (int i = 0; i < MS; ++i) { bar_init(&s_mfull[i], 32); bar_init(&s_mempty[i], cwarps + 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t items = nchunks * nslices;
+
+  if (warp == cwarps + 1) {
+    // --------------------------------------------- metadata warp (runs ahead)
+    int it = 0;
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      const int64_t c0 = (w % nchunks) * kChunk;
+      const int ms = it % MS;
+      const uint32_t mu = uint32_t(it / MS);
+      if (mu > 0) bar_wait(&s_mempty[ms], (mu - 1) & 1);
+      int kmin = 0x7fffffff, kmax = -1;
+#pragma unroll
+      for (int r = 0; r < (kMeta + 31) / 32; ++r) {
+        const int k = lane + 32 * r;
+        if (k >= kMeta) break;
+        const int64_t i = c0 + k;
+        SegMeta m{0, 0, 0, 0, 0, 0, 0, 0.f};
+        if (i < p.P) {
+          m.pos = p.spos[i];
+          m.key = p.skey[i];
+          m.rr = p.excl[i] - 1 + p.flags[i];
+          m.w = p.w[m.pos];
+          m.t = m.pos / p.B;
+          m.rb = p.run_begin[m.rr];
+          m.re = p.run_begin[m.rr + 1];
+          const int32_t ps = m.rb + ((int32_t(i) - m.rb) / L) * L;
+          const int32_t pe = min(m.re, ps + L);
+          m.fl = (int32_t(i) == ps ? 1 : 0) | (int32_t(i) == pe - 1 ? 2 : 0);
+          if ((m.fl & 1) && k < kChunk) {
+            kmin = min(kmin, k);
+            kmax = max(kmax, int(pe - c0));
+          }
+        }
+        s_meta[ms][k] = m;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+      }
+      if (lane == 0) { s_rng[ms][0] = kmin; s_rng[ms][1] = kmax; }
+      __syncwarp();
+      bar_arrive(&s_mfull[ms]);                 // 32 arrivals: every lane's writes released
+    }
+    return;
+  }
+  if (warp == cwarps) {
+    // ------------------------------------------------ copy-issue warp (lane 0)
+    if (lane != 0) return;
+    const uint64_t pol_keep = l2_evict_last_policy();     // dy: re-read ~B times
+    const uint64_t pol_stream = l2_evict_first_policy();  // V: once per piece
+    const uint32_t lds = uint32_t(p.lds_bytes);
+    const uint64_t ldv = uint64_t(p.ldv_bytes);
+    int ps_slot = 0;            // next stage, its phase, whether the ring has wrapped once
+    uint32_t ps_phase = 0;
+    bool ps_used = false;
+    int it = 0;
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      const int slice = int(w / nchunks);
+      const int ms = it % MS;
+      bar_wait(&s_mfull[ms], uint32_t(it / MS) & 1);
+      const int kmin = s_rng[ms][0], kmax = s_rng[ms][1];
+      const char* srcb = p.src + (int64_t(p.src_col0) + int64_t(slice) * team * VEC) * int64_t(sizeof(T));
+      const char* vb = DW ? p.V + (int64_t(p.v_col0) + int64_t(slice) * team * VEC) * int64_t(sizeof(T))
+                          : nullptr;
+      for (int kb = kmin; kb < kmax; kb += NB) {   // one stage per consumer batch
+        const int sl = ps_slot;
+        if (ps_used) bar_wait(&empty[sl], ps_phase ^ 1u);
+        if (++ps_slot == nslots) { ps_slot = 0; ps_phase ^= 1u; ps_used = true; }
+        const int nb = min(NB, kmax - kb);
+        uint32_t rows_in = uint32_t(nb);
+        if constexpr (DW) {
+          for (int j = 0; j < nb; ++j) rows_in += uint32_t(s_meta[ms][kb + j].fl & 1);
+        }
+        bar_expect_tx(&full[sl], rows_in * RB);
+        for (int j = 0; j < nb; ++j) {
+          const SegMeta& m = s_meta[ms][kb + j];
+          bulk_g2s(slot_dy(sl, j), srcb + uint64_t(uint32_t(m.t)) * lds, RB, &full[sl], pol_keep);
+          if (DW && (m.fl & 1))
+            bulk_g2s(slot_v(sl, j), vb + uint64_t(uint32_t(m.key)) * ldv, RB, &full[sl], pol_stream);
+        }
+      }
+      bar_arrive(&s_mempty[ms]);                // done reading this chunk's metadata
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const bool act = tid < slice_units;
+  constexpr int V2 = VEC / 2;
+  float2 acc[V2], g[V2];
+#pragma unroll
+  for (int v = 0; v < V2; ++v) acc[v] = g[v] = make_float2(0.f, 0.f);
+  int cs_slot = 0;               // slot of the next position and its full-barrier phase
+  uint32_t cs_phase = 0;
+  int it = 0, buf = 0;
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+    const int slice = int(w / nchunks);
+    const int64_t c0 = (w % nchunks) * kChunk;
+    const int ms = it % MS;
+    bar_wait(&s_mfull[ms], uint32_t(it / MS) & 1);
+    const SegMeta* M = s_meta[ms];
+    const int k_first = s_rng[ms][0], k_end = s_rng[ms][1];
+    const int64_t col = int64_t(slice) * team * VEC + int64_t(tid) * VEC;
+    for (int kb = k_first; kb < k_end; kb += NB) {
+      const int nb = min(NB, k_end - kb);
+      uint4 d[NB];
+      uint4 vr[DW ? NB : 1];
+      int fl[NB];
+      bar_wait(&full[cs_slot], cs_phase);
+      // every thread reads its 16 bytes of each row slot (slots past nb, or
+      // value slots not filled this batch, hold stale data that is never used;
+      // threads past the slice read the padding after the ring)
+      {
+        const unsigned char* sd = slot_dy(cs_slot, 0) + tid * 16;
+        const unsigned char* sv = slot_v(cs_slot, 0) + tid * 16;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          fl[j] = j < nb ? M[kb + j].fl : 0;
+          d[j] = *reinterpret_cast<const uint4*>(sd + size_t(j) * RB);
+          if constexpr (DW) vr[j] = *reinterpret_cast<const uint4*>(sv + size_t(j) * RB);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&empty[cs_slot]);
+      if (++cs_slot == nslots) { cs_slot = 0; cs_phase ^= 1u; }
+      float part[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        part[j] = 0.f;
+        if (j >= nb) continue;
+        const int k = kb + j;
+        if (fl[j] & 1) {
+#pragma unroll
+          for (int v = 0; v < V2; ++v) acc[v] = make_float2(0.f, 0.f);
+          if constexpr (DW) Vec<T>::load(vr[j], reinterpret_cast<float*>(g));
+        }
+        float2 f[V2];
+        Vec<T>::load(d[j], reinterpret_cast<float*>(f));
+        const float wv = M[k].w;
+        const float2 w2 = make_float2(wv, wv);
+        if constexpr (DW) {
+          float2 pr = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int v = 0; v < V2; ++v) pr = ffma2(f[v], g[v], pr);
+          part[j] = act ? pr.x + pr.y : 0.f;   // threads past the slice read padding
+        }
+#pragma unroll
+        for (int v = 0; v < V2; ++v) acc[v] = ffma2(w2, f[v], acc[v]);
+        if (fl[j] & 2) {
+          const int32_t rr = M[k].rr, rb = M[k].rb, re = M[k].re;
+          const float* accf = reinterpret_cast<const float*>(acc);
+          if (re - rb <= L) {
+            if (act) store_vec<VEC>(p.out + int64_t(rr) * p.ldo + col, accf, false);
+          } else {
+            const int32_t i = int32_t(c0) + k;
+            const int32_t ps = rb + ((i - rb) / L) * L;
+            FVec<VEC> av;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) av.v[v] = accf[v];
+            finish_long_piece<VEC, true>(p, av, act, col, slice, rr, rb, re, ps, &s_flag, team);
+          }
+        }
+      }
+      if constexpr (DW) {
+        TransposeReduce<NB, 16>::run(part, lane);   // lane l: warp sum of slot (l >> 2) & 7
+        if ((lane & 3) == 0) s_red[buf][warp][lane >> 2] = part[0];
+        team_sync<true>(team);
+        if (tid < nb) {
+          float t = 0.f;
+          for (int w2 = 0; w2 < cwarps; ++w2) t += s_red[buf][w2][tid];
+          p.dw_part[int64_t(slice) * p.P + M[kb + tid].pos] = t;
+        }
+        buf ^= 1;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) bar_arrive(&s_mempty[ms]);
+  }
+}
+
 __global__ void sum_slices_kernel(const float* part, int ns, int64_t P, float* dw) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= P) return;
@@ -332,7 +615,18 @@ __global__ void sum_slices_kernel(const float* part, int ns, int64_t P, float* d
 }
 
 // team size: one thread per 16-byte row vector, 32..256 threads
-int team_threads(int64_t vu) { return vu <= 32 ? 32 : (vu >= 256 ? 256 : int(vu)); }
+static int team_cap() {
+  static const int v = [] {
+    const char* e = std::getenv("ML_SEG_TEAM");
+    const int c = e ? std::atoi(e) : 256;
+    return (c == 32 || c == 64 || c == 128) ? c : 256;
+  }();
+  return v;
+}
+int team_threads(int64_t vu) {
+  const int cap = team_cap();
+  return vu <= 32 ? 32 : (vu >= cap ? cap : int(vu));
+}
 
 template <typename T>
 mlStatus dispatch_seg(int threads, bool dw, dim3 grid, const SegParams& p, cudaStream_t s,
@@ -343,11 +637,42 @@ mlStatus dispatch_seg(int threads, bool dw, dim3 grid, const SegParams& p, cudaS
   return ML_OK;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+// pipelined kernel: CTAs per SM (1 or 2) and row-slot ring from the smem budget
+template <typename T, bool DW>
+mlStatus dispatch_pipe(int team, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
+                       const char* name) {
+  static const int ctas = std::max(1, std::min(2, env_int("ML_SEG_CTAS", 1)));
+  const int slice_units = std::min<int64_t>(team, p.vec_units);
+  const size_t rb = size_t(slice_units) * 16;
+  const size_t budget = (ctas == 1 ? 200 * 1024 : 100 * 1024);
+  const size_t stage = 2 * 8 * rb;   // NB = 8 dy + 8 value row slices
+  int nslots = int((budget - 128) / (stage + 16));
+  nslots = std::max(2, std::min(nslots, env_int("ML_SEG_SLOTS", 64)));
+  const size_t smem = ((2 * size_t(nslots) * 8 + 127) / 128) * 128 + size_t(nslots) * stage +
+                      size_t(team) * 16;   // padding: reads of threads past a narrow slice
+  static bool attr = false;
+  if (!attr) {
+    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(210 * 1024)));
+    attr = true;
+  }
+  const int64_t items = nchunks * ns;
+  const unsigned grid = unsigned(std::min<int64_t>(items, int64_t(num_sms()) * ctas));
+  seg_pipe_kernel<T, DW><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
+  ML_LAUNCH_CHECK(name);
+  return ML_OK;
+}
+
 }  // namespace
 
 int seg_slices(int32_t dv, mlDtype dt) {
   const int64_t vu = int64_t(dv) * int64_t(dtype_size(dt)) / 16;
-  return vu <= 256 ? 1 : int(vu / 256);
+  return vu <= team_cap() ? 1 : int(vu / team_cap());
 }
 
 static int64_t nslots_cap(int64_t P) { return 2 * (P / kPieceLen) + 2; }
@@ -366,7 +691,7 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   const int64_t vu = int64_t(a.dv) * int64_t(dtype_size(a.dtype)) / 16;
   const int threads = team_threads(vu);
   const int ns = seg_slices(a.dv, a.dtype);
-  if (vu > 256 && vu % 256) return fail(ML_ERR_CONFIG, "segreduce: row vectors must divide into slices of 256");
+  if (vu > team_cap() && vu % team_cap()) return fail(ML_ERR_CONFIG, "segreduce: row vectors must divide into slices of 256");
   if (a.P >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "segreduce: too many positions");
   if (a.lds * int64_t(dtype_size(a.dtype)) >= (int64_t(1) << 32))
     return fail(ML_ERR_UNSUPPORTED, "segreduce: source row pitch too large");
@@ -388,6 +713,19 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   const int64_t nchunks = (a.P + kChunk - 1) / kChunk;
   dim3 grid{unsigned(nchunks), unsigned(ns), 1u};
   const bool dw = a.V != nullptr;
+  // bulk copies need 16-byte aligned row slices (row pitches and column offsets)
+  const bool aligned = p.lds_bytes % 16 == 0 && (a.src_col0 * es) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(a.src) % 16 == 0 &&
+                       (!dw || (p.ldv_bytes % 16 == 0 && (a.v_col0 * es) % 16 == 0 &&
+                                reinterpret_cast<uintptr_t>(a.V) % 16 == 0));
+  static const bool pipe = env_int("ML_SEG_PIPE", 1) != 0;
+  if (pipe && !a.dense_accumulate && aligned) {
+    if (a.dtype == ML_BF16)
+      return dw ? dispatch_pipe<__nv_bfloat16, true>(threads, ns, nchunks, p, s, a.name)
+                : dispatch_pipe<__nv_bfloat16, false>(threads, ns, nchunks, p, s, a.name);
+    return dw ? dispatch_pipe<float, true>(threads, ns, nchunks, p, s, a.name)
+              : dispatch_pipe<float, false>(threads, ns, nchunks, p, s, a.name);
+  }
   if (a.dtype == ML_BF16) return dispatch_seg<__nv_bfloat16>(threads, dw, grid, p, s, a.name);
   return dispatch_seg<float>(threads, dw, grid, p, s, a.name);
 }
