@@ -85,15 +85,18 @@ __device__ __forceinline__ void st_v8(float* o, const float* a) {
 // thread owns 32 contiguous bytes: one 256-bit store (full sectors).
 template <int VEC, bool WIDE = true>
 __device__ __forceinline__ void store_vec(float* o, const float* acc, bool dense) {
-  if constexpr (VEC == 8 && WIDE) {
-    if (dense) {
-      const float4 b0 = *reinterpret_cast<const float4*>(o);
-      const float4 b1 = *reinterpret_cast<const float4*>(o + 4);
-      float c[8] = {acc[0] + b0.x, acc[1] + b0.y, acc[2] + b0.z, acc[3] + b0.w,
-                    acc[4] + b1.x, acc[5] + b1.y, acc[6] + b1.z, acc[7] + b1.w};
-      st_v8(o, c);
-    } else {
-      st_v8(o, acc);
+  if constexpr (VEC % 8 == 0 && WIDE) {
+#pragma unroll
+    for (int h = 0; h < VEC; h += 8) {
+      if (dense) {
+        const float4 b0 = *reinterpret_cast<const float4*>(o + h);
+        const float4 b1 = *reinterpret_cast<const float4*>(o + h + 4);
+        float c[8] = {acc[h] + b0.x, acc[h + 1] + b0.y, acc[h + 2] + b0.z, acc[h + 3] + b0.w,
+                      acc[h + 4] + b1.x, acc[h + 5] + b1.y, acc[h + 6] + b1.z, acc[h + 7] + b1.w};
+        st_v8(o + h, c);
+      } else {
+        st_v8(o + h, acc + h);
+      }
     }
   } else {
 #pragma unroll
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
 // from shared memory: the copies of the next ~nslots positions are in flight
 // while a batch is reduced, instead of one register batch per round trip.
 constexpr uint32_t kSegSpin = 1u << 28;   // bounded waits: trap instead of hanging
-constexpr int kMetaStages = 4;
+constexpr int kMetaStages = 3;
 
 struct SegMeta { int t, key, fl, pos, rr, rb, re; float w; };
 
@@ -385,20 +388,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(sm_addr(b)), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ uint4 lds_v4(const void* p) {
-  uint4 r;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "r"(sm_addr(p)));
-  return r;
-}
 
-// dynamic smem: [2*nslots] mbarriers (full, empty), pad to 128, nslots x (dy, V) row slots
-template <typename T, bool DW>
-__global__ void __launch_bounds__(320, 1) seg_pipe_kernel(SegParams p, int nslots, int64_t nchunks,
-                                                          int nslices) {
+// dynamic smem: [2*nslots] mbarriers (full, empty), pad to 128, nslots x (dy, V) row slots.
+// UPT = 16-byte row vectors per consumer thread, NB = positions per batch / stage.
+template <typename T, bool DW, int UPT, int NB>
+__global__ void __launch_bounds__(UPT == 2 ? 192 : 320, UPT == 2 ? 2 : 1)
+    seg_pipe_kernel(SegParams p, int nslots, int64_t nchunks, int nslices) {
   constexpr int VEC = Vec<T>::N;
-  constexpr int NB = 8;
+  constexpr int TV = VEC * UPT;                 // elements per consumer thread
   constexpr int L = kPieceLen;
   constexpr int MS = kMetaStages;
   __shared__ SegMeta s_meta[MS][kMeta];
@@ -411,7 +408,7 @@ __global__ void __launch_bounds__(320, 1) seg_pipe_kernel(SegParams p, int nslot
   uint64_t* empty = full + nslots;
   const int team = blockDim.x - 64;             // consumer threads (+ issue warp + metadata warp)
   const int cwarps = team >> 5;
-  const int slice_units = min(team, p.vec_units);
+  const int slice_units = min(team * UPT, p.vec_units);
   const uint32_t RB = uint32_t(slice_units) * 16u;   // bytes of one row slice
   // nslots = stages of NB positions: [NB dy row slices][NB value row slices]
   unsigned char* rows = dsm + ((2 * nslots * 8 + 127) / 128) * 128;
@@ -487,8 +484,8 @@ __global__ void __launch_bounds__(320, 1) seg_pipe_kernel(SegParams p, int nslot
       const int ms = it % MS;
       bar_wait(&s_mfull[ms], uint32_t(it / MS) & 1);
       const int kmin = s_rng[ms][0], kmax = s_rng[ms][1];
-      const char* srcb = p.src + (int64_t(p.src_col0) + int64_t(slice) * team * VEC) * int64_t(sizeof(T));
-      const char* vb = DW ? p.V + (int64_t(p.v_col0) + int64_t(slice) * team * VEC) * int64_t(sizeof(T))
+      const char* srcb = p.src + (int64_t(p.src_col0) + int64_t(slice) * team * TV) * int64_t(sizeof(T));
+      const char* vb = DW ? p.V + (int64_t(p.v_col0) + int64_t(slice) * team * TV) * int64_t(sizeof(T))
                           : nullptr;
       for (int kb = kmin; kb < kmax; kb += NB) {   // one stage per consumer batch
         const int sl = ps_slot;
@@ -513,12 +510,14 @@ __global__ void __launch_bounds__(320, 1) seg_pipe_kernel(SegParams p, int nslot
   }
 
   // -------------------------------------------------------------- consumers
-  const bool act = tid < slice_units;
-  constexpr int V2 = VEC / 2;
+  const bool act = tid * UPT < slice_units;
+  constexpr int V2 = TV / 2;
+  constexpr int LG = NB == 8 ? 3 : (NB == 4 ? 2 : 1);
+  static_assert(NB == (1 << LG), "NB must be 2, 4 or 8");
   float2 acc[V2], g[V2];
 #pragma unroll
   for (int v = 0; v < V2; ++v) acc[v] = g[v] = make_float2(0.f, 0.f);
-  int cs_slot = 0;               // slot of the next position and its full-barrier phase
+  int cs_slot = 0;               // stage of the next batch and its full-barrier phase
   uint32_t cs_phase = 0;
   int it = 0, buf = 0;
   for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++it) {
@@ -528,70 +527,75 @@ __global__ void __launch_bounds__(320, 1) seg_pipe_kernel(SegParams p, int nslot
     bar_wait(&s_mfull[ms], uint32_t(it / MS) & 1);
     const SegMeta* M = s_meta[ms];
     const int k_first = s_rng[ms][0], k_end = s_rng[ms][1];
-    const int64_t col = int64_t(slice) * team * VEC + int64_t(tid) * VEC;
+    const int64_t col = int64_t(slice) * team * TV + int64_t(tid) * TV;
     for (int kb = k_first; kb < k_end; kb += NB) {
       const int nb = min(NB, k_end - kb);
-      uint4 d[NB];
-      uint4 vr[DW ? NB : 1];
-      int fl[NB];
       bar_wait(&full[cs_slot], cs_phase);
-      // every thread reads its 16 bytes of each row slot (slots past nb, or
-      // value slots not filled this batch, hold stale data that is never used;
-      // threads past the slice read the padding after the ring)
-      {
-        const unsigned char* sd = slot_dy(cs_slot, 0) + tid * 16;
-        const unsigned char* sv = slot_v(cs_slot, 0) + tid * 16;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          fl[j] = j < nb ? M[kb + j].fl : 0;
-          d[j] = *reinterpret_cast<const uint4*>(sd + size_t(j) * RB);
-          if constexpr (DW) vr[j] = *reinterpret_cast<const uint4*>(sv + size_t(j) * RB);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) bar_arrive(&empty[cs_slot]);
-      if (++cs_slot == nslots) { cs_slot = 0; cs_phase ^= 1u; }
+      // every thread reads its UPT x 16 bytes of each row slot at use (value
+      // slots not filled this batch hold stale data that is never selected;
+      // threads past a narrow slice read the padding after the ring).  The
+      // per-position work is branch-free except for long-run pieces, so the
+      // unrolled batch schedules as one block.
+      const unsigned char* sd = slot_dy(cs_slot, 0) + tid * 16 * UPT;
+      const unsigned char* sv = slot_v(cs_slot, 0) + tid * 16 * UPT;
       float part[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         part[j] = 0.f;
         if (j >= nb) continue;
         const int k = kb + j;
-        if (fl[j] & 1) {
-#pragma unroll
-          for (int v = 0; v < V2; ++v) acc[v] = make_float2(0.f, 0.f);
-          if constexpr (DW) Vec<T>::load(vr[j], reinterpret_cast<float*>(g));
-        }
-        float2 f[V2];
-        Vec<T>::load(d[j], reinterpret_cast<float*>(f));
+        const int flj = M[k].fl;
         const float wv = M[k].w;
-        const float2 w2 = make_float2(wv, wv);
+        const bool st = (flj & 1) != 0;
+        float2 f[V2];
+#pragma unroll
+        for (int u = 0; u < UPT; ++u)
+          Vec<T>::load(*reinterpret_cast<const uint4*>(sd + size_t(j) * RB + u * 16),
+                       reinterpret_cast<float*>(f) + u * VEC);
         if constexpr (DW) {
+          float2 gn[V2];
+#pragma unroll
+          for (int u = 0; u < UPT; ++u)
+            Vec<T>::load(*reinterpret_cast<const uint4*>(sv + size_t(j) * RB + u * 16),
+                         reinterpret_cast<float*>(gn) + u * VEC);
+#pragma unroll
+          for (int v = 0; v < V2; ++v) {
+            g[v].x = st ? gn[v].x : g[v].x;
+            g[v].y = st ? gn[v].y : g[v].y;
+          }
           float2 pr = make_float2(0.f, 0.f);
 #pragma unroll
           for (int v = 0; v < V2; ++v) pr = ffma2(f[v], g[v], pr);
           part[j] = act ? pr.x + pr.y : 0.f;   // threads past the slice read padding
         }
+        const float2 w2 = make_float2(wv, wv);
 #pragma unroll
-        for (int v = 0; v < V2; ++v) acc[v] = ffma2(w2, f[v], acc[v]);
-        if (fl[j] & 2) {
+        for (int v = 0; v < V2; ++v) {
+          acc[v].x = st ? 0.f : acc[v].x;
+          acc[v].y = st ? 0.f : acc[v].y;
+          acc[v] = ffma2(w2, f[v], acc[v]);
+        }
+        if (flj & 2) {
           const int32_t rr = M[k].rr, rb = M[k].rb, re = M[k].re;
           const float* accf = reinterpret_cast<const float*>(acc);
           if (re - rb <= L) {
-            if (act) store_vec<VEC>(p.out + int64_t(rr) * p.ldo + col, accf, false);
+            if (act) store_vec<TV>(p.out + int64_t(rr) * p.ldo + col, accf, false);
           } else {
             const int32_t i = int32_t(c0) + k;
             const int32_t ps = rb + ((i - rb) / L) * L;
-            FVec<VEC> av;
+            FVec<TV> av;
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) av.v[v] = accf[v];
-            finish_long_piece<VEC, true>(p, av, act, col, slice, rr, rb, re, ps, &s_flag, team);
+            for (int v = 0; v < TV; ++v) av.v[v] = accf[v];
+            finish_long_piece<TV, true>(p, av, act, col, slice, rr, rb, re, ps, &s_flag, team);
           }
         }
       }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&empty[cs_slot]);
+      if (++cs_slot == nslots) { cs_slot = 0; cs_phase ^= 1u; }
       if constexpr (DW) {
-        TransposeReduce<NB, 16>::run(part, lane);   // lane l: warp sum of slot (l >> 2) & 7
-        if ((lane & 3) == 0) s_red[buf][warp][lane >> 2] = part[0];
+        TransposeReduce<NB, 16>::run(part, lane);   // lane l: warp sum of slot l >> (5 - LG)
+        if ((lane & ((32 >> LG) - 1)) == 0) s_red[buf][warp][lane >> (5 - LG)] = part[0];
         team_sync<true>(team);
         if (tid < nb) {
           float t = 0.f;
@@ -642,30 +646,39 @@ static int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
-// pipelined kernel: CTAs per SM (1 or 2) and row-slot ring from the smem budget
-template <typename T, bool DW>
-mlStatus dispatch_pipe(int team, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
-                       const char* name) {
-  static const int ctas = std::max(1, std::min(2, env_int("ML_SEG_CTAS", 1)));
-  const int slice_units = std::min<int64_t>(team, p.vec_units);
+// pipelined kernel. cfg 2 (default): 2 CTAs per SM, 32 bytes per consumer
+// thread, batches of 4; cfg 1: 1 CTA per SM, 16 bytes per thread, batches of 8.
+template <typename T, bool DW, int UPT, int NB>
+mlStatus launch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
+                     const char* name, int ctas, size_t budget) {
+  const int team = threads / UPT;
+  const int slice_units = int(std::min<int64_t>(int64_t(team) * UPT, p.vec_units));
   const size_t rb = size_t(slice_units) * 16;
-  const size_t budget = (ctas == 1 ? 200 * 1024 : 100 * 1024);
-  const size_t stage = 2 * 8 * rb;   // NB = 8 dy + 8 value row slices
-  int nslots = int((budget - 128) / (stage + 16));
+  const size_t stage = 2 * size_t(NB) * rb;   // NB dy + NB value row slices
+  const size_t pad = (size_t(team) * UPT - size_t(slice_units)) * 16;
+  int nslots = int((budget - 128 - pad) / (stage + 16));
   nslots = std::max(2, std::min(nslots, env_int("ML_SEG_SLOTS", 64)));
-  const size_t smem = ((2 * size_t(nslots) * 8 + 127) / 128) * 128 + size_t(nslots) * stage +
-                      size_t(team) * 16;   // padding: reads of threads past a narrow slice
+  const size_t smem = ((2 * size_t(nslots) * 8 + 127) / 128) * 128 + size_t(nslots) * stage + pad;
   static bool attr = false;
   if (!attr) {
-    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(210 * 1024)));
+    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW, UPT, NB>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(210 * 1024)));
     attr = true;
   }
   const int64_t items = nchunks * ns;
   const unsigned grid = unsigned(std::min<int64_t>(items, int64_t(num_sms()) * ctas));
-  seg_pipe_kernel<T, DW><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
+  seg_pipe_kernel<T, DW, UPT, NB><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
   ML_LAUNCH_CHECK(name);
   return ML_OK;
+}
+
+template <typename T, bool DW>
+mlStatus dispatch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
+                       const char* name) {
+  static const int cfg = env_int("ML_SEG_PIPE_CFG", 2);
+  if (cfg == 2 && threads >= 64)
+    return launch_pipe<T, DW, 2, 4>(threads, ns, nchunks, p, s, name, 2, 100 * 1024);
+  return launch_pipe<T, DW, 1, 8>(threads, ns, nchunks, p, s, name, 1, 200 * 1024);
 }
 
 }  // namespace
