@@ -380,6 +380,23 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
     if (++n > kSegSpin) __trap();
   }
 }
+// waits of the metadata / copy-issue warps: back off so their spinning does
+// not take issue slots from the consumer warps
+__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t parity) {
+  const uint32_t a = sm_addr(b);
+  uint32_t ok = 0, n = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (++n > kSegSpin) __trap();
+    __nanosleep(64);
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b,
                                          uint64_t pol) {
   asm volatile(
@@ -391,8 +408,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // dynamic smem: [2*nslots] mbarriers (full, empty), pad to 128, nslots x (dy, V) row slots.
 // UPT = 16-byte row vectors per consumer thread, NB = positions per batch / stage.
-template <typename T, bool DW, int UPT, int NB>
-__global__ void __launch_bounds__(UPT == 2 ? 192 : 320, UPT == 2 ? 2 : 1)
+template <typename T, bool DW, int UPT, int NB, int CT>
+__global__ void __launch_bounds__(256 / UPT + 64, CT)
     seg_pipe_kernel(SegParams p, int nslots, int64_t nchunks, int nslices) {
   constexpr int VEC = Vec<T>::N;
   constexpr int TV = VEC * UPT;                 // elements per consumer thread
@@ -431,7 +448,7 @@ __global__ void __launch_bounds__(UPT == 2 ? 192 : 320, UPT == 2 ? 2 : 1)
       const int64_t c0 = (w % nchunks) * kChunk;
       const int ms = it % MS;
       const uint32_t mu = uint32_t(it / MS);
-      if (mu > 0) bar_wait(&s_mempty[ms], (mu - 1) & 1);
+      if (mu > 0) bar_wait_sleep(&s_mempty[ms], (mu - 1) & 1);
       int kmin = 0x7fffffff, kmax = -1;
 #pragma unroll
       for (int r = 0; r < (kMeta + 31) / 32; ++r) {
@@ -482,14 +499,14 @@ __global__ void __launch_bounds__(UPT == 2 ? 192 : 320, UPT == 2 ? 2 : 1)
     for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int slice = int(w / nchunks);
       const int ms = it % MS;
-      bar_wait(&s_mfull[ms], uint32_t(it / MS) & 1);
+      bar_wait_sleep(&s_mfull[ms], uint32_t(it / MS) & 1);
       const int kmin = s_rng[ms][0], kmax = s_rng[ms][1];
       const char* srcb = p.src + (int64_t(p.src_col0) + int64_t(slice) * team * TV) * int64_t(sizeof(T));
       const char* vb = DW ? p.V + (int64_t(p.v_col0) + int64_t(slice) * team * TV) * int64_t(sizeof(T))
                           : nullptr;
       for (int kb = kmin; kb < kmax; kb += NB) {   // one stage per consumer batch
         const int sl = ps_slot;
-        if (ps_used) bar_wait(&empty[sl], ps_phase ^ 1u);
+        if (ps_used) bar_wait_sleep(&empty[sl], ps_phase ^ 1u);
         if (++ps_slot == nslots) { ps_slot = 0; ps_phase ^= 1u; ps_used = true; }
         const int nb = min(NB, kmax - kb);
         uint32_t rows_in = uint32_t(nb);
@@ -648,7 +665,7 @@ static int env_int(const char* name, int dflt) {
 
 // pipelined kernel. cfg 2 (default): 2 CTAs per SM, 32 bytes per consumer
 // thread, batches of 4; cfg 1: 1 CTA per SM, 16 bytes per thread, batches of 8.
-template <typename T, bool DW, int UPT, int NB>
+template <typename T, bool DW, int UPT, int NB, int CT>
 mlStatus launch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
                      const char* name, int ctas, size_t budget) {
   const int team = threads / UPT;
@@ -661,13 +678,13 @@ mlStatus launch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, c
   const size_t smem = ((2 * size_t(nslots) * 8 + 127) / 128) * 128 + size_t(nslots) * stage + pad;
   static bool attr = false;
   if (!attr) {
-    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW, UPT, NB>,
+    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW, UPT, NB, CT>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(210 * 1024)));
     attr = true;
   }
   const int64_t items = nchunks * ns;
   const unsigned grid = unsigned(std::min<int64_t>(items, int64_t(num_sms()) * ctas));
-  seg_pipe_kernel<T, DW, UPT, NB><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
+  seg_pipe_kernel<T, DW, UPT, NB, CT><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
   ML_LAUNCH_CHECK(name);
   return ML_OK;
 }
@@ -676,9 +693,9 @@ template <typename T, bool DW>
 mlStatus dispatch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
                        const char* name) {
   static const int cfg = env_int("ML_SEG_PIPE_CFG", 2);
-  if (cfg == 2 && threads >= 64)
-    return launch_pipe<T, DW, 2, 4>(threads, ns, nchunks, p, s, name, 2, 100 * 1024);
-  return launch_pipe<T, DW, 1, 8>(threads, ns, nchunks, p, s, name, 1, 200 * 1024);
+  if (cfg >= 2 && threads >= 64)
+    return launch_pipe<T, DW, 2, 4, 2>(threads, ns, nchunks, p, s, name, 2, 100 * 1024);
+  return launch_pipe<T, DW, 1, 8, 1>(threads, ns, nchunks, p, s, name, 1, 200 * 1024);
 }
 
 }  // namespace
