@@ -224,6 +224,31 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
                           float* dW1, float* dW2, float* dw_out,
                           void* ws, size_t ws_bytes, void* stream);
 
+/* Forward/backward pair with a precomputed backward state.  The bag
+ * backward's inverse index map ("reverse_indices" preprocessing, PAPER.md
+ * §3.1.4: sort of (idx, position) + runs) depends only on idx_saved,
+ * so memory_layer_fwd_state builds it into the caller-owned `state` buffer
+ * (memory_layer_state_bytes) on a library side stream, concurrent with the
+ * HBM-bound bag forward, and memory_layer_bwd_state consumes it instead of
+ * sorting.  state must not be modified between the two calls; the state is
+ * complete when the forward's stream work is.  Results are bit-identical
+ * to memory_layer_fwd / memory_layer_bwd (same kernels, same order).  Errors:
+ * ML_ERR_WORKSPACE when state_bytes is too small. */
+mlStatus memory_layer_state_bytes(const mlLayerShape* shape, size_t* bytes);
+mlStatus memory_layer_fwd_state(const mlLayerShape* shape, const void* x, const void* q,
+                                const void* K1, const void* K2, const void* V, const void* W1,
+                                const void* W2, void* out, int32_t* idx_saved, float* w_saved,
+                                void* g_saved, void* y_saved, void* state, size_t state_bytes,
+                                void* ws, size_t ws_bytes, void* stream);
+mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, const void* x,
+                                const void* q, const void* K1, const void* K2, const void* V,
+                                const void* W1, const void* W2, const int32_t* idx_saved,
+                                const float* w_saved, const void* g_saved, const void* y_saved,
+                                const void* state, size_t state_bytes, void* dx, float* dq,
+                                float* dK1, float* dK2, int32_t* dV_rows, float* dV, int32_t* U,
+                                float* dW1, float* dW2, float* dw_out, void* ws, size_t ws_bytes,
+                                void* stream);
+
 /* ------------------------------------------- memory group pieces (a7, a12)
  * Parallel memory (§3.1.2, Fig. 2): the value table is
  * sharded along the embedding dim over the G ranks of a memory group; the

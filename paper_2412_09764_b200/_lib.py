@@ -73,6 +73,9 @@ SIGNATURES = {
     "memory_layer_fwd": [C.POINTER(LayerShape)] + [P] * 13 + [SZ, P],
     "memory_layer_bwd_workspace": [C.POINTER(LayerShape), C.POINTER(SZ)],
     "memory_layer_bwd": [C.POINTER(LayerShape)] + [P] * 23 + [SZ, P],
+    "memory_layer_state_bytes": [C.POINTER(LayerShape), C.POINTER(SZ)],
+    "memory_layer_fwd_state": [C.POINTER(LayerShape)] + [P] * 13 + [SZ, P, SZ, P],
+    "memory_layer_bwd_state": [C.POINTER(LayerShape)] + [P] * 13 + [SZ] + [P] * 11 + [SZ, P],
     "ml_group_unpack": [P, C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int, P],
     "ml_group_pack": [P, C.c_int32, C.c_int32, C.c_int32, P, C.c_int, P],
     "ml_gate_bwd": [P, P, P, P, P, P, I64, C.c_int, P],

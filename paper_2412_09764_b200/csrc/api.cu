@@ -53,7 +53,13 @@ static mlStatus aux_for(cudaStream_t caller, Aux** out) {
     return ML_OK;
   }
   Aux* a = new Aux();
-  for (auto& x : a->s) ML_CUDA_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  // aux 1 runs at the highest priority: the inverse-map sort it carries
+  // during the forward interleaves with the (long, HBM-bound) bag forward
+  // instead of waiting for its CTAs to drain
+  int lo = 0, hi = 0;
+  ML_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[0], cudaStreamNonBlocking));
+  ML_CUDA_TRY(cudaStreamCreateWithPriority(&a->s[1], cudaStreamNonBlocking, hi));
   for (auto& e : a->ev) ML_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   m[caller] = a;
   *out = a;
@@ -584,6 +590,30 @@ static void layer_bwd_carve(Carver& c, const mlLayerShape& s, LayerBwdBufs& b) {
   b.gemm_ws2 = c.take<char>(kGemmWs);
 }
 
+// Backward state built by the forward: the sorted inverse index map of the
+// bag backward depends only on the indices, so the forward can compute it on
+// a side stream while the bag forward streams V (HBM-bound).
+struct BagPrepState { SortBufs sort; RunBufs runs; int32_t* rows; int32_t* U; };
+static void state_carve(Carver& c, const mlBagShape& s, BagPrepState& st) {
+  const int64_t P = int64_t(s.T) * s.B;
+  sort_carve(c, P, ceil_log2(s.N), st.sort);
+  runs_carve(c, P, st.runs);
+  st.rows = c.take<int32_t>(std::max<int64_t>(P, 1));
+  st.U = c.take<int32_t>(1);
+}
+
+mlStatus memory_layer_state_bytes(const mlLayerShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_layer(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  BagPrepState b;
+  state_carve(c, bag_of(*shape), b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
 mlStatus memory_layer_fwd_workspace(const mlLayerShape* shape, size_t* bytes) {
   ML_API_BEGIN
   ML_TRY(check_layer(shape));
@@ -600,6 +630,15 @@ mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* 
                           const void* K2, const void* V, const void* W1, const void* W2, void* out,
                           int32_t* idx_saved, float* w_saved, void* g_saved, void* y_saved,
                           void* ws, size_t ws_bytes, void* stream) {
+  return memory_layer_fwd_state(shape, x, q, K1, K2, V, W1, W2, out, idx_saved, w_saved, g_saved,
+                                y_saved, nullptr, 0, ws, ws_bytes, stream);
+}
+
+mlStatus memory_layer_fwd_state(const mlLayerShape* shape, const void* x, const void* q,
+                                const void* K1, const void* K2, const void* V, const void* W1,
+                                const void* W2, void* out, int32_t* idx_saved, float* w_saved,
+                                void* g_saved, void* y_saved, void* state, size_t state_bytes,
+                                void* ws, size_t ws_bytes, void* stream) {
   ML_API_BEGIN
   ML_TRY(check_layer(shape));
   const mlLayerShape& s = *shape;
@@ -623,7 +662,25 @@ mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* 
     ML_TRY(gemm_rm(false, false, T, s.dv, s.D, x, s.D, W1, s.dv, g_saved, s.dv, s.pkm.dtype, false,
                    b.gemm_ws, kGemmWs, aux->s[0]));
   }
+  if (state) {
+    size_t sneed = 0;
+    ML_TRY(memory_layer_state_bytes(shape, &sneed));
+    if (state_bytes < sneed) return fail(ML_ERR_WORKSPACE, "memory_layer_fwd_state: state too small");
+  }
   ML_TRY(pkm_fwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, nullptr, b.pkm, st));
+  if (state) {
+    // the backward's sort + runs on aux 1, overlapping the bag forward
+    if (!aux) ML_TRY(aux_for(st, &aux));
+    Carver sc(state);
+    BagPrepState ps;
+    state_carve(sc, bag_of(s), ps);
+    BagBwdBufs pb{};
+    pb.sort = ps.sort;
+    pb.runs = ps.runs;
+    int32_t *sk = nullptr, *sp = nullptr;
+    ML_TRY(stream_dep(st, aux->s[1], aux->ev[4]));
+    ML_TRY(bag_bwd_prepare(bag_of(s), idx_saved, ps.rows, ps.U, pb, &sk, &sp, aux->s[1]));
+  }
   BagFwdArgs a;
   a.V = V; a.ldv = s.dv; a.N = s.N;
   a.idx = idx_saved; a.w = w_saved; a.B = s.pkm.H * s.pkm.k; a.nbags = T; a.dv = s.dv;
@@ -635,6 +692,7 @@ mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* 
     if (y_saved && y_saved != out)
       ML_CUDA_TRY(cudaMemcpyAsync(y_saved, out, size_t(T) * s.dv * dtype_size(s.pkm.dtype),
                                   cudaMemcpyDeviceToDevice, st));
+    if (state) ML_TRY(stream_dep(aux->s[1], st, aux->ev[5]));   // join the state build
     return check_index_flag(st);
   }
   ML_TRY(stream_dep(aux->s[0], st, aux->ev[1]));   // join: g ready
@@ -644,6 +702,7 @@ mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* 
   // out = z W2  [T, D]
   ML_TRY(gemm_rm(false, false, T, s.D, s.dv, b.z, s.dv, W2, s.D, out, s.D, s.pkm.dtype, false,
                  b.gemm_ws, kGemmWs, st));
+  if (state) ML_TRY(stream_dep(aux->s[1], st, aux->ev[5]));     // join the state build
   return check_index_flag(st);
   ML_API_END
 }
@@ -667,6 +726,19 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
                           void* dx, float* dq, float* dK1, float* dK2, int32_t* dV_rows,
                           float* dV, int32_t* U, float* dW1, float* dW2, float* dw_out, void* ws,
                           size_t ws_bytes, void* stream) {
+  return memory_layer_bwd_state(shape, dout, x, q, K1, K2, V, W1, W2, idx_saved, w_saved, g_saved,
+                                y_saved, nullptr, 0, dx, dq, dK1, dK2, dV_rows, dV, U, dW1, dW2,
+                                dw_out, ws, ws_bytes, stream);
+}
+
+mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, const void* x,
+                                const void* q, const void* K1, const void* K2, const void* V,
+                                const void* W1, const void* W2, const int32_t* idx_saved,
+                                const float* w_saved, const void* g_saved, const void* y_saved,
+                                const void* state, size_t state_bytes, void* dx, float* dq,
+                                float* dK1, float* dK2, int32_t* dV_rows, float* dV, int32_t* U,
+                                float* dW1, float* dW2, float* dw_out, void* ws, size_t ws_bytes,
+                                void* stream) {
   ML_API_BEGIN
   ML_TRY(check_layer(shape));
   const mlLayerShape& s = *shape;
@@ -692,10 +764,32 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
   timing_mark(nullptr, st);
   Aux* aux = nullptr;
   ML_TRY(aux_for(st, &aux));
-  // aux 0: the value-row sort + runs need only the saved indices
-  ML_TRY(stream_dep(st, aux->s[0], aux->ev[0]));
   int32_t *skey = nullptr, *spos = nullptr;
-  ML_TRY(bag_bwd_prepare(bs, idx_saved, dV_rows, U, b.bag, &skey, &spos, aux->s[0]));
+  if (state) {
+    // sorted map from the forward (memory_layer_fwd_state)
+    size_t sneed = 0;
+    ML_TRY(memory_layer_state_bytes(shape, &sneed));
+    if (state_bytes < sneed) return fail(ML_ERR_WORKSPACE, "memory_layer_bwd_state: state too small");
+    Carver sc(const_cast<void*>(state));
+    BagPrepState ps;
+    state_carve(sc, bs, ps);
+    b.bag.sort = ps.sort;
+    b.bag.runs = ps.runs;
+    const int64_t P = int64_t(bs.T) * bs.B;
+    ML_TRY(sorted_result(P, ceil_log2(bs.N), ps.sort, &skey, &spos));
+    if (P == 0) {
+      ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
+    } else {
+      ML_CUDA_TRY(cudaMemcpyAsync(dV_rows, ps.rows, sizeof(int32_t) * size_t(P),
+                                  cudaMemcpyDeviceToDevice, st));
+      ML_CUDA_TRY(cudaMemcpyAsync(U, ps.U, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    }
+    ML_TRY(stream_dep(st, aux->s[0], aux->ev[0]));
+  } else {
+    // aux 0: the value-row sort + runs need only the saved indices
+    ML_TRY(stream_dep(st, aux->s[0], aux->ev[0]));
+    ML_TRY(bag_bwd_prepare(bs, idx_saved, dV_rows, U, b.bag, &skey, &spos, aux->s[0]));
+  }
   if (s.gated) {
     // dz = dout W2^T ; elementwise gate backward -> z, dy, dg
     ML_TRY(gemm_rm(false, true, T, s.dv, s.D, dout, s.D, W2, s.D, b.dz, s.dv, dt, false, b.gemm_ws,

@@ -39,6 +39,8 @@ void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b);
 // On return *keys / *vals point at the sorted arrays (inside b).
 mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b,
                     int32_t** keys, int32_t** vals, cudaStream_t s);
+// Where sort_pairs(n, bits) leaves its result inside b (without sorting).
+mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t** vals);
 
 // --------------------------------------------------- runs of sorted keys
 constexpr int kPieceLen = 32;  // positions per reduction piece (L)

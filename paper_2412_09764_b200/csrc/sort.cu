@@ -264,6 +264,19 @@ void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b) {
   b.scan_tmp = c.take<int32_t>(scan_tmp_elems(int64_t(256) * nb));
 }
 
+mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t** vals) {
+  if (n <= 0) {
+    *keys = b.k[0];
+    *vals = b.v[0];
+    return ML_OK;
+  }
+  if (bits < 1) bits = 1;
+  const int passes = (bits + 7) / 8;
+  *keys = b.k[(passes - 1) & 1];
+  *vals = b.v[(passes - 1) & 1];
+  return ML_OK;
+}
+
 mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, int32_t** keys,
                     int32_t** vals, cudaStream_t s) {
   if (n <= 0) {

@@ -232,8 +232,10 @@ def layer_shape(x, q, K1, V, k, gated, qk_norm=False):
                       V.shape[1], D, 1 if gated else 0)
 
 
-def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, qk_norm=False):
-    """Eq. 1 + Eq. 2 forward.  Returns out [T,D] and the saved tensors."""
+def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, qk_norm=False, keep_state=True):
+    """Eq. 1 + Eq. 2 forward.  Returns out [T,D] and the saved tensors.
+    keep_state: also build the backward's sorted inverse index map (a side
+    stream, overlapping the bag forward) into saved["state"]."""
     sh = layer_shape(x, q, K1, V, k, gated, qk_norm)
     T, H = q.shape[0], q.shape[1]
     dev = q.device
@@ -244,10 +246,16 @@ def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, qk_norm=False):
     y = torch.empty((T, V.shape[1]), dtype=V.dtype, device=dev) if gated else None
     n = _size(lib().memory_layer_fwd_workspace, sh)
     ws = workspace(n, dev)
-    check(lib().memory_layer_fwd(C.byref(sh), _p(x if gated else None), _p(q), _p(K1), _p(K2),
-                                 _p(V), _p(W1 if gated else None), _p(W2 if gated else None),
-                                 _p(out), _p(idx), _p(w), _p(g), _p(y), _p(ws), n, _stream()))
-    return out, dict(idx=idx, w=w, g=g, y=y, k=k, gated=gated, qk_norm=qk_norm)
+    state, ns = None, 0
+    if keep_state:
+        ns = _size(lib().memory_layer_state_bytes, sh)
+        state = torch.empty((max(ns, 1),), dtype=torch.uint8, device=dev)
+    check(lib().memory_layer_fwd_state(C.byref(sh), _p(x if gated else None), _p(q), _p(K1),
+                                       _p(K2), _p(V), _p(W1 if gated else None),
+                                       _p(W2 if gated else None), _p(out), _p(idx), _p(w), _p(g),
+                                       _p(y), _p(state), ns, _p(ws), n, _stream()))
+    return out, dict(idx=idx, w=w, g=g, y=y, k=k, gated=gated, qk_norm=qk_norm, state=state,
+                     state_bytes=ns)
 
 
 class LayerGrads(dict):
@@ -284,10 +292,11 @@ def memory_layer_bwd(dout, x, q, K1, K2, V, W1, W2, saved, dK1=None, dK2=None, w
     dw = buf("dw", (T, H, k), torch.float32) if want_dw else None
     n = _size(lib().memory_layer_bwd_workspace, sh)
     ws = workspace(n, dev, tag="bwd")
-    check(lib().memory_layer_bwd(
+    check(lib().memory_layer_bwd_state(
         C.byref(sh), _p(dout), _p(x if gated else None), _p(q), _p(K1), _p(K2), _p(V),
         _p(W1 if gated else None), _p(W2 if gated else None), _p(saved["idx"]), _p(saved["w"]),
-        _p(saved["g"]), _p(saved["y"]), _p(dx), _p(dq), _p(dK1), _p(dK2), _p(rows), _p(dV),
+        _p(saved["g"]), _p(saved["y"]), _p(saved.get("state")), saved.get("state_bytes", 0),
+        _p(dx), _p(dq), _p(dK1), _p(dK2), _p(rows), _p(dV),
         _p(U), _p(dW1), _p(dW2), _p(dw), _p(ws), n, _stream()))
     return LayerGrads(dq=dq, dK1=dK1, dK2=dK2, rows=rows, dV=dV, U=U, dx=dx, dW1=dW1, dW2=dW2,
                       dw=dw)

@@ -284,6 +284,34 @@ def test_memory_layer_fwd_bwd(dtype, T, H, S, Dk, k, dv, D, gated):
         assert_close(host(g["dW2"]), r["dW2"], tol, "dW2")
 
 
+@pytest.mark.parametrize("dtype,T,H,S,Dk,k,dv,D,gated", [LAYER_CASES[0], LAYER_CASES[3]])
+def test_memory_layer_state_path_bit_identical(dtype, T, H, S, Dk, k, dv, D, gated):
+    """memory_layer_fwd_state / memory_layer_bwd_state (inverse map built by
+    the forward on a side stream) == the plain pair, bit for bit."""
+    seed = 13
+    f = lambda tag, shape, sc=1.0: gen.tensor(seed, tag, shape, scale=sc, dtype=dtype)
+    h = dict(x=f("x", (T, D)), q=f("q", (T, H, Dk)),
+             K1=f("K1", (H, S, Dk // 2), gen.scale_for("K1", Dk=Dk)),
+             K2=f("K2", (H, S, Dk // 2), gen.scale_for("K2", Dk=Dk)),
+             V=f("V", (S * S, dv)), W1=f("W1", (D, dv), gen.scale_for("W1", D=D)),
+             W2=f("W2", (dv, D), gen.scale_for("W2", dv=dv)), dout=f("dout", (T, D)))
+    t = {n: dev(a, dtype) for n, a in h.items()}
+    o = ops()
+    res = []
+    for keep in (False, True):
+        out, saved = o.memory_layer_fwd(t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"],
+                                        t["W2"], k, gated=gated, keep_state=keep)
+        assert (saved["state"] is not None) == keep
+        g = o.memory_layer_bwd(t["dout"], t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"],
+                               t["W2"], saved, want_dw=True)
+        U = int(g["U"].item())
+        res.append(dict(out=host(out), U=U, rows=host(g["rows"][:U]), dV=host(g["dV"][:U]),
+                        dw=host(g["dw"]), dq=host(g["dq"]), dK1=host(g["dK1"]), dx=host(g["dx"])))
+    a, b = res
+    for n in a:
+        assert np.array_equal(a[n], b[n]), n
+
+
 # ------------------------------------------------------------ edge cases
 def test_out_of_range_index_reported_under_check_mode():
     """S:233 index error: with ML_CHECK_INDICES=1 an index >= N is reported
