@@ -9,7 +9,9 @@
 // its 512 keys with __match_any_sync and warp-private digit counters, the
 // CTA combines warps in order, a device-wide exclusive scan over the
 // digit-major [digit][block] count matrix gives every (digit, block) its
-// output offset.  Digits are <= 8 bits; passes = ceil(bits / 8).
+// output offset; the scatter stages the block's pairs in digit order in
+// shared memory and writes each digit run contiguously.  Digits are <= 11
+// bits; passes = ceil(bits / 11) (2 for a 2^20-row table).
 #include "internal.cuh"
 
 namespace ml {
@@ -107,6 +109,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const int32_t* 
 constexpr int kSortWarps = 8;
 constexpr int kSortRounds = 16;
 constexpr int kSortTile = kSortWarps * kSortRounds * 32;  // 4096
+constexpr int kMaxDigitBits = 11;
 
 struct SortPassParams {
   const int32_t* kin; const int32_t* vin;  // vin == nullptr -> value = position
@@ -125,40 +128,62 @@ __device__ __forceinline__ int32_t load_key(const SortPassParams& p, int64_t i, 
   return k;
 }
 
+// dynamic smem: s_cnt[kSortWarps][nbins]
 __global__ void __launch_bounds__(256) sort_hist_kernel(SortPassParams p, bool first) {
-  __shared__ int s_cnt[kSortWarps][256];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  extern __shared__ int s_dyn[];
   const int nbins = 1 << p.dbits;
-  for (int d = lane; d < 256; d += 32) s_cnt[wid][d] = 0;
-  __syncwarp();
+  int* s_cnt = s_dyn;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int d = threadIdx.x; d < kSortWarps * nbins; d += 256) s_cnt[d] = 0;
+  __syncthreads();
   const int64_t wbase = int64_t(blockIdx.x) * kSortTile + int64_t(wid) * kSortRounds * 32;
   const uint32_t mask = uint32_t(nbins - 1);
+  int32_t key[kSortRounds];
+#pragma unroll
+  for (int r = 0; r < kSortRounds; ++r) {       // all loads first
+    const int64_t i = wbase + r * 32 + lane;
+    key[r] = i < p.n ? load_key(p, i, first) : 0;
+  }
+#pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
     const int64_t i = wbase + r * 32 + lane;
     const bool valid = i < p.n;
-    const uint32_t dig = valid ? ((uint32_t(load_key(p, i, first)) >> p.shift) & mask) : 0x10000u;
+    const uint32_t dig = valid ? ((uint32_t(key[r]) >> p.shift) & mask) : 0x10000u;
     const unsigned peers = __match_any_sync(0xffffffffu, dig);
-    if (valid && lane == __ffs(peers) - 1) s_cnt[wid][dig] += __popc(peers);
+    if (valid && lane == __ffs(peers) - 1) s_cnt[wid * nbins + dig] += __popc(peers);
     __syncwarp();
   }
   __syncthreads();
   for (int d = threadIdx.x; d < nbins; d += 256) {
     int t = 0;
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) t += s_cnt[w][d];
+    for (int w = 0; w < kSortWarps; ++w) t += s_cnt[w * nbins + d];
     p.counts[int64_t(d) * p.nblocks + blockIdx.x] = t;
   }
 }
 
+// Stable scatter of one pass.  Each warp ranks its 512 keys (match_any), the
+// block places all 4096 (key, value) pairs in digit order in shared memory,
+// then writes every digit's run contiguously (coalesced) at its global offset.
+// dynamic smem: s_cnt[kSortWarps][nbins], s_dstart[nbins], s_goff[nbins],
+//               s_key[kSortTile], s_val[kSortTile]
 __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, bool first) {
-  __shared__ int s_cnt[kSortWarps][256];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  extern __shared__ int s_dyn[];
   const int nbins = 1 << p.dbits;
+  int* s_cnt = s_dyn;
+  int* s_dstart = s_cnt + kSortWarps * nbins;
+  int* s_goff = s_dstart + nbins;
+  int32_t* s_key = s_goff + nbins;
+  int32_t* s_val = s_key + kSortTile;
+  __shared__ int s_warp[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t mask = uint32_t(nbins - 1);
-  for (int d = lane; d < 256; d += 32) s_cnt[wid][d] = 0;
-  __syncwarp();
-  const int64_t wbase = int64_t(blockIdx.x) * kSortTile + int64_t(wid) * kSortRounds * 32;
-  int32_t key[kSortRounds];
+  for (int d = threadIdx.x; d < kSortWarps * nbins; d += 256) s_cnt[d] = 0;
+  __syncthreads();
+  const int64_t bbase = int64_t(blockIdx.x) * kSortTile;
+  const int64_t wbase = bbase + int64_t(wid) * kSortRounds * 32;
+  const int nvalid = int(p.n - bbase < kSortTile ? p.n - bbase : kSortTile);
+  int32_t key[kSortRounds], val[kSortRounds];
   uint32_t dig[kSortRounds];
   unsigned peers[kSortRounds];
 #pragma unroll
@@ -166,21 +191,47 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
     const int64_t i = wbase + r * 32 + lane;
     const bool valid = i < p.n;
     key[r] = valid ? load_key(p, i, first) : 0;
+    val[r] = valid ? (p.vin ? p.vin[i] : int32_t(i)) : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < kSortRounds; ++r) {
+    const int64_t i = wbase + r * 32 + lane;
+    const bool valid = i < p.n;
     dig[r] = valid ? ((uint32_t(key[r]) >> p.shift) & mask) : 0x10000u;
     peers[r] = __match_any_sync(0xffffffffu, dig[r]);
-    if (valid && lane == __ffs(peers[r]) - 1) s_cnt[wid][dig[r]] += __popc(peers[r]);
+    if (valid && lane == __ffs(peers[r]) - 1) s_cnt[wid * nbins + dig[r]] += __popc(peers[r]);
     __syncwarp();
   }
   __syncthreads();
-  // per (warp, digit) base offsets: global offset of (digit, block) + earlier warps
-  for (int d = threadIdx.x; d < nbins; d += 256) {
-    int run = p.counts[int64_t(d) * p.nblocks + blockIdx.x];
-#pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) {
-      const int c = s_cnt[w][d];
-      s_cnt[w][d] = run;
-      run += c;
+  // block-local digit starts (exclusive scan of the block's digit totals),
+  // per-(warp, digit) local offsets, global offsets of the block's digit runs
+  const int per = nbins / 256 > 0 ? nbins / 256 : 1;   // digits per thread (nbins >= 256 or 1 each)
+  int tot_local[8];
+  int sum = 0;
+  for (int j = 0; j < per; ++j) {
+    const int d = threadIdx.x * per + j;
+    int t = 0;
+    if (d < nbins) {
+      for (int w = 0; w < kSortWarps; ++w) t += s_cnt[w * nbins + d];
     }
+    tot_local[j] = t;
+    sum += t;
+  }
+  int total;
+  int ex = block_excl_scan(sum, s_warp, &total);
+  for (int j = 0; j < per; ++j) {
+    const int d = threadIdx.x * per + j;
+    if (d < nbins) {
+      s_dstart[d] = ex;
+      s_goff[d] = p.counts[int64_t(d) * p.nblocks + blockIdx.x];
+      int run = ex;
+      for (int w = 0; w < kSortWarps; ++w) {
+        const int c = s_cnt[w * nbins + d];
+        s_cnt[w * nbins + d] = run;
+        run += c;
+      }
+    }
+    ex += tot_local[j];
   }
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
@@ -189,14 +240,22 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
     const int64_t i = wbase + r * 32 + lane;
     const bool valid = i < p.n;
     int dst = 0;
-    if (valid) dst = s_cnt[wid][dig[r]] + __popc(peers[r] & lt);
+    if (valid) dst = s_cnt[wid * nbins + dig[r]] + __popc(peers[r] & lt);
     __syncwarp();
-    if (valid && lane == __ffs(peers[r]) - 1) s_cnt[wid][dig[r]] += __popc(peers[r]);
+    if (valid && lane == __ffs(peers[r]) - 1) s_cnt[wid * nbins + dig[r]] += __popc(peers[r]);
     __syncwarp();
     if (valid) {
-      p.kout[dst] = key[r];
-      p.vout[dst] = p.vin ? p.vin[i] : int32_t(i);
+      s_key[dst] = key[r];
+      s_val[dst] = val[r];
     }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nvalid; e += 256) {
+    const int32_t k = s_key[e];
+    const int d = int((uint32_t(k) >> p.shift) & mask);
+    const int64_t g = int64_t(s_goff[d]) + (e - s_dstart[d]);
+    p.kout[g] = k;
+    p.vout[g] = s_val[e];
   }
 }
 
@@ -260,9 +319,11 @@ void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b) {
   b.v[0] = c.take<int32_t>(n);
   b.k[1] = c.take<int32_t>(n);
   b.v[1] = c.take<int32_t>(n);
-  b.counts = c.take<int32_t>(int64_t(256) * nb);
-  b.scan_tmp = c.take<int32_t>(scan_tmp_elems(int64_t(256) * nb));
+  b.counts = c.take<int32_t>((int64_t(1) << kMaxDigitBits) * nb);
+  b.scan_tmp = c.take<int32_t>(scan_tmp_elems((int64_t(1) << kMaxDigitBits) * nb));
 }
+
+static int sort_passes(int bits) { return (bits + kMaxDigitBits - 1) / kMaxDigitBits; }
 
 mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t** vals) {
   if (n <= 0) {
@@ -271,7 +332,7 @@ mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t
     return ML_OK;
   }
   if (bits < 1) bits = 1;
-  const int passes = (bits + 7) / 8;
+  const int passes = sort_passes(bits);
   *keys = b.k[(passes - 1) & 1];
   *vals = b.v[(passes - 1) & 1];
   return ML_OK;
@@ -286,9 +347,21 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
   }
   if (bits < 1) bits = 1;
   if (bits > 31) return fail(ML_ERR_CONFIG, "sort: keys must fit in 31 bits");
-  const int passes = (bits + 7) / 8;
+  const int passes = sort_passes(bits);
   const int dbits = (bits + passes - 1) / passes;
+  const int nbins = 1 << dbits;
   const int nb = sort_nblocks(n);
+  static bool attr = false;
+  if (!attr) {
+    const int max_smem = int(sizeof(int)) * ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile);
+    ML_CUDA_TRY(cudaFuncSetAttribute(sort_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     max_smem));
+    ML_CUDA_TRY(cudaFuncSetAttribute(sort_scatter_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    attr = true;
+  }
+  const size_t smem_hist = sizeof(int) * size_t(kSortWarps) * nbins;
+  const size_t smem_scatter = sizeof(int) * (size_t(kSortWarps + 2) * nbins + 2 * kSortTile);
   SortPassParams p;
   p.n = n;
   p.nblocks = nb;
@@ -307,10 +380,10 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
     p.vout = b.v[cur];
     p.shift = pass * dbits;
     const bool first = pass == 0;
-    sort_hist_kernel<<<nb, 256, 0, s>>>(p, first);
+    sort_hist_kernel<<<nb, 256, smem_hist, s>>>(p, first);
     ML_LAUNCH_CHECK("sort_hist");
     ML_TRY(scan_exclusive(b.counts, b.counts, ncounts, b.scan_tmp, nullptr, s));
-    sort_scatter_kernel<<<nb, 256, 0, s>>>(p, first);
+    sort_scatter_kernel<<<nb, 256, smem_scatter, s>>>(p, first);
     ML_LAUNCH_CHECK("sort_scatter");
     kin = b.k[cur];
     vin = b.v[cur];
