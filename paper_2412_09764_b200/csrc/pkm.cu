@@ -236,6 +236,112 @@ __device__ __forceinline__ uint64_t warp_theta_max(uint64_t lane_max, int k) {
   return __shfl_sync(FULL, sorted, k - 1);
 }
 
+// Bitonic sort of one float per lane, descending across lanes 0..31.
+__device__ __forceinline__ float warp_sort_desc_f(float x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const float y = __shfl_xor_sync(FULL, x, stride);
+      const bool take_max = (((lane & size) == 0) == ((lane & stride) == 0));
+      x = take_max ? fmaxf(x, y) : fminf(x, y);
+    }
+  }
+  return x;
+}
+
+// Fast exact path for rows of raw scores with S % 128 == 0 and k <= 32.
+//  1. every lane keeps the two largest of its S/32 values;
+//  2. theta = the k-th largest of those 64 values (two 32-lane sorts + the
+//     merge-path identity kth(A u B) = max_i min(A[i-1], B[k-1-i])) is a
+//     lower bound of the row's k-th largest value (64 distinct elements);
+//  3. survivors v >= theta (~k + 4 on continuous data) go to shared memory;
+//  4. each survivor's rank in (score desc, index asc) order is counted
+//     against all survivors and ranks < k are written directly.
+// Returns false (nothing written) when more than 64 values survive (ties).
+__device__ __forceinline__ bool row_topk_fast(const float* sr, int S, int k, TopkSmem& sm,
+                                              int64_t row, int32_t* hI, float* hs, int* count_out) {
+  constexpr int R = 8;                         // float4 rounds held in registers (S <= 1024)
+  const int lane = threadIdx.x & 31;
+  const int rounds = S / 128;
+  float4 v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    v[r] = r < rounds ? *reinterpret_cast<const float4*>(sr + r * 128 + lane * 4)
+                      : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const float vs[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float lo = fminf(m0, vs[c]);
+      m0 = fmaxf(m0, vs[c]);
+      m1 = fmaxf(m1, lo);
+    }
+  }
+  const float A = warp_sort_desc_f(m0), B = warp_sort_desc_f(m1);
+  // k-th largest of A u B (both descending): max over i = 0..k of min(A[i-1], B[k-1-i])
+  float c = -INFINITY;
+  {
+    const int i = lane;
+    const float a = __shfl_sync(FULL, A, (i + 31) & 31);
+    const float b = __shfl_sync(FULL, B, (k - 1 - i) & 31);
+    if (i <= k - 1) c = fminf(i == 0 ? INFINITY : a, b);
+  }
+  const float ak = __shfl_sync(FULL, A, k - 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c = fmaxf(c, __shfl_xor_sync(FULL, c, o));
+  const float theta = fmaxf(c, ak);
+  // survivors v >= theta: one lane-order scan per row, keys to shared memory
+  uint32_t mask = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    mask |= (v[r].x >= theta ? 1u : 0u) << (4 * r);
+    mask |= (v[r].y >= theta ? 2u : 0u) << (4 * r);
+    mask |= (v[r].z >= theta ? 4u : 0u) << (4 * r);
+    mask |= (v[r].w >= theta ? 8u : 0u) << (4 * r);
+  }
+  const int cnt = __popc(mask);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int count = __shfl_sync(FULL, incl, 31);
+  *count_out = count;
+  int pos = incl - cnt;
+  uint64_t* ck = sm.cand;
+  while (mask) {
+    const int b = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int r = b >> 2, cc = b & 3;
+    const float4 q = v[0];
+    float val = q.x;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+      if (rr == r) val = cc == 0 ? v[rr].x : cc == 1 ? v[rr].y : cc == 2 ? v[rr].z : v[rr].w;
+    if (pos < kCandCap) ck[pos] = make_key(val, uint32_t(r * 128 + lane * 4 + cc));
+    ++pos;
+  }
+  if (count > 64) return false;
+  __syncwarp();
+  // rank of the keys at lane and lane + 32 among all survivors (keys unique)
+  const bool h0 = lane < count, h1 = lane + 32 < count;
+  const uint64_t k0 = h0 ? ck[lane] : ~0ull, k1 = h1 ? ck[lane + 32] : ~0ull;
+  int r0 = 0, r1 = 0;
+  for (int l = 0; l < count; ++l) {
+    const uint64_t kl = ck[l];
+    r0 += kl > k0 ? 1 : 0;
+    r1 += kl > k1 ? 1 : 0;
+  }
+  if (h0 && r0 < k) { hI[row * k + r0] = int32_t(key_id(k0)); hs[row * k + r0] = key_score(k0); }
+  if (h1 && r1 < k) { hI[row * k + r1] = int32_t(key_id(k1)); hs[row * k + r1] = key_score(k1); }
+  return true;
+}
+
 // one warp per (t, h, half) row of S scores
 __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int64_t rows, int S,
                                                         int k, int32_t* hI, float* hs, QkNorm qn,
@@ -250,6 +356,22 @@ __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int
   const float qi = qn.qinv ? qn.qinv[row] : 1.f;
   const float* ki = qn.qinv ? ((row & 1) ? qn.kinv2 : qn.kinv1) + int64_t((row >> 1) % H) * S : nullptr;
   auto score_at = [=](int e) { return ki ? (sr[e] * qi) * ki[e] : sr[e]; };
+  if ((S % 128) == 0 && S <= 1024 && ki == nullptr && k <= 32) {
+    int count = 0;
+    if (row_topk_fast(sr, S, k, sm, row, hI, hs, &count)) return;
+    uint64_t key;
+    if (count <= kCandCap) {     // many ties: exact select over the survivors
+      key = select_cand(count, k, sm);
+    } else {
+      auto gen = [=](int e) { return make_key(sr[e], uint32_t(e)); };
+      key = warp_topk(gen, S, k, sm.hist, sm.sel);
+    }
+    if (lane < k) {
+      hI[row * k + lane] = int32_t(key_id(key));
+      hs[row * k + lane] = key_score(key);
+    }
+    return;
+  }
   // phase 1: each lane's maximum (float compares; the first index of a tied
   // maximum is kept, which is the larger 64-bit key)
   float ms = -INFINITY;
