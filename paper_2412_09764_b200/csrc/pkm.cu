@@ -430,6 +430,94 @@ __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int
   }
 }
 
+// Top-32 (descending, one per lane) of the union of two descending lists
+// a, b held one per lane: the elementwise max of a and reversed b is bitonic
+// and holds the 32 largest; a 5-stage half-cleaner network sorts it.
+__device__ __forceinline__ float merge_top_desc(float a, float b) {
+  const int lane = threadIdx.x & 31;
+  float x = fmaxf(a, __shfl_sync(FULL, b, 31 - lane));
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    const float y = __shfl_xor_sync(FULL, x, stride);
+    x = ((lane & stride) == 0) ? fmaxf(x, y) : fminf(x, y);
+  }
+  return x;
+}
+
+// Fast exact combine for k <= 32 using the sortedness of the grid
+// c[i][j] = s1[i] + s2[j] (s1, s2 descending, fp32 addition is monotone):
+//  theta = the k-th largest value of rows 0..15 (a merge tree of the sorted
+//  rows) bounds the k-th largest cell from below; in every column the cells
+//  >= theta are a prefix; their keys (score, flat index) are ranked by
+//  counting and ranks < k written out.  Returns false (nothing written) when
+//  more than 64 cells survive.
+__device__ __forceinline__ bool combine_fast(const float* s1p, const int32_t* i1p, float s2,
+                                             uint32_t i2, int S, int k, uint64_t* cand,
+                                             uint64_t* sel, int64_t th, int32_t* idx, float* w,
+                                             float* score) {
+  const int lane = threadIdx.x & 31;
+  constexpr int R = 16;
+  float L[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) L[r] = (lane < k && r < k) ? s1p[r] + s2 : -INFINITY;
+#pragma unroll
+  for (int n = R; n > 2; n >>= 1) {
+#pragma unroll
+    for (int r = 0; r < n / 2; ++r) L[r] = merge_top_desc(L[2 * r], L[2 * r + 1]);
+  }
+  // k-th largest of L[0] u L[1] (descending): max over i = 0..k of min(A[i-1], B[k-1-i])
+  float c = -INFINITY;
+  {
+    const float a = __shfl_sync(FULL, L[0], (lane + 31) & 31);
+    const float b = __shfl_sync(FULL, L[1], (k - 1 - lane) & 31);
+    if (lane <= k - 1) c = fminf(lane == 0 ? INFINITY : a, b);
+  }
+  const float ak = __shfl_sync(FULL, L[0], k - 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c = fmaxf(c, __shfl_xor_sync(FULL, c, o));
+  const float theta = fmaxf(c, ak);
+  // column prefix of survivors
+  int n = 0;
+  if (lane < k)
+    while (n < k && s1p[n] + s2 >= theta) ++n;
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int count = __shfl_sync(FULL, incl, 31);
+  if (count > 64) return false;
+  int pos = incl - n;
+  for (int i = 0; i < n; ++i)
+    cand[pos + i] = make_key(s1p[i] + s2, uint32_t(i1p[i]) * uint32_t(S) + i2);
+  __syncwarp();
+  const bool h0 = lane < count, h1 = lane + 32 < count;
+  const uint64_t k0 = h0 ? cand[lane] : ~0ull, k1 = h1 ? cand[lane + 32] : ~0ull;
+  int r0 = 0, r1 = 0;
+  for (int l = 0; l < count; ++l) {
+    const uint64_t kl = cand[l];
+    r0 += kl > k0 ? 1 : 0;
+    r1 += kl > k1 ? 1 : 0;
+  }
+  if (h0 && r0 < k) sel[r0] = k0;
+  if (h1 && r1 < k) sel[r1] = k1;
+  __syncwarp();
+  const uint64_t key = lane < k ? sel[lane] : 0ull;
+  const float sc = key_score(key);
+  const float m = __shfl_sync(FULL, sc, 0);
+  const float ex = lane < k ? expf(sc - m) : 0.f;
+  float sum = ex;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+  if (lane < k) {
+    idx[th * k + lane] = int32_t(key_id(key));
+    w[th * k + lane] = ex / sum;
+    if (score) score[th * k + lane] = sc;
+  }
+  return true;
+}
+
 // one warp per (t, h): combine the two half lists (k*k Cartesian sums), softmax
 __global__ void __launch_bounds__(256) combine_kernel(const int32_t* hI, const float* hs,
                                                       int64_t TH, int S, int k, int32_t* idx,
@@ -451,6 +539,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* hI, const f
   }
   __syncwarp();
   // lane j owns column j of the k x k grid: c[i][j] = s1[i] + s2[j]
+  if (combine_fast(s_s1[wid], s_i1[wid], s2, i2, S, k, sm.cand, sm.sel, th, idx, w, score)) return;
+  __syncwarp();
   auto key_of = [&](int i) {
     return make_key(s_s1[wid][i] + s2, uint32_t(s_i1[wid][i]) * uint32_t(S) + i2);
   };
