@@ -585,13 +585,11 @@ __global__ void __launch_bounds__(256 / UPT + 64, CT)
           for (int v = 0; v < V2; ++v) pr = ffma2(f[v], g[v], pr);
           part[j] = act ? pr.x + pr.y : 0.f;   // threads past the slice read padding
         }
+        // acc is zero at every piece start: it is cleared after each piece's
+        // flush below (pieces are contiguous and every chunk starts on one)
         const float2 w2 = make_float2(wv, wv);
 #pragma unroll
-        for (int v = 0; v < V2; ++v) {
-          acc[v].x = st ? 0.f : acc[v].x;
-          acc[v].y = st ? 0.f : acc[v].y;
-          acc[v] = ffma2(w2, f[v], acc[v]);
-        }
+        for (int v = 0; v < V2; ++v) acc[v] = ffma2(w2, f[v], acc[v]);
         if (flj & 2) {
           const int32_t rr = M[k].rr, rb = M[k].rb, re = M[k].re;
           const float* accf = reinterpret_cast<const float*>(acc);
@@ -605,6 +603,8 @@ __global__ void __launch_bounds__(256 / UPT + 64, CT)
             for (int v = 0; v < TV; ++v) av.v[v] = accf[v];
             finish_long_piece<TV, true>(p, av, act, col, slice, rr, rb, re, ps, &s_flag, team);
           }
+#pragma unroll
+          for (int v = 0; v < V2; ++v) acc[v] = make_float2(0.f, 0.f);
         }
       }
       __syncwarp();
