@@ -336,7 +336,13 @@ def roofline(res, cfg, G, peaks):
     if dom in per:
         r = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["achieved_GBs"], "peak": hbm,
              "unit": "GB/s", "frac": per[dom]["frac"], "traffic": traffic,
-             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+             "note": "achieved counts SURVEY §8(d) algorithmic bytes, incl. the B dy-row gathers "
+                     "per token that the kernel serves from L2; dram = ncu DRAM bytes "
+                     "(profiles/traffic.json) over the same live launch time"}
+        if traffic:
+            g = traffic / (per[dom]["avg_ms"] / 1e3) / 1e9
+            r["dram"] = {"achieved": round(g, 1), "frac": round(g / hbm, 4), "unit": "GB/s"}
     else:
         cnt, tot = kern[dom] if dom else (1, 0.0)
         r = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": None,
