@@ -17,4 +17,4 @@ SPEC.md hand examples, finite differences of the forward for every gradient,
 dense-matrix re-formulations of the sparse bag, and sharded == unsharded.
 Parity unpinned: none of the functions here.
 """
-from . import pkm, bag, gate, layer, group, optim  # noqa: F401
+from . import pkm, bag, gate, layer, group, optim, peer  # noqa: F401
