@@ -249,6 +249,32 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
                                 float* dW1, float* dW2, float* dw_out, void* ws, size_t ws_bytes,
                                 void* stream);
 
+/* ------------------------------------------------ PEER
+ * Product-key retrieval of rank-1 experts ("replacing vector
+ * values with rank-one matrices"; "it retrieves a pair of embeddings,
+ * which combine into a rank-1 matrix.  Several of these are assembled
+ * together into a dynamic feed-forward layer").  Reading Q21:
+ * key i owns U[i], V[i] in R^D; with idx, w from pkm_topk (B = H*k per token)
+ *   h[t,j] = U[idx[t,j]] . x[t],  a = w * silu(h),  y[t] = sum_j a[t,j] V[idx[t,j]].
+ * x, y [T,D]; U, V [N,D] (dtype); saved: idx_saved [T,H,k] i32, w_saved,
+ * h_saved [T,H,k] f32.  N must equal S*S; D*e a multiple of 16 bytes and
+ * (D*e/16) a power of two or a multiple of 256 (as embbag).
+ * Backward given dy [T,D]: dV/dU compact over the same rows (rows [U] ascending,
+ * dU, dV [P,D] fp32 capacity, *Ucount = U), dx [T,D] dtype (expert path only),
+ * dq overwrite, dK1/dK2 ACCUMULATE (as pkm_topk_bwd), dwr_out [T,H,k] (nullable)
+ * = dL/dw of the router weights.  Errors as the other entry points. */
+typedef struct { mlPkmShape pkm; int64_t N; int32_t D; } mlPeerShape;
+mlStatus peer_fwd_workspace(const mlPeerShape* shape, size_t* bytes);
+mlStatus peer_fwd(const mlPeerShape* shape, const void* x, const void* q, const void* K1,
+                  const void* K2, const void* U, const void* V, void* y, int32_t* idx_saved,
+                  float* w_saved, float* h_saved, void* ws, size_t ws_bytes, void* stream);
+mlStatus peer_bwd_workspace(const mlPeerShape* shape, size_t* bytes);
+mlStatus peer_bwd(const mlPeerShape* shape, const void* dy, const void* x, const void* q,
+                  const void* K1, const void* K2, const void* U, const void* V,
+                  const int32_t* idx_saved, const float* w_saved, const float* h_saved, void* dx,
+                  float* dq, float* dK1, float* dK2, int32_t* rows, float* dU, float* dV,
+                  int32_t* Ucount, float* dwr_out, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------- memory group pieces (a7, a12)
  * Parallel memory (§3.1.2, Fig. 2): the value table is
  * sharded along the embedding dim over the G ranks of a memory group; the

@@ -32,6 +32,10 @@ class LayerShape(C.Structure):
                 ("gated", C.c_int32)]
 
 
+class PeerShape(C.Structure):
+    _fields_ = [("pkm", PkmShape), ("N", C.c_int64), ("D", C.c_int32)]
+
+
 class AdamParams(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("weight_decay", C.c_float)]
@@ -74,6 +78,10 @@ SIGNATURES = {
     "memory_layer_bwd_workspace": [C.POINTER(LayerShape), C.POINTER(SZ)],
     "memory_layer_bwd": [C.POINTER(LayerShape)] + [P] * 23 + [SZ, P],
     "memory_layer_state_bytes": [C.POINTER(LayerShape), C.POINTER(SZ)],
+    "peer_fwd_workspace": [C.POINTER(PeerShape), C.POINTER(SZ)],
+    "peer_fwd": [C.POINTER(PeerShape)] + [P] * 11 + [SZ, P],
+    "peer_bwd_workspace": [C.POINTER(PeerShape), C.POINTER(SZ)],
+    "peer_bwd": [C.POINTER(PeerShape)] + [P] * 20 + [SZ, P],
     "memory_layer_fwd_state": [C.POINTER(LayerShape)] + [P] * 13 + [SZ, P, SZ, P],
     "memory_layer_bwd_state": [C.POINTER(LayerShape)] + [P] * 13 + [SZ] + [P] * 11 + [SZ, P],
     "ml_group_unpack": [P, C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int, P],

@@ -863,6 +863,150 @@ mlStatus ml_gate_bwd(const void* dz, const void* g, const void* y, void* z, void
   ML_API_END
 }
 
+// ------------------------------------------------------------ PEER (f4)
+static mlStatus check_peer(const mlPeerShape* s) {
+  if (!s) return fail(ML_ERR_ARG, "null shape");
+  ML_TRY(check_pkm(&s->pkm));
+  if (s->N != int64_t(s->pkm.S) * s->pkm.S) return fail(ML_ERR_CONFIG, "peer: N must equal S*S");
+  mlBagShape bs{s->N, s->D, s->pkm.T, s->pkm.H * s->pkm.k, s->pkm.dtype};
+  ML_TRY(check_bag(&bs));
+  return ML_OK;
+}
+static mlBagShape peer_bag_of(const mlPeerShape& s) {
+  return mlBagShape{s.N, s.D, s.pkm.T, s.pkm.H * s.pkm.k, s.pkm.dtype};
+}
+
+struct PeerFwdBufs { PkmFwdBufs pkm; float* h_part; float* a; };
+static void peer_fwd_carve(Carver& c, const mlPeerShape& s, PeerFwdBufs& b) {
+  const int64_t P = int64_t(s.pkm.T) * s.pkm.H * s.pkm.k;
+  pkm_fwd_carve(c, s.pkm, b.pkm);
+  b.h_part = c.take<float>(int64_t(peer_dot_slices(s.D, s.pkm.dtype)) * std::max<int64_t>(P, 1));
+  b.a = c.take<float>(std::max<int64_t>(P, 1));
+}
+
+mlStatus peer_fwd_workspace(const mlPeerShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_peer(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  PeerFwdBufs b;
+  peer_fwd_carve(c, *shape, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus peer_fwd(const mlPeerShape* shape, const void* x, const void* q, const void* K1,
+                  const void* K2, const void* Ut, const void* V, void* y, int32_t* idx_saved,
+                  float* w_saved, float* h_saved, void* ws, size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_peer(shape));
+  const mlPeerShape& s = *shape;
+  if (s.pkm.T == 0) return ML_OK;
+  ML_TRY(check_ptrs({x, q, K1, K2, Ut, V, y, idx_saved, w_saved, h_saved, ws}));
+  size_t need = 0;
+  ML_TRY(peer_fwd_workspace(shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "peer_fwd: workspace too small");
+  Carver c(ws);
+  PeerFwdBufs b;
+  peer_fwd_carve(c, s, b);
+  cudaStream_t st = S(stream);
+  const int T = s.pkm.T, B = s.pkm.H * s.pkm.k;
+  const int64_t P = int64_t(T) * B;
+  timing_mark(nullptr, st);
+  ML_TRY(pkm_fwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, nullptr, b.pkm, st));
+  ML_TRY(launch_peer_dot(Ut, s.N, s.D, idx_saved, T, B, x, s.pkm.dtype, b.h_part, st));
+  ML_TRY(launch_peer_act(b.h_part, peer_dot_slices(s.D, s.pkm.dtype), P, w_saved, h_saved, b.a, st));
+  BagFwdArgs a;
+  a.V = V; a.ldv = s.D; a.N = s.N;
+  a.idx = idx_saved; a.w = b.a; a.B = B; a.nbags = T; a.dv = s.D;
+  a.out = y; a.ldo = s.D; a.dtype = s.pkm.dtype;
+  a.name = "peer_bag_fwd";
+  ML_TRY(launch_bag_fwd(a, st));
+  return check_index_flag(st);
+  ML_API_END
+}
+
+struct PeerBwdBufs { BagBwdBufs bag; PkmBwdBufs pkm; float *h, *a, *dh, *dwr; };
+static void peer_bwd_carve(Carver& c, const mlPeerShape& s, PeerBwdBufs& b) {
+  const int64_t P = std::max<int64_t>(int64_t(s.pkm.T) * s.pkm.H * s.pkm.k, 1);
+  bag_bwd_carve(c, peer_bag_of(s), b.bag);
+  pkm_bwd_carve(c, s.pkm, b.pkm);
+  b.h = c.take<float>(P);
+  b.a = c.take<float>(P);
+  b.dh = c.take<float>(P);
+  b.dwr = c.take<float>(P);
+}
+
+mlStatus peer_bwd_workspace(const mlPeerShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_peer(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  PeerBwdBufs b;
+  peer_bwd_carve(c, *shape, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus peer_bwd(const mlPeerShape* shape, const void* dy, const void* x, const void* q,
+                  const void* K1, const void* K2, const void* Ut, const void* V,
+                  const int32_t* idx_saved, const float* w_saved, const float* h_saved, void* dx,
+                  float* dq, float* dK1, float* dK2, int32_t* rows, float* dU, float* dV,
+                  int32_t* Ucount, float* dwr_out, void* ws, size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_peer(shape));
+  const mlPeerShape& s = *shape;
+  if (!Ucount) return fail(ML_ERR_ARG, "null U");
+  cudaStream_t st = S(stream);
+  if (s.pkm.T == 0) {
+    ML_CUDA_TRY(cudaMemsetAsync(Ucount, 0, sizeof(int32_t), st));
+    return ML_OK;
+  }
+  ML_TRY(check_ptrs({dy, x, q, K1, K2, Ut, V, idx_saved, w_saved, h_saved, dx, dq, dK1, dK2, rows,
+                     dU, dV, ws}));
+  size_t need = 0;
+  ML_TRY(peer_bwd_workspace(shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "peer_bwd: workspace too small");
+  Carver c(ws);
+  PeerBwdBufs b;
+  peer_bwd_carve(c, s, b);
+  const mlBagShape bs = peer_bag_of(s);
+  const int T = s.pkm.T, B = bs.B;
+  const int64_t P = int64_t(T) * B;
+  timing_mark(nullptr, st);
+  // a = w * silu(h) (recomputed), then the bag backward over V with weights a:
+  // dV rows and da = <dy, V[idx]> (its score gradient)
+  ML_TRY(launch_peer_act(h_saved, 1, P, w_saved, b.h, b.a, st));
+  int32_t *skey = nullptr, *spos = nullptr;
+  ML_TRY(bag_bwd_prepare(bs, idx_saved, rows, Ucount, b.bag, &skey, &spos, st));
+  ML_TRY(bag_bwd_reduce(bs, V, b.a, dy, dV, b.bag, skey, spos, st));
+  ML_TRY(launch_peer_dact(b.bag.dw_part, seg_slices(s.D, s.pkm.dtype), P, w_saved, h_saved, b.dh,
+                          b.dwr, st));
+  // dU[r] = sum_{p: idx = r} dh[p] x[t(p)]: the same sorted segments, source x
+  SegArgs g;
+  g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.bag.runs; g.w = b.dh;
+  g.src = x; g.lds = s.D; g.src_col0 = 0; g.B = B;
+  g.out = dU; g.ldo = s.D; g.dense_accumulate = false;
+  g.partial = b.bag.partial; g.counters = b.bag.counters; g.dv = s.D; g.dtype = s.pkm.dtype;
+  g.name = "peer_dU_segreduce";
+  ML_TRY(launch_segreduce(g, st));
+  // dx[t] = sum_j dh[t,j] U[idx[t,j]]
+  BagFwdArgs a;
+  a.V = Ut; a.ldv = s.D; a.N = s.N;
+  a.idx = idx_saved; a.w = b.dh; a.B = B; a.nbags = T; a.dv = s.D;
+  a.out = dx; a.ldo = s.D; a.dtype = s.pkm.dtype;
+  a.name = "peer_dx_bag";
+  ML_TRY(launch_bag_fwd(a, st));
+  // router: the product-key backward with dw = dwr
+  ML_TRY(pkm_bwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, b.dwr, 1, P, dq, dK1, dK2, b.pkm, st));
+  if (dwr_out)
+    ML_CUDA_TRY(cudaMemcpyAsync(dwr_out, b.dwr, sizeof(float) * size_t(P), cudaMemcpyDeviceToDevice, st));
+  return check_index_flag(st);
+  ML_API_END
+}
+
 mlStatus ml_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                  const void* B, int64_t ldb, void* C, int64_t ldc, mlDtype ab, int c_f32, void* ws,
                  size_t ws_bytes, void* stream) {

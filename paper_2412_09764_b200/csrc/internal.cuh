@@ -19,6 +19,18 @@ struct BagFwdArgs {
 mlStatus check_cols(int32_t dv, mlDtype dt, const char* what);
 mlStatus launch_bag_fwd(const BagFwdArgs& a, cudaStream_t s);
 
+// ------------------------------------------------------------ PEER (f4)
+// h_part[slice][t*B+j] = U[idx[t,j]] . x[t] over the slice's columns
+int peer_dot_slices(int32_t D, mlDtype dt);
+mlStatus launch_peer_dot(const void* Ut, int64_t N, int32_t D, const int32_t* idx, int32_t T,
+                         int32_t B, const void* x, mlDtype dt, float* h_part, cudaStream_t s);
+// h = sum of slices, a = w * silu(h)
+mlStatus launch_peer_act(const float* h_part, int ns, int64_t P, const float* w, float* h, float* a,
+                         cudaStream_t s);
+// da = sum of slices; dh = da * w * silu'(h), dwr = da * silu(h)
+mlStatus launch_peer_dact(const float* da_part, int ns, int64_t P, const float* w, const float* h,
+                          float* dh, float* dwr, cudaStream_t s);
+
 // --------------------------------------------------------------- scan
 // Exclusive prefix sum of n int32 values; total (device int, nullable) gets
 // the sum.  tmp needs scan_tmp_elems(n) ints.

@@ -10,7 +10,7 @@ import ctypes as C
 import torch
 
 from . import _lib
-from ._lib import PkmShape, BagShape, LayerShape, check, lib
+from ._lib import PkmShape, BagShape, LayerShape, PeerShape, check, lib
 
 _DT = {torch.bfloat16: _lib.ML_BF16, torch.float32: _lib.ML_F32}
 _WS = {}
@@ -300,6 +300,59 @@ def memory_layer_bwd(dout, x, q, K1, K2, V, W1, W2, saved, dK1=None, dK2=None, w
         _p(U), _p(dW1), _p(dW2), _p(dw), _p(ws), n, _stream()))
     return LayerGrads(dq=dq, dK1=dK1, dK2=dK2, rows=rows, dV=dV, U=U, dx=dx, dW1=dW1, dW2=dW2,
                       dw=dw)
+
+
+# ------------------------------------------------------------ PEER (f4)
+def peer_shape(x, q, K1, U, k, qk_norm=False):
+    T, H, Dk = q.shape
+    return PeerShape(PkmShape(T, H, K1.shape[1], Dk, k, _dt(q), 1 if qk_norm else 0), U.shape[0],
+                     U.shape[1])
+
+
+def peer_fwd(x, q, K1, K2, U, V, k, qk_norm=False):
+    """PEER-style rank-1 experts (include/memlayer.h peer_fwd).  Returns
+    y [T,D] and the saved tensors (idx, w, h)."""
+    sh = peer_shape(x, q, K1, U, k, qk_norm)
+    T, H = q.shape[0], q.shape[1]
+    dev = q.device
+    y = torch.empty((T, U.shape[1]), dtype=V.dtype, device=dev)
+    idx = torch.empty((T, H, k), dtype=torch.int32, device=dev)
+    w = torch.empty((T, H, k), dtype=torch.float32, device=dev)
+    h = torch.empty((T, H, k), dtype=torch.float32, device=dev)
+    n = _size(lib().peer_fwd_workspace, sh)
+    ws = workspace(n, dev)
+    check(lib().peer_fwd(C.byref(sh), _p(x), _p(q), _p(K1), _p(K2), _p(U), _p(V), _p(y), _p(idx),
+                         _p(w), _p(h), _p(ws), n, _stream()))
+    return y, dict(idx=idx, w=w, h=h, k=k, qk_norm=qk_norm)
+
+
+def peer_bwd(dy, x, q, K1, K2, U, V, saved, dK1=None, dK2=None, want_dwr=False):
+    """Backward of peer_fwd: dx, dq, dK1/dK2 (accumulate), rows/dU/dV compact
+    (capacity buffers + device count), dwr (router weight gradient)."""
+    k = saved["k"]
+    sh = peer_shape(x, q, K1, U, k, saved.get("qk_norm", False))
+    T, H = q.shape[0], q.shape[1]
+    dev = q.device
+    P = T * H * k
+    D = U.shape[1]
+    dx = torch.empty_like(x)
+    dq = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    if dK1 is None:
+        dK1 = torch.zeros(K1.shape, dtype=torch.float32, device=dev)
+    if dK2 is None:
+        dK2 = torch.zeros(K2.shape, dtype=torch.float32, device=dev)
+    rows = torch.empty((P,), dtype=torch.int32, device=dev)
+    dU = torch.empty((P, D), dtype=torch.float32, device=dev)
+    dV = torch.empty((P, D), dtype=torch.float32, device=dev)
+    cnt = torch.empty((1,), dtype=torch.int32, device=dev)
+    dwr = torch.empty((T, H, k), dtype=torch.float32, device=dev) if want_dwr else None
+    n = _size(lib().peer_bwd_workspace, sh)
+    ws = workspace(n, dev, tag="bwd")
+    check(lib().peer_bwd(C.byref(sh), _p(dy), _p(x), _p(q), _p(K1), _p(K2), _p(U), _p(V),
+                         _p(saved["idx"]), _p(saved["w"]), _p(saved["h"]), _p(dx), _p(dq),
+                         _p(dK1), _p(dK2), _p(rows), _p(dU), _p(dV), _p(cnt), _p(dwr), _p(ws), n,
+                         _stream()))
+    return LayerGrads(dx=dx, dq=dq, dK1=dK1, dK2=dK2, rows=rows, dU=dU, dV=dV, U=cnt, dwr=dwr)
 
 
 # ------------------------------------------------------- group / gate pieces
