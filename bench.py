@@ -37,6 +37,11 @@ CONFIGS = {
                desc="1.3B-base memory layer: N=1024^2 x 2048, 4 heads, k=32, 16K tokens, bf16"),
     "c3": dict(S=4096, dv=2048, D=2048, Dk=1024, H=4, k=32, T=16384, dtype="bf16",
                desc="N=4096^2 x 2048 bf16, dim-sharded"),
+    # value-dim sweep of the paper's range (north_star: value dims 1024 to 4096), N = 1024^2
+    "c2_dv1024": dict(S=1024, dv=1024, D=1024, Dk=1024, H=4, k=32, T=16384, dtype="bf16",
+                      desc="N=1024^2 x 1024, 4 heads, k=32, 16K tokens, bf16"),
+    "c2_dv4096": dict(S=1024, dv=4096, D=4096, Dk=1024, H=4, k=32, T=16384, dtype="bf16",
+                      desc="N=1024^2 x 4096, 4 heads, k=32, 16K tokens, bf16"),
 }
 METRIC = "memory-layer fwd+bwd tok/s (EmbeddingBag fwd/bwd HBM GB/s, % peak)"
 SEED = 0

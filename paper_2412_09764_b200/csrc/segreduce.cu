@@ -408,8 +408,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // dynamic smem: [2*nslots] mbarriers (full, empty), pad to 128, nslots x (dy, V) row slots.
 // UPT = 16-byte row vectors per consumer thread, NB = positions per batch / stage.
-template <typename T, bool DW, int UPT, int NB, int CT>
-__global__ void __launch_bounds__(256 / UPT + 64, CT)
+template <typename T, bool DW, int UPT, int NB, int CT, int TEAM>
+__global__ void __launch_bounds__(TEAM + 64, CT)
     seg_pipe_kernel(SegParams p, int nslots, int64_t nchunks, int nslices) {
   constexpr int VEC = Vec<T>::N;
   constexpr int TV = VEC * UPT;                 // elements per consumer thread
@@ -665,7 +665,7 @@ static int env_int(const char* name, int dflt) {
 
 // pipelined kernel. cfg 2 (default): 2 CTAs per SM, 32 bytes per consumer
 // thread, batches of 4; cfg 1: 1 CTA per SM, 16 bytes per thread, batches of 8.
-template <typename T, bool DW, int UPT, int NB, int CT>
+template <typename T, bool DW, int UPT, int NB, int CT, int TEAM>
 mlStatus launch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
                      const char* name, int ctas, size_t budget) {
   const int team = threads / UPT;
@@ -678,13 +678,13 @@ mlStatus launch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, c
   const size_t smem = ((2 * size_t(nslots) * 8 + 127) / 128) * 128 + size_t(nslots) * stage + pad;
   static bool attr = false;
   if (!attr) {
-    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW, UPT, NB, CT>,
+    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW, UPT, NB, CT, TEAM>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(210 * 1024)));
     attr = true;
   }
   const int64_t items = nchunks * ns;
   const unsigned grid = unsigned(std::min<int64_t>(items, int64_t(num_sms()) * ctas));
-  seg_pipe_kernel<T, DW, UPT, NB, CT><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
+  seg_pipe_kernel<T, DW, UPT, NB, CT, TEAM><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
   ML_LAUNCH_CHECK(name);
   return ML_OK;
 }
@@ -692,10 +692,14 @@ mlStatus launch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, c
 template <typename T, bool DW>
 mlStatus dispatch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
                        const char* name) {
+  // 4 KiB row slices: 4 consumer warps of 32-byte threads, 2 CTAs/SM;
+  // 1-2 KiB rows: 16-byte threads, 3 CTAs/SM (more rows in flight per SM)
   static const int cfg = env_int("ML_SEG_PIPE_CFG", 2);
+  if (cfg >= 2 && threads >= 256)
+    return launch_pipe<T, DW, 2, 4, 2, 128>(threads, ns, nchunks, p, s, name, 2, 100 * 1024);
   if (cfg >= 2 && threads >= 64)
-    return launch_pipe<T, DW, 2, 4, 2>(threads, ns, nchunks, p, s, name, 2, 100 * 1024);
-  return launch_pipe<T, DW, 1, 8, 1>(threads, ns, nchunks, p, s, name, 1, 200 * 1024);
+    return launch_pipe<T, DW, 1, 4, 3, 128>(threads, ns, nchunks, p, s, name, 3, 62 * 1024);
+  return launch_pipe<T, DW, 1, 8, 1, 256>(threads, ns, nchunks, p, s, name, 1, 200 * 1024);
 }
 
 }  // namespace
