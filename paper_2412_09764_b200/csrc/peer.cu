@@ -90,6 +90,55 @@ __global__ void __launch_bounds__(256) peer_dot_kernel(const char* Ut, int64_t l
   }
 }
 
+// Warp-per-row variant for rows of 512-byte multiples: one CTA (8 warps) per
+// (token, <= 4 KiB column slice); each warp keeps its lanes' 16-byte pieces of
+// x[t] in registers and owns rows j = warp, warp + 8, ...; two rows per step
+// (2 x NCH 16-byte loads per lane in flight), warp-shuffle reductions only.
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) peer_dot_warp_kernel(const char* Ut, int64_t ld_bytes,
+                                                            int64_t N, const int32_t* idx, int32_t B,
+                                                            const char* x, float* h_part, int64_t P) {
+  constexpr int VEC = Vec<T>::N;
+  const int64_t t = blockIdx.x;
+  const int slice = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t col0 = int64_t(slice) * 4096 + lane * 16;
+  float2 xf[NCH][VEC / 2];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+    Vec<T>::load(ldg_nc_v4(x + t * ld_bytes + col0 + c * 512), reinterpret_cast<float*>(xf[c]));
+  const int32_t* ib = idx + t * B;
+  for (int j0 = warp; j0 < B; j0 += 16) {
+    const int j1 = j0 + 8;
+    int r0 = ib[j0];
+    int r1 = j1 < B ? ib[j1] : r0;
+    if (uint64_t(uint32_t(r0)) >= uint64_t(N)) r0 = 0;
+    if (uint64_t(uint32_t(r1)) >= uint64_t(N)) r1 = 0;
+    uint4 a[NCH], b[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      a[c] = ldg_nc_v4(Ut + int64_t(r0) * ld_bytes + col0 + c * 512);
+      b[c] = ldg_nc_v4(Ut + int64_t(r1) * ld_bytes + col0 + c * 512);
+    }
+    float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      float2 fa[VEC / 2], fb[VEC / 2];
+      Vec<T>::load(a[c], reinterpret_cast<float*>(fa));
+      Vec<T>::load(b[c], reinterpret_cast<float*>(fb));
+#pragma unroll
+      for (int v = 0; v < VEC / 2; ++v) {
+        pa = ffma2(xf[c][v], fa[v], pa);
+        pb = ffma2(xf[c][v], fb[v], pb);
+      }
+    }
+    float sv[2] = {pa.x + pa.y, pb.x + pb.y};
+    WarpTR<2, 16>::run(sv, lane);              // lane l: warp sum of row (l >> 4)
+    if (lane == 0) h_part[int64_t(slice) * P + t * B + j0] = sv[0];
+    if (lane == 16 && j1 < B) h_part[int64_t(slice) * P + t * B + j1] = sv[0];
+  }
+}
+
 __global__ void peer_act_kernel(const float* h_part, int ns, int64_t P, const float* w, float* h,
                                 float* a) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -114,8 +163,15 @@ __global__ void peer_dact_kernel(const float* da_part, int ns, int64_t P, const 
 
 }  // namespace
 
+// rows of 512, 1024, 2048 or k*4096 bytes take the warp-per-row kernel
+static bool peer_warp_path(int64_t rowb) {
+  return rowb == 512 || rowb == 1024 || rowb == 2048 || (rowb >= 4096 && rowb % 4096 == 0);
+}
+
 int peer_dot_slices(int32_t D, mlDtype dt) {
-  const int64_t vu = int64_t(D) * int64_t(dtype_size(dt)) / 16;
+  const int64_t rowb = int64_t(D) * int64_t(dtype_size(dt));
+  if (peer_warp_path(rowb)) return int(rowb >= 4096 ? rowb / 4096 : 1);
+  const int64_t vu = rowb / 16;
   return int(vu <= 256 ? 1 : (vu + 255) / 256);
 }
 
@@ -127,9 +183,30 @@ mlStatus launch_peer_dot(const void* Ut, int64_t N, int32_t D, const int32_t* id
   const int64_t vu = int64_t(D) * es / 16;
   const int threads = vu <= 32 ? 32 : (vu >= 256 ? 256 : int(vu));
   const int ns = int((vu + threads - 1) / threads);
-  dim3 grid{unsigned(T), unsigned(ns), 1u};
   const int64_t P = int64_t(T) * B;
   auto c = [](const void* p) { return static_cast<const char*>(p); };
+  const int64_t rowb = int64_t(D) * es;
+  if (peer_warp_path(rowb)) {
+    // warp-per-row path: slices of <= 4 KiB, NCH 512-byte chunks each
+    const int nch = int(rowb >= 4096 ? 8 : rowb / 512);
+    dim3 g2{unsigned(T), unsigned(rowb >= 4096 ? rowb / 4096 : 1), 1u};
+#define ML_PEER_DOT(TT, NC)                                                                      \
+  peer_dot_warp_kernel<TT, NC><<<g2, 256, 0, s>>>(c(Ut), rowb, N, idx, B, c(x), h_part, P)
+#define ML_PEER_DOT_T(TT)                                                                        \
+  switch (nch) {                                                                                 \
+    case 1: ML_PEER_DOT(TT, 1); break;                                                           \
+    case 2: ML_PEER_DOT(TT, 2); break;                                                           \
+    case 4: ML_PEER_DOT(TT, 4); break;                                                           \
+    case 8: ML_PEER_DOT(TT, 8); break;                                                           \
+    default: return fail(ML_ERR_UNSUPPORTED, "peer: row width");                                 \
+  }
+    if (dt == ML_BF16) { ML_PEER_DOT_T(__nv_bfloat16) } else { ML_PEER_DOT_T(float) }
+#undef ML_PEER_DOT_T
+#undef ML_PEER_DOT
+    ML_LAUNCH_CHECK("peer_dot");
+    return ML_OK;
+  }
+  dim3 grid{unsigned(T), unsigned(ns), 1u};
   if (dt == ML_BF16)
     peer_dot_kernel<__nv_bfloat16><<<grid, threads, 0, s>>>(c(Ut), D * es, N, idx, B, c(x), int(vu),
                                                             h_part, P);
