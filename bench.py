@@ -430,13 +430,24 @@ def run_reference(args, cfg, world, rank):
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg["desc"], "tokens_per_step_sample": T_o},
+            "config": dict(config_keys(cfg, cfg.get("name", "c2"), world, "single GPU"),
+                           tokens_per_step_sample=T_o),
             "cpu_baseline": {"value": v, "unit": "tok/s", "kind": "oracle", "cores": blas_threads(),
                              "sample": f"{T_o} tokens per step of {cfg['desc']}"},
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 # ------------------------------------------------------------------- main
+def config_keys(cfg, cfg_name, G, parallelism):
+    """The workload description shared by both arms' JSON lines."""
+    return {"workload": cfg["desc"], "config": cfg_name, "tokens_per_rank": cfg["T"],
+            "global_tokens": cfg["T"] * G, "N_values": cfg["S"] ** 2, "value_dim": cfg["dv"],
+            "heads": cfg["H"], "k": cfg["k"], "key_dim": cfg["Dk"], "gated": True,
+            "parallelism": parallelism,
+            "l2": "inputs_larger_than_L2 (value table >= 4 GiB vs 126 MB L2; no flush)",
+            "seed": SEED}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -481,14 +492,11 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_step"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": cfg["dtype"], "data": "synthetic",
-        "config": {"workload": cfg["desc"], "config": cfg_name, "tokens_per_rank": cfg["T"],
-                   "global_tokens": res["tokens_per_step"], "N_values": cfg["S"] ** 2,
-                   "value_dim": cfg["dv"], "heads": cfg["H"], "k": cfg["k"],
-                   "key_dim": cfg["Dk"], "gated": True, "qk_norm": bool(args.qk_norm),
-                   "parallelism": (f"memory-group dim-shard G={G} ({args.mode})"
-                                   if (G > 1 or args.force_group) else "single GPU"),
-                   "l2": "inputs_larger_than_L2 (value table >= 4 GiB vs 126 MB L2; no flush)",
-                   "unique_rows_per_position": round(res["U"] / P, 4), "seed": SEED},
+        "config": dict(config_keys(cfg, cfg_name, G,
+                                   (f"memory-group dim-shard G={G} ({args.mode})"
+                                    if (G > 1 or args.force_group) else "single GPU")),
+                       qk_norm=bool(args.qk_norm),
+                       unique_rows_per_position=round(res["U"] / P, 4)),
         "roofline": roof,
         "bag_kernels": per,
         "kernel_ms_per_step": {n: round(v[1] / args.steps, 4) for n, v in sorted(
