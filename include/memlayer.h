@@ -153,6 +153,20 @@ mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, 
 /* With V == NULL and dw == NULL only the value gradient is computed (rows /
  * dV / U), as in the strategy comparison below. */
 
+/* The inverse index map of embbag_bwd as a separate, caller-owned state
+ * ("preprocessing to inverse the token_id to embedding_id mapping"): it
+ * depends only on idx, so a caller can build it early on another stream
+ * (the memory group builds it during its forward).  embbag_bwd_state then
+ * runs only the segmented reduction; results are bit-identical to embbag_bwd
+ * with the same idx.  state [embbag_bwd_state_bytes(shape)] must not change
+ * in between.  Errors: ML_ERR_WORKSPACE when too small; others as embbag_bwd. */
+mlStatus embbag_bwd_state_bytes(const mlBagShape* shape, size_t* bytes);
+mlStatus embbag_bwd_prepare(const mlBagShape* shape, const int32_t* idx, void* state,
+                            size_t state_bytes, void* stream);
+mlStatus embbag_bwd_state(const mlBagShape* shape, const void* V, const float* w, const void* dy,
+                          const void* state, size_t state_bytes, int32_t* rows, float* dV,
+                          int32_t* U, float* dw, void* ws, size_t ws_bytes, void* stream);
+
 /* Controls: the other two backward strategies of PAPER.md §3.1.4,
  * for the strategy benchmark.  Both ACCUMULATE
  * dV_dense[idx[p],:] += w[p] * dy[t(p),:] into a dense fp32 [N,dv] table the

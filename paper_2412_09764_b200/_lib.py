@@ -69,6 +69,9 @@ SIGNATURES = {
     "embbag_bwd_workspace": [C.POINTER(BagShape), C.POINTER(SZ)],
     "embbag_bwd": [C.POINTER(BagShape), P, P, P, P, P, P, P, P, P, SZ, P],
     "embbag_grad_apply": [C.POINTER(BagShape), P, P, P, P, P],
+    "embbag_bwd_state_bytes": [C.POINTER(BagShape), C.POINTER(SZ)],
+    "embbag_bwd_prepare": [C.POINTER(BagShape), P, P, SZ, P],
+    "embbag_bwd_state": [C.POINTER(BagShape), P, P, P, P, SZ, P, P, P, P, P, SZ, P],
     "embbag_bwd_atomics": [C.POINTER(BagShape), P, P, P, P, P],
     "embbag_bwd_lock": [C.POINTER(BagShape), P, P, P, P, P, P],
     "embbag_bwd_lock_count": [C.POINTER(BagShape)],

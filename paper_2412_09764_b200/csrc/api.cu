@@ -614,6 +614,80 @@ mlStatus memory_layer_state_bytes(const mlLayerShape* shape, size_t* bytes) {
   ML_API_END
 }
 
+// bag-level state (the memory group builds it during its forward)
+mlStatus embbag_bwd_state_bytes(const mlBagShape* shape, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  BagPrepState b;
+  state_carve(c, *shape, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus embbag_bwd_prepare(const mlBagShape* shape, const int32_t* idx, void* state,
+                            size_t state_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  size_t need = 0;
+  ML_TRY(embbag_bwd_state_bytes(shape, &need));
+  if (state_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_bwd_prepare: state too small");
+  ML_TRY(check_ptrs({state}));
+  if (shape->T > 0) ML_TRY(check_ptrs({idx}));
+  Carver sc(state);
+  BagPrepState ps;
+  state_carve(sc, *shape, ps);
+  BagBwdBufs pb{};
+  pb.sort = ps.sort;
+  pb.runs = ps.runs;
+  int32_t *sk = nullptr, *sp = nullptr;
+  timing_mark(nullptr, S(stream));
+  ML_TRY(bag_bwd_prepare(*shape, idx, ps.rows, ps.U, pb, &sk, &sp, S(stream)));
+  return check_index_flag(S(stream));
+  ML_API_END
+}
+
+mlStatus embbag_bwd_state(const mlBagShape* shape, const void* V, const float* w, const void* dy,
+                          const void* state, size_t state_bytes, int32_t* rows, float* dV,
+                          int32_t* U, float* dw, void* ws, size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shape));
+  if (!U) return fail(ML_ERR_ARG, "null U");
+  cudaStream_t st = S(stream);
+  const int64_t P = int64_t(shape->T) * shape->B;
+  if (P == 0) {
+    ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
+    return ML_OK;
+  }
+  ML_TRY(check_ptrs({w, dy, rows, dV, ws, state}));
+  if ((V == nullptr) != (dw == nullptr)) return fail(ML_ERR_ARG, "embbag_bwd_state: V and dw are both set or both NULL");
+  if (V) ML_TRY(check_ptrs({V, dw}));
+  size_t need = 0, sneed = 0;
+  ML_TRY(embbag_bwd_workspace(shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_bwd_state: workspace too small");
+  ML_TRY(embbag_bwd_state_bytes(shape, &sneed));
+  if (state_bytes < sneed) return fail(ML_ERR_WORKSPACE, "embbag_bwd_state: state too small");
+  Carver c(ws);
+  BagBwdBufs b;
+  bag_bwd_carve(c, *shape, b);
+  Carver sc(const_cast<void*>(state));
+  BagPrepState ps;
+  state_carve(sc, *shape, ps);
+  b.sort = ps.sort;
+  b.runs = ps.runs;
+  int32_t *skey = nullptr, *spos = nullptr;
+  ML_TRY(sorted_result(P, ceil_log2(shape->N), ps.sort, &skey, &spos));
+  timing_mark(nullptr, st);
+  ML_CUDA_TRY(cudaMemcpyAsync(rows, ps.rows, sizeof(int32_t) * size_t(P), cudaMemcpyDeviceToDevice, st));
+  ML_CUDA_TRY(cudaMemcpyAsync(U, ps.U, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  ML_TRY(bag_bwd_reduce(*shape, V, w, dy, dV, b, skey, spos, st));
+  if (dw) ML_TRY(launch_sum_slices(b.dw_part, seg_slices(shape->dv, shape->dtype), P, dw, st));
+  return check_index_flag(st);
+  ML_API_END
+}
+
 mlStatus memory_layer_fwd_workspace(const mlLayerShape* shape, size_t* bytes) {
   ML_API_BEGIN
   ML_TRY(check_layer(shape));

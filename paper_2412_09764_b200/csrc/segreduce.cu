@@ -752,8 +752,11 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
                        reinterpret_cast<uintptr_t>(a.src) % 16 == 0 &&
                        (!dw || (p.ldv_bytes % 16 == 0 && (a.v_col0 * es) % 16 == 0 &&
                                 reinterpret_cast<uintptr_t>(a.V) % 16 == 0));
+  // the pipelined kernel pays off once a row slice spans >= 4 warps (2 KiB,
+  // measured); narrower slices (the 4- and 8-way dim-sharded group) keep one
+  // CTA per chunk
   static const bool pipe = env_int("ML_SEG_PIPE", 1) != 0;
-  if (pipe && !a.dense_accumulate && aligned) {
+  if (pipe && !a.dense_accumulate && aligned && threads >= 128) {
     if (a.dtype == ML_BF16)
       return dw ? dispatch_pipe<__nv_bfloat16, true>(threads, ns, nchunks, p, s, a.name)
                 : dispatch_pipe<__nv_bfloat16, false>(threads, ns, nchunks, p, s, a.name);

@@ -61,9 +61,34 @@ class CudaLocal:
     def __init__(self):
         from . import ops
         self.ops = ops
+        self._side = None
 
     def empty(self, shape, dtype, like):
         return torch.empty(shape, dtype=dtype, device=like.device)
+
+    # ---- side stream: work that only depends on already computed tensors
+    # (the inverse index map during the forward, the gate weight gradients
+    # during the exchange + bag backward) runs concurrently on a
+    # high-priority stream; join() makes the current stream wait for it.
+    def side(self, like):
+        cur = torch.cuda.current_stream(like.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=like.device, priority=-100)   # the highest
+        self._side.wait_stream(cur)
+        return torch.cuda.stream(self._side)
+
+    def join(self, *tensors):
+        if self._side is None:
+            return
+        cur = torch.cuda.current_stream()
+        cur.wait_stream(self._side)
+        for t in tensors:
+            if t is not None:
+                t.record_stream(cur)
+
+    def embbag_bwd_prepare(self, N, dv, idx, dtype):
+        with self.side(idx):
+            return self.ops.embbag_bwd_prepare(N, dv, idx, dtype)
 
     def pkm_topk(self, q, K1, K2, k):
         return self.ops.pkm_topk(q, K1, K2, k)
@@ -71,8 +96,8 @@ class CudaLocal:
     def embbag_fwd(self, V, idx, w):
         return self.ops.embbag_fwd(V, idx, w)
 
-    def embbag_bwd(self, V, idx, w, dy):
-        rows, dV, U, dw = self.ops.embbag_bwd(V, idx, w, dy, sync=False)
+    def embbag_bwd(self, V, idx, w, dy, state=None):
+        rows, dV, U, dw = self.ops.embbag_bwd(V, idx, w, dy, sync=False, state=state)
         return rows, dV, U, dw
 
     def pkm_topk_bwd(self, q, K1, K2, idx, w, dw, dK1, dK2):
@@ -120,6 +145,10 @@ class GroupMemoryLayer:
         idx_all = L.empty((G * T_loc, H, k), idx.dtype, idx)
         w_all = L.empty((G * T_loc, H, k), w.dtype, w)
         C.all_gather(idx_all, idx)                                      # 2
+        state = None
+        if hasattr(L, "embbag_bwd_prepare"):      # the backward's inverse map, concurrently
+            state = L.embbag_bwd_prepare(V_shard.shape[0], dvG, idx_all.view(G * T_loc, B),
+                                         V_shard.dtype)
         C.all_gather(w_all, w)
         y_part = L.embbag_fwd(V_shard, idx_all.view(G * T_loc, B), w_all.view(G * T_loc, B))  # 3
         gpre = L.gemm(x, W1)
@@ -135,8 +164,10 @@ class GroupMemoryLayer:
             y = y_all[rank * T_loc:(rank + 1) * T_loc]
             _, z = L.unpack(y.reshape(1, T_loc, dv), 1, T_loc, dv, gate=gpre, want_y=False)
         out = L.gemm(z, W2)                                             # 5
+        if state is not None:
+            L.join(state)
         saved = dict(x=x, q=q, K1=K1, K2=K2, V=V_shard, W1=W1, W2=W2, idx=idx, w=w,
-                     idx_all=idx_all, w_all=w_all, g=gpre, y=y, y_all=y_all)
+                     idx_all=idx_all, w_all=w_all, g=gpre, y=y, y_all=y_all, state=state)
         return out, saved
 
     def backward(self, dout, saved, dK1=None, dK2=None):
@@ -148,14 +179,25 @@ class GroupMemoryLayer:
         dvG = V_shard.shape[1]
         dz = L.gemm(dout, saved["W2"], transB=True)                     # gate backward
         z, dy, dg = L.gate_bwd(dz, saved["g"], saved["y"])
-        dW2 = L.gemm(z, dout, transA=True, out_f32=True)
-        dW1 = L.gemm(saved["x"], dg, transA=True, out_f32=True)
-        dx = L.gemm(dg, saved["W1"], transB=True)
+        side = hasattr(L, "side")
+        if side:      # gate weight gradients overlap the exchange and the bag backward
+            with L.side(dz):
+                dW2 = L.gemm(z, dout, transA=True, out_f32=True)
+                dW1 = L.gemm(saved["x"], dg, transA=True, out_f32=True)
+                dx = L.gemm(dg, saved["W1"], transB=True)
+        else:
+            dW2 = L.gemm(z, dout, transA=True, out_f32=True)
+            dW1 = L.gemm(saved["x"], dg, transA=True, out_f32=True)
+            dx = L.gemm(dg, saved["W1"], transB=True)
         send = L.pack(dy, G)                                            # [G, T_loc, dv/G]
         recv = L.empty((G * T_loc, dvG), dy.dtype, dy)
         C.all_to_all(recv, send.view(G * T_loc, dvG))                  # dy slices of all tokens
-        rows, dV, U, dw_part = L.embbag_bwd(V_shard, saved["idx_all"].view(G * T_loc, B),
-                                            saved["w_all"].view(G * T_loc, B), recv)
+        bag_args = (V_shard, saved["idx_all"].view(G * T_loc, B), saved["w_all"].view(G * T_loc, B),
+                    recv)
+        if saved.get("state") is not None:
+            rows, dV, U, dw_part = L.embbag_bwd(*bag_args, state=saved["state"])
+        else:
+            rows, dV, U, dw_part = L.embbag_bwd(*bag_args)
         dw = L.empty((T_loc, B), dw_part.dtype, dw_part)
         C.reduce_scatter(dw, dw_part)                                   # sum over column shards
         if dK1 is None:
@@ -164,5 +206,7 @@ class GroupMemoryLayer:
             dK2 = torch.zeros(saved["K2"].shape, dtype=L.grad_dtype, device=dw.device)
         dq, dK1, dK2 = L.pkm_topk_bwd(q, saved["K1"], saved["K2"], saved["idx"], saved["w"],
                                       dw.view(T_loc, H, k), dK1, dK2)
+        if side:
+            L.join(dW1, dW2, dx, z, dg)
         return dict(dx=dx, dq=dq, dK1=dK1, dK2=dK2, dW1=dW1, dW2=dW2, rows=rows, dV=dV, U=U,
                     dw=dw.view(T_loc, H, k))

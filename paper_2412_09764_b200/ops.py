@@ -148,10 +148,11 @@ def embbag_fwd(V, idx, w, gate_pre=None, return_ungated=False):
     return (y, yu) if return_ungated else y
 
 
-def embbag_bwd(V, idx, w, dy, sync=True):
+def embbag_bwd(V, idx, w, dy, sync=True, state=None):
     """"reverse_indices" backward.  Returns rows [U] int32 (ascending),
     dV [U, dv] fp32, dw [T,B] fp32 (sync=True trims to U on the host);
-    with sync=False returns the capacity-sized buffers and the device U."""
+    with sync=False returns the capacity-sized buffers and the device U.
+    state: from embbag_bwd_prepare(N, dv, idx) (skips the sort)."""
     sh = bag_shape(V, idx)
     P = idx.numel()
     rows = torch.empty(P, dtype=torch.int32, device=V.device)
@@ -160,12 +161,27 @@ def embbag_bwd(V, idx, w, dy, sync=True):
     dw = torch.empty(idx.shape, dtype=torch.float32, device=V.device)
     n = _size(lib().embbag_bwd_workspace, sh)
     ws = workspace(n, V.device)
-    check(lib().embbag_bwd(C.byref(sh), _p(V), _p(idx), _p(w), _p(dy), _p(rows), _p(dV), _p(U),
-                           _p(dw), _p(ws), n, _stream()))
+    if state is not None:
+        check(lib().embbag_bwd_state(C.byref(sh), _p(V), _p(w), _p(dy), _p(state), state.numel(),
+                                     _p(rows), _p(dV), _p(U), _p(dw), _p(ws), n, _stream()))
+    else:
+        check(lib().embbag_bwd(C.byref(sh), _p(V), _p(idx), _p(w), _p(dy), _p(rows), _p(dV),
+                               _p(U), _p(dw), _p(ws), n, _stream()))
     if not sync:
         return rows, dV, U, dw
     u = int(U.item())
     return rows[:u], dV[:u], dw
+
+
+def embbag_bwd_prepare(N, dv, idx, dtype=torch.bfloat16):
+    """The inverse index map of embbag_bwd for indices idx [T,B] into an
+    N-row table of width dv (include/memlayer.h embbag_bwd_prepare); returns
+    the state tensor for embbag_bwd(..., state=)."""
+    sh = BagShape(N, dv, idx.shape[0], idx.shape[1], _DT[dtype])
+    n = _size(lib().embbag_bwd_state_bytes, sh)
+    state = torch.empty((max(n, 1),), dtype=torch.uint8, device=idx.device)
+    check(lib().embbag_bwd_prepare(C.byref(sh), _p(idx), _p(state), n, _stream()))
+    return state
 
 
 def embbag_bwd_dv_only(N, idx, w, dy, sync=True):

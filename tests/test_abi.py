@@ -22,7 +22,8 @@ def test_header_parsed():
     names = declared_functions()
     for n in ("pkm_topk", "pkm_topk_bwd", "embbag_fwd", "embbag_bwd", "memory_layer_fwd",
               "memory_layer_bwd", "memory_layer_state_bytes", "memory_layer_fwd_state",
-              "memory_layer_bwd_state", "peer_fwd", "peer_bwd", "ml_last_error",
+              "memory_layer_bwd_state", "peer_fwd", "peer_bwd", "embbag_bwd_prepare",
+              "embbag_bwd_state", "ml_last_error",
               "ml_synth_fill"):
         assert n in names
 

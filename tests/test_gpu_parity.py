@@ -312,6 +312,23 @@ def test_memory_layer_state_path_bit_identical(dtype, T, H, S, Dk, k, dv, D, gat
         assert np.array_equal(a[n], b[n]), n
 
 
+@pytest.mark.parametrize("dtype,dv", [("f32", 64), ("bf16", 256), ("bf16", 2048)])
+def test_embbag_bwd_prepared_state_bit_identical(dtype, dv):
+    """embbag_bwd_prepare + embbag_bwd(state=) == embbag_bwd, bit for bit."""
+    N, T, B = 4096, 300, 64
+    idx = streams.uniform_indices(3, T, B, N)
+    w = gen.tensor(3, "w", (T, B)).astype(np.float32)
+    dy = gen.tensor(3, "dout", (T, dv), dtype=dtype)
+    V = gen.tensor(3, "V", (N, dv), dtype=dtype)
+    o = ops()
+    Vd, idd, wd, dyd = dev(V, dtype), dev(idx), dev(w), dev(dy, dtype)
+    a = o.embbag_bwd(Vd, idd, wd, dyd)
+    st = o.embbag_bwd_prepare(N, dv, idd, Vd.dtype)
+    b = o.embbag_bwd(Vd, idd, wd, dyd, state=st)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
 # ------------------------------------------------------------ edge cases
 def test_out_of_range_index_reported_under_check_mode():
     """S:233 index error: with ML_CHECK_INDICES=1 an index >= N is reported
