@@ -122,13 +122,13 @@ struct FVec { float v[VEC]; };
 template <int VEC>
 __device__ __forceinline__ void sum_slots(const SegParams& p, int slice, int64_t slice_w,
                                           int32_t first, int32_t count, int32_t stride,
-                                          bool act, float* tot) {
+                                          bool act, float* tot, int ttid) {
 #pragma unroll
   for (int v = 0; v < VEC; ++v) tot[v] = 0.f;
   if (!act) return;
   for (int32_t q = 0; q < count; ++q) {
     const float* srcp = p.partial + (int64_t(slice) * p.nslots_cap + first + q * stride) * slice_w +
-                        threadIdx.x * VEC;
+                        ttid * VEC;
 #pragma unroll
     for (int v = 0; v < VEC; v += 4) {
       const float4 a = __ldcg(reinterpret_cast<const float4*>(srcp + v));
@@ -137,15 +137,22 @@ __device__ __forceinline__ void sum_slots(const SegParams& p, int slice, int64_t
   }
 }
 
-// Barrier over the reducing threads: the whole CTA, or (pipelined kernel) the
-// consumer warps only (named barrier 1; the producer warp never joins).
-template <bool NAMED>
+// Barrier over the reducing threads: the whole CTA (SYNC 0), the consumer
+// warps of the pipelined kernel (SYNC 1: named barrier 1, the producer warps
+// never join), or one warp (SYNC 2: the warp-per-chunk kernel).
+template <int SYNC>
 __device__ __forceinline__ void team_sync(int team) {
-  if constexpr (NAMED) asm volatile("bar.sync 1, %0;" ::"r"(team) : "memory");
+  if constexpr (SYNC == 1) asm volatile("bar.sync 1, %0;" ::"r"(team) : "memory");
+  else if constexpr (SYNC == 2) __syncwarp();
   else __syncthreads();
 }
+template <int SYNC>
+__device__ __forceinline__ int team_tid() {
+  if constexpr (SYNC == 2) return int(threadIdx.x & 31);
+  else return int(threadIdx.x);
+}
 
-template <int VEC, bool NAMED = false>
+template <int VEC, int SYNC = 0>
 __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VEC> accv, bool act,
                                                int64_t col, int slice, int32_t row, int32_t rbb,
                                                int32_t re, int32_t ps, int* s_flag, int team) {
@@ -162,42 +169,43 @@ __device__ __noinline__ void finish_long_piece(const SegParams& p, const FVec<VE
   const int32_t gn = min(GRP, npieces - g0);
   int32_t* cnt1 = p.counters + int64_t(slice) * 2 * p.nslots_cap;
   int32_t* cnt2 = cnt1 + p.nslots_cap;
-  float* pp = p.partial + (int64_t(slice) * p.nslots_cap + base + piece) * slice_w + threadIdx.x * VEC;
+  const int ttid = team_tid<SYNC>();
+  float* pp = p.partial + (int64_t(slice) * p.nslots_cap + base + piece) * slice_w + ttid * VEC;
   if (act) {
 #pragma unroll
     for (int v = 0; v < VEC; v += 4)
       __stcg(reinterpret_cast<float4*>(pp + v), make_float4(acc[v], acc[v + 1], acc[v + 2], acc[v + 3]));
   }
   __threadfence();
-  team_sync<NAMED>(team);
-  if (threadIdx.x == 0) *s_flag = atomicAdd(cnt1 + base + g0, 1) == gn - 1;
-  team_sync<NAMED>(team);
+  team_sync<SYNC>(team);
+  if (ttid == 0) *s_flag = atomicAdd(cnt1 + base + g0, 1) == gn - 1;
+  team_sync<SYNC>(team);
   if (*s_flag) {                       // last piece of its group: sum the group
     __threadfence();
     float tot[VEC];
-    sum_slots<VEC>(p, slice, slice_w, base + g0, gn, 1, act, tot);
+    sum_slots<VEC>(p, slice, slice_w, base + g0, gn, 1, act, tot, ttid);
     if (ngroups == 1) {
       if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
     } else {
-      team_sync<NAMED>(team);                 // every thread has read the group's slots
-      float* gp = p.partial + (int64_t(slice) * p.nslots_cap + base + g0) * slice_w + threadIdx.x * VEC;
+      team_sync<SYNC>(team);                 // every thread has read the group's slots
+      float* gp = p.partial + (int64_t(slice) * p.nslots_cap + base + g0) * slice_w + ttid * VEC;
       if (act) {
 #pragma unroll
         for (int v = 0; v < VEC; v += 4)
           __stcg(reinterpret_cast<float4*>(gp + v), make_float4(tot[v], tot[v + 1], tot[v + 2], tot[v + 3]));
       }
       __threadfence();
-      team_sync<NAMED>(team);
-      if (threadIdx.x == 0) *s_flag = atomicAdd(cnt2 + base, 1) == ngroups - 1;
-      team_sync<NAMED>(team);
+      team_sync<SYNC>(team);
+      if (ttid == 0) *s_flag = atomicAdd(cnt2 + base, 1) == ngroups - 1;
+      team_sync<SYNC>(team);
       if (*s_flag) {                   // last group: sum the group partials in order
         __threadfence();
-        sum_slots<VEC>(p, slice, slice_w, base, ngroups, GRP, act, tot);
+        sum_slots<VEC>(p, slice, slice_w, base, ngroups, GRP, act, tot, ttid);
         if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
       }
     }
   }
-  team_sync<NAMED>(team);
+  team_sync<SYNC>(team);
 }
 
 // blockDim.x = row vectors of one column slice (32..256); one CTA per chunk.
@@ -601,7 +609,7 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
             FVec<TV> av;
 #pragma unroll
             for (int v = 0; v < TV; ++v) av.v[v] = accf[v];
-            finish_long_piece<TV, true>(p, av, act, col, slice, rr, rb, re, ps, &s_flag, team);
+            finish_long_piece<TV, 1>(p, av, act, col, slice, rr, rb, re, ps, &s_flag, team);
           }
 #pragma unroll
           for (int v = 0; v < V2; ++v) acc[v] = make_float2(0.f, 0.f);
@@ -613,7 +621,7 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
       if constexpr (DW) {
         TransposeReduce<NB, 16>::run(part, lane);   // lane l: warp sum of slot l >> (5 - LG)
         if ((lane & ((32 >> LG) - 1)) == 0) s_red[buf][warp][lane >> (5 - LG)] = part[0];
-        team_sync<true>(team);
+        team_sync<1>(team);
         if (tid < nb) {
           float t = 0.f;
           for (int w2 = 0; w2 < cwarps; ++w2) t += s_red[buf][w2][tid];
