@@ -12,8 +12,9 @@
 //   warp 1   MMA issuer (one elected thread), commits free smem stages and
 //            signals a double-buffered TMEM accumulator
 //   warp 2   TMEM allocator
-//   warps 4-7 epilogue: tcgen05.ld 32x32b (thread = token row) -> shared-memory
-//            transpose -> row-contiguous fp32 score stores
+//   warps 4-7 epilogue: tcgen05.ld 32x32b (thread = token row) -> a 32x32 fp32
+//            tile in shared memory (128-byte swizzle, double-buffered per warp)
+//            -> TMA tensor store to the [T, H*2, S] scores (bulk async groups)
 // The selection (half top-k) consumes the scores in pkm.cu.
 #include "internal.cuh"
 
@@ -28,7 +29,7 @@ namespace {
 constexpr int kBM = 128;     // tokens per tile (UMMA_M)
 constexpr int kBK = 64;      // K elements per stage = one 128-byte swizzle atom of bf16
 constexpr int kStages = 3;
-constexpr int kStageLd = 36;  // epilogue staging row pitch (floats): 16-B aligned, conflict-free
+constexpr int kStageFloats = 32 * 32;  // one epilogue staging tile: 32 token rows x 32 scores
 constexpr int kThreads = 256;
 constexpr uint32_t kSpinLimit = 1u << 28;  // bounded waits: trap instead of hanging
 
@@ -76,6 +77,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// TMA tensor store of one [32 tokens][1][32 scores] box (bulk async group)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -121,7 +131,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
 __global__ void __launch_bounds__(kThreads, 1)
     pkm_scores_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                          const __grid_constant__ CUtensorMap tmK1,
-                         const __grid_constant__ CUtensorMap tmK2, TcParams p) {
+                         const __grid_constant__ CUtensorMap tmK2,
+                         const __grid_constant__ CUtensorMap tmS, TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned carve-up (swizzle-128B atoms need it)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -134,8 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  // epilogue staging: one [32 rows][kStageLd] fp32 tile per epilogue warp
-  float* stage_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
+  // epilogue staging: two [32 rows][32] fp32 tiles per epilogue warp (1024-byte aligned)
+  float* stage_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -153,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK1)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmS)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -225,35 +237,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q4 = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int it = 0;
+    float* stg0 = stage_all + (warp - 4) * 2 * kStageFloats;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
       const int mt = t % p.m_tiles, hh = t / p.m_tiles;
-      const int h = hh >> 1, half = hh & 1;
       const int row0 = mt * kBM + q4 * 32;   // this warp's 32 token rows
-      float* stg = stage_all + (warp - 4) * 32 * kStageLd;
-      const int64_t row_pitch = int64_t(p.H) * 2 * p.S;   // floats between consecutive tokens
-      float* out0 = p.scores + (int64_t(row0) * p.H * 2 + h * 2 + half) * int64_t(p.S);
       for (int n = 0; n < p.n_sub; ++n) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        for (int c0 = 0; c0 < p.BN; c0 += 32, ++it) {
           uint32_t r[32];
           tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
-          // transpose through shared memory so global stores are row-contiguous:
-          // lane = token row on the TMEM side, 8 lanes x 16 B = one 128-B row segment
-          // on the store side (4 rows per store instruction instead of 32)
+          float* stg = stg0 + (it & 1) * kStageFloats;
+          // the store issued from this buffer two chunks ago must have read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          // row `lane`, 16-byte chunk v at position v ^ (lane & 7): the 128-byte
+          // swizzle of the tensor map (conflict-free, 8 lanes per 128-B phase)
 #pragma unroll
           for (int v = 0; v < 8; ++v)
-            *reinterpret_cast<uint4*>(stg + lane * kStageLd + 4 * v) =
+            *reinterpret_cast<uint4*>(stg + lane * 32 + ((v ^ (lane & 7)) << 2)) =
                 make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = 4 * i + (lane >> 3), cv = (lane & 7) * 4;
-            if (row0 + rr < p.T)
-              *reinterpret_cast<float4*>(out0 + rr * row_pitch + n * p.BN + c0 + cv) =
-                  *reinterpret_cast<const float4*>(stg + rr * kStageLd + cv);
+          if (lane == 0) {   // rows past T are clipped by the tensor map
+            tma_store_3d(&tmS, stg, n * p.BN + c0, hh, row0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          __syncwarp();
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
@@ -263,6 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -346,8 +358,22 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
   ML_TRY(make_map(&mq, q, uint64_t(sh.H) * sh.Dk, uint64_t(sh.T), uint64_t(sh.H) * sh.Dk * 2, kBK, kBM));
   ML_TRY(make_map(&mk1, K1, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN));
   ML_TRY(make_map(&mk2, K2, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN));
-  const size_t smem = 1024 + size_t(kStages) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 256 +
-                      size_t(4) * 32 * kStageLd * sizeof(float);
+  CUtensorMap ms;
+  {
+    EncodeFn f = encode_fn();
+    if (!f) return fail(ML_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    // scores [T][H*2][S] fp32; box = 32 scores x 1 (head, half) x 32 tokens
+    cuuint64_t dims[3] = {uint64_t(sh.S), uint64_t(sh.H) * 2, uint64_t(sh.T)};
+    cuuint64_t strides[2] = {uint64_t(sh.S) * 4, uint64_t(sh.H) * 2 * sh.S * 4};
+    cuuint32_t box[3] = {32, 1, 32};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = f(&ms, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, scores, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ML_ERR_CUDA, "cuTensorMapEncodeTiled (scores) failed: " + std::to_string(int(r)));
+  }
+  const size_t smem = 1024 + size_t(kStages) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 1024 +
+                      size_t(4) * 2 * kStageFloats * sizeof(float);
   static size_t configured = 0;
   if (smem > configured) {
     ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -355,7 +381,7 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
     configured = smem;
   }
   const int grid = std::min(p.tiles, num_sms());
-  pkm_scores_tc_kernel<<<grid, kThreads, smem, s>>>(mq, mk1, mk2, p);
+  pkm_scores_tc_kernel<<<grid, kThreads, smem, s>>>(mq, mk1, mk2, ms, p);
   ML_LAUNCH_CHECK("pkm_scores_tc");
   return ML_OK;
 }
