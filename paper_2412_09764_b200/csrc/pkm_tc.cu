@@ -28,8 +28,9 @@ namespace {
 
 constexpr int kBM = 128;     // tokens per tile (UMMA_M)
 constexpr int kBK = 64;      // K elements per stage = one 128-byte swizzle atom of bf16
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kStageFloats = 32 * 32;  // one epilogue staging tile: 32 token rows x 32 scores
+constexpr int kStageBufs = kStages > 3 ? 1 : 2;   // staging tiles per epilogue warp
 constexpr int kThreads = 256;
 constexpr uint32_t kSpinLimit = 1u << 28;  // bounded waits: trap instead of hanging
 
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int it = 0;
-    float* stg0 = stage_all + (warp - 4) * 2 * kStageFloats;
+    float* stg0 = stage_all + (warp - 4) * kStageBufs * kStageFloats;
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
       const int mt = t % p.m_tiles, hh = t / p.m_tiles;
       const int row0 = mt * kBM + q4 * 32;   // this warp's 32 token rows
@@ -248,9 +249,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c0 = 0; c0 < p.BN; c0 += 32, ++it) {
           uint32_t r[32];
           tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
-          float* stg = stg0 + (it & 1) * kStageFloats;
-          // the store issued from this buffer two chunks ago must have read it
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          float* stg = stg0 + (it % kStageBufs) * kStageFloats;
+          // the store issued from this buffer kStageBufs chunks ago must have read it
+          if (lane == 0) {
+            if constexpr (kStageBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
           __syncwarp();
           // row `lane`, 16-byte chunk v at position v ^ (lane & 7): the 128-byte
           // swizzle of the tensor map (conflict-free, 8 lanes per 128-B phase)
@@ -373,7 +377,7 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
     if (r != CUDA_SUCCESS) return fail(ML_ERR_CUDA, "cuTensorMapEncodeTiled (scores) failed: " + std::to_string(int(r)));
   }
   const size_t smem = 1024 + size_t(kStages) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 1024 +
-                      size_t(4) * 2 * kStageFloats * sizeof(float);
+                      size_t(4) * kStageBufs * kStageFloats * sizeof(float);
   static size_t configured = 0;
   if (smem > configured) {
     ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
