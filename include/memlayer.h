@@ -244,11 +244,16 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
  * so memory_layer_fwd_state builds it into the caller-owned `state` buffer
  * (memory_layer_state_bytes) on a library side stream, concurrent with the
  * HBM-bound bag forward, and memory_layer_bwd_state consumes it instead of
- * sorting.  state must not be modified between the two calls; the state is
- * complete when the forward's stream work is.  Results are bit-identical
- * to memory_layer_fwd / memory_layer_bwd (same kernels, same order).  Errors:
- * ML_ERR_WORKSPACE when state_bytes is too small. */
+ * sorting.  state must not be modified between the two calls.  The state is
+ * built asynchronously on a library stream (it fills the SMs the bag forward's
+ * tail and the gate GEMMs leave idle); memory_layer_bwd_state orders its
+ * segmented pass after it, and memory_layer_state_wait(state, stream) makes
+ * any other stream wait for it (e.g. before the buffer is freed or reused).
+ * Results are bit-identical to memory_layer_fwd / memory_layer_bwd (same
+ * kernels, same order).  Errors: ML_ERR_WORKSPACE when state_bytes is too
+ * small. */
 mlStatus memory_layer_state_bytes(const mlLayerShape* shape, size_t* bytes);
+mlStatus memory_layer_state_wait(const void* state, void* stream);
 mlStatus memory_layer_fwd_state(const mlLayerShape* shape, const void* x, const void* q,
                                 const void* K1, const void* K2, const void* V, const void* W1,
                                 const void* W2, void* out, int32_t* idx_saved, float* w_saved,

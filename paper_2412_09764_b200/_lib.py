@@ -81,6 +81,7 @@ SIGNATURES = {
     "memory_layer_bwd_workspace": [C.POINTER(LayerShape), C.POINTER(SZ)],
     "memory_layer_bwd": [C.POINTER(LayerShape)] + [P] * 23 + [SZ, P],
     "memory_layer_state_bytes": [C.POINTER(LayerShape), C.POINTER(SZ)],
+    "memory_layer_state_wait": [P, P],
     "peer_fwd_workspace": [C.POINTER(PeerShape), C.POINTER(SZ)],
     "peer_fwd": [C.POINTER(PeerShape)] + [P] * 11 + [SZ, P],
     "peer_bwd_workspace": [C.POINTER(PeerShape), C.POINTER(SZ)],

@@ -40,9 +40,26 @@ int num_sms() {
 // events, so tensor-core GEMMs overlap the HBM-bound bag kernels.  One set
 // per caller stream (calls on different streams never share them).
 struct Aux {
-  cudaStream_t s[2];
+  cudaStream_t s[3];
   cudaEvent_t ev[8];
 };
+
+// Completion event of the backward state a forward built into a caller buffer
+// (keyed by the buffer): memory_layer_bwd_state orders its segmented pass after
+// it, so the forward need not wait for the sort.
+static mlStatus state_event(const void* state, cudaEvent_t* ev) {
+  static std::mutex mu;
+  static std::map<const void*, cudaEvent_t> m;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = m.find(state);
+  if (it == m.end()) {
+    cudaEvent_t e;
+    ML_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    it = m.emplace(state, e).first;
+  }
+  *ev = it->second;
+  return ML_OK;
+}
 static mlStatus aux_for(cudaStream_t caller, Aux** out) {
   static std::mutex mu;
   static std::map<cudaStream_t, Aux*> m;
@@ -60,6 +77,7 @@ static mlStatus aux_for(cudaStream_t caller, Aux** out) {
   ML_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[0], cudaStreamNonBlocking));
   ML_CUDA_TRY(cudaStreamCreateWithPriority(&a->s[1], cudaStreamNonBlocking, hi));
+  ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[2], cudaStreamNonBlocking));
   for (auto& e : a->ev) ML_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   m[caller] = a;
   *out = a;
@@ -688,6 +706,16 @@ mlStatus embbag_bwd_state(const mlBagShape* shape, const void* V, const float* w
   ML_API_END
 }
 
+mlStatus memory_layer_state_wait(const void* state, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_ptrs({state}));
+  cudaEvent_t done;
+  ML_TRY(state_event(state, &done));
+  ML_CUDA_TRY(cudaStreamWaitEvent(S(stream), done, 0));
+  return ML_OK;
+  ML_API_END
+}
+
 mlStatus memory_layer_fwd_workspace(const mlLayerShape* shape, size_t* bytes) {
   ML_API_BEGIN
   ML_TRY(check_layer(shape));
@@ -743,7 +771,9 @@ mlStatus memory_layer_fwd_state(const mlLayerShape* shape, const void* x, const 
   }
   ML_TRY(pkm_fwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, nullptr, b.pkm, st));
   if (state) {
-    // the backward's sort + runs on aux 1, overlapping the bag forward
+    // the backward's sort + runs on aux 2 (normal priority): it fills the SMs
+    // the bag forward's tail and the gate GEMMs leave idle; the backward's
+    // segmented pass waits for its completion event (no join here)
     if (!aux) ML_TRY(aux_for(st, &aux));
     Carver sc(state);
     BagPrepState ps;
@@ -752,8 +782,11 @@ mlStatus memory_layer_fwd_state(const mlLayerShape* shape, const void* x, const 
     pb.sort = ps.sort;
     pb.runs = ps.runs;
     int32_t *sk = nullptr, *sp = nullptr;
-    ML_TRY(stream_dep(st, aux->s[1], aux->ev[4]));
-    ML_TRY(bag_bwd_prepare(bag_of(s), idx_saved, ps.rows, ps.U, pb, &sk, &sp, aux->s[1]));
+    cudaEvent_t done;
+    ML_TRY(state_event(state, &done));
+    ML_TRY(stream_dep(st, aux->s[2], aux->ev[4]));
+    ML_TRY(bag_bwd_prepare(bag_of(s), idx_saved, ps.rows, ps.U, pb, &sk, &sp, aux->s[2]));
+    ML_CUDA_TRY(cudaEventRecord(done, aux->s[2]));
   }
   BagFwdArgs a;
   a.V = V; a.ldv = s.dv; a.N = s.N;
@@ -766,7 +799,6 @@ mlStatus memory_layer_fwd_state(const mlLayerShape* shape, const void* x, const 
     if (y_saved && y_saved != out)
       ML_CUDA_TRY(cudaMemcpyAsync(y_saved, out, size_t(T) * s.dv * dtype_size(s.pkm.dtype),
                                   cudaMemcpyDeviceToDevice, st));
-    if (state) ML_TRY(stream_dep(aux->s[1], st, aux->ev[5]));   // join the state build
     return check_index_flag(st);
   }
   ML_TRY(stream_dep(aux->s[0], st, aux->ev[1]));   // join: g ready
@@ -776,7 +808,6 @@ mlStatus memory_layer_fwd_state(const mlLayerShape* shape, const void* x, const 
   // out = z W2  [T, D]
   ML_TRY(gemm_rm(false, false, T, s.D, s.dv, b.z, s.dv, W2, s.D, out, s.D, s.pkm.dtype, false,
                  b.gemm_ws, kGemmWs, st));
-  if (state) ML_TRY(stream_dep(aux->s[1], st, aux->ev[5]));     // join the state build
   return check_index_flag(st);
   ML_API_END
 }
@@ -839,6 +870,7 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
   Aux* aux = nullptr;
   ML_TRY(aux_for(st, &aux));
   int32_t *skey = nullptr, *spos = nullptr;
+  const int32_t *state_rows = nullptr, *state_U = nullptr;
   if (state) {
     // sorted map from the forward (memory_layer_fwd_state)
     size_t sneed = 0;
@@ -851,13 +883,8 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
     b.bag.runs = ps.runs;
     const int64_t P = int64_t(bs.T) * bs.B;
     ML_TRY(sorted_result(P, ceil_log2(bs.N), ps.sort, &skey, &spos));
-    if (P == 0) {
-      ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
-    } else {
-      ML_CUDA_TRY(cudaMemcpyAsync(dV_rows, ps.rows, sizeof(int32_t) * size_t(P),
-                                  cudaMemcpyDeviceToDevice, st));
-      ML_CUDA_TRY(cudaMemcpyAsync(U, ps.U, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-    }
+    state_rows = ps.rows;
+    state_U = ps.U;
     ML_TRY(stream_dep(st, aux->s[0], aux->ev[0]));
   } else {
     // aux 0: the value-row sort + runs need only the saved indices
@@ -880,6 +907,19 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
     dy = b.dy;
   }
   ML_TRY(stream_dep(aux->s[0], st, aux->ev[2]));     // sorted runs ready
+  if (state) {   // the forward's state build (its own stream) must be complete
+    cudaEvent_t done;
+    ML_TRY(state_event(state, &done));
+    ML_CUDA_TRY(cudaStreamWaitEvent(st, done, 0));
+    const int64_t P = int64_t(bs.T) * bs.B;
+    if (P == 0) {
+      ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
+    } else {
+      ML_CUDA_TRY(cudaMemcpyAsync(dV_rows, state_rows, sizeof(int32_t) * size_t(P),
+                                  cudaMemcpyDeviceToDevice, st));
+      ML_CUDA_TRY(cudaMemcpyAsync(U, state_U, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    }
+  }
   ML_TRY(bag_bwd_reduce(bs, V, w_saved, dy, dV, b.bag, skey, spos, st));
   const int ns = seg_slices(s.dv, dt);
   const int64_t P = int64_t(T) * bs.B;

@@ -6,6 +6,7 @@ CUDA stream.  No arithmetic of the method happens in Python.  Names follow
 include/memlayer.h.
 """
 import ctypes as C
+import weakref
 
 import torch
 
@@ -270,6 +271,10 @@ def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, qk_norm=False, keep
                                        _p(K2), _p(V), _p(W1 if gated else None),
                                        _p(W2 if gated else None), _p(out), _p(idx), _p(w), _p(g),
                                        _p(y), _p(state), ns, _p(ws), n, _stream()))
+    if state is not None:
+        # the state is written on a library stream: before its memory can go
+        # back to the caching allocator, this stream must wait for that work
+        weakref.finalize(state, lib().memory_layer_state_wait, state.data_ptr(), _stream())
     return out, dict(idx=idx, w=w, g=g, y=y, k=k, gated=gated, qk_norm=qk_norm, state=state,
                      state_bytes=ns)
 
