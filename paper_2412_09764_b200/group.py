@@ -87,8 +87,23 @@ class CudaLocal:
                 t.record_stream(cur)
 
     def embbag_bwd_prepare(self, N, dv, idx, dtype):
-        with self.side(idx):
-            return self.ops.embbag_bwd_prepare(N, dv, idx, dtype)
+        """The backward's inverse map on a normal-priority background stream
+        (it fills SMs the forward's tail leaves idle); returns (state, event):
+        the backward waits on the event, the forward does not."""
+        cur = torch.cuda.current_stream(idx.device)
+        if getattr(self, "_bg", None) is None:
+            self._bg = torch.cuda.Stream(device=idx.device)
+        self._bg.wait_stream(cur)
+        with torch.cuda.stream(self._bg):
+            state = self.ops.embbag_bwd_prepare(N, dv, idx, dtype)
+            ev = torch.cuda.Event()
+            ev.record(self._bg)
+        idx.record_stream(self._bg)
+        state.record_stream(cur)
+        return state, ev
+
+    def wait(self, ev):
+        torch.cuda.current_stream().wait_event(ev)
 
     def pkm_topk(self, q, K1, K2, k):
         return self.ops.pkm_topk(q, K1, K2, k)
@@ -145,10 +160,10 @@ class GroupMemoryLayer:
         idx_all = L.empty((G * T_loc, H, k), idx.dtype, idx)
         w_all = L.empty((G * T_loc, H, k), w.dtype, w)
         C.all_gather(idx_all, idx)                                      # 2
-        state = None
+        state = state_ev = None
         if hasattr(L, "embbag_bwd_prepare"):      # the backward's inverse map, concurrently
-            state = L.embbag_bwd_prepare(V_shard.shape[0], dvG, idx_all.view(G * T_loc, B),
-                                         V_shard.dtype)
+            state, state_ev = L.embbag_bwd_prepare(V_shard.shape[0], dvG,
+                                                   idx_all.view(G * T_loc, B), V_shard.dtype)
         C.all_gather(w_all, w)
         y_part = L.embbag_fwd(V_shard, idx_all.view(G * T_loc, B), w_all.view(G * T_loc, B))  # 3
         gpre = L.gemm(x, W1)
@@ -164,10 +179,9 @@ class GroupMemoryLayer:
             y = y_all[rank * T_loc:(rank + 1) * T_loc]
             _, z = L.unpack(y.reshape(1, T_loc, dv), 1, T_loc, dv, gate=gpre, want_y=False)
         out = L.gemm(z, W2)                                             # 5
-        if state is not None:
-            L.join(state)
         saved = dict(x=x, q=q, K1=K1, K2=K2, V=V_shard, W1=W1, W2=W2, idx=idx, w=w,
-                     idx_all=idx_all, w_all=w_all, g=gpre, y=y, y_all=y_all, state=state)
+                     idx_all=idx_all, w_all=w_all, g=gpre, y=y, y_all=y_all, state=state,
+                     state_ev=state_ev)
         return out, saved
 
     def backward(self, dout, saved, dK1=None, dK2=None):
@@ -195,6 +209,7 @@ class GroupMemoryLayer:
         bag_args = (V_shard, saved["idx_all"].view(G * T_loc, B), saved["w_all"].view(G * T_loc, B),
                     recv)
         if saved.get("state") is not None:
+            L.wait(saved["state_ev"])              # the forward's state build is complete
             rows, dV, U, dw_part = L.embbag_bwd(*bag_args, state=saved["state"])
         else:
             rows, dV, U, dw_part = L.embbag_bwd(*bag_args)
