@@ -253,9 +253,11 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
     timing_mark("memset", st);
   }
   if (b.ds_dense) {
-    timing_mark(nullptr, st);
-    ML_CUDA_TRY(cudaMemsetAsync(b.ds_dense, 0, sizeof(__nv_bfloat16) * size_t(s.T) * s.H * 2 * s.S, st));
-    timing_mark("memset", st);
+    if (!softmax_bwd_full_rows(s)) {
+      timing_mark(nullptr, st);
+      ML_CUDA_TRY(cudaMemsetAsync(b.ds_dense, 0, sizeof(__nv_bfloat16) * size_t(s.T) * s.H * 2 * s.S, st));
+      timing_mark("memset", st);
+    }
     ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, b.ds_dense, qn,
                               nullptr, nullptr, st));
     const int64_t lds = int64_t(s.H) * 2 * s.S;  // row pitch of ds_dense per token

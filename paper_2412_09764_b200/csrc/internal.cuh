@@ -116,6 +116,8 @@ mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const f
 // If ds_dense != nullptr (bf16 [T*H, 2, S], pre-zeroed) the selected
 // half-key score gradients are also scattered densely (duplicates of one
 // (t,h) summed in lane order): ds_dense[th][0][a_j] += ds_j, [1][b_j] += ds_j.
+// true when softmax_bwd writes whole rows of ds_dense (no memset needed)
+bool softmax_bwd_full_rows(const mlPkmShape& sh);
 mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
                             const float* dw_part, int nslices, int64_t slice_stride,
                             float* ds, int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,

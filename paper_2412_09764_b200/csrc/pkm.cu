@@ -592,7 +592,8 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
                                                           int64_t sstride, int64_t TH, int H,
                                                           int S, int k, float* ds, int32_t* key1,
                                                           int32_t* key2, __nv_bfloat16* ds_dense,
-                                                          QkNorm qn, float* ds1w, float* ds2w) {
+                                                          QkNorm qn, float* ds1w, float* ds2w,
+                                                          int full_rows) {
   __shared__ int s_sub[8][2][32];
   __shared__ float s_ds[8][32];
   __shared__ float s_sc[8][2][32];
@@ -630,12 +631,21 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
   }
   if (ds_dense) {
     // dense half-key gradients of this (t, h); a sub-key selected by several
-    // of the k pairs is summed in lane order (deterministic, no atomics)
+    // of the k pairs is summed in lane order (deterministic, no atomics).
+    // full_rows: the two rows [2][S] are assembled in shared memory (zeros
+    // included) and written with coalesced 16-byte stores, so ds_dense needs
+    // no separate memset; otherwise the sums are scattered into a zeroed matrix.
     s_sub[wid][0][lane] = lane < k ? ix / S : -1;
     s_sub[wid][1][lane] = lane < k ? ix % S : -1;
     s_ds[wid][lane] = dsv;
     s_sc[wid][0][lane] = sc1;
     s_sc[wid][1][lane] = sc2;
+    extern __shared__ __align__(16) __nv_bfloat16 s_rows[];   // [8 warps][2][S] when full_rows
+    __nv_bfloat16* rows = s_rows + int64_t(wid) * 2 * S;
+    if (full_rows) {
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      for (int c = lane; c < (2 * S) / 8; c += 32) reinterpret_cast<uint4*>(rows)[c] = z;
+    }
     __syncwarp();
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -648,7 +658,15 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
           sum += s_ds[wid][l] * s_sc[wid][half][l];
         }
       }
-      if (leader) ds_dense[(th * 2 + half) * S + a] = __float2bfloat16_rn(sum);
+      if (leader) {
+        if (full_rows) rows[half * S + a] = __float2bfloat16_rn(sum);
+        else ds_dense[(th * 2 + half) * S + a] = __float2bfloat16_rn(sum);
+      }
+    }
+    if (full_rows) {
+      __syncwarp();
+      uint4* dst = reinterpret_cast<uint4*>(ds_dense + th * 2 * S);
+      for (int c = lane; c < (2 * S) / 8; c += 32) dst[c] = reinterpret_cast<const uint4*>(rows)[c];
     }
   }
 }
@@ -692,15 +710,25 @@ mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const f
   return ML_OK;
 }
 
+bool softmax_bwd_full_rows(const mlPkmShape& sh) { return sh.S % 8 == 0 && sh.S <= 2048; }
+
 mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
                             const float* dw_part, int nslices, int64_t slice_stride, float* ds,
                             int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,
                             const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s) {
   const int64_t TH = int64_t(sh.T) * sh.H;
   if (TH <= 0) return ML_OK;
-  softmax_bwd_kernel<<<unsigned((TH + 7) / 8), 256, 0, s>>>(
+  const bool full = ds_dense && softmax_bwd_full_rows(sh);
+  const size_t smem = full ? size_t(8) * 2 * sh.S * sizeof(__nv_bfloat16) : 0;
+  static bool attr = false;
+  if (full && !attr) {
+    ML_CUDA_TRY(cudaFuncSetAttribute(softmax_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(8 * 2 * 2048 * sizeof(__nv_bfloat16))));
+    attr = true;
+  }
+  softmax_bwd_kernel<<<unsigned((TH + 7) / 8), 256, smem, s>>>(
       idx, w, dw_part, nslices, slice_stride, TH, sh.H, sh.S, sh.k, ds, key1, key2, ds_dense, qn,
-      ds1w, ds2w);
+      ds1w, ds2w, full ? 1 : 0);
   ML_LAUNCH_CHECK("softmax_bwd");
   return ML_OK;
 }
