@@ -26,7 +26,9 @@ LABEL = OrderedDict([("seg_pipe_kernel", "embbag_bwd_segreduce"),
 
 
 def short(name):
-    n = name.replace("ml::<unnamed>::", "").replace("void ", "")
+    n = name.replace("void ", "")
+    for pre in ("ml::<unnamed>::", "ml::(anonymous namespace)::", "unnamed>::"):
+        n = n.replace(pre, "")
     return n.split("(")[0][:60]
 
 
