@@ -96,3 +96,27 @@ def test_null_pointer_rejected_before_any_launch():
     sh = _lib.BagShape(1024, 64, 16, 8, _lib.ML_F32)
     st = lib.embbag_fwd(C.byref(sh), None, None, None, None, None, None, None)
     assert st == _lib.ML_ERR_ARG
+
+
+def test_state_and_peer_queries_and_validation():
+    """The state / PEER entry points validate on the host (no device needed)."""
+    lib = _lib.lib()
+    bag = _lib.BagShape(1024, 64, 16, 8, _lib.ML_F32)
+    st, n = _size(lib.embbag_bwd_state_bytes, bag)
+    assert st == _lib.ML_OK and n > 16 * 8 * 4
+    st, n = _size(lib.memory_layer_state_bytes, _lib.LayerShape(_pkm(), 1024, 64, 64, 1))
+    assert st == _lib.ML_OK and n > 0
+    peer = _lib.PeerShape(_pkm(), 1024, 64)
+    for fn in (lib.peer_fwd_workspace, lib.peer_bwd_workspace):
+        st, n = _size(fn, peer)
+        assert st == _lib.ML_OK and n > 0
+    st, _ = _size(lib.peer_fwd_workspace, _lib.PeerShape(_pkm(), 1000, 64))
+    assert st == _lib.ML_ERR_CONFIG          # N != S^2
+    st, _ = _size(lib.peer_fwd_workspace, _lib.PeerShape(_pkm(), 1024, 3))
+    assert st == _lib.ML_ERR_CONFIG          # 12-byte rows
+    # a too-small state is refused before any launch
+    buf = (C.c_char * 16)()
+    st = lib.embbag_bwd_prepare(C.byref(bag), C.cast(buf, C.c_void_p), C.cast(buf, C.c_void_p), 16,
+                                None)
+    assert st == _lib.ML_ERR_WORKSPACE
+    assert lib.memory_layer_state_wait(None, None) == _lib.ML_ERR_ARG
