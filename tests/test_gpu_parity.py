@@ -329,6 +329,33 @@ def test_embbag_bwd_prepared_state_bit_identical(dtype, dv):
         assert torch.equal(x, y)
 
 
+@pytest.mark.parametrize("keep_state", [False, True])
+def test_memory_layer_deterministic(keep_state):
+    """SURVEY §8 determinism pin: two runs give bitwise-equal idx / w / out /
+    dV / dw / dq / dK / dx / dW (sorted segments, fixed orders, no atomics)."""
+    dtype, T, H, S, Dk, k, dv, D = "bf16", 150, 4, 64, 128, 8, 256, 256
+    seed = 14
+    f = lambda tag, shape, sc=1.0: gen.tensor(seed, tag, shape, scale=sc, dtype=dtype)
+    h = dict(x=f("x", (T, D)), q=f("q", (T, H, Dk)),
+             K1=f("K1", (H, S, Dk // 2), gen.scale_for("K1", Dk=Dk)),
+             K2=f("K2", (H, S, Dk // 2), gen.scale_for("K2", Dk=Dk)),
+             V=f("V", (S * S, dv)), W1=f("W1", (D, dv), gen.scale_for("W1", D=D)),
+             W2=f("W2", (dv, D), gen.scale_for("W2", dv=dv)), dout=f("dout", (T, D)))
+    t = {n: dev(a, dtype) for n, a in h.items()}
+    o = ops()
+    runs = []
+    for _ in range(2):
+        out, saved = o.memory_layer_fwd(t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"],
+                                        k, keep_state=keep_state)
+        g = o.memory_layer_bwd(t["dout"], t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"],
+                               t["W2"], saved, want_dw=True)
+        U = int(g["U"].item())
+        runs.append([out, saved["idx"], saved["w"], g["rows"][:U], g["dV"][:U], g["dw"], g["dq"],
+                     g["dK1"], g["dK2"], g["dx"], g["dW1"], g["dW2"]])
+    for a, b in zip(*runs):
+        assert torch.equal(a, b)
+
+
 # ------------------------------------------------------------ edge cases
 def test_out_of_range_index_reported_under_check_mode():
     """S:233 index error: with ML_CHECK_INDICES=1 an index >= N is reported
