@@ -136,21 +136,27 @@ def test_embbag_bwd_continuous_and_deterministic(dtype, dv):
     assert_close(host(a[2]), rdw, TOL["f32"], "dw")
 
 
-def test_embbag_bwd_long_runs_and_grad_apply():
-    """A hot row hit by 3000 positions: split into 32-position pieces and
-    combined in piece order; dense apply equals A^T dy."""
+@pytest.mark.parametrize("dtype,dv", [("f32", 64), ("bf16", 1024), ("bf16", 2048), ("bf16", 4096)])
+def test_embbag_bwd_long_runs_and_grad_apply(dtype, dv):
+    """A hot row hit by ~2600 positions: split into 32-position pieces and
+    combined in piece order (two-level, counters), for every segmented-kernel
+    configuration (one CTA per chunk; pipelined 16- and 32-byte threads; two
+    column slices); dense apply equals A^T dy."""
     o = ops()
-    N, dv, T, B = 256, 64, 300, 10
+    N, T, B = 256, 300, 10
     idx = np.full((T, B), 7, np.int32)
     idx.flat[::7] = (np.arange(0, T * B, 7) * 13) % N
-    V = gen.tensor(6, "V", (N, dv), dtype="f32")
+    V = gen.tensor(6, "V", (N, dv), dtype=dtype)
     w = streams.softmax_free_weights(6, T, B)
-    dy = gen.tensor(6, "dout", (T, dv), dtype="f32")
-    rows, dV, U, dw = o.embbag_bwd(dev(V), dev(idx), dev(w), dev(dy), sync=False)
+    dy = gen.tensor(6, "dout", (T, dv), dtype=dtype)
+    rows, dV, U, dw = o.embbag_bwd(dev(V, dtype), dev(idx), dev(w), dev(dy, dtype), sync=False)
     rr, rdV, rdw = obag.embbag_bwd(V, idx, w, dy)
     u = int(U.item())
     assert np.array_equal(host(rows[:u]), rr)
     assert_close(host(dV[:u]), rdV, TOL["f32"], "dV")
+    assert_close(host(dw), rdw, TOL["f32"], "dw")
+    if dtype != "f32":
+        return
     dense = torch.zeros((N, dv), dtype=torch.float32, device="cuda")
     o.embbag_grad_apply(dev(V), dev(idx), rows, dV, U, dense)
     A = obag.dense_selection_matrix(idx, w, N)
