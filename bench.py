@@ -264,7 +264,7 @@ def run_e2e(args, t, step, stream, torch, cfg, G, world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    n = max(3, args.steps // 2)
+    n = max(3, args.steps)           # the first upload (pipeline fill) is inside the timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     copy.wait_event(e0)
