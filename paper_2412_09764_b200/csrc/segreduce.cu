@@ -24,6 +24,15 @@
 // (blockIdx.y); every load is a coalesced 512 B row segment.
 // Per chunk the warp loads all position metadata in one round (lane <->
 // position), so each piece costs one memory round trip (V row + dy rows).
+//
+// Two kernels implement this contract:
+//  * seg_kernel: one CTA per 64-position chunk, register batches (above).
+//    Used for row slices < 2 KiB (e.g. the 4-/8-way dim-sharded group) and
+//    for the dense-accumulating key gradients.
+//  * seg_pipe_kernel (further below): persistent and warp-specialised, rows
+//    staged in shared memory by cp.async.bulk; used for the bag backward when
+//    a row slice spans >= 2 KiB (C2: 4 KiB rows).  Same pieces, same order of
+//    summation -> identical results.
 #include "internal.cuh"
 
 #include <algorithm>
