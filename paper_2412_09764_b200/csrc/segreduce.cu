@@ -31,8 +31,9 @@
 //    for the dense-accumulating key gradients.
 //  * seg_pipe_kernel (further below): persistent and warp-specialised, rows
 //    staged in shared memory by cp.async.bulk; used for the bag backward when
-//    a row slice spans >= 2 KiB (C2: 4 KiB rows).  Same pieces, same order of
-//    summation -> identical results.
+//    a row slice spans >= 2 KiB (C2: 4 KiB rows).  Same pieces and the same
+//    position order inside each dV row (identical dV); the dw dot products
+//    group their partial sums by thread width (equal up to rounding).
 #include "internal.cuh"
 
 #include <algorithm>
