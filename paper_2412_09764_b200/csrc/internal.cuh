@@ -46,6 +46,7 @@ struct SortBufs {
   int32_t* v[2] = {nullptr, nullptr};
   int32_t* counts = nullptr;
   int32_t* scan_tmp = nullptr;
+  int32_t* ghist = nullptr;     // single-pass mode: per-pass digit offsets + tile tickets
 };
 void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b);
 // On return *keys / *vals point at the sorted arrays (inside b).

@@ -14,6 +14,9 @@
 // bits; passes = ceil(bits / 11) (2 for a 2^20-row table).
 #include "internal.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace ml {
 namespace {
 
@@ -117,7 +120,15 @@ struct SortPassParams {
   int64_t n; int nblocks; int shift; int dbits; uint32_t key_limit;
   int32_t* counts;  // [nbins][nblocks]; scanned in place between the kernels
   int* flag;
+  // single-pass ("onesweep") mode: per-(tile, digit) status words published
+  // and looked back over, global digit offsets of this pass, a tile ticket
+  uint32_t* status; const int32_t* goff; int32_t* tile_ctr;
 };
+
+constexpr uint32_t kStAgg = 1u << 30;     // tile's own count available
+constexpr uint32_t kStInc = 2u << 30;     // inclusive prefix available
+constexpr uint32_t kStMask = (1u << 30) - 1;
+constexpr uint32_t kSortSpin = 1u << 26;
 
 __device__ __forceinline__ int32_t load_key(const SortPassParams& p, int64_t i, bool first) {
   int32_t k = p.kin[i];
@@ -167,6 +178,7 @@ __global__ void __launch_bounds__(256) sort_hist_kernel(SortPassParams p, bool f
 // then writes every digit's run contiguously (coalesced) at its global offset.
 // dynamic smem: s_cnt[kSortWarps][nbins], s_dstart[nbins], s_goff[nbins],
 //               s_key[kSortTile], s_val[kSortTile]
+template <bool ONESWEEP>
 __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, bool first) {
   extern __shared__ int s_dyn[];
   const int nbins = 1 << p.dbits;
@@ -178,9 +190,14 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
   __shared__ int s_warp[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t mask = uint32_t(nbins - 1);
+  __shared__ int s_tile;
   for (int d = threadIdx.x; d < kSortWarps * nbins; d += 256) s_cnt[d] = 0;
+  if constexpr (ONESWEEP) {   // tiles in ticket order: every predecessor is resident or done
+    if (threadIdx.x == 0) s_tile = atomicAdd(p.tile_ctr, 1);
+  }
   __syncthreads();
-  const int64_t bbase = int64_t(blockIdx.x) * kSortTile;
+  const int tile = ONESWEEP ? s_tile : int(blockIdx.x);
+  const int64_t bbase = int64_t(tile) * kSortTile;
   const int64_t wbase = bbase + int64_t(wid) * kSortRounds * 32;
   const int nvalid = int(p.n - bbase < kSortTile ? p.n - bbase : kSortTile);
   int32_t key[kSortRounds], val[kSortRounds];
@@ -219,11 +236,65 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
   }
   int total;
   int ex = block_excl_scan(sum, s_warp, &total);
+  if constexpr (ONESWEEP) {
+    // publish this tile's digit counts, then look back over the predecessors
+    // (decoupled look-back) for the exclusive prefix of every digit
+    for (int j = 0; j < per; ++j) {
+      const int d = threadIdx.x * per + j;
+      if (d < nbins) {
+        volatile uint32_t* st = p.status + int64_t(tile) * nbins + d;
+        *st = (tile == 0 ? kStInc : kStAgg) | uint32_t(tot_local[j]);
+      }
+    }
+    __threadfence();
+    // all of this thread's digits walk back together: one round of independent
+    // status loads per predecessor tile, until every digit found an inclusive
+    // prefix (tile 0 publishes inclusive values)
+    uint32_t excl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t open = 0;
+    for (int j = 0; j < per; ++j)
+      if (threadIdx.x * per + j < nbins) open |= 1u << j;
+    uint32_t spins = 0;
+    for (int pt = tile - 1; pt >= 0 && open; ) {
+      const volatile uint32_t* row = p.status + int64_t(pt) * nbins + threadIdx.x * per;
+      uint32_t v[8];
+      bool ready = true;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[j] = 0;
+        if (j < per && (open >> j & 1u)) {
+          v[j] = row[j];
+          ready = ready && (v[j] >> 30) != 0;
+        }
+      }
+      if (!ready) {              // some predecessor has not published yet
+        if (++spins > kSortSpin) __trap();
+        continue;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < per && (open >> j & 1u)) {
+          excl[j] += v[j] & kStMask;
+          if ((v[j] >> 30) == 2) open &= ~(1u << j);
+        }
+      }
+      --pt;
+    }
+    for (int j = 0; j < per; ++j) {
+      const int d = threadIdx.x * per + j;
+      if (d >= nbins) continue;
+      if (tile > 0) {
+        volatile uint32_t* st = p.status + int64_t(tile) * nbins + d;
+        *st = kStInc | (excl[j] + uint32_t(tot_local[j]));
+      }
+      s_goff[d] = p.goff[d] + int(excl[j]);
+    }
+  }
   for (int j = 0; j < per; ++j) {
     const int d = threadIdx.x * per + j;
     if (d < nbins) {
       s_dstart[d] = ex;
-      s_goff[d] = p.counts[int64_t(d) * p.nblocks + blockIdx.x];
+      if constexpr (!ONESWEEP) s_goff[d] = p.counts[int64_t(d) * p.nblocks + blockIdx.x];
       int run = ex;
       for (int w = 0; w < kSortWarps; ++w) {
         const int c = s_cnt[w * nbins + d];
@@ -257,6 +328,55 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
     p.kout[g] = k;
     p.vout[g] = s_val[e];
   }
+}
+
+// ---- single-pass sort support: one read of the keys builds the global digit
+// histograms of every pass; one CTA turns them into per-pass digit offsets.
+// ghist: [passes][nbins] counts -> exclusive offsets; ghist[passes*nbins + pass]
+// are the tile tickets (zeroed here).
+__global__ void __launch_bounds__(256) sort_ghist_kernel(const int32_t* keys, int64_t n,
+                                                         uint32_t key_limit, int passes,
+                                                         int dbits, int32_t* ghist, int* flag) {
+  extern __shared__ int s_h[];   // [passes][nbins]
+  const int nbins = 1 << dbits;
+  for (int i = threadIdx.x; i < passes * nbins; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  const uint32_t mask = uint32_t(nbins - 1);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t k = uint32_t(keys[i]);
+    if (k >= key_limit) {
+      atomicExch(flag, 1);
+      k = 0;
+    }
+    for (int ps = 0; ps < passes; ++ps) atomicAdd(&s_h[ps * nbins + ((k >> (ps * dbits)) & mask)], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * nbins; i += blockDim.x)
+    if (s_h[i]) atomicAdd(&ghist[i], s_h[i]);
+}
+
+__global__ void __launch_bounds__(1024) sort_gscan_kernel(int32_t* ghist, int passes, int nbins) {
+  __shared__ int s_warp[32];
+  for (int ps = 0; ps < passes; ++ps) {
+    int32_t* h = ghist + ps * nbins;
+    const int per = (nbins + 1023) / 1024;
+    int v[2] = {0, 0}, sum = 0;
+    for (int j = 0; j < per; ++j) {
+      const int d = threadIdx.x * per + j;
+      v[j] = d < nbins ? h[d] : 0;
+      sum += v[j];
+    }
+    int tot;
+    int ex = block_excl_scan(sum, s_warp, &tot);
+    for (int j = 0; j < per; ++j) {
+      const int d = threadIdx.x * per + j;
+      if (d < nbins) h[d] = ex;
+      ex += v[j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < passes) ghist[passes * nbins + threadIdx.x] = 0;
 }
 
 // ------------------------------------------------------------ runs
@@ -321,6 +441,7 @@ void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b) {
   b.v[1] = c.take<int32_t>(n);
   b.counts = c.take<int32_t>((int64_t(1) << kMaxDigitBits) * nb);
   b.scan_tmp = c.take<int32_t>(scan_tmp_elems((int64_t(1) << kMaxDigitBits) * nb));
+  b.ghist = c.take<int32_t>(3 * (int64_t(1) << kMaxDigitBits) + 8);
 }
 
 static int sort_passes(int bits) { return (bits + kMaxDigitBits - 1) / kMaxDigitBits; }
@@ -356,7 +477,7 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
     const int max_smem = int(sizeof(int)) * ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile);
     ML_CUDA_TRY(cudaFuncSetAttribute(sort_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      max_smem));
-    ML_CUDA_TRY(cudaFuncSetAttribute(sort_scatter_kernel,
+    ML_CUDA_TRY(cudaFuncSetAttribute(sort_scatter_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
     attr = true;
   }
@@ -373,6 +494,47 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
   const int32_t* kin = keys_in;
   const int32_t* vin = nullptr;
   int cur = 0;
+  static const bool onesweep = [] {
+    const char* e = std::getenv("ML_SORT_ONESWEEP");
+    return !(e && e[0] == '0');
+  }();
+  if (onesweep && passes <= 3 && n < (int64_t(1) << 30)) {
+    // one read of the keys for all passes' global histograms, then one
+    // decoupled-look-back scatter kernel per pass
+    ML_CUDA_TRY(cudaMemsetAsync(b.ghist, 0, sizeof(int32_t) * size_t(passes) * nbins, s));
+    const unsigned gh = unsigned(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+    sort_ghist_kernel<<<gh, 256, sizeof(int) * size_t(passes) * nbins, s>>>(
+        keys_in, n, p.key_limit, passes, dbits, b.ghist, p.flag);
+    ML_LAUNCH_CHECK("sort_hist");
+    sort_gscan_kernel<<<1, 1024, 0, s>>>(b.ghist, passes, nbins);
+    ML_LAUNCH_CHECK("scan_blocks");
+    static bool attr1 = false;
+    if (!attr1) {
+      const int max_smem = int(sizeof(int)) * ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile);
+      ML_CUDA_TRY(cudaFuncSetAttribute(sort_scatter_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+      attr1 = true;
+    }
+    p.status = reinterpret_cast<uint32_t*>(b.counts);
+    for (int pass = 0; pass < passes; ++pass) {
+      p.kin = kin;
+      p.vin = vin;
+      p.kout = b.k[cur];
+      p.vout = b.v[cur];
+      p.shift = pass * dbits;
+      p.goff = b.ghist + pass * nbins;
+      p.tile_ctr = b.ghist + passes * nbins + pass;
+      ML_CUDA_TRY(cudaMemsetAsync(b.counts, 0, sizeof(uint32_t) * size_t(ncounts), s));
+      sort_scatter_kernel<true><<<nb, 256, smem_scatter, s>>>(p, pass == 0);
+      ML_LAUNCH_CHECK("sort_scatter");
+      kin = b.k[cur];
+      vin = b.v[cur];
+      cur ^= 1;
+    }
+    *keys = const_cast<int32_t*>(kin);
+    *vals = const_cast<int32_t*>(vin);
+    return ML_OK;
+  }
   for (int pass = 0; pass < passes; ++pass) {
     p.kin = kin;
     p.vin = vin;
@@ -383,7 +545,7 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
     sort_hist_kernel<<<nb, 256, smem_hist, s>>>(p, first);
     ML_LAUNCH_CHECK("sort_hist");
     ML_TRY(scan_exclusive(b.counts, b.counts, ncounts, b.scan_tmp, nullptr, s));
-    sort_scatter_kernel<<<nb, 256, smem_scatter, s>>>(p, first);
+    sort_scatter_kernel<false><<<nb, 256, smem_scatter, s>>>(p, first);
     ML_LAUNCH_CHECK("sort_scatter");
     kin = b.k[cur];
     vin = b.v[cur];
