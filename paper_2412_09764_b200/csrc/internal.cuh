@@ -65,6 +65,7 @@ struct RunBufs {
   int32_t* piece_base = nullptr; // [n] exclusive scan of pieces
   int32_t* n_slots = nullptr;    // device scalar
   int32_t* scan_tmp = nullptr;
+  int32_t* lb = nullptr;         // single-pass mode: look-back status words + tickets
 };
 void runs_carve(Carver& c, int64_t n, RunBufs& r);
 // rows_out (nullable) [n]: distinct keys ascending; U (device int) count.
