@@ -499,3 +499,34 @@ def test_memory_layer_qk_norm(dtype, T, H, S, Dk, k, dv, D):
     assert_close(host(g["dq"]), r["dq"], tol, "dq")
     assert_close(host(g["dK1"]), r["dK1"], tol, "dK1")
     assert_close(host(g["dK2"]), r["dK2"], tol, "dK2")
+
+
+@pytest.mark.slow
+def test_embbag_bwd_large_position_count():
+    """8.4M positions (the 4-/8-way group's per-rank size): the single-pass
+    run kernels and the look-back sort; rows are the distinct indices and
+    sampled rows' dV equal their oracle sums (Zipf stream: long runs too)."""
+    o = ops()
+    N, dv, T, B = 1 << 20, 64, 65536, 128
+    idx = streams.zipf_indices(15, T, B, N, 0.8)
+    w = streams.softmax_free_weights(15, T, B)
+    dy = gen.tensor(15, "dout", (T, dv), dtype="f32")
+    V = gen.tensor(15, "V", (N, dv), dtype="f32")
+    rows, dV, U, dw = o.embbag_bwd(dev(V), dev(idx), dev(w), dev(dy), sync=False)
+    u = int(U.item())
+    flat = idx.reshape(-1)
+    ur = np.unique(flat)
+    assert u == ur.size and np.array_equal(host(rows[:u]), ur)
+    rng = np.random.default_rng(0)
+    order = np.argsort(flat, kind="stable")
+    starts = np.searchsorted(flat[order], ur)
+    ends = np.searchsorted(flat[order], ur, side="right")
+    pick = np.concatenate([np.argsort(ends - starts)[-8:], rng.choice(ur.size, 56, replace=False)])
+    gdV = host(dV[:u])
+    for j in pick:
+        pos = order[starts[j]:ends[j]]
+        ref = (w.reshape(-1)[pos, None].astype(np.float64) * dy[pos // B].astype(np.float64)).sum(0)
+        assert_close(gdV[j], ref, TOL["f32"], f"dV[{ur[j]}]")
+    sp = rng.choice(T * B, 256, replace=False)
+    refdw = np.einsum("pd,pd->p", dy[sp // B].astype(np.float64), V[flat[sp]].astype(np.float64))
+    assert_close(host(dw).reshape(-1)[sp], refdw, TOL["f32"], "dw")
