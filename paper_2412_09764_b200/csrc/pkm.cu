@@ -314,17 +314,16 @@ __device__ __forceinline__ bool row_topk_fast(const float* sr, int S, int k, Top
   *count_out = count;
   int pos = incl - cnt;
   uint64_t* ck = sm.cand;
-  while (mask) {
-    const int b = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const int r = b >> 2, cc = b & 3;
-    const float4 q = v[0];
-    float val = q.x;
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr)
-      if (rr == r) val = cc == 0 ? v[rr].x : cc == 1 ? v[rr].y : cc == 2 ? v[rr].z : v[rr].w;
-    if (pos < kCandCap) ck[pos] = make_key(val, uint32_t(r * 128 + lane * 4 + cc));
-    ++pos;
+  for (int r = 0; r < R; ++r) {        // static round index: no dynamic register indexing
+    uint32_t bits = (mask >> (4 * r)) & 15u;
+    while (bits) {
+      const int cc = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const float val = cc == 0 ? v[r].x : cc == 1 ? v[r].y : cc == 2 ? v[r].z : v[r].w;
+      if (pos < kCandCap) ck[pos] = make_key(val, uint32_t(r * 128 + lane * 4 + cc));
+      ++pos;
+    }
   }
   if (count > 64) return false;
   __syncwarp();
