@@ -28,8 +28,9 @@ CASES = [  # (dtype, T, H, S, Dk, k, D)
 ]
 
 
-@pytest.mark.parametrize("dtype,T,H,S,Dk,k,D", CASES)
-def test_peer_fwd_bwd(dtype, T, H, S, Dk, k, D):
+@pytest.mark.parametrize("dtype,T,H,S,Dk,k,D,qk_norm", [c + (False,) for c in CASES] +
+                         [("bf16", 150, 4, 64, 128, 8, 256, True), ("f32", 77, 2, 32, 64, 8, 128, True)])
+def test_peer_fwd_bwd(dtype, T, H, S, Dk, k, D, qk_norm):
     from paper_2412_09764_b200 import ops as o
     seed = 21
     f = lambda tag, shape, sc=1.0: gen.tensor(seed, tag, shape, scale=sc, dtype=dtype)
@@ -39,11 +40,17 @@ def test_peer_fwd_bwd(dtype, T, H, S, Dk, k, D):
              U=f("W1", (S * S, D), gen.scale_for("W1", D=D)), V=f("V", (S * S, D)),
              dy=f("dout", (T, D)))
     t = {n: dev(a, dtype) for n, a in h.items()}
-    y, saved = o.peer_fwd(t["x"], t["q"], t["K1"], t["K2"], t["U"], t["V"], k)
+    y, saved = o.peer_fwd(t["x"], t["q"], t["K1"], t["K2"], t["U"], t["V"], k, qk_norm=qk_norm)
     g = o.peer_bwd(t["dy"], t["x"], t["q"], t["K1"], t["K2"], t["U"], t["V"], saved, want_dwr=True)
     h64 = {n: a.astype(np.float64) for n, a in h.items()}
-    ry, rs = opeer.peer_fwd(h64["x"], h64["q"], h64["K1"], h64["K2"], h64["U"], h64["V"], k)
-    near = compare_topk(host(saved["idx"]), rs["idx"], h64["q"], h64["K1"], h64["K2"])
+    ry, rs = opeer.peer_fwd(h64["x"], h64["q"], h64["K1"], h64["K2"], h64["U"], h64["V"], k,
+                            qk_norm=qk_norm)
+    if qk_norm:   # near-tie rule on the normalised operands
+        from oracle import pkm as opkm
+        qn, K1n, K2n = opkm._qk(h64["q"], h64["K1"], h64["K2"])
+        near = compare_topk(host(saved["idx"]), rs["idx"], qn, K1n, K2n)
+    else:
+        near = compare_topk(host(saved["idx"]), rs["idx"], h64["q"], h64["K1"], h64["K2"])
     assert not near, f"near ties in a small case: {near}"
     r = opeer.peer_bwd(h64["dy"], h64["x"], h64["q"], h64["K1"], h64["K2"], h64["U"], h64["V"], rs)
     tol = TOL[dtype]
