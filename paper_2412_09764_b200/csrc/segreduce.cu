@@ -29,8 +29,9 @@
 //  * seg_kernel: one CTA per 64-position chunk, register batches (above).
 //    Used for row slices < 2 KiB (e.g. the 4-/8-way dim-sharded group) and
 //    for the dense-accumulating key gradients.
-//  * seg_pipe_kernel (further below): persistent and warp-specialised, rows
-//    staged in shared memory by cp.async.bulk; used for the bag backward when
+//  * seg_pipe_kernel (further below): persistent and warp-specialised (chunks
+//    drawn from a global work ticket), rows staged in shared memory by
+//    cp.async.bulk; used for the bag backward when
 //    a row slice spans >= 2 KiB (C2: 4 KiB rows).  Same pieces and the same
 //    position order inside each dV row (identical dV); the dw dot products
 //    group their partial sums by thread width (equal up to rounding).
@@ -51,6 +52,7 @@ struct SegParams {
   float* dw_part;
   float* out; int64_t ldo; int dense;
   float* partial; int32_t* counters; int64_t nslots_cap;
+  int32_t* ticket;   // work-item counter of the persistent kernel (zeroed)
   int32_t vec_units;  // 16-byte vectors per row (whole dv)
 };
 
@@ -447,6 +449,7 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
   constexpr int MS = kMetaStages;
   __shared__ SegMeta s_meta[MS][kMeta];
   __shared__ int s_rng[MS][2];
+  __shared__ int s_item[MS];                    // work item of each metadata stage, -1 = done
   __shared__ uint64_t s_mfull[MS], s_mempty[MS];
   __shared__ float s_red[2][8][NB];
   __shared__ int s_flag;
@@ -473,12 +476,22 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
 
   if (warp == cwarps + 1) {
     // --------------------------------------------- metadata warp (runs ahead)
-    int it = 0;
-    for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-      const int64_t c0 = (w % nchunks) * kChunk;
+    // Work items are taken from a global ticket (dynamic: CTAs that start late
+    // behind a concurrent kernel, or draw cheap chunks, take more items).
+    for (int it = 0;; ++it) {
+      int64_t w = 0;
+      if (lane == 0) w = atomicAdd(p.ticket, 1);
+      w = __shfl_sync(0xffffffffu, w, 0);
       const int ms = it % MS;
       const uint32_t mu = uint32_t(it / MS);
       if (mu > 0) bar_wait_sleep(&s_mempty[ms], (mu - 1) & 1);
+      if (w >= items) {
+        if (lane == 0) s_item[ms] = -1;
+        __syncwarp();
+        bar_arrive(&s_mfull[ms]);
+        break;
+      }
+      const int64_t c0 = (w % nchunks) * kChunk;
       int kmin = 0x7fffffff, kmax = -1;
 #pragma unroll
       for (int r = 0; r < (kMeta + 31) / 32; ++r) {
@@ -509,7 +522,7 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
       }
-      if (lane == 0) { s_rng[ms][0] = kmin; s_rng[ms][1] = kmax; }
+      if (lane == 0) { s_rng[ms][0] = kmin; s_rng[ms][1] = kmax; s_item[ms] = int(w); }
       __syncwarp();
       bar_arrive(&s_mfull[ms]);                 // 32 arrivals: every lane's writes released
     }
@@ -525,11 +538,12 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
     int ps_slot = 0;            // next stage, its phase, whether the ring has wrapped once
     uint32_t ps_phase = 0;
     bool ps_used = false;
-    int it = 0;
-    for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-      const int slice = int(w / nchunks);
+    for (int it = 0;; ++it) {
       const int ms = it % MS;
       bar_wait_sleep(&s_mfull[ms], uint32_t(it / MS) & 1);
+      const int w = s_item[ms];
+      if (w < 0) break;
+      const int slice = int(w / nchunks);
       const int kmin = s_rng[ms][0], kmax = s_rng[ms][1];
       const char* srcb = p.src + (int64_t(p.src_col0) + int64_t(slice) * team * TV) * int64_t(sizeof(T));
       const char* vb = DW ? p.V + (int64_t(p.v_col0) + int64_t(slice) * team * TV) * int64_t(sizeof(T))
@@ -566,12 +580,14 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
   for (int v = 0; v < V2; ++v) acc[v] = g[v] = make_float2(0.f, 0.f);
   int cs_slot = 0;               // stage of the next batch and its full-barrier phase
   uint32_t cs_phase = 0;
-  int it = 0, buf = 0;
-  for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-    const int slice = int(w / nchunks);
-    const int64_t c0 = (w % nchunks) * kChunk;
+  int buf = 0;
+  for (int it = 0;; ++it) {
     const int ms = it % MS;
     bar_wait(&s_mfull[ms], uint32_t(it / MS) & 1);
+    const int w = s_item[ms];
+    if (w < 0) break;
+    const int slice = int(w / nchunks);
+    const int64_t c0 = (w % nchunks) * kChunk;
     const SegMeta* M = s_meta[ms];
     const int k_first = s_rng[ms][0], k_end = s_rng[ms][1];
     const int64_t col = int64_t(slice) * team * TV + int64_t(tid) * TV;
@@ -746,7 +762,7 @@ void seg_carve(Carver& c, int64_t P, int32_t dv, mlDtype dt, float** partial, in
   const int ns = seg_slices(dv, dt);
   const int64_t slice_w = int64_t(team_threads(vu)) * (16 / int64_t(dtype_size(dt)));
   *partial = c.take<float>(ns * nslots_cap(P) * slice_w);
-  *counters = c.take<int32_t>(ns * 2 * nslots_cap(P));
+  *counters = c.take<int32_t>(ns * 2 * nslots_cap(P) + 1);   // + the work ticket
 }
 
 mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
@@ -770,9 +786,10 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   p.dw_part = a.dw_part;
   p.out = a.out; p.ldo = a.ldo; p.dense = a.dense_accumulate ? 1 : 0;
   p.partial = a.partial; p.counters = a.counters; p.nslots_cap = nslots_cap(a.P);
+  p.ticket = a.counters + 2 * int64_t(ns) * p.nslots_cap;
   p.vec_units = int32_t(vu);
   timing_mark(nullptr, s);
-  ML_CUDA_TRY(cudaMemsetAsync(a.counters, 0, sizeof(int32_t) * 2 * size_t(ns) * size_t(p.nslots_cap), s));
+  ML_CUDA_TRY(cudaMemsetAsync(a.counters, 0, sizeof(int32_t) * (2 * size_t(ns) * size_t(p.nslots_cap) + 1), s));
   timing_mark("memset", s);
   const int64_t nchunks = (a.P + kChunk - 1) / kChunk;
   dim3 grid{unsigned(nchunks), unsigned(ns), 1u};
