@@ -95,25 +95,32 @@ __global__ void __launch_bounds__(256) peer_dot_kernel(const char* Ut, int64_t l
 // x[t] in registers and owns rows j = warp, warp + 8, ...; two rows per step
 // (2 x NCH 16-byte loads per lane in flight), warp-shuffle reductions only.
 template <typename T, int NCH>
-__global__ void __launch_bounds__(256) peer_dot_warp_kernel(const char* Ut, int64_t ld_bytes,
+__global__ void __launch_bounds__(256, 3) peer_dot_warp_kernel(const char* Ut, int64_t ld_bytes,
                                                             int64_t N, const int32_t* idx, int32_t B,
                                                             const char* x, float* h_part, int64_t P) {
   constexpr int VEC = Vec<T>::N;
+  __shared__ int s_idx[1024];
   const int64_t t = blockIdx.x;
   const int slice = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t col0 = int64_t(slice) * 4096 + lane * 16;
-  float2 xf[NCH][VEC / 2];
-#pragma unroll
-  for (int c = 0; c < NCH; ++c)
-    Vec<T>::load(ldg_nc_v4(x + t * ld_bytes + col0 + c * 512), reinterpret_cast<float*>(xf[c]));
-  const int32_t* ib = idx + t * B;
+  // the bag's indices are staged once (clamped): the row loads of every step
+  // then depend on a shared-memory read, not a global one
+  for (int j = threadIdx.x; j < B; j += blockDim.x) {
+    int ix = idx[t * B + j];
+    if (uint64_t(uint32_t(ix)) >= uint64_t(N)) ix = 0;
+    s_idx[j] = ix;
+  }
+  // x[t]'s slice in shared memory (read at use): the registers go to the row
+  // loads in flight, 3 CTAs/SM
+  __shared__ uint4 s_x[NCH * 32];
+  for (int e = threadIdx.x; e < NCH * 32; e += blockDim.x)
+    s_x[e] = ldg_nc_v4(x + t * ld_bytes + int64_t(slice) * 4096 + int64_t(e) * 16);
+  __syncthreads();
   for (int j0 = warp; j0 < B; j0 += 16) {
     const int j1 = j0 + 8;
-    int r0 = ib[j0];
-    int r1 = j1 < B ? ib[j1] : r0;
-    if (uint64_t(uint32_t(r0)) >= uint64_t(N)) r0 = 0;
-    if (uint64_t(uint32_t(r1)) >= uint64_t(N)) r1 = 0;
+    const int r0 = s_idx[j0];
+    const int r1 = j1 < B ? s_idx[j1] : r0;
     uint4 a[NCH], b[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
@@ -123,13 +130,14 @@ __global__ void __launch_bounds__(256) peer_dot_warp_kernel(const char* Ut, int6
     float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
-      float2 fa[VEC / 2], fb[VEC / 2];
+      float2 xf[VEC / 2], fa[VEC / 2], fb[VEC / 2];
+      Vec<T>::load(s_x[c * 32 + lane], reinterpret_cast<float*>(xf));
       Vec<T>::load(a[c], reinterpret_cast<float*>(fa));
       Vec<T>::load(b[c], reinterpret_cast<float*>(fb));
 #pragma unroll
       for (int v = 0; v < VEC / 2; ++v) {
-        pa = ffma2(xf[c][v], fa[v], pa);
-        pb = ffma2(xf[c][v], fb[v], pb);
+        pa = ffma2(xf[v], fa[v], pa);
+        pb = ffma2(xf[v], fb[v], pb);
       }
     }
     float sv[2] = {pa.x + pa.y, pb.x + pb.y};
