@@ -191,7 +191,7 @@ __device__ __forceinline__ void insert4(uint64_t key, uint64_t& t0, uint64_t& t1
 
 constexpr int kCandCap = 256;
 
-struct TopkSmem {           // per warp
+struct alignas(16) TopkSmem {   // per warp
   uint32_t hist[256];
   uint64_t sel[32];
   uint64_t u128[128];
@@ -314,27 +314,35 @@ __device__ __forceinline__ bool row_topk_fast(const float* sr, int S, int k, Top
   *count_out = count;
   int pos = incl - cnt;
   uint64_t* ck = sm.cand;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {        // static round index: no dynamic register indexing
-    uint32_t bits = (mask >> (4 * r)) & 15u;
-    while (bits) {
-      const int cc = __ffs(bits) - 1;
-      bits &= bits - 1;
-      const float val = cc == 0 ? v[r].x : cc == 1 ? v[r].y : cc == 2 ? v[r].z : v[r].w;
-      if (pos < kCandCap) ck[pos] = make_key(val, uint32_t(r * 128 + lane * 4 + cc));
-      ++pos;
-    }
+  // the lane's survivors (~1 per lane) are re-read from the row (L1/L2 hits):
+  // bit 4r + c of mask <-> element r*128 + lane*4 + c
+  for (uint32_t bits = mask; bits; bits &= bits - 1) {
+    const int b = __ffs(bits) - 1;
+    const int e = (b >> 2) * 128 + lane * 4 + (b & 3);
+    if (pos < kCandCap) ck[pos] = make_key(sr[e], uint32_t(e));
+    ++pos;
   }
   if (count > 64) return false;
   __syncwarp();
-  // rank of the keys at lane and lane + 32 among all survivors (keys unique)
+  // rank of the keys at lane and lane + 32 among all survivors (keys unique),
+  // two survivors per shared-memory load
   const bool h0 = lane < count, h1 = lane + 32 < count;
   const uint64_t k0 = h0 ? ck[lane] : ~0ull, k1 = h1 ? ck[lane + 32] : ~0ull;
   int r0 = 0, r1 = 0;
-  for (int l = 0; l < count; ++l) {
-    const uint64_t kl = ck[l];
-    r0 += kl > k0 ? 1 : 0;
-    r1 += kl > k1 ? 1 : 0;
+  if ((count & 1) != 0) ck[count] = 0ull;   // pad: ranks nothing
+  __syncwarp();
+  const int pairs = (count + 1) >> 1;
+  if (count <= 32) {
+    for (int l = 0; l < pairs; ++l) {
+      const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(ck)[l];
+      r0 += (kk.x > k0 ? 1 : 0) + (kk.y > k0 ? 1 : 0);
+    }
+  } else {
+    for (int l = 0; l < pairs; ++l) {
+      const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(ck)[l];
+      r0 += (kk.x > k0 ? 1 : 0) + (kk.y > k0 ? 1 : 0);
+      r1 += (kk.x > k1 ? 1 : 0) + (kk.y > k1 ? 1 : 0);
+    }
   }
   if (h0 && r0 < k) { hI[row * k + r0] = int32_t(key_id(k0)); hs[row * k + r0] = key_score(k0); }
   if (h1 && r1 < k) { hI[row * k + r1] = int32_t(key_id(k1)); hs[row * k + r1] = key_score(k1); }

@@ -8,6 +8,6 @@ import json,sys
 l = [x for x in open('gpurun_out/ab.log') if x.startswith('{')]
 if not l: print(sys.argv[1], "FAILED", open('gpurun_out/ab.log').read()[-1500:]); sys.exit()
 d = json.loads(l[-1]); k = d["kernel_ms_per_step"]
-print(f"{sys.argv[1]:28s} ms {d['ms_per_step']:.3f} seg {k.get('embbag_bwd_segreduce')} smbwd {k.get('softmax_bwd')}")
+print(f"{sys.argv[1]:28s} ms {d["ms_per_step"]:.3f} seg {k.get("embbag_bwd_segreduce")} smbwd {k.get("softmax_bwd")} topk {k.get("half_topk")} comb {k.get("combine_softmax")}")
 PY
 done; done
