@@ -498,14 +498,23 @@ __device__ __forceinline__ bool combine_fast(const float* s1p, const int32_t* i1
   int pos = incl - n;
   for (int i = 0; i < n; ++i)
     cand[pos + i] = make_key(s1p[i] + s2, uint32_t(i1p[i]) * uint32_t(S) + i2);
+  if ((count & 1) != 0) cand[count] = 0ull;   // pad: ranks nothing
   __syncwarp();
   const bool h0 = lane < count, h1 = lane + 32 < count;
   const uint64_t k0 = h0 ? cand[lane] : ~0ull, k1 = h1 ? cand[lane + 32] : ~0ull;
   int r0 = 0, r1 = 0;
-  for (int l = 0; l < count; ++l) {
-    const uint64_t kl = cand[l];
-    r0 += kl > k0 ? 1 : 0;
-    r1 += kl > k1 ? 1 : 0;
+  const int pairs = (count + 1) >> 1;   // two survivors per shared-memory load
+  if (count <= 32) {
+    for (int l = 0; l < pairs; ++l) {
+      const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(cand)[l];
+      r0 += (kk.x > k0 ? 1 : 0) + (kk.y > k0 ? 1 : 0);
+    }
+  } else {
+    for (int l = 0; l < pairs; ++l) {
+      const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(cand)[l];
+      r0 += (kk.x > k0 ? 1 : 0) + (kk.y > k0 ? 1 : 0);
+      r1 += (kk.x > k1 ? 1 : 0) + (kk.y > k1 ? 1 : 0);
+    }
   }
   if (h0 && r0 < k) sel[r0] = k0;
   if (h1 && r1 < k) sel[r1] = k1;
