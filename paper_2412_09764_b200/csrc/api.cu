@@ -913,16 +913,19 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
     cudaEvent_t done;
     ML_TRY(state_event(state, &done));
     ML_CUDA_TRY(cudaStreamWaitEvent(st, done, 0));
+    // the row list / count copies run on aux 0, beside the segmented pass
+    ML_CUDA_TRY(cudaStreamWaitEvent(aux->s[0], done, 0));
     const int64_t P = int64_t(bs.T) * bs.B;
     if (P == 0) {
-      ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
+      ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), aux->s[0]));
     } else {
       ML_CUDA_TRY(cudaMemcpyAsync(dV_rows, state_rows, sizeof(int32_t) * size_t(P),
-                                  cudaMemcpyDeviceToDevice, st));
-      ML_CUDA_TRY(cudaMemcpyAsync(U, state_U, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+                                  cudaMemcpyDeviceToDevice, aux->s[0]));
+      ML_CUDA_TRY(cudaMemcpyAsync(U, state_U, sizeof(int32_t), cudaMemcpyDeviceToDevice, aux->s[0]));
     }
   }
   ML_TRY(bag_bwd_reduce(bs, V, w_saved, dy, dV, b.bag, skey, spos, st));
+  if (state) ML_TRY(stream_dep(aux->s[0], st, aux->ev[5]));   // join the copies
   const int ns = seg_slices(s.dv, dt);
   const int64_t P = int64_t(T) * bs.B;
   ML_TRY(pkm_bwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, b.bag.dw_part, ns, P, dq, dK1, dK2,
