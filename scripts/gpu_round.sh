@@ -20,4 +20,4 @@ for f in ("gpurun_out/bench.log", "gpurun_out/bench_group.log", "gpurun_out/benc
     print(f, "value", d.get("value"), "ms", d.get("ms_per_step"), "e2e", (d.get("e2e") or {}).get("value"))
     print("  roofline", d.get("roofline")); print("  cpu", d.get("cpu_baseline")); print("  clocks", d.get("clocks"), "launches", d.get("gpu_launches"))
 PY
-tail -3 gpurun_out/bench.err gpurun_out/bench_group.err gpurun_out/bench_ref.err
+tail -n 3 gpurun_out/bench.err gpurun_out/bench_group.err gpurun_out/bench_ref.err
