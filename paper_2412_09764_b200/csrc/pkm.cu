@@ -260,11 +260,13 @@ __device__ __forceinline__ float warp_sort_desc_f(float x) {
 //  4. each survivor's rank in (score desc, index asc) order is counted
 //     against all survivors and ranks < k are written directly.
 // Returns false (nothing written) when more than 64 values survive (ties).
+// FULL: S == 1024 (all R rounds present: no padding of absent rounds)
+template <bool FULL>
 __device__ __forceinline__ bool row_topk_fast(const float* sr, int S, int k, TopkSmem& sm,
                                               int64_t row, int32_t* hI, float* hs, int* count_out) {
   constexpr int R = 8;                         // float4 rounds held in registers (S <= 1024)
   const int lane = threadIdx.x & 31;
-  const int rounds = S / 128;
+  const int rounds = FULL ? R : S / 128;
   float4 v[R];
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -365,7 +367,9 @@ __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int
   auto score_at = [=](int e) { return ki ? (sr[e] * qi) * ki[e] : sr[e]; };
   if ((S % 128) == 0 && S <= 1024 && ki == nullptr && k <= 32) {
     int count = 0;
-    if (row_topk_fast(sr, S, k, sm, row, hI, hs, &count)) return;
+    if (S == 1024 ? row_topk_fast<true>(sr, S, k, sm, row, hI, hs, &count)
+                  : row_topk_fast<false>(sr, S, k, sm, row, hI, hs, &count))
+      return;
     uint64_t key;
     if (count <= kCandCap) {     // many ties: exact select over the survivors
       key = select_cand(count, k, sm);
