@@ -670,11 +670,13 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int a = s_sub[wid][half][lane];
-      bool leader = lane < k;
+      // lanes selecting the same sub-key: the lowest one sums the group in lane order
+      const unsigned grp = __match_any_sync(FULL, a);
+      const bool leader = lane < k && (__ffs(grp) - 1) == lane;
       float sum = 0.f;
-      for (int l = 0; l < k; ++l) {
-        if (s_sub[wid][half][l] == a) {
-          if (l < lane) leader = false;
+      if (leader) {
+        for (unsigned m = grp; m; m &= m - 1) {
+          const int l = __ffs(m) - 1;
           sum += s_ds[wid][l] * s_sc[wid][half][l];
         }
       }
