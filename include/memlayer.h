@@ -15,7 +15,11 @@
  *  - Every data pointer is a DEVICE pointer owned by the caller, pointing to a
  *    dense row-major array with the stated shape; 16-byte aligned.  The
  *    library never allocates device memory inside a call and never
- *    synchronises the host (except under ML_CHECK_INDICES=1, see below).
+ *    synchronises the host, except (a) under ML_CHECK_INDICES=1 (see below)
+ *    and (b) once per GEMM shape: the first call that runs a cuBLASLt GEMM of
+ *    a new shape (the gated layer, the key/query backward, ml_gemm) times the
+ *    top heuristic candidates with events on `stream` and caches the fastest.
+ *    Set ML_GEMM_TUNE=0 to disable (e.g. before capturing a CUDA graph).
  *  - `stream` is a cudaStream_t passed as void*; all work is enqueued on it in
  *    order.  NULL means the legacy default stream.
  *  - Scratch comes from a caller workspace `ws` of at least the size returned
