@@ -218,7 +218,7 @@ static void bag_bwd_carve(Carver& c, const mlBagShape& s, BagBwdBufs& b) {
   sort_carve(c, P, ceil_log2(s.N), b.sort);
   runs_carve(c, P, b.runs);
   seg_carve(c, P, s.dv, s.dtype, &b.partial, &b.counters);
-  b.dw_part = c.take<float>(int64_t(seg_slices(s.dv, s.dtype)) * P);
+  b.dw_part = c.take<float>(int64_t(seg_slices(s.dv, s.dtype)) * kDwWarps * P);
 }
 
 // ------------------------------------------------------------ cores
@@ -324,10 +324,12 @@ static mlStatus bag_bwd_prepare(const mlBagShape& s, const int32_t* idx, int32_t
   return ML_OK;
 }
 
+// *nsw (nullable): number of dw partial slices written to b.dw_part
 static mlStatus bag_bwd_reduce(const mlBagShape& s, const void* V, const float* w, const void* dy,
                                float* dV, BagBwdBufs& b, int32_t* skey, int32_t* spos,
-                               cudaStream_t st) {
+                               cudaStream_t st, int* nsw = nullptr) {
   const int64_t P = int64_t(s.T) * s.B;
+  if (nsw) *nsw = seg_slices(s.dv, s.dtype);
   if (P == 0) return ML_OK;
   SegArgs g;
   g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = w;
@@ -336,16 +338,17 @@ static mlStatus bag_bwd_reduce(const mlBagShape& s, const void* V, const float* 
   g.out = dV; g.ldo = s.dv; g.dense_accumulate = false;
   g.partial = b.partial; g.counters = b.counters; g.dv = s.dv; g.dtype = s.dtype;
   g.name = "embbag_bwd_segreduce";
+  g.dw_slices_out = nsw;
   ML_TRY(launch_segreduce(g, st));
   return ML_OK;
 }
 
 static mlStatus bag_bwd_core(const mlBagShape& s, const void* V, const int32_t* idx, const float* w,
                              const void* dy, int32_t* rows, float* dV, int32_t* U, BagBwdBufs& b,
-                             cudaStream_t st) {
+                             cudaStream_t st, int* nsw = nullptr) {
   int32_t *skey = nullptr, *spos = nullptr;
   ML_TRY(bag_bwd_prepare(s, idx, rows, U, b, &skey, &spos, st));
-  return bag_bwd_reduce(s, V, w, dy, dV, b, skey, spos, st);
+  return bag_bwd_reduce(s, V, w, dy, dV, b, skey, spos, st, nsw);
 }
 
 }  // namespace ml
@@ -503,9 +506,10 @@ mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, 
   BagBwdBufs b;
   bag_bwd_carve(c, *shape, b);
   timing_mark(nullptr, S(stream));
-  ML_TRY(bag_bwd_core(*shape, V, idx, w, dy, rows, dV, U, b, S(stream)));
+  int nsw = 0;
+  ML_TRY(bag_bwd_core(*shape, V, idx, w, dy, rows, dV, U, b, S(stream), &nsw));
   const int64_t P = int64_t(shape->T) * shape->B;
-  if (dw) ML_TRY(launch_sum_slices(b.dw_part, seg_slices(shape->dv, shape->dtype), P, dw, S(stream)));
+  if (dw) ML_TRY(launch_sum_slices(b.dw_part, nsw, P, dw, S(stream)));
   return check_index_flag(S(stream));
   ML_API_END
 }
@@ -702,8 +706,9 @@ mlStatus embbag_bwd_state(const mlBagShape* shape, const void* V, const float* w
   timing_mark(nullptr, st);
   ML_CUDA_TRY(cudaMemcpyAsync(rows, ps.rows, sizeof(int32_t) * size_t(P), cudaMemcpyDeviceToDevice, st));
   ML_CUDA_TRY(cudaMemcpyAsync(U, ps.U, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-  ML_TRY(bag_bwd_reduce(*shape, V, w, dy, dV, b, skey, spos, st));
-  if (dw) ML_TRY(launch_sum_slices(b.dw_part, seg_slices(shape->dv, shape->dtype), P, dw, st));
+  int nsw = 0;
+  ML_TRY(bag_bwd_reduce(*shape, V, w, dy, dV, b, skey, spos, st, &nsw));
+  if (dw) ML_TRY(launch_sum_slices(b.dw_part, nsw, P, dw, st));
   return check_index_flag(st);
   ML_API_END
 }
@@ -924,9 +929,9 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
       ML_CUDA_TRY(cudaMemcpyAsync(U, state_U, sizeof(int32_t), cudaMemcpyDeviceToDevice, aux->s[0]));
     }
   }
-  ML_TRY(bag_bwd_reduce(bs, V, w_saved, dy, dV, b.bag, skey, spos, st));
+  int ns = 0;   // dw partial slices
+  ML_TRY(bag_bwd_reduce(bs, V, w_saved, dy, dV, b.bag, skey, spos, st, &ns));
   if (state) ML_TRY(stream_dep(aux->s[0], st, aux->ev[5]));   // join the copies
-  const int ns = seg_slices(s.dv, dt);
   const int64_t P = int64_t(T) * bs.B;
   ML_TRY(pkm_bwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, b.bag.dw_part, ns, P, dq, dK1, dK2,
                       b.pkm, st));
@@ -1100,8 +1105,9 @@ mlStatus peer_bwd(const mlPeerShape* shape, const void* dy, const void* x, const
   ML_TRY(launch_peer_act(h_saved, 1, P, w_saved, b.h, b.a, st));
   int32_t *skey = nullptr, *spos = nullptr;
   ML_TRY(bag_bwd_prepare(bs, idx_saved, rows, Ucount, b.bag, &skey, &spos, st));
-  ML_TRY(bag_bwd_reduce(bs, V, b.a, dy, dV, b.bag, skey, spos, st));
-  ML_TRY(launch_peer_dact(b.bag.dw_part, seg_slices(s.D, s.pkm.dtype), P, w_saved, h_saved, b.dh,
+  int nsw = 0;
+  ML_TRY(bag_bwd_reduce(bs, V, b.a, dy, dV, b.bag, skey, spos, st, &nsw));
+  ML_TRY(launch_peer_dact(b.bag.dw_part, nsw, P, w_saved, h_saved, b.dh,
                           b.dwr, st));
   // dU[r] = sum_{p: idx = r} dh[p] x[t(p)]: the same sorted segments, source x
   SegArgs g;

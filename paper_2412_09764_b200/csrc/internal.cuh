@@ -75,7 +75,9 @@ mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out
 // ------------------------------------------------ segmented reduction
 // For every run of equal sorted keys (one output row per run):
 //   out[row, c] (=|+=) sum_{p in run} w[pos_p] * src[pos_p / B, src_col0 + c]
-// and, if V != nullptr, dw_part[slice*P + pos_p] = <src row, V[key] slice>.
+// and, if V != nullptr, partial dot products of <src row, V[key]>:
+// dw[p] = sum_{s < *dw_slices_out} dw_part[s*P + p] (the pipelined kernel
+// writes one partial per consumer warp: seg_slices * kDwWarps slices).
 struct SegArgs {
   const int32_t* skey = nullptr; const int32_t* spos = nullptr; int64_t P = 0;
   const RunBufs* runs = nullptr;
@@ -87,7 +89,9 @@ struct SegArgs {
   float* partial = nullptr; int32_t* counters = nullptr;
   int32_t dv = 0; mlDtype dtype = ML_BF16;
   const char* name = "segreduce";  // timing / profiling label
+  int* dw_slices_out = nullptr;      // set: number of dw_part slices written
 };
+constexpr int kDwWarps = 4;          // dw partial slices per column slice (capacity)
 int seg_slices(int32_t dv, mlDtype dt);
 void seg_carve(Carver& c, int64_t P, int32_t dv, mlDtype dt, float** partial, int32_t** counters);
 mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s);

@@ -451,7 +451,6 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
   __shared__ int s_rng[MS][2];
   __shared__ int s_item[MS];                    // work item of each metadata stage, -1 = done
   __shared__ uint64_t s_mfull[MS], s_mempty[MS];
-  __shared__ float s_red[2][8][NB];
   __shared__ int s_flag;
   extern __shared__ __align__(128) unsigned char dsm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
@@ -580,7 +579,6 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
   for (int v = 0; v < V2; ++v) acc[v] = g[v] = make_float2(0.f, 0.f);
   int cs_slot = 0;               // stage of the next batch and its full-barrier phase
   uint32_t cs_phase = 0;
-  int buf = 0;
   for (int it = 0;; ++it) {
     const int ms = it % MS;
     bar_wait(&s_mfull[ms], uint32_t(it / MS) & 1);
@@ -657,15 +655,12 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
       if (lane == 0) bar_arrive(&empty[cs_slot]);
       if (++cs_slot == nslots) { cs_slot = 0; cs_phase ^= 1u; }
       if constexpr (DW) {
+        // each consumer warp writes its own partial dot products (dw part
+        // slice * kDwWarps + warp): no cross-warp exchange or barrier per batch
         TransposeReduce<NB, 16>::run(part, lane);   // lane l: warp sum of slot l >> (5 - LG)
-        if ((lane & ((32 >> LG) - 1)) == 0) s_red[buf][warp][lane >> (5 - LG)] = part[0];
-        team_sync<1>(team);
-        if (tid < nb) {
-          float t = 0.f;
-          for (int w2 = 0; w2 < cwarps; ++w2) t += s_red[buf][w2][tid];
-          p.dw_part[int64_t(slice) * p.P + M[kb + tid].pos] = t;
-        }
-        buf ^= 1;
+        const int jj = lane >> (5 - LG);
+        if ((lane & ((32 >> LG) - 1)) == 0 && jj < nb)
+          p.dw_part[(int64_t(slice) * kDwWarps + warp) * p.P + M[kb + jj].pos] = part[0];
       }
     }
     __syncwarp();
@@ -740,12 +735,10 @@ mlStatus dispatch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p,
                        const char* name) {
   // 4 KiB row slices: 4 consumer warps of 32-byte threads, 2 CTAs/SM;
   // 1-2 KiB rows: 16-byte threads, 3 CTAs/SM (more rows in flight per SM)
-  static const int cfg = env_int("ML_SEG_PIPE_CFG", 2);
-  if (cfg >= 2 && threads >= 256)
+  // both configurations run kDwWarps = 4 consumer warps (one dw partial each)
+  if (threads >= 256)
     return launch_pipe<T, DW, 2, 4, 2, 128>(threads, ns, nchunks, p, s, name, 2, 100 * 1024);
-  if (cfg >= 2 && threads >= 64)
-    return launch_pipe<T, DW, 1, 4, 3, 128>(threads, ns, nchunks, p, s, name, 3, 62 * 1024);
-  return launch_pipe<T, DW, 1, 8, 1, 256>(threads, ns, nchunks, p, s, name, 1, 200 * 1024);
+  return launch_pipe<T, DW, 1, 4, 3, 128>(threads, ns, nchunks, p, s, name, 3, 62 * 1024);
 }
 
 }  // namespace
@@ -803,7 +796,9 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   // measured); narrower slices (the 4- and 8-way dim-sharded group) keep one
   // CTA per chunk
   static const bool pipe = env_int("ML_SEG_PIPE", 1) != 0;
-  if (pipe && !a.dense_accumulate && aligned && threads >= 128) {
+  const bool use_pipe = pipe && !a.dense_accumulate && aligned && threads >= 128;
+  if (a.dw_slices_out) *a.dw_slices_out = use_pipe ? ns * kDwWarps : ns;
+  if (use_pipe) {
     if (a.dtype == ML_BF16)
       return dw ? dispatch_pipe<__nv_bfloat16, true>(threads, ns, nchunks, p, s, a.name)
                 : dispatch_pipe<__nv_bfloat16, false>(threads, ns, nchunks, p, s, a.name);
