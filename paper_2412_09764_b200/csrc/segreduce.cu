@@ -528,8 +528,8 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
     return;
   }
   if (warp == cwarps) {
-    // ------------------------------------------------ copy-issue warp (lane 0)
-    if (lane != 0) return;
+    // ------------------------------------------------ copy-issue warp: lane 0
+    // arms each stage's barrier, lane j issues position j's copies
     const uint64_t pol_keep = l2_evict_last_policy();     // dy: re-read ~B times
     const uint64_t pol_stream = l2_evict_first_policy();  // V: once per piece
     const uint32_t lds = uint32_t(p.lds_bytes);
@@ -556,15 +556,17 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
         if constexpr (DW) {
           for (int j = 0; j < nb; ++j) rows_in += uint32_t(s_meta[ms][kb + j].fl & 1);
         }
-        bar_expect_tx(&full[sl], rows_in * RB);
-        for (int j = 0; j < nb; ++j) {
-          const SegMeta& m = s_meta[ms][kb + j];
-          bulk_g2s(slot_dy(sl, j), srcb + uint64_t(uint32_t(m.t)) * lds, RB, &full[sl], pol_keep);
+        if (lane == 0) bar_expect_tx(&full[sl], rows_in * RB);
+        __syncwarp();
+        if (lane < nb) {
+          const SegMeta& m = s_meta[ms][kb + lane];
+          bulk_g2s(slot_dy(sl, lane), srcb + uint64_t(uint32_t(m.t)) * lds, RB, &full[sl], pol_keep);
           if (DW && (m.fl & 1))
-            bulk_g2s(slot_v(sl, j), vb + uint64_t(uint32_t(m.key)) * ldv, RB, &full[sl], pol_stream);
+            bulk_g2s(slot_v(sl, lane), vb + uint64_t(uint32_t(m.key)) * ldv, RB, &full[sl], pol_stream);
         }
       }
-      bar_arrive(&s_mempty[ms]);                // done reading this chunk's metadata
+      __syncwarp();
+      if (lane == 0) bar_arrive(&s_mempty[ms]);   // done reading this chunk's metadata
     }
     return;
   }
