@@ -12,7 +12,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # lazy import of the torch binding so `import paper_2412_09764_b200`
     # works (e.g. for build()) before torch / the library is needed
-    if name in ("ops", "group"):
+    if name in ("ops", "group", "graph"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)
