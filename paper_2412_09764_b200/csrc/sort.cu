@@ -110,7 +110,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const int32_t* 
 
 // ------------------------------------------------------------ radix sort
 constexpr int kSortWarps = 8;
-constexpr int kSortRounds = 16;
+#ifndef ML_SORT_ROUNDS
+#define ML_SORT_ROUNDS 16
+#endif
+constexpr int kSortRounds = ML_SORT_ROUNDS;   // keys per thread per tile (A/B: -DML_SORT_ROUNDS)
 constexpr int kSortTile = kSortWarps * kSortRounds * 32;  // 4096
 constexpr int kMaxDigitBits = 11;
 
