@@ -2,26 +2,39 @@
 """Benchmark of the memory-layer hot path (arXiv 2412.09764) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1)
+                    [--config c2|c3|c4|c5|...] [--per-rank G]
 
-A step is one pass of the whole hot path (SURVEY.md §8(a) a1-a11) over one
+A step is one pass of the whole hot path (SURVEY.md §8(a) a1-a12) over one
 batch: memory_layer_fwd + memory_layer_bwd (product-key top-k, softmax,
 EmbeddingBag fwd with the Memory+ silu gate, gate backward, the sorted
 "reverse_indices" EmbeddingBag backward, softmax / key / query backward).
-N = 1: BASELINE config[1] (N = 1024^2 values x 2048, 4 heads, k = 32, 16K
-tokens, bf16).  N > 1: the dim-sharded memory group of §3.1.2 with
-16K tokens per rank (weak scaling) and the value table sharded G ways.
+
+N = 1: BASELINE config[1] (C2: N = 1024^2 values x 2048, 4 heads, k = 32,
+16K tokens, bf16).  N > 1 (`--gpus N` re-executes itself under
+torch.distributed.run, one rank per GPU, unless WORLD_SIZE is already set):
+the dim-sharded memory group of §3.1.2 -- every rank scores its own
+tokens, the value table is sharded G ways along the value dim.  c1-c3 keep
+16K tokens per rank (weak scaling); c4/c5 (8192^2 keys)
+split a fixed global batch over the ranks.
+
+`--per-rank G` runs, on ONE GPU, the per-rank work of the G-rank step with
+the collectives replaced by local copies (SURVEY §8(e) t_ref(G)): a1-a4 on
+this rank's tokens, the bag forward/backward over all G ranks' tokens on an
+[N, dv/G] value shard, the gate on this rank's tokens.  That is how the
+8192^2-key configurations (256-512 GiB of values, more than one B200 holds)
+are measured on one GPU.  Under N > 1 the same loopback step is also timed
+after the real one and E(G) = t_ref(G) / t_G is reported.
 
 Inputs are synthetic (counter-based generator), generated
-on the device before timing.  The value table (4 GiB) is > 30x the 126 MB
+on the device before timing.  The value table (>= 4 GiB) is > 30x the 126 MB
 L2, so no L2 flush is needed between steps ("inputs_larger_than_L2").
 Prints ONE JSON line on rank 0.
 """
 import argparse
 import json
-import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -30,13 +43,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (S, dv, D, Dk, H, k, T_per_rank, dtype)
+    # T: tokens per rank (weak scaling); T_global: fixed global batch split over the ranks
     "c1": dict(S=32, dv=64, D=64, Dk=32, H=1, k=4, T=256, dtype="f32",
                desc="tiny PKM: N=1024, d=64, 1 head, k=4, 256 tokens, fp32"),
     "c2": dict(S=1024, dv=2048, D=2048, Dk=1024, H=4, k=32, T=16384, dtype="bf16",
                desc="1.3B-base memory layer: N=1024^2 x 2048, 4 heads, k=32, 16K tokens, bf16"),
     "c3": dict(S=4096, dv=2048, D=2048, Dk=1024, H=4, k=32, T=16384, dtype="bf16",
-               desc="N=4096^2 x 2048 bf16, dim-sharded"),
+               desc="N=4096^2 x 2048 bf16, 4 heads, k=32, 16K tokens per rank, dim-sharded"),
+    "c4": dict(S=8192, dv=2048, D=2048, Dk=1024, H=4, k=32, T_global=16384, dtype="bf16",
+               desc="N=8192^2 x 2048 bf16 (256 GiB of values), gated, 4 heads, k=32, "
+                    "16K tokens per step over the group, dim-sharded"),
+    "c5": dict(S=8192, dv=4096, D=4096, Dk=2048, H=4, k=32, T_global=65536, dtype="bf16",
+               desc="8B-base scale: N=8192^2 x 4096 bf16 (512 GiB of values), 4 heads, k=32, "
+                    "64K tokens per step over the group, dim-sharded"),
     # value-dim sweep of the paper's range (north_star: value dims 1024 to 4096), N = 1024^2
     "c2_dv1024": dict(S=1024, dv=1024, D=1024, Dk=1024, H=4, k=32, T=16384, dtype="bf16",
                       desc="N=1024^2 x 1024, 4 heads, k=32, 16K tokens, bf16"),
@@ -45,6 +64,15 @@ CONFIGS = {
 }
 METRIC = "memory-layer fwd+bwd tok/s (EmbeddingBag fwd/bwd HBM GB/s, % peak)"
 SEED = 0
+NVLINK_PEER_GBS = 770.0    # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+
+
+def tokens_per_rank(cfg, G):
+    if "T_global" in cfg:
+        if cfg["T_global"] % G:
+            raise SystemExit(f"{cfg['name']}: G={G} must divide the global batch {cfg['T_global']}")
+        return cfg["T_global"] // G
+    return cfg["T"]
 
 
 def load_peaks():
@@ -111,6 +139,106 @@ def dist_env():
     return world, rank, local
 
 
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def respawn_under_torchrun(n):
+    """`--gpus N` without a torchrun environment: re-execute this command with
+    one rank per GPU (rendezvous on 127.0.0.1) and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# ------------------------------------------------------------- comm wrappers
+class TimedComm:
+    """Wraps a communicator; records CUDA events around each collective while
+    `on` so the bench can report per-collective NVLink GB/s (bytes a rank
+    sends and receives over the link / time)."""
+
+    def __init__(self, inner):
+        self.inner, self.size, self.rank = inner, inner.size, inner.rank
+        self.on, self.rec = False, []
+
+    def _run(self, kind, fn, out, inp, link_bytes):
+        import torch
+        if not self.on:
+            return fn(out, inp)
+        s = torch.cuda.current_stream()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        r = fn(out, inp)
+        b.record(s)
+        self.rec.append((kind, a, b, link_bytes))
+        return r
+
+    def all_gather(self, out, inp):
+        nb = out.numel() * out.element_size() * (self.size - 1) // self.size
+        return self._run("all_gather", self.inner.all_gather, out, inp, nb)
+
+    def all_to_all(self, out, inp):
+        nb = inp.numel() * inp.element_size() * (self.size - 1) // self.size
+        return self._run("all_to_all", self.inner.all_to_all, out, inp, nb)
+
+    def reduce_scatter(self, out, inp):
+        nb = inp.numel() * inp.element_size() * (self.size - 1) // self.size
+        return self._run("reduce_scatter", self.inner.reduce_scatter, out, inp, nb)
+
+    def report(self, steps):
+        agg = {}
+        for kind, a, b, nb in self.rec:
+            t = a.elapsed_time(b)
+            e = agg.setdefault(kind, [0, 0.0, 0])
+            e[0] += 1
+            e[1] += t
+            e[2] += nb
+        out = {}
+        for kind, (cnt, ms, nb) in agg.items():
+            gbs = nb / (ms / 1e3) / 1e9 if ms > 0 else None
+            out[kind] = {"calls_per_step": cnt / steps, "ms_per_step": round(ms / steps, 4),
+                         "link_bytes_per_step": nb // steps,
+                         "GBps": round(gbs, 1) if gbs else None,
+                         "frac_of_peer_copy": round(gbs / NVLINK_PEER_GBS, 4) if gbs else None}
+        return out
+
+
+class LoopbackComm:
+    """The collectives of rank `rank` of a G-rank group with the network
+    removed (SURVEY §8(e) t_ref(G)): this rank's own chunk is copied into
+    place and the other ranks' chunks come from `others` (captured from a real
+    exchange, or computed once before timing), so the local work sees the
+    data -- and the index distribution -- of a real G-rank step."""
+
+    def __init__(self, G, rank, others):
+        self.size, self.rank, self.others = G, rank, others
+
+    def all_gather(self, out, inp):
+        n = inp.shape[0]
+        src = self.others.get(str(inp.dtype))
+        if src is not None and src.shape[1:] == inp.shape[1:] and src.shape[0] == out.shape[0]:
+            if self.rank > 0:
+                out[:self.rank * n].copy_(src[:self.rank * n])
+            if self.rank < self.size - 1:
+                out[(self.rank + 1) * n:].copy_(src[(self.rank + 1) * n:])
+        else:   # no captured data of this kind: replicate this rank's chunk
+            out.view(self.size, *inp.shape).copy_(inp.unsqueeze(0).expand(self.size, *inp.shape))
+        out[self.rank * n:(self.rank + 1) * n].copy_(inp)
+
+    def all_to_all(self, out, inp):
+        n = inp.shape[0] // self.size
+        chunk = inp[self.rank * n:(self.rank + 1) * n]
+        out.view(self.size, n, *inp.shape[1:]).copy_(chunk.unsqueeze(0).expand(self.size, *chunk.shape))
+
+    def reduce_scatter(self, out, inp):
+        n = out.shape[0]
+        out.copy_(inp[self.rank * n:(self.rank + 1) * n])
+
+
 # ------------------------------------------------------------- our arm
 def synth_value_shard(N, dv, G, rank, dt, dev, ops, torch):
     """This rank's [N, dv/G] column shard of the synthetic value table,
@@ -123,12 +251,14 @@ def synth_value_shard(N, dv, G, rank, dt, dev, ops, torch):
         n = min(buf.shape[0], N - r0)
         ops.synth_fill(buf[:n], SEED, gen.TAGS["V"], row0=r0)
         out[r0:r0 + n].copy_(buf[:n, lo:hi])
+    del buf
     return out
 
 
-def make_inputs(cfg, dev, G, rank, ops, torch, force_group=False):
+def make_inputs(cfg, dev, G, rank, ops, torch, sharded):
     from synthetic import gen
-    S, dv, D, Dk, H, k, T = (cfg[n] for n in ("S", "dv", "D", "Dk", "H", "k", "T"))
+    S, dv, D, Dk, H = (cfg[n] for n in ("S", "dv", "D", "Dk", "H"))
+    T = tokens_per_rank(cfg, G)
     dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     N = S * S
     t = {}
@@ -146,7 +276,7 @@ def make_inputs(cfg, dev, G, rank, ops, torch, force_group=False):
     fill("K2", (H, S, Dk // 2), "K2", gen.scale_for("K2", Dk=Dk))
     fill("W1", (D, dv), "W1", gen.scale_for("W1", D=D))
     fill("W2", (dv, D), "W2", gen.scale_for("W2", dv=dv))
-    if G == 1 and not force_group:
+    if not sharded:
         fill("V", (N, dv), "V")
     else:
         # this rank's column shard [N, dv/G] of V (regenerated from the same
@@ -155,32 +285,40 @@ def make_inputs(cfg, dev, G, rank, ops, torch, force_group=False):
     return t
 
 
-def run_ours(args, cfg, world, rank, local):
-    import torch
-    from paper_2412_09764_b200 import ops
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    G = world
-    pg = None
-    use_group = world > 1 or args.force_group
-    if use_group:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist.group.WORLD
-    t = make_inputs(cfg, dev, G, rank, ops, torch, use_group)
+def group_others(cfg, G, rank, t, ops, torch):
+    """The (idx, w) every other rank of a G-rank group would contribute to
+    the all-gather, computed on this GPU once before timing (--per-rank)."""
+    from synthetic import gen
+    H, Dk, k = cfg["H"], cfg["Dk"], cfg["k"]
+    T = tokens_per_rank(cfg, G)
+    idx_all = torch.empty((G * T, H, k), dtype=torch.int32, device=t["q"].device)
+    w_all = torch.empty((G * T, H, k), dtype=torch.float32, device=t["q"].device)
+    q = torch.empty_like(t["q"])
+    for g in range(G):
+        ops.synth_fill(q, SEED, gen.TAGS["q"], row0=g * T * H)
+        i, w = ops.pkm_topk(q, t["K1"], t["K2"], k)
+        idx_all[g * T:(g + 1) * T].copy_(i)
+        w_all[g * T:(g + 1) * T].copy_(w)
+    return {str(torch.int32): idx_all, str(torch.float32): w_all}
+
+
+def build_step(args, cfg, t, ops, torch, comm=None):
+    """One fwd + bwd step through the public API; `comm` selects the memory
+    group path (GroupMemoryLayer over that communicator)."""
     k = cfg["k"]
-    dK1 = torch.zeros(t["K1"].shape, dtype=torch.float32, device=dev)
-    dK2 = torch.zeros(t["K2"].shape, dtype=torch.float32, device=dev)
+    dK1 = torch.zeros(t["K1"].shape, dtype=torch.float32, device=t["q"].device)
+    dK2 = torch.zeros(t["K2"].shape, dtype=torch.float32, device=t["q"].device)
     bufs = {}
-    if use_group:
+    if comm is not None:
         from paper_2412_09764_b200 import group
-        layer = group.GroupMemoryLayer(pg, k=k, mode=args.mode)
+        layer = group.GroupMemoryLayer(comm, k=k, mode=args.mode)
 
         def step(inp=t):
             dK1.zero_()
             dK2.zero_()
             out, saved = layer.forward(inp["x"], inp["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"])
             g = layer.backward(inp["dout"], saved, dK1, dK2)
+            step.last_saved = saved
             return out, g
     else:
         def step(inp=t):
@@ -192,58 +330,122 @@ def run_ours(args, cfg, world, rank, local):
             g = ops.memory_layer_bwd(inp["dout"], inp["x"], inp["q"], t["K1"], t["K2"], t["V"],
                                      t["W1"], t["W2"], saved, dK1=dK1, dK2=dK2, bufs=bufs)
             return out, g
+    step.last_saved = None
+    return step
+
+
+def time_steps(step, steps, world, torch, dev):
+    """Device time of `steps` steps on the launch stream (barrier + sync on
+    both sides, max over ranks)."""
+    stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
-
-    for _ in range(args.warmup):
-        out, g = step()
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-
-    # ---- timed region (device events, per-kernel events inside the library)
-    ops.timing_reset()
-    ops.timing_enable(True)
-    launches0 = ops.launch_count()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            out, g = step()
-        e1.record(stream)
-        torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        out, g = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
     barrier()
-    launches = ops.launch_count() - launches0
-    ops.timing_enable(False)
-    kern = ops.timing_report()
     ms = e0.elapsed_time(e1)
     if world > 1:
         import torch.distributed as dist
         m = torch.tensor([ms], device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         ms = float(m.item())
+    return ms, out, g
+
+
+def run_ours(args, cfg, world, rank, local):
+    import torch
+    from paper_2412_09764_b200 import ops
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    per_rank = args.per_rank if world == 1 else 0
+    G = world if world > 1 else max(1, per_rank)
+    group_path = world > 1 or args.force_group or per_rank > 1
+    if "T_global" in cfg and G == 1:
+        raise SystemExit(f"{cfg['name']} does not fit one B200 ({cfg['desc']}): run it with "
+                         f"--gpus 8 or measure one rank's work with --per-rank 8")
+    comm = None
+    if world > 1 or args.force_group:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        from paper_2412_09764_b200.group import TorchComm
+        comm = TimedComm(TorchComm(dist.group.WORLD))
+    t = make_inputs(cfg, dev, G, rank if world > 1 else 0, ops, torch, group_path)
+    if per_rank > 1:
+        comm = TimedComm(LoopbackComm(G, 0, group_others(cfg, G, 0, t, ops, torch)))
+    step = build_step(args, cfg, t, ops, torch, comm)
+    T_loc = tokens_per_rank(cfg, G)
+
+    for _ in range(args.warmup):
+        out, g = step()
+    torch.cuda.synchronize()
+
+    # ---- headline: device events around K steps, library timing OFF
+    launches0 = ops.launch_count()
+    with ClockSampler(local) as clk:
+        ms, out, g = time_steps(step, args.steps, world, torch, dev)
+    launches = ops.launch_count() - launches0
     U = int((g["U"] if isinstance(g, dict) else g.U).item())
     ms_step = ms / args.steps
-    tokens_per_step = cfg["T"] * G
-    value = tokens_per_step / (ms_step / 1e3)
+    # per_rank emulates ONE rank: the group would process G times its tokens
+    tokens_per_step = T_loc * (world if world > 1 else 1)
+
+    # ---- per-kernel pass (separate, not timed into the headline): every
+    # kernel on the caller's stream so each timing event brackets one launch
+    kern_steps = max(1, min(args.steps, 5))
+    ops.set_serial(True)
+    ops.timing_reset()
+    ops.timing_enable(True)
+    if comm is not None:
+        comm.on = True
+    for _ in range(kern_steps):
+        step()
+    torch.cuda.synchronize()
+    ops.timing_enable(False)
+    ops.set_serial(False)
+    kern = ops.timing_report()
+    coll = None
+    if comm is not None:
+        comm.on = False
+        coll = comm.report(kern_steps) if world > 1 else None
+        comm.rec = []
+
+    # ---- t_ref(G): the same rank's work with the collectives removed
+    eff = None
+    if world > 1:
+        saved = step.last_saved
+        others = {str(torch.int32): saved["idx_all"].clone(), str(torch.float32): saved["w_all"].clone()}
+        ref_step = build_step(args, cfg, t, ops, torch, LoopbackComm(world, rank, others))
+        for _ in range(max(2, args.warmup // 2)):
+            ref_step()
+        ms_ref, _, _ = time_steps(ref_step, args.steps, world, torch, dev)
+        eff = {"t_G_ms": round(ms_step, 4), "t_ref_ms": round(ms_ref / args.steps, 4),
+               "E": round((ms_ref / args.steps) / ms_step, 4),
+               "definition": "SURVEY §8(e): E(G) = t_ref(G) / t_G, t_ref = this rank's work with "
+                             "the collectives replaced by local copies (max over ranks)"}
 
     # ---- e2e: host (pinned) inputs -> device, step, result -> host
-    e2e = run_e2e(args, t, step, stream, torch, cfg, G, world)
+    e2e = run_e2e(args, t, step, torch, tokens_per_step, world)
+    return dict(value=tokens_per_step / (ms_step / 1e3), ms_step=ms_step, kern=kern,
+                kern_steps=kern_steps, launches=launches, clocks=clk.summary(), U=U, e2e=e2e,
+                tokens_per_step=tokens_per_step, G=G, T_loc=T_loc, coll=coll, eff=eff)
 
-    return dict(value=value, ms_step=ms_step, kern=kern, launches=launches, clocks=clk.summary(),
-                U=U, e2e=e2e, tokens_per_step=tokens_per_step)
 
-
-def run_e2e(args, t, step, stream, torch, cfg, G, world):
+def run_e2e(args, t, step, torch, tokens_per_step, world):
     """End to end through the public API with HOST buffers: every step copies
     its inputs (q, x, dout) from pinned host memory and copies the result
     `out` back.  The copies run on a copy stream, double-buffered, so step
     i+1's upload overlaps step i's compute (the intended way to feed the
     layer); all of it is inside the timed region."""
+    stream = torch.cuda.current_stream()
     names = ("q", "x", "dout")
     hostbufs = {n: t[n].cpu().pin_memory() for n in names}
     h2d = sum(hostbufs[n].numel() * hostbufs[n].element_size() for n in names)
@@ -253,84 +455,101 @@ def run_e2e(args, t, step, stream, torch, cfg, G, world):
                                     # hold back the next upload)
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(2)]
-    for e in ev_done:
-        e.record(stream)
     # the pinned result buffer is allocated before the timed region (page
     # locking is a synchronous host call, not part of a step)
     out_probe, _ = step({**t, **dbuf[0]})
     out_host = torch.empty(out_probe.shape, dtype=out_probe.dtype, pin_memory=True)
     del out_probe
-    torch.cuda.synchronize()
+
+    def loop(n):
+        for e in ev_done:
+            e.record(stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        copy.wait_event(e0)
+        for i in range(n):
+            b = i % 2
+            with torch.cuda.stream(copy):
+                copy.wait_event(ev_done[b])             # buffer b no longer read by step i-2
+                for nm in names:
+                    dbuf[b][nm].copy_(hostbufs[nm], non_blocking=True)
+                ev_in[b].record(copy)
+            stream.wait_event(ev_in[b])
+            out, g = step({**t, **dbuf[b]})
+            ev_done[b].record(stream)
+            with torch.cuda.stream(down):
+                down.wait_event(ev_done[b])
+                out.record_stream(down)
+                out_host.copy_(out, non_blocking=True)
+        ev_last = torch.cuda.Event()
+        ev_last.record(down)
+        stream.wait_event(ev_last)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    loop(3)                          # warm-up of the pipelined loop (first-touch of pinned pages)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    n = max(3, args.steps)           # the first upload (pipeline fill) is inside the timed region
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    copy.wait_event(e0)
-    for i in range(n):
-        b = i % 2
-        with torch.cuda.stream(copy):
-            copy.wait_event(ev_done[b])             # buffer b no longer read by step i-2
-            for nm in names:
-                dbuf[b][nm].copy_(hostbufs[nm], non_blocking=True)
-            ev_in[b].record(copy)
-        stream.wait_event(ev_in[b])
-        out, g = step({**t, **dbuf[b]})
-        ev_done[b].record(stream)
-        with torch.cuda.stream(down):
-            down.wait_event(ev_done[b])
-            out.record_stream(down)
-            out_host.copy_(out, non_blocking=True)
-    ev_last = torch.cuda.Event()
-    ev_last.record(down)
-    stream.wait_event(ev_last)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / n
+    ms = loop(max(3, args.steps))   # the first upload (pipeline fill) is inside the timed region
     if world > 1:
         import torch.distributed as dist
         m = torch.tensor([ms], device=t["q"].device)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         ms = float(m.item())
     d2h = out_host.numel() * out_host.element_size()
-    return {"value": cfg["T"] * G / (ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": h2d,
+    return {"value": tokens_per_step / (ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
             "note": "pinned host inputs uploaded on a copy stream, double-buffered against compute; "
                     "results downloaded on a second copy stream"}
 
 
 # ------------------------------------------------- roofline accounting
-def bag_bytes(cfg, G, U=None):
-    """Algorithmic bytes per launch (SURVEY.md §8(d) per-token figures x
-    tokens per launch), for the per-rank launch at group size G."""
+def bag_bytes(cfg, G, T_loc, U=None):
+    """Bytes per launch of the two bag kernels for the per-rank launch at
+    group size G (the bag runs over all G*T_loc group tokens on a dv/G
+    column slice).  Returns dict with:
+      fwd            a5 (+ a6 epilogue at G = 1): rows + (idx, w) + gate/out/y
+      bwd_l2_incl    a9, SURVEY §8(d) per-position count: B dy-row gathers per
+                     token (served from L2 by design) + V and fp32 dV once
+                     per distinct row + metadata + dy
+      bwd_hbm        a9 compulsory HBM bytes: V once per distinct row, fp32
+                     dV written once, dy read once, sorted key/pos + w (12 B
+                     per position), dw partials (16 B per position and slice)
+    """
     e = 2 if cfg["dtype"] == "bf16" else 4
     B = cfg["H"] * cfg["k"]
-    T_all = cfg["T"] * G            # the bag runs over all group tokens
-    dvs = cfg["dv"] // G             # on this rank's column slice
+    T_all = T_loc * G
+    dvs = cfg["dv"] // G
     P = T_all * B
-    fwd = P * (dvs * e + 8) + T_all * dvs * e * (3 if G == 1 else 1)   # rows + (idx,w) + gate/out/y
+    fwd = P * (dvs * e + 8) + T_all * dvs * e * (3 if G == 1 else 1)
     u = (U / P) if U else 1.0
-    ns = max(1, dvs * e // 16 // 128)
-    bwd = P * dvs * e + u * P * dvs * (e + 4) + P * (12 + 4 * ns) + T_all * dvs * e
-    return fwd, bwd, P
+    ns = max(1, (dvs * e // 16) // 256)
+    bwd_l2 = P * dvs * e + u * P * dvs * (e + 4) + P * (12 + 4 * ns) + T_all * dvs * e
+    bwd_hbm = u * P * dvs * (e + 4) + T_all * dvs * e + 12 * P + 16 * ns * P
+    return {"fwd": fwd, "bwd_l2_incl": bwd_l2, "bwd_hbm": bwd_hbm, "P": P}
 
 
-def roofline(res, cfg, G, peaks):
+def roofline(res, cfg, peaks):
     kern = res["kern"]
+    ks = res["kern_steps"]
     mine = {n: v for n, v in kern.items() if n not in ("cublasLt_gemm", "memset")}
     dom = max(mine, key=lambda n: mine[n][1]) if mine else None
-    fwd_b, bwd_b, P = bag_bytes(cfg, G, res["U"])
+    bb = bag_bytes(cfg, res["G"], res["T_loc"], res["U"])
     hbm = peaks.get("hbm_gbs", 6650.0)
-    algo = {"embbag_fwd_gate": fwd_b, "embbag_fwd": fwd_b, "embbag_bwd_segreduce": bwd_b}
     per = {}
-    for n in ("embbag_fwd_gate", "embbag_fwd", "embbag_bwd_segreduce"):
+    for n, algo, l2 in (("embbag_fwd_gate", bb["fwd"], None), ("embbag_fwd", bb["fwd"], None),
+                        ("embbag_bwd_segreduce", bb["bwd_hbm"], bb["bwd_l2_incl"])):
         if n in kern:
             cnt, tot = kern[n]
             avg_s = tot / cnt / 1e3
-            gbs = algo[n] / avg_s / 1e9
+            gbs = algo / avg_s / 1e9
             per[n] = {"achieved_GBs": round(gbs, 1), "frac": round(gbs / hbm, 4),
-                      "avg_ms": round(tot / cnt, 4), "bytes_per_launch": int(algo[n])}
+                      "avg_ms": round(tot / cnt, 4), "bytes_per_launch": int(algo)}
+            if l2:
+                per[n]["l2_inclusive"] = {"bytes_per_launch": int(l2),
+                                          "GBs": round(l2 / avg_s / 1e9, 1)}
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if dom and os.path.exists(tf):
@@ -341,18 +560,42 @@ def roofline(res, cfg, G, peaks):
     if dom in per:
         r = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["achieved_GBs"], "peak": hbm,
              "unit": "GB/s", "frac": per[dom]["frac"], "traffic": traffic,
-             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
-             "note": "achieved counts SURVEY §8(d) algorithmic bytes, incl. the B dy-row gathers "
-                     "per token that the kernel serves from L2; dram = ncu DRAM bytes "
-                     "(profiles/traffic.json) over the same live launch time"}
+             "avg_ms": per[dom]["avg_ms"], "bytes_per_launch": per[dom]["bytes_per_launch"],
+             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks
+             else "fallback 6650 (B200_PROFILING.md)",
+             "timing": f"per-launch CUDA events on the launch stream, separate pass of {ks} steps "
+                       "with every kernel on one stream (ml_set_serial)"}
+        if "l2_inclusive" in per[dom]:
+            r["achieved_note"] = ("bytes that must cross HBM (V once per distinct row, fp32 dV, "
+                                  "dy once, 12 B/position metadata, dw partials); l2_inclusive adds "
+                                  "the B dy-row gathers per token the kernel serves from L2")
+            r["l2_inclusive"] = per[dom]["l2_inclusive"]
         if traffic:
             g = traffic / (per[dom]["avg_ms"] / 1e3) / 1e9
-            r["dram"] = {"achieved": round(g, 1), "frac": round(g / hbm, 4), "unit": "GB/s"}
+            r["dram"] = {"achieved": round(g, 1), "frac": round(g / hbm, 4), "unit": "GB/s",
+                         "source": "ncu dram__bytes (profiles/traffic.json) over the live launch time"}
     else:
         cnt, tot = kern[dom] if dom else (1, 0.0)
         r = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": None,
              "frac": None, "traffic": traffic, "avg_ms": tot / max(cnt, 1)}
-    return r, per
+    # the scoring contraction (a1): tensor-bound
+    sc = None
+    for n in ("pkm_scores_tc", "pkm_scores_topk_tc"):
+        if n in kern:
+            cnt, tot = kern[n]
+            flops = 2.0 * res["T_loc"] * cfg["H"] * cfg["S"] * cfg["Dk"]
+            tf_s = flops / (tot / cnt / 1e3) / 1e12
+            pk = peaks.get("bf16_tflops", 1590.0)
+            sc = {"kernel": n, "bound": "tensor", "achieved": round(tf_s, 1), "unit": "TFLOP/s",
+                  "peak": pk, "frac": round(tf_s / pk, 4), "avg_ms": round(tot / cnt, 4),
+                  "flops_per_launch": flops,
+                  "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS, burst)"}
+            try:
+                util = json.load(open(os.path.join(ROOT, "profiles", "tensor_util.json")))
+                sc["tensor_pipe_util_ncu"] = util.get(cfg.get("name", ""), {}).get(n)
+            except Exception:
+                pass
+    return r, per, sc
 
 
 # ------------------------------------------------------------- oracle arm
@@ -397,55 +640,97 @@ def oracle_sample(cfg, T_o, seed=SEED, chunk=256, t0=0):
     return el, T_o
 
 
-def blas_threads():
+def host_threads():
     try:
-        from threadpoolctl import threadpool_info
-        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def timed_oracle(cfg, T_o, threads):
+    """The oracle on T_o tokens with the BLAS pool limited to `threads` (the
+    oracle's only parallel part: numpy fp64 matmuls)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=threads):
+            return oracle_sample(cfg, T_o)
+    except ImportError:
+        return oracle_sample(cfg, T_o)
+
+
 def cpu_baseline(cfg, T_o):
-    el, n = oracle_sample(cfg, T_o)
-    return {"value": n / el, "unit": "tok/s", "cores": blas_threads(), "kind": "oracle",
-            "sample": f"{n} tokens (chunks of 256) of {cfg['desc']}: full-size tables, rows "
-                      f"regenerated on demand outside the timed parts; numpy fp64, BLAS threads "
-                      f"in matmuls only",
-            "seconds": round(el, 3)}
+    n = host_threads()
+    el_n, tok = timed_oracle(cfg, T_o, n)
+    el_1, tok1 = timed_oracle(cfg, max(1, T_o // 2), 1)
+    return {"value": tok / el_n, "unit": "tok/s", "cores": n, "kind": "oracle",
+            "sample": f"{tok} tokens (chunks of 256) of {cfg['desc']}: full-size tables, rows "
+                      f"regenerated on demand outside the timed parts; numpy fp64, BLAS pool of "
+                      f"{n} threads (the matmuls are the oracle's only parallel part)",
+            "seconds": round(el_n, 3), "cpu_model": cpu_model(),
+            "single_thread": {"value": tok1 / el_1, "unit": "tok/s", "cores": 1,
+                              "tokens": tok1, "seconds": round(el_1, 3)}}
 
 
 def run_reference(args, cfg, world, rank):
     if rank != 0:
         return None
     T_o = args.ref_tokens
+    n = host_threads()
     for _ in range(args.warmup):
-        oracle_sample(cfg, max(2, T_o // 4))
+        timed_oracle(cfg, max(2, T_o // 4), n)
     tot, toks = 0.0, 0
     for _ in range(args.steps):
-        el, n = oracle_sample(cfg, T_o)
+        el, m = timed_oracle(cfg, T_o, n)
         tot += el
-        toks += n
+        toks += m
     v = toks / tot
-    return {"metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps,
+    return {"metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": dict(config_keys(cfg, cfg.get("name", "c2"), world, "single GPU"),
+            "config": dict(config_keys(cfg, cfg.get("name", "c2"), 1, "single GPU",
+                                       tokens_per_rank(cfg, 1) if "T" in cfg else cfg["T_global"]),
                            tokens_per_step_sample=T_o),
-            "cpu_baseline": {"value": v, "unit": "tok/s", "kind": "oracle", "cores": blas_threads(),
+            "cpu_baseline": {"value": v, "unit": "tok/s", "kind": "oracle", "cores": n,
+                             "cpu_model": cpu_model(),
                              "sample": f"{T_o} tokens per step of {cfg['desc']}"},
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 # ------------------------------------------------------------------- main
-def config_keys(cfg, cfg_name, G, parallelism):
+def config_keys(cfg, cfg_name, G, parallelism, T_loc):
     """The workload description shared by both arms' JSON lines."""
-    return {"workload": cfg["desc"], "config": cfg_name, "tokens_per_rank": cfg["T"],
-            "global_tokens": cfg["T"] * G, "N_values": cfg["S"] ** 2, "value_dim": cfg["dv"],
+    return {"workload": cfg["desc"], "config": cfg_name, "tokens_per_rank": T_loc,
+            "global_tokens": T_loc * G, "N_values": cfg["S"] ** 2, "value_dim": cfg["dv"],
             "heads": cfg["H"], "k": cfg["k"], "key_dim": cfg["Dk"], "gated": True,
             "parallelism": parallelism,
             "l2": "inputs_larger_than_L2 (value table >= 4 GiB vs 126 MB L2; no flush)",
             "seed": SEED}
+
+
+def dry_run(args, world, rank):
+    """CPU rendezvous check of the multi-rank launch (gloo): every rank joins,
+    barriers, and reduces a per-rank number with MAX; rank 0 prints."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "world_size": dist.get_world_size(),
+                          "max_over_ranks": float(t.item())}), flush=True)
+    dist.destroy_process_group()
 
 
 def main():
@@ -456,7 +741,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None)
     ap.add_argument("--mode", default="alltoall", choices=["alltoall", "allgather"])
-    ap.add_argument("--cpu-tokens", type=int, default=2048)
+    ap.add_argument("--per-rank", type=int, default=0,
+                    help="on one GPU: time one rank's work of a G-rank group (collectives removed)")
+    ap.add_argument("--cpu-tokens", type=int, default=1024)
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--qk-norm", action="store_true", help="qk-normalisation (SURVEY f2)")
@@ -464,8 +751,19 @@ def main():
                     help="backward sorts the indices itself (no forward-built state)")
     ap.add_argument("--force-group", action="store_true",
                     help="run the memory-group (NCCL) path even at N=1 (torchrun)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU: only the multi-rank launch + rendezvous (gloo), no GPU work")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(respawn_under_torchrun(args.gpus))
     world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch with matching "
+              f"--nproc-per-node", file=sys.stderr)
+        sys.exit(2)
+    if args.dry_run:
+        dry_run(args, world, rank)
+        return
     if args.warmup < 3:
         args.warmup = 3
     cfg_name = args.config or "c2"
@@ -481,26 +779,42 @@ def main():
     if rank != 0:
         return
     peaks = load_peaks()
-    G = world
-    roof, per = roofline(res, cfg, G, peaks)
+    G = res["G"]
+    roof, per, scoring = roofline(res, cfg, peaks)
     cb = None
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(cfg, args.cpu_tokens if cfg_name != "c1" else cfg["T"])
-    fwd_b, bwd_b, P = bag_bytes(cfg, G, res["U"])
+    bb = bag_bytes(cfg, G, res["T_loc"], res["U"])
+    if world > 1:
+        par = f"memory-group dim-shard G={G} ({args.mode}), NCCL"
+    elif args.per_rank > 1:
+        par = (f"one rank of a G={G} memory group on one GPU (collectives replaced by local "
+               f"copies: SURVEY §8(e) t_ref(G)), {args.mode}")
+    elif args.force_group:
+        par = f"memory-group path G=1 ({args.mode}), NCCL"
+    else:
+        par = "single GPU"
     line = {
         "metric": METRIC, "value": res["value"], "unit": "tok/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_step"],
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": cfg["dtype"], "data": "synthetic",
-        "config": dict(config_keys(cfg, cfg_name, G,
-                                   (f"memory-group dim-shard G={G} ({args.mode})"
-                                    if (G > 1 or args.force_group) else "single GPU")),
-                       qk_norm=bool(args.qk_norm),
-                       unique_rows_per_position=round(res["U"] / P, 4)),
+        "higher_is_better": True, "scaling": "strong" if "T_global" in cfg else "weak",
+        "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "config": dict(config_keys(cfg, cfg_name, world if world > 1 else 1, par, res["T_loc"]),
+                       qk_norm=bool(args.qk_norm), per_rank_G=args.per_rank or None,
+                       unique_rows_per_position=round(res["U"] / bb["P"], 4)),
         "roofline": roof,
+        "scoring_roofline": scoring,
         "bag_kernels": per,
-        "kernel_ms_per_step": {n: round(v[1] / args.steps, 4) for n, v in sorted(
+        "kernel_ms_per_step": {n: round(v[1] / res["kern_steps"], 4) for n, v in sorted(
             res["kern"].items(), key=lambda kv: -kv[1][1])},
+        "kernel_timing": "separate pass, kernels serialised on the caller's stream (ml_set_serial)",
+        "per_rank": ({"G": G, "t_ref_ms": round(res["ms_step"], 4),
+                      "group_tokens_per_step": G * res["T_loc"],
+                      "group_tok_s_at_E1": G * res["T_loc"] / (res["ms_step"] / 1e3),
+                      "note": "value = this one rank's tokens per second"}
+                     if (world == 1 and args.per_rank > 1) else None),
+        "collectives": res["coll"],
+        "scaling_efficiency": res["eff"],
         "cpu_baseline": cb,
         "e2e": res["e2e"],
         "gpu_launches": res["launches"],

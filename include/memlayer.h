@@ -75,6 +75,11 @@ int ml_device_info(int* sm_count, int* cc_major, int* cc_minor);
 void ml_timing_enable(int on);
 void ml_timing_reset(void);
 size_t ml_timing_report(char* buf, size_t len);
+/* Serial mode (measurement only): with on != 0, the layer calls issue every
+ * kernel on the caller's stream instead of forking independent parts onto the
+ * library's auxiliary streams, so the timing events above bracket one kernel
+ * each (bench.py's per-kernel pass).  Results are bit-identical either way. */
+void ml_set_serial(int on);
 
 /* Counter-based synthetic generator (not method arithmetic).
  * Fills out[r - row0][c] for rows r in [row0, row0 + n_rows), c < n_cols of a

@@ -58,6 +58,7 @@ SIGNATURES = {
     "ml_launch_count": [],
     "ml_device_info": [C.POINTER(C.c_int)] * 3,
     "ml_timing_enable": [C.c_int],
+    "ml_set_serial": [C.c_int],
     "ml_timing_reset": [],
     "ml_timing_report": [C.c_char_p, SZ],
     "ml_synth_fill": [P, I64, I64, I64, C.c_uint64, C.c_uint32, C.c_float, C.c_int, C.c_int, I64, P],
@@ -94,7 +95,7 @@ SIGNATURES = {
     "ml_gemm": [C.c_int, C.c_int, I64, I64, I64, P, I64, P, I64, P, I64, C.c_int, C.c_int, P, SZ, P],
 }
 _RESTYPES = {"ml_last_error": C.c_char_p, "ml_version": C.c_int, "ml_launch_count": C.c_uint64,
-             "ml_device_info": C.c_int, "ml_timing_enable": None, "ml_timing_reset": None,
+             "ml_device_info": C.c_int, "ml_timing_enable": None, "ml_set_serial": None, "ml_timing_reset": None,
              "ml_timing_report": C.c_size_t, "embbag_bwd_lock_count": C.c_int64}
 
 _lib = None

@@ -49,9 +49,13 @@ struct SortBufs {
   int32_t* ghist = nullptr;     // single-pass mode: per-pass digit offsets + tile tickets
 };
 void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b);
-// On return *keys / *vals point at the sorted arrays (inside b).
+// On return *keys / *vals point at the sorted arrays (inside b).  Values are
+// the input positions; a key outside [0, key_limit) (default 2^bits) is sorted
+// as 0 and its position carries kClampedPos (the segmented pass gives it
+// weight 0).
+constexpr int32_t kClampedPos = int32_t(0x80000000u);
 mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b,
-                    int32_t** keys, int32_t** vals, cudaStream_t s);
+                    int32_t** keys, int32_t** vals, cudaStream_t s, int64_t key_limit = -1);
 // Where sort_pairs(n, bits) leaves its result inside b (without sorting).
 mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t** vals);
 

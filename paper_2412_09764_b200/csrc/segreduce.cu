@@ -260,9 +260,11 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
     float w = 0.f;
     if (i < p.P) {
       pos = p.spos[i];
+      const bool clamped = pos < 0;   // index outside [0, N): row 0, weight 0
+      pos &= ~kClampedPos;
       key = p.skey[i];
       r = p.excl[i] - 1 + p.flags[i];
-      w = p.w[pos];
+      w = clamped ? 0.f : p.w[pos];
       t = pos / p.B;
       rb = p.run_begin[r];
       re = p.run_begin[r + 1];
@@ -500,9 +502,11 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
         SegMeta m{0, 0, 0, 0, 0, 0, 0, 0.f};
         if (i < p.P) {
           m.pos = p.spos[i];
+          const bool clamped = m.pos < 0;   // index outside [0, N): row 0, weight 0
+          m.pos &= ~kClampedPos;
           m.key = p.skey[i];
           m.rr = p.excl[i] - 1 + p.flags[i];
-          m.w = p.w[m.pos];
+          m.w = clamped ? 0.f : p.w[m.pos];
           m.t = m.pos / p.B;
           m.rb = p.run_begin[m.rr];
           m.re = p.run_begin[m.rr + 1];

@@ -133,11 +133,17 @@ constexpr uint32_t kStInc = 2u << 30;     // inclusive prefix available
 constexpr uint32_t kStMask = (1u << 30) - 1;
 constexpr uint32_t kSortSpin = 1u << 26;
 
-__device__ __forceinline__ int32_t load_key(const SortPassParams& p, int64_t i, bool first) {
+// First pass: a key outside [0, key_limit) (an index outside [0, N)) is
+// sorted as row 0 and its position value carries kClampedPos, so the
+// segmented pass gives it weight 0 (memlayer.h: "clamped to row 0 with
+// weight 0"); the index flag is raised for ML_CHECK_INDICES.
+__device__ __forceinline__ int32_t load_key(const SortPassParams& p, int64_t i, bool first,
+                                            bool* clamped = nullptr) {
   int32_t k = p.kin[i];
   if (first && static_cast<uint32_t>(k) >= p.key_limit) {
     atomicExch(p.flag, 1);
     k = 0;
+    if (clamped) *clamped = true;
   }
   return k;
 }
@@ -210,8 +216,9 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
   for (int r = 0; r < kSortRounds; ++r) {
     const int64_t i = wbase + r * 32 + lane;
     const bool valid = i < p.n;
-    key[r] = valid ? load_key(p, i, first) : 0;
-    val[r] = valid ? (p.vin ? p.vin[i] : int32_t(i)) : 0;
+    bool clamped = false;
+    key[r] = valid ? load_key(p, i, first, &clamped) : 0;
+    val[r] = valid ? (p.vin ? p.vin[i] : (int32_t(i) | (clamped ? kClampedPos : 0))) : 0;
   }
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
@@ -572,7 +579,7 @@ mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t
 }
 
 mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, int32_t** keys,
-                    int32_t** vals, cudaStream_t s) {
+                    int32_t** vals, cudaStream_t s, int64_t key_limit) {
   if (n <= 0) {
     *keys = b.k[0];
     *vals = b.v[0];
@@ -599,7 +606,8 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
   p.n = n;
   p.nblocks = nb;
   p.dbits = dbits;
-  p.key_limit = uint32_t(1) << bits;
+  p.key_limit = (key_limit > 0 && key_limit < (int64_t(1) << bits)) ? uint32_t(key_limit)
+                                                                   : uint32_t(1) << bits;
   p.counts = b.counts;
   p.flag = index_flag_ptr();
   const int64_t ncounts = int64_t(nb) << dbits;

@@ -51,6 +51,9 @@ def workspace(nbytes, device=None, tag="default"):
 
 
 def release_workspaces():
+    """Drop the cached workspaces.  Must not be called while a captured
+    MemoryLayerStepGraph (graph.py) is alive: the graph replays kernels whose
+    workspace pointers were baked in at capture time."""
     _WS.clear()
 
 
@@ -61,6 +64,13 @@ def launch_count():
 
 def timing_enable(on=True):
     lib().ml_timing_enable(1 if on else 0)
+
+
+def set_serial(on=True):
+    """Measurement only: issue every kernel of a layer call on the caller's
+    stream (no auxiliary-stream concurrency) so per-launch timing events
+    bracket one kernel each."""
+    lib().ml_set_serial(1 if on else 0)
 
 
 def timing_reset():
@@ -426,3 +436,30 @@ def embbag_bwd_pool(V, idx_list, w_list, dy_list):
     dy = torch.cat(dy_list, 0)
     rows, dV, U, dw = embbag_bwd(V, idx, w, dy, sync=False)
     return rows, dV, U, list(torch.split(dw, [i.shape[0] for i in idx_list], 0))
+
+
+# ------------------------------------------------------------ device guard
+def _on_device(fn):
+    """Run `fn` with the device of its first CUDA tensor argument current, so
+    the library launches on that device and on that device's current stream
+    (tensors on a non-current device otherwise get the wrong stream)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        for a in list(args) + list(kwargs.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                if a.device.index == torch.cuda.current_device():
+                    return fn(*args, **kwargs)
+                with torch.cuda.device(a.device):
+                    return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+    return wrapped
+
+
+for _name in ("synth_fill", "pkm_topk", "pkm_topk_bwd", "embbag_fwd", "embbag_bwd",
+              "embbag_bwd_prepare", "embbag_bwd_dv_only", "embbag_bwd_atomics", "embbag_bwd_lock",
+              "sparse_adam", "embbag_grad_apply", "memory_layer_fwd", "memory_layer_bwd", "peer_fwd",
+              "peer_bwd", "group_unpack", "group_pack", "gate_bwd", "gemm", "embbag_bwd_pool"):
+    globals()[_name] = _on_device(globals()[_name])
+del _name

@@ -44,8 +44,8 @@ def test_reference_arm_json_line():
 
 
 def test_reference_arm_nonzero_rank_is_silent():
-    r = _bench(["--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "1"],
-               {"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2"})
+    r = _bench(["--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "1",
+                "--gpus", "2"], {"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert not [x for x in r.stdout.splitlines() if x.startswith("{")]
 
@@ -55,3 +55,26 @@ def test_product_arm_fails_loudly_without_cuda():
     r = _bench(["--config", "c1", "--steps", "1", "--warmup", "1"])
     assert r.returncode != 0
     assert not [x for x in r.stdout.splitlines() if x.startswith("{")]
+
+
+def test_gpus_mismatch_with_world_size_fails():
+    r = _bench(["--impl", "reference", "--config", "c1", "--steps", "1", "--gpus", "4"],
+               {"RANK": "0", "LOCAL_RANK": "0", "WORLD_SIZE": "2"})
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
+
+
+def test_gpus_n_spawns_n_rendezvousing_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-executes itself
+    under torch.distributed.run: 2 ranks rendezvous (gloo dry run on CPU), the
+    max over ranks reaches rank 0, and only rank 0 prints (n_gpus = 2)."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--dry-run"], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = lines[0]
+    assert d["dry_run"] and d["n_gpus"] == 2 and d["world_size"] == 2
+    assert d["max_over_ranks"] == 2.0
