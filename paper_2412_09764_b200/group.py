@@ -72,6 +72,8 @@ class CudaLocal:
     # high-priority stream; join() makes the current stream wait for it.
     def side(self, like):
         cur = torch.cuda.current_stream(like.device)
+        if self.ops.SERIAL:       # measurement mode: one in-order stream
+            return torch.cuda.stream(cur)
         if self._side is None:
             self._side = torch.cuda.Stream(device=like.device, priority=-100)   # the highest
         self._side.wait_stream(cur)
@@ -91,6 +93,11 @@ class CudaLocal:
         (it fills SMs the forward's tail leaves idle); returns (state, event):
         the backward waits on the event, the forward does not."""
         cur = torch.cuda.current_stream(idx.device)
+        if self.ops.SERIAL:       # measurement mode: one in-order stream
+            state = self.ops.embbag_bwd_prepare(N, dv, idx, dtype)
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            return state, ev
         if getattr(self, "_bg", None) is None:
             self._bg = torch.cuda.Stream(device=idx.device)
         self._bg.wait_stream(cur)

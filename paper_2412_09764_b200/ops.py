@@ -15,6 +15,7 @@ from ._lib import PkmShape, BagShape, LayerShape, PeerShape, check, lib
 
 _DT = {torch.bfloat16: _lib.ML_BF16, torch.float32: _lib.ML_F32}
 _WS = {}
+SERIAL = False      # set_serial(): measurement mode, no side-stream concurrency
 
 
 def _dt(t):
@@ -70,6 +71,8 @@ def set_serial(on=True):
     """Measurement only: issue every kernel of a layer call on the caller's
     stream (no auxiliary-stream concurrency) so per-launch timing events
     bracket one kernel each."""
+    global SERIAL
+    SERIAL = bool(on)
     lib().ml_set_serial(1 if on else 0)
 
 

@@ -37,7 +37,7 @@ class Full:
     def run(self):
         import bench
         from paper_2412_09764_b200 import ops
-        t = bench.make_inputs(self.cfg, torch.device("cuda", 0), 1, 0, ops, torch)
+        t = bench.make_inputs(self.cfg, torch.device("cuda", 0), 1, 0, ops, torch, False)
         k = self.k
         out, saved = ops.memory_layer_fwd(t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"], k)
         g = ops.memory_layer_bwd(t["dout"], t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"],
@@ -85,7 +85,22 @@ class Full:
         dy = gb["dy"]
         dw = np.stack([self.Vrows(bidx[i]) @ dy[i] for i in range(n)])
         dq, _, _, _ = opkm.pkm_bwd(q, tb["K1"], tb["K2"], idx, w, dw.reshape(n, H, k))
-        return dict(q=q, idx=idx, w=w, y=y, out=out, dy=dy, dw=dw, dq=dq)
+        # rounding-model magnitudes sum|terms| (tests/gpu_util.py assert_close mag=)
+        A = np.abs
+        sg = A(ogate.silu(gpre))
+        mdy = (A(dout) @ A(tb["W2"]).T) * sg
+        mw = np.stack([A(self.Vrows(bidx[i])) @ mdy[i] for i in range(n)])
+        mds = (w * (mw.reshape(n, H, k) + (w * mw.reshape(n, H, k)).sum(-1, keepdims=True)))
+        S, Dh = self.S, self.Dh
+        mdq = np.zeros(q.shape)
+        for hh in range(H):
+            for j in range(k):
+                a, b = idx[:, hh, j] // S, idx[:, hh, j] % S
+                mdq[:, hh, :Dh] += mds[:, hh, j, None] * A(tb["K1"][hh, a])
+                mdq[:, hh, Dh:] += mds[:, hh, j, None] * A(tb["K2"][hh, b])
+        mag = dict(y=np.stack([bw[i] @ A(self.Vrows(bidx[i])) for i in range(n)]),
+                   out=(A(y) * sg) @ A(tb["W2"]), dy=mdy, dw=mw, dq=mdq)
+        return dict(q=q, idx=idx, w=w, y=y, out=out, dy=dy, dw=dw, dq=dq, mag=mag)
 
     def sample(self):
         T = self.T
@@ -105,10 +120,15 @@ class Full:
         assert tok_ok.sum() >= len(SAMPLE) - 2, f"too many near ties: {near}"
         assert_close(run["w"][SAMPLE][ok], r["w"][ok], TOL["f32"], "w")
         s = SAMPLE[tok_ok]
-        assert_close(host(run["y"][torch.as_tensor(s)]), r["y"][tok_ok], TOL["bf16"], "y")
-        assert_close(host(run["out"][torch.as_tensor(s)]), r["out"][tok_ok], TOL["bf16"], "out")
-        assert_close(run["dw"][s].reshape(len(s), -1), r["dw"][tok_ok], TOL["bf16"], "dw")
-        assert_close(host(run["dq"][torch.as_tensor(s)]), r["dq"][tok_ok], TOL["bf16"], "dq")
+        m = r["mag"]
+        assert_close(host(run["y"][torch.as_tensor(s)]), r["y"][tok_ok], TOL["bf16"], "y",
+                     mag=m["y"][tok_ok])
+        assert_close(host(run["out"][torch.as_tensor(s)]), r["out"][tok_ok], TOL["bf16"], "out",
+                     mag=m["out"][tok_ok])
+        assert_close(run["dw"][s].reshape(len(s), -1), r["dw"][tok_ok], TOL["bf16"], "dw",
+                     mag=m["dw"][tok_ok])
+        assert_close(host(run["dq"][torch.as_tensor(s)]), r["dq"][tok_ok], TOL["bf16"], "dq",
+                     mag=m["dq"][tok_ok])
 
     def check_sampled_value_rows(self, run, tb, n_rows=6):
         """dV of rows chosen by the oracle, with their complete contributor sets."""
@@ -135,13 +155,15 @@ class Full:
         toks = sorted({t for v in contrib.values() for (t, _, _, _) in v})
         ro = self.token_oracle(np.array(toks), tb)
         dy = {t: ro["dy"][i] for i, t in enumerate(toks)}
+        mdy = {t: ro["mag"]["dy"][i] for i, t in enumerate(toks)}
         gpu_rows = run["rows"]
         for rr in rows:
             assert contrib[rr], rr
             ref = sum(wj * dy[t] for (t, h, j, wj) in contrib[rr])
+            mag = sum(wj * mdy[t] for (t, h, j, wj) in contrib[rr])
             pos = np.searchsorted(gpu_rows, rr)
             assert pos < len(gpu_rows) and gpu_rows[pos] == rr, f"row {rr} missing from the GPU dV rows"
-            assert_close(host(run["dV"][pos]), ref, TOL["bf16"], f"dV[{rr}]")
+            assert_close(host(run["dV"][pos]), ref, TOL["bf16"], f"dV[{rr}]", mag=mag)
 
     def check_key_gradient_identity(self, run, tb):
         Dh, T = self.Dh, self.T
