@@ -309,9 +309,11 @@ def build_step(args, cfg, t, ops, torch, comm=None):
     dK1 = torch.zeros(t["K1"].shape, dtype=torch.float32, device=t["q"].device)
     dK2 = torch.zeros(t["K2"].shape, dtype=torch.float32, device=t["q"].device)
     bufs = {}
+    dV_dtype = torch.bfloat16 if args.dv_dtype == "bf16" else torch.float32
     if comm is not None:
         from paper_2412_09764_b200 import group
-        layer = group.GroupMemoryLayer(comm, k=k, mode=args.mode)
+        layer = group.GroupMemoryLayer(comm, k=k, mode=args.mode,
+                                       local=group.CudaLocal(dV_dtype=dV_dtype))
 
         def step(inp=t):
             dK1.zero_()
@@ -328,7 +330,8 @@ def build_step(args, cfg, t, ops, torch, comm=None):
                                               t["W1"], t["W2"], k, qk_norm=args.qk_norm,
                                               keep_state=not args.no_state)
             g = ops.memory_layer_bwd(inp["dout"], inp["x"], inp["q"], t["K1"], t["K2"], t["V"],
-                                     t["W1"], t["W2"], saved, dK1=dK1, dK2=dK2, bufs=bufs)
+                                     t["W1"], t["W2"], saved, dK1=dK1, dK2=dK2, bufs=bufs,
+                                     dV_dtype=dV_dtype)
             return out, g
     step.last_saved = None
     return step
@@ -343,14 +346,18 @@ def time_steps(step, steps, world, torch, dev):
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
+    import gc
     barrier()
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()         # no collector pause between launches inside the timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
         out, g = step()
     e1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
@@ -418,6 +425,23 @@ def run_ours(args, cfg, world, rank, local):
         coll = comm.report(kern_steps) if world > 1 else None
         comm.rec = []
 
+    # ---- variant: the compact value gradient stored as bf16 (memlayer.h
+    # grad_dtype; fp32 sums rounded once) -- same step otherwise
+    variants = None
+    if args.dv_dtype == "f32" and cfg["dtype"] == "bf16" and not args.no_variants:
+        import copy
+        a2 = copy.copy(args)
+        a2.dv_dtype = "bf16"
+        vstep = build_step(a2, cfg, t, ops, torch, comm)
+        for _ in range(args.warmup):
+            vstep()
+        ms_v, _, _ = time_steps(vstep, args.steps, world, torch, dev)
+        variants = {"dV_bf16": {"ms_per_step": round(ms_v / args.steps, 4),
+                                "value": tokens_per_step / (ms_v / args.steps / 1e3),
+                                "note": "compact value gradient stored as bf16 (grad_dtype=ML_BF16; "
+                                        "fp32 sums rounded once); the headline keeps fp32 dV"}}
+        del vstep
+
     # ---- t_ref(G): the same rank's work with the collectives removed
     eff = None
     if world > 1:
@@ -436,7 +460,8 @@ def run_ours(args, cfg, world, rank, local):
     e2e = run_e2e(args, t, step, torch, tokens_per_step, world)
     return dict(value=tokens_per_step / (ms_step / 1e3), ms_step=ms_step, kern=kern,
                 kern_steps=kern_steps, launches=launches, clocks=clk.summary(), U=U, e2e=e2e,
-                tokens_per_step=tokens_per_step, G=G, T_loc=T_loc, coll=coll, eff=eff)
+                tokens_per_step=tokens_per_step, G=G, T_loc=T_loc, coll=coll, eff=eff,
+                variants=variants)
 
 
 def run_e2e(args, t, step, torch, tokens_per_step, world):
@@ -749,6 +774,10 @@ def main():
     ap.add_argument("--qk-norm", action="store_true", help="qk-normalisation (SURVEY f2)")
     ap.add_argument("--no-state", action="store_true",
                     help="backward sorts the indices itself (no forward-built state)")
+    ap.add_argument("--dv-dtype", default="f32", choices=["f32", "bf16"],
+                    help="storage of the compact value gradient (memlayer.h grad_dtype)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the bf16-dV variant timing")
     ap.add_argument("--force-group", action="store_true",
                     help="run the memory-group (NCCL) path even at N=1 (torchrun)")
     ap.add_argument("--dry-run", action="store_true",
@@ -801,6 +830,7 @@ def main():
         "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
         "config": dict(config_keys(cfg, cfg_name, world if world > 1 else 1, par, res["T_loc"]),
                        qk_norm=bool(args.qk_norm), per_rank_G=args.per_rank or None,
+                       dV_dtype=args.dv_dtype,
                        unique_rows_per_position=round(res["U"] / bb["P"], 4)),
         "roofline": roof,
         "scoring_roofline": scoring,
@@ -813,6 +843,7 @@ def main():
                       "group_tok_s_at_E1": G * res["T_loc"] / (res["ms_step"] / 1e3),
                       "note": "value = this one rank's tokens per second"}
                      if (world == 1 and args.per_rank > 1) else None),
+        "variants": res["variants"],
         "collectives": res["coll"],
         "scaling_efficiency": res["eff"],
         "cpu_baseline": cb,

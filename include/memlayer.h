@@ -139,7 +139,12 @@ mlStatus pkm_topk_bwd(const mlPkmShape* shape, const void* q, const void* K1, co
  * stored there too.  V [N,dv], idx/w [T,B], gate_pre/y/y_ungated [T,dv].
  * Rules: dv*e a multiple of 16 B; dv/(16/e) a power of two <= 256 or a
  * multiple of 256; 1 <= B <= 1024. */
-typedef struct { int64_t N; int32_t dv; int32_t T; int32_t B; mlDtype dtype; } mlBagShape;
+/* grad_dtype: storage type of the compact value gradient dV of the backward
+ * calls (ML_F32, the default of a zero-initialised shape; or ML_BF16, only
+ * with a bf16 table: each element is accumulated in fp32 and rounded once,
+ * half the dV bytes -- the table's own dtype, as a bf16 framework's
+ * EmbeddingBag gradient).  The forward ignores it. */
+typedef struct { int64_t N; int32_t dv; int32_t T; int32_t B; mlDtype dtype; mlDtype grad_dtype; } mlBagShape;
 
 mlStatus embbag_fwd(const mlBagShape* shape, const void* V, const int32_t* idx, const float* w,
                     const void* gate_pre, void* y, void* y_ungated, void* stream);
@@ -147,16 +152,17 @@ mlStatus embbag_fwd(const mlBagShape* shape, const void* V, const int32_t* idx, 
 /* Backward, "reverse_indices" strategy: the P = T*B (idx, position)
  * pairs are stably radix-sorted by idx (the inverted token->row map); each
  * distinct row r is reduced by one owner in position order:
- *   dV[r,:] = sum_{p: idx[p]=r} w[p] * dy[t(p),:]   (fp32; V[r] read once per row)
+ *   dV[r,:] = sum_{p: idx[p]=r} w[p] * dy[t(p),:]   (fp32 sums; V[r] read once per row)
  *   dw[p]   = <dy[t(p),:], V[idx[p],:]>
- * Outputs: rows[0..U) ascending distinct indices, dV[0..U) their fp32
- * gradient rows (compact SparseGrad), *U (device int32), dw [T,B]
- * fp32.  rows / dV need capacity T*B rows.  Deterministic: bitwise equal
+ * Outputs: rows[0..U) ascending distinct indices, dV[0..U) their gradient
+ * rows in shape->grad_dtype (compact SparseGrad), *U (device
+ * int32), dw [T,B] fp32.  An index outside [0, N) is treated as row 0 with
+ * weight 0 (as the forward; ML_ERR_INDEX under ML_CHECK_INDICES=1).  rows / dV need capacity T*B rows.  Deterministic: bitwise equal
  * across runs (no float atomics; runs longer than 32 positions are split into
  * fixed pieces combined in piece order). */
 mlStatus embbag_bwd_workspace(const mlBagShape* shape, size_t* bytes);
 mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, const float* w,
-                    const void* dy, int32_t* rows, float* dV, int32_t* U, float* dw,
+                    const void* dy, int32_t* rows, void* dV, int32_t* U, float* dw,
                     void* ws, size_t ws_bytes, void* stream);
 
 /* With V == NULL and dw == NULL only the value gradient is computed (rows /
@@ -173,7 +179,7 @@ mlStatus embbag_bwd_state_bytes(const mlBagShape* shape, size_t* bytes);
 mlStatus embbag_bwd_prepare(const mlBagShape* shape, const int32_t* idx, void* state,
                             size_t state_bytes, void* stream);
 mlStatus embbag_bwd_state(const mlBagShape* shape, const void* V, const float* w, const void* dy,
-                          const void* state, size_t state_bytes, int32_t* rows, float* dV,
+                          const void* state, size_t state_bytes, int32_t* rows, void* dV,
                           int32_t* U, float* dw, void* ws, size_t ws_bytes, void* stream);
 
 /* Controls: the other two backward strategies of PAPER.md §3.1.4,
@@ -193,8 +199,8 @@ mlStatus embbag_bwd_lock(const mlBagShape* shape, const int32_t* idx, const floa
 int64_t embbag_bwd_lock_count(const mlBagShape* shape);
 
 /* dV_dense[rows[i],:] += dV[i,:] for i < *U (unique rows: no atomics).
- * dV_dense [N,dv] fp32. */
-mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const float* dV,
+ * dV in shape->grad_dtype; dV_dense [N,dv] fp32. */
+mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const void* dV,
                            const int32_t* U, float* dV_dense, void* stream);
 
 /* Sparse (lazy, row-wise) Adam(W) for the memory values (SPEC.md
@@ -206,9 +212,9 @@ mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const f
  * Untouched rows (and their moments / counters) are unchanged.  V [N,dv] of
  * shape->dtype; V_master [N,dv] fp32 (nullable: if given, the update is done
  * on it and V receives its rounding); m, v [N,dv] fp32; steps [N] int32.
- * shape->T * shape->B = capacity of rows / dV. */
+ * shape->T * shape->B = capacity of rows / dV; dV in shape->grad_dtype. */
 typedef struct { float lr, beta1, beta2, eps, weight_decay; } mlAdamParams;
-mlStatus ml_sparse_adam(const mlBagShape* shape, const int32_t* rows, const float* dV,
+mlStatus ml_sparse_adam(const mlBagShape* shape, const int32_t* rows, const void* dV,
                         const int32_t* U, void* V, float* V_master, float* m, float* v,
                         int32_t* steps, const mlAdamParams* hp, void* stream);
 
@@ -221,7 +227,8 @@ mlStatus ml_sparse_adam(const mlBagShape* shape, const int32_t* rows, const floa
  * w_saved [T,H,k] f32, g_saved [T,dv] (dtype, gated only), y_saved [T,dv]
  * (dtype).  N must equal S*S.  W1/W2 products run on cuBLASLt (library GEMM,
  * fp32 accumulation). */
-typedef struct { mlPkmShape pkm; int64_t N; int32_t dv; int32_t D; int32_t gated; } mlLayerShape;
+typedef struct { mlPkmShape pkm; int64_t N; int32_t dv; int32_t D; int32_t gated;
+                 mlDtype grad_dtype; /* dV storage, as mlBagShape.grad_dtype */ } mlLayerShape;
 
 mlStatus memory_layer_fwd_workspace(const mlLayerShape* shape, size_t* bytes);
 mlStatus memory_layer_fwd(const mlLayerShape* shape, const void* x, const void* q,
@@ -243,7 +250,7 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
                           const int32_t* idx_saved, const float* w_saved,
                           const void* g_saved, const void* y_saved,
                           void* dx, float* dq, float* dK1, float* dK2,
-                          int32_t* dV_rows, float* dV, int32_t* U,
+                          int32_t* dV_rows, void* dV, int32_t* U,
                           float* dW1, float* dW2, float* dw_out,
                           void* ws, size_t ws_bytes, void* stream);
 
@@ -273,7 +280,7 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
                                 const void* W1, const void* W2, const int32_t* idx_saved,
                                 const float* w_saved, const void* g_saved, const void* y_saved,
                                 const void* state, size_t state_bytes, void* dx, float* dq,
-                                float* dK1, float* dK2, int32_t* dV_rows, float* dV, int32_t* U,
+                                float* dK1, float* dK2, int32_t* dV_rows, void* dV, int32_t* U,
                                 float* dW1, float* dW2, float* dw_out, void* ws, size_t ws_bytes,
                                 void* stream);
 

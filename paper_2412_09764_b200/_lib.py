@@ -24,12 +24,12 @@ class PkmShape(C.Structure):
 
 class BagShape(C.Structure):
     _fields_ = [("N", C.c_int64), ("dv", C.c_int32), ("T", C.c_int32), ("B", C.c_int32),
-                ("dtype", C.c_int)]
+                ("dtype", C.c_int), ("grad_dtype", C.c_int)]
 
 
 class LayerShape(C.Structure):
     _fields_ = [("pkm", PkmShape), ("N", C.c_int64), ("dv", C.c_int32), ("D", C.c_int32),
-                ("gated", C.c_int32)]
+                ("gated", C.c_int32), ("grad_dtype", C.c_int)]
 
 
 class PeerShape(C.Structure):

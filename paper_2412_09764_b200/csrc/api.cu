@@ -134,6 +134,9 @@ static mlStatus check_pkm(const mlPkmShape* s) {
 static mlStatus check_bag(const mlBagShape* s) {
   if (!s) return fail(ML_ERR_ARG, "null shape");
   if (s->dtype != ML_F32 && s->dtype != ML_BF16) return fail(ML_ERR_ARG, "unknown dtype");
+  if (s->grad_dtype != ML_F32 && s->grad_dtype != ML_BF16) return fail(ML_ERR_ARG, "unknown grad_dtype");
+  if (s->grad_dtype == ML_BF16 && s->dtype != ML_BF16)
+    return fail(ML_ERR_UNSUPPORTED, "bag: a bf16 value gradient needs a bf16 value table");
   if (s->N < 1 || s->N >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "bag: need 1 <= N < 2^31");
   if (s->T < 0) return fail(ML_ERR_CONFIG, "bag: T < 0");
   if (s->B < 1 || s->B > 1024) return fail(ML_ERR_CONFIG, "bag: need 1 <= B <= 1024");
@@ -344,7 +347,7 @@ static mlStatus bag_bwd_prepare(const mlBagShape& s, const int32_t* idx, int32_t
 
 // *nsw (nullable): number of dw partial slices written to b.dw_part
 static mlStatus bag_bwd_reduce(const mlBagShape& s, const void* V, const float* w, const void* dy,
-                               float* dV, BagBwdBufs& b, int32_t* skey, int32_t* spos,
+                               void* dV, BagBwdBufs& b, int32_t* skey, int32_t* spos,
                                cudaStream_t st, int* nsw = nullptr) {
   const int64_t P = int64_t(s.T) * s.B;
   if (nsw) *nsw = seg_slices(s.dv, s.dtype);
@@ -353,7 +356,8 @@ static mlStatus bag_bwd_reduce(const mlBagShape& s, const void* V, const float* 
   g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = w;
   g.src = dy; g.lds = s.dv; g.src_col0 = 0; g.B = s.B;
   g.V = V; g.ldv = s.dv; g.v_col0 = 0; g.dw_part = b.dw_part;
-  g.out = dV; g.ldo = s.dv; g.dense_accumulate = false;
+  g.out = static_cast<float*>(dV); g.ldo = s.dv; g.dense_accumulate = false;
+  g.out_bf16 = s.grad_dtype == ML_BF16;
   g.partial = b.partial; g.counters = b.counters; g.dv = s.dv; g.dtype = s.dtype;
   g.name = "embbag_bwd_segreduce";
   g.dw_slices_out = nsw;
@@ -362,7 +366,7 @@ static mlStatus bag_bwd_reduce(const mlBagShape& s, const void* V, const float* 
 }
 
 static mlStatus bag_bwd_core(const mlBagShape& s, const void* V, const int32_t* idx, const float* w,
-                             const void* dy, int32_t* rows, float* dV, int32_t* U, BagBwdBufs& b,
+                             const void* dy, int32_t* rows, void* dV, int32_t* U, BagBwdBufs& b,
                              cudaStream_t st, int* nsw = nullptr) {
   int32_t *skey = nullptr, *spos = nullptr;
   ML_TRY(bag_bwd_prepare(s, idx, rows, U, b, &skey, &spos, st));
@@ -507,7 +511,7 @@ mlStatus embbag_bwd_workspace(const mlBagShape* shape, size_t* bytes) {
 }
 
 mlStatus embbag_bwd(const mlBagShape* shape, const void* V, const int32_t* idx, const float* w,
-                    const void* dy, int32_t* rows, float* dV, int32_t* U, float* dw, void* ws,
+                    const void* dy, int32_t* rows, void* dV, int32_t* U, float* dw, void* ws,
                     size_t ws_bytes, void* stream) {
   ML_API_BEGIN
   ML_TRY(check_bag(shape));
@@ -564,7 +568,7 @@ mlStatus embbag_bwd_lock(const mlBagShape* shape, const int32_t* idx, const floa
   ML_API_END
 }
 
-mlStatus ml_sparse_adam(const mlBagShape* shape, const int32_t* rows, const float* dV,
+mlStatus ml_sparse_adam(const mlBagShape* shape, const int32_t* rows, const void* dV,
                         const int32_t* U, void* V, float* V_master, float* m, float* v,
                         int32_t* steps, const mlAdamParams* hp, void* stream) {
   ML_API_BEGIN
@@ -574,19 +578,19 @@ mlStatus ml_sparse_adam(const mlBagShape* shape, const int32_t* rows, const floa
   ML_TRY(check_ptrs({rows, dV, U, V, m, v, steps}));
   if (V_master) ML_TRY(check_ptrs({V_master}));
   timing_mark(nullptr, S(stream));
-  return launch_sparse_adam(rows, dV, U, int64_t(shape->T) * shape->B, shape->dv, V, shape->dtype,
+  return launch_sparse_adam(rows, dV, shape->grad_dtype, U, int64_t(shape->T) * shape->B, shape->dv, V, shape->dtype,
                             V_master, m, v, steps, *hp, S(stream));
   ML_API_END
 }
 
-mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const float* dV,
+mlStatus embbag_grad_apply(const mlBagShape* shape, const int32_t* rows, const void* dV,
                            const int32_t* U, float* dV_dense, void* stream) {
   ML_API_BEGIN
   ML_TRY(check_bag(shape));
   if (shape->T == 0) return ML_OK;
   ML_TRY(check_ptrs({rows, dV, U, dV_dense}));
   timing_mark(nullptr, S(stream));
-  return launch_scatter_rows(rows, dV, U, int64_t(shape->T) * shape->B, shape->dv, dV_dense,
+  return launch_scatter_rows(rows, dV, shape->grad_dtype, U, int64_t(shape->T) * shape->B, shape->dv, dV_dense,
                              S(stream));
   ML_API_END
 }
@@ -596,7 +600,7 @@ static mlStatus check_layer(const mlLayerShape* s) {
   if (!s) return fail(ML_ERR_ARG, "null shape");
   ML_TRY(check_pkm(&s->pkm));
   if (s->N != int64_t(s->pkm.S) * s->pkm.S) return fail(ML_ERR_CONFIG, "layer: N must equal S*S");
-  mlBagShape bs{s->N, s->dv, s->pkm.T, s->pkm.H * s->pkm.k, s->pkm.dtype};
+  mlBagShape bs{s->N, s->dv, s->pkm.T, s->pkm.H * s->pkm.k, s->pkm.dtype, s->grad_dtype};
   ML_TRY(check_bag(&bs));
   if (s->gated) {
     if (s->D < 1) return fail(ML_ERR_CONFIG, "layer: D < 1");
@@ -609,7 +613,7 @@ static mlStatus check_layer(const mlLayerShape* s) {
 }
 
 static mlBagShape bag_of(const mlLayerShape& s) {
-  return mlBagShape{s.N, s.dv, s.pkm.T, s.pkm.H * s.pkm.k, s.pkm.dtype};
+  return mlBagShape{s.N, s.dv, s.pkm.T, s.pkm.H * s.pkm.k, s.pkm.dtype, s.grad_dtype};
 }
 
 struct LayerFwdBufs { PkmFwdBufs pkm; void* z; void* gemm_ws; };
@@ -694,7 +698,7 @@ mlStatus embbag_bwd_prepare(const mlBagShape* shape, const int32_t* idx, void* s
 }
 
 mlStatus embbag_bwd_state(const mlBagShape* shape, const void* V, const float* w, const void* dy,
-                          const void* state, size_t state_bytes, int32_t* rows, float* dV,
+                          const void* state, size_t state_bytes, int32_t* rows, void* dV,
                           int32_t* U, float* dw, void* ws, size_t ws_bytes, void* stream) {
   ML_API_BEGIN
   ML_TRY(check_bag(shape));
@@ -856,7 +860,7 @@ mlStatus memory_layer_bwd(const mlLayerShape* shape, const void* dout, const voi
                           const void* W1, const void* W2, const int32_t* idx_saved,
                           const float* w_saved, const void* g_saved, const void* y_saved,
                           void* dx, float* dq, float* dK1, float* dK2, int32_t* dV_rows,
-                          float* dV, int32_t* U, float* dW1, float* dW2, float* dw_out, void* ws,
+                          void* dV, int32_t* U, float* dW1, float* dW2, float* dw_out, void* ws,
                           size_t ws_bytes, void* stream) {
   return memory_layer_bwd_state(shape, dout, x, q, K1, K2, V, W1, W2, idx_saved, w_saved, g_saved,
                                 y_saved, nullptr, 0, dx, dq, dK1, dK2, dV_rows, dV, U, dW1, dW2,
@@ -868,7 +872,7 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
                                 const void* W1, const void* W2, const int32_t* idx_saved,
                                 const float* w_saved, const void* g_saved, const void* y_saved,
                                 const void* state, size_t state_bytes, void* dx, float* dq,
-                                float* dK1, float* dK2, int32_t* dV_rows, float* dV, int32_t* U,
+                                float* dK1, float* dK2, int32_t* dV_rows, void* dV, int32_t* U,
                                 float* dW1, float* dW2, float* dw_out, void* ws, size_t ws_bytes,
                                 void* stream) {
   ML_API_BEGIN

@@ -40,15 +40,24 @@ __global__ void gate_bwd_kernel(const char* dz, const char* g, const char* y, ch
   stg_v4(dg + off, Vec<T>::pack(odg));
 }
 
-__global__ void scatter_rows_kernel(const int32_t* rows, const float* dV, const int32_t* U,
+__device__ __forceinline__ float4 load4(const float* p, int64_t i) {
+  return reinterpret_cast<const float4*>(p)[i];
+}
+__device__ __forceinline__ float4 load4(const __nv_bfloat16* p, int64_t i) {
+  const uint2 u = reinterpret_cast<const uint2*>(p)[i];
+  const float2 a = bf2_to_f2(u.x), b = bf2_to_f2(u.y);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename G>
+__global__ void scatter_rows_kernel(const int32_t* rows, const G* dV, const int32_t* U,
                                     int32_t dv4, float* dense) {
   const int64_t r = blockIdx.x;
   if (r >= *U) return;
   const int64_t dst = rows[r];
-  const float4* s = reinterpret_cast<const float4*>(dV + r * int64_t(dv4) * 4);
   float4* d = reinterpret_cast<float4*>(dense + dst * int64_t(dv4) * 4);
   for (int c = threadIdx.x; c < dv4; c += blockDim.x) {
-    float4 a = s[c], b = d[c];
+    float4 a = load4(dV, r * int64_t(dv4) + c), b = d[c];
     b.x += a.x; b.y += a.y; b.z += a.z; b.w += a.w;
     d[c] = b;
   }
@@ -79,11 +88,16 @@ mlStatus launch_gate_bwd(const void* dz, const void* g, const void* y, void* z, 
   return ML_OK;
 }
 
-mlStatus launch_scatter_rows(const int32_t* rows, const float* dV, const int32_t* U, int64_t cap,
-                             int32_t dv, float* dense, cudaStream_t s) {
+mlStatus launch_scatter_rows(const int32_t* rows, const void* dV, mlDtype gdt, const int32_t* U,
+                             int64_t cap, int32_t dv, float* dense, cudaStream_t s) {
   if (cap <= 0) return ML_OK;
   if (dv % 4) return fail(ML_ERR_CONFIG, "grad_apply: dv must be a multiple of 4");
-  scatter_rows_kernel<<<unsigned(cap), 128, 0, s>>>(rows, dV, U, dv / 4, dense);
+  if (gdt == ML_BF16)
+    scatter_rows_kernel<__nv_bfloat16><<<unsigned(cap), 128, 0, s>>>(
+        rows, static_cast<const __nv_bfloat16*>(dV), U, dv / 4, dense);
+  else
+    scatter_rows_kernel<float><<<unsigned(cap), 128, 0, s>>>(rows, static_cast<const float*>(dV),
+                                                             U, dv / 4, dense);
   ML_LAUNCH_CHECK("scatter_rows");
   return ML_OK;
 }

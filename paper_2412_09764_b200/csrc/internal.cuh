@@ -90,6 +90,7 @@ struct SegArgs {
   const void* V = nullptr; int64_t ldv = 0; int32_t v_col0 = 0;
   float* dw_part = nullptr;
   float* out = nullptr; int64_t ldo = 0; bool dense_accumulate = false;
+  bool out_bf16 = false;             // out holds bf16 rows (grad_dtype ML_BF16)
   float* partial = nullptr; int32_t* counters = nullptr;
   int32_t dv = 0; mlDtype dtype = ML_BF16;
   const char* name = "segreduce";  // timing / profiling label
@@ -137,7 +138,7 @@ mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const floa
 // z = y*silu(g); dy = dz*silu(g); dg = dz*y*silu'(g)   (elementwise, n elems)
 mlStatus launch_gate_bwd(const void* dz, const void* g, const void* y, void* z, void* dy,
                          void* dg, int64_t n, mlDtype dt, cudaStream_t s);
-mlStatus launch_scatter_rows(const int32_t* rows, const float* dV, const int32_t* U,
+mlStatus launch_scatter_rows(const int32_t* rows, const void* dV, mlDtype gdt, const int32_t* U,
                              int64_t cap, int32_t dv, float* dense, cudaStream_t s);
 
 // Row-major GEMM on cuBLASLt: C[M,N] = op(A) op(B), fp32 accumulation.
@@ -159,7 +160,7 @@ mlStatus launch_bag_bwd_ctrl(int strategy, const mlBagShape& sh, const int32_t* 
                              const void* dy, float* dV, int* locks, cudaStream_t s);
 
 // ------------------------------------------------ sparse optimizer (f1)
-mlStatus launch_sparse_adam(const int32_t* rows, const float* dV, const int32_t* U, int64_t cap,
+mlStatus launch_sparse_adam(const int32_t* rows, const void* dV, mlDtype gdt, const int32_t* U, int64_t cap,
                             int32_t dv, void* V, mlDtype dt, float* Vm, float* m, float* v,
                             int32_t* steps, const mlAdamParams& hp, cudaStream_t s);
 

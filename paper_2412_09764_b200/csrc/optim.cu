@@ -9,8 +9,17 @@
 namespace ml {
 namespace {
 
-template <typename T>
-__global__ void __launch_bounds__(256) sparse_adam_kernel(const int32_t* rows, const float* dV,
+__device__ __forceinline__ float4 grad4(const float* p, int64_t i) {
+  return *reinterpret_cast<const float4*>(p + i);
+}
+__device__ __forceinline__ float4 grad4(const __nv_bfloat16* p, int64_t i) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p + i);
+  const float2 a = bf2_to_f2(u.x), b = bf2_to_f2(u.y);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename T, typename G>
+__global__ void __launch_bounds__(256) sparse_adam_kernel(const int32_t* rows, const G* dV,
                                                           const int32_t* Uptr, int32_t dv, T* V,
                                                           float* Vm, float* m, float* v,
                                                           int32_t* steps, mlAdamParams hp) {
@@ -26,7 +35,7 @@ __global__ void __launch_bounds__(256) sparse_adam_kernel(const int32_t* rows, c
     __syncthreads();
     const float bc1 = s_bc1, bc2 = s_bc2;
     for (int c0 = threadIdx.x * 4; c0 < dv; c0 += blockDim.x * 4) {
-      const float4 g = *reinterpret_cast<const float4*>(dV + int64_t(i) * dv + c0);
+      const float4 g = grad4(dV, int64_t(i) * dv + c0);
       float4* mp = reinterpret_cast<float4*>(m + r * dv + c0);
       float4* vp = reinterpret_cast<float4*>(v + r * dv + c0);
       float4 mm = *mp, vv = *vp;
@@ -64,19 +73,24 @@ __global__ void __launch_bounds__(256) sparse_adam_kernel(const int32_t* rows, c
 
 }  // namespace
 
-mlStatus launch_sparse_adam(const int32_t* rows, const float* dV, const int32_t* U, int64_t cap,
-                            int32_t dv, void* V, mlDtype dt, float* Vm, float* m, float* v,
-                            int32_t* steps, const mlAdamParams& hp, cudaStream_t s) {
+mlStatus launch_sparse_adam(const int32_t* rows, const void* dV, mlDtype gdt, const int32_t* U,
+                            int64_t cap, int32_t dv, void* V, mlDtype dt, float* Vm, float* m,
+                            float* v, int32_t* steps, const mlAdamParams& hp, cudaStream_t s) {
   if (cap <= 0) return ML_OK;
   if (dv % 4) return fail(ML_ERR_CONFIG, "sparse_adam: dv must be a multiple of 4");
   const unsigned grid = unsigned(std::min<int64_t>(cap, int64_t(num_sms()) * 8));
-  if (dt == ML_BF16)
-    sparse_adam_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(rows, dV, U, dv,
-                                                           static_cast<__nv_bfloat16*>(V), Vm, m, v,
-                                                           steps, hp);
-  else
-    sparse_adam_kernel<float><<<grid, 256, 0, s>>>(rows, dV, U, dv, static_cast<float*>(V), Vm, m,
-                                                   v, steps, hp);
+  const float* g32 = static_cast<const float*>(dV);
+  const __nv_bfloat16* g16 = static_cast<const __nv_bfloat16*>(dV);
+  if (dt == ML_BF16) {
+    __nv_bfloat16* Vb = static_cast<__nv_bfloat16*>(V);
+    if (gdt == ML_BF16)
+      sparse_adam_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(rows, g16, U, dv, Vb, Vm, m, v, steps, hp);
+    else
+      sparse_adam_kernel<__nv_bfloat16, float><<<grid, 256, 0, s>>>(rows, g32, U, dv, Vb, Vm, m, v, steps, hp);
+  } else {
+    sparse_adam_kernel<float, float><<<grid, 256, 0, s>>>(rows, g32, U, dv, static_cast<float*>(V),
+                                                          Vm, m, v, steps, hp);
+  }
   ML_LAUNCH_CHECK("sparse_adam");
   return ML_OK;
 }

@@ -51,6 +51,7 @@ struct SegParams {
   const char* V; int64_t ldv_bytes; int32_t v_col0;
   float* dw_part;
   float* out; int64_t ldo; int dense;
+  int out_bf16;      // dV rows stored as bf16 (fp32 accumulation, one rounding per element)
   float* partial; int32_t* counters; int64_t nslots_cap;
   int32_t* ticket;   // work-item counter of the persistent kernel (zeroed)
   int32_t vec_units;  // 16-byte vectors per row (whole dv)
@@ -121,6 +122,30 @@ __device__ __forceinline__ void store_vec(float* o, const float* acc, bool dense
       *reinterpret_cast<float4*>(o + v) = a;
     }
   }
+}
+
+// One finished output row slice: fp32 (optionally added into a dense table),
+// or rounded once to bf16 (grad_dtype = ML_BF16; half the dV bytes).
+template <int VEC, bool WIDE = true>
+__device__ __forceinline__ void store_out(const SegParams& p, int64_t row, int64_t col,
+                                          const float* acc) {
+  if constexpr (VEC % 8 == 0) {
+    if (p.out_bf16) {
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + col;
+#pragma unroll
+      for (int h = 0; h < VEC; h += 8) {
+        const uint4 u = make_uint4(f2_to_bf2(acc[h], acc[h + 1]), f2_to_bf2(acc[h + 2], acc[h + 3]),
+                                   f2_to_bf2(acc[h + 4], acc[h + 5]), f2_to_bf2(acc[h + 6], acc[h + 7]));
+        asm volatile(
+            "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+            " st.global.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, pol;\n}" ::"l"(o + h),
+            "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+            : "memory");
+      }
+      return;
+    }
+  }
+  store_vec<VEC, WIDE>(p.out + row * p.ldo + col, acc, p.dense != 0);
 }
 
 // Piece of a run longer than kPieceLen: park the partial; pieces are combined
@@ -197,7 +222,7 @@ __device__ __forceinline__ void finish_long_piece(const SegParams& p, const FVec
     float tot[VEC];
     sum_slots<VEC>(p, slice, slice_w, base + g0, gn, 1, act, tot, ttid);
     if (ngroups == 1) {
-      if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
+      if (act) store_out<VEC, false>(p, row, col, tot);
     } else {
       team_sync<SYNC>(team);                 // every thread has read the group's slots
       float* gp = p.partial + (int64_t(slice) * p.nslots_cap + base + g0) * slice_w + ttid * VEC;
@@ -213,7 +238,7 @@ __device__ __forceinline__ void finish_long_piece(const SegParams& p, const FVec
       if (*s_flag) {                   // last group: sum the group partials in order
         __threadfence();
         sum_slots<VEC>(p, slice, slice_w, base, ngroups, GRP, act, tot, ttid);
-        if (act) store_vec<VEC, false>(p.out + int64_t(row) * p.ldo + col, tot, p.dense != 0);
+        if (act) store_out<VEC, false>(p, row, col, tot);
       }
     }
   }
@@ -346,7 +371,7 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
         const int32_t row = p.dense ? s_key[k] : rr;
         const float* accf = reinterpret_cast<const float*>(acc);
         if (re - rb <= L) {
-          if (act) store_vec<VEC>(p.out + int64_t(row) * p.ldo + col, accf, p.dense != 0);
+          if (act) store_out<VEC>(p, row, col, accf);
         } else {
           const int32_t i = int32_t(c0) + k;
           const int32_t ps = rb + ((i - rb) / L) * L;
@@ -644,7 +669,7 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
           const int32_t rr = M[k].rr, rb = M[k].rb, re = M[k].re;
           const float* accf = reinterpret_cast<const float*>(acc);
           if (re - rb <= L) {
-            if (act) store_vec<TV>(p.out + int64_t(rr) * p.ldo + col, accf, false);
+            if (act) store_out<TV>(p, rr, col, accf);
           } else {
             const int32_t i = int32_t(c0) + k;
             const int32_t ps = rb + ((i - rb) / L) * L;
@@ -784,6 +809,9 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   p.V = static_cast<const char*>(a.V); p.ldv_bytes = a.ldv * es; p.v_col0 = a.v_col0;
   p.dw_part = a.dw_part;
   p.out = a.out; p.ldo = a.ldo; p.dense = a.dense_accumulate ? 1 : 0;
+  p.out_bf16 = a.out_bf16 ? 1 : 0;
+  if (a.out_bf16 && (a.dense_accumulate || a.dtype != ML_BF16))
+    return fail(ML_ERR_UNSUPPORTED, "segreduce: bf16 output needs bf16 sources, no dense accumulate");
   p.partial = a.partial; p.counters = a.counters; p.nslots_cap = nslots_cap(a.P);
   p.ticket = a.counters + 2 * int64_t(ns) * p.nslots_cap;
   p.vec_units = int32_t(vu);

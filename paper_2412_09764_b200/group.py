@@ -58,10 +58,11 @@ class CudaLocal:
 
     grad_dtype = torch.float32
 
-    def __init__(self):
+    def __init__(self, dV_dtype=torch.float32):
         from . import ops
         self.ops = ops
         self._side = None
+        self.dV_dtype = dV_dtype        # storage of the compact value gradient (memlayer.h)
 
     def empty(self, shape, dtype, like):
         return torch.empty(shape, dtype=dtype, device=like.device)
@@ -119,7 +120,8 @@ class CudaLocal:
         return self.ops.embbag_fwd(V, idx, w)
 
     def embbag_bwd(self, V, idx, w, dy, state=None):
-        rows, dV, U, dw = self.ops.embbag_bwd(V, idx, w, dy, sync=False, state=state)
+        rows, dV, U, dw = self.ops.embbag_bwd(V, idx, w, dy, sync=False, state=state,
+                                              grad_dtype=self.dV_dtype)
         return rows, dV, U, dw
 
     def pkm_topk_bwd(self, q, K1, K2, idx, w, dw, dK1, dK2):

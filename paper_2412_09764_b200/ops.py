@@ -148,8 +148,8 @@ def pkm_topk_bwd(q, K1, K2, idx, w, dw, dK1=None, dK2=None, qk_norm=False):
 
 
 # ------------------------------------------------------------- EmbeddingBag
-def bag_shape(V, idx):
-    return BagShape(V.shape[0], V.shape[1], idx.shape[0], idx.shape[1], _dt(V))
+def bag_shape(V, idx, grad_dtype=torch.float32):
+    return BagShape(V.shape[0], V.shape[1], idx.shape[0], idx.shape[1], _dt(V), _DT[grad_dtype])
 
 
 def embbag_fwd(V, idx, w, gate_pre=None, return_ungated=False):
@@ -162,15 +162,16 @@ def embbag_fwd(V, idx, w, gate_pre=None, return_ungated=False):
     return (y, yu) if return_ungated else y
 
 
-def embbag_bwd(V, idx, w, dy, sync=True, state=None):
+def embbag_bwd(V, idx, w, dy, sync=True, state=None, grad_dtype=torch.float32):
     """"reverse_indices" backward.  Returns rows [U] int32 (ascending),
-    dV [U, dv] fp32, dw [T,B] fp32 (sync=True trims to U on the host);
-    with sync=False returns the capacity-sized buffers and the device U.
+    dV [U, dv] (grad_dtype: fp32, or bf16 for a bf16 table), dw [T,B] fp32
+    (sync=True trims to U on the host); with sync=False returns the
+    capacity-sized buffers and the device U.
     state: from embbag_bwd_prepare(N, dv, idx) (skips the sort)."""
-    sh = bag_shape(V, idx)
+    sh = bag_shape(V, idx, grad_dtype)
     P = idx.numel()
     rows = torch.empty(P, dtype=torch.int32, device=V.device)
-    dV = torch.empty((P, V.shape[1]), dtype=torch.float32, device=V.device)
+    dV = torch.empty((P, V.shape[1]), dtype=grad_dtype, device=V.device)
     U = torch.empty(1, dtype=torch.int32, device=V.device)
     dw = torch.empty(idx.shape, dtype=torch.float32, device=V.device)
     n = _size(lib().embbag_bwd_workspace, sh)
@@ -241,7 +242,7 @@ def sparse_adam(V, rows, dV, U, m, v, steps, lr, beta1=0.9, beta2=0.999, eps=1e-
                 weight_decay=0.0, V_master=None):
     """Lazy row-wise Adam(W) on the touched value rows (in place); rows/dV/U
     as returned by embbag_bwd(sync=False) or memory_layer_bwd."""
-    sh = BagShape(V.shape[0], V.shape[1], rows.shape[0], 1, _dt(V))
+    sh = BagShape(V.shape[0], V.shape[1], rows.shape[0], 1, _dt(V), _dt(dV))
     hp = _lib.AdamParams(lr, beta1, beta2, eps, weight_decay)
     check(lib().ml_sparse_adam(C.byref(sh), _p(rows), _p(dV), _p(U), _p(V), _p(V_master), _p(m),
                                _p(v), _p(steps), C.byref(hp), _stream()))
@@ -249,17 +250,17 @@ def sparse_adam(V, rows, dV, U, m, v, steps, lr, beta1=0.9, beta2=0.999, eps=1e-
 
 
 def embbag_grad_apply(V, idx, rows, dV, U, dV_dense):
-    sh = bag_shape(V, idx)
+    sh = bag_shape(V, idx, dV.dtype)
     check(lib().embbag_grad_apply(C.byref(sh), _p(rows), _p(dV), _p(U), _p(dV_dense), _stream()))
     return dV_dense
 
 
 # ------------------------------------------------------------ memory layer
-def layer_shape(x, q, K1, V, k, gated, qk_norm=False):
+def layer_shape(x, q, K1, V, k, gated, qk_norm=False, grad_dtype=torch.float32):
     T, H, Dk = q.shape
     D = x.shape[1] if (gated and x is not None) else V.shape[1]
     return LayerShape(PkmShape(T, H, K1.shape[1], Dk, k, _dt(q), 1 if qk_norm else 0), V.shape[0],
-                      V.shape[1], D, 1 if gated else 0)
+                      V.shape[1], D, 1 if gated else 0, _DT[grad_dtype])
 
 
 def memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, qk_norm=False, keep_state=True):
@@ -297,11 +298,12 @@ class LayerGrads(dict):
 
 
 def memory_layer_bwd(dout, x, q, K1, K2, V, W1, W2, saved, dK1=None, dK2=None, want_dw=False,
-                     bufs=None):
+                     bufs=None, dV_dtype=torch.float32):
     """Backward of memory_layer_fwd.  dK1/dK2 accumulate (zeros if None).
-    dV is compact: rows[:U], dV[:U] (capacity-sized buffers + device U)."""
+    dV is compact: rows[:U], dV[:U] (capacity-sized buffers + device U),
+    stored as dV_dtype (fp32, or bf16 for a bf16 table)."""
     k, gated = saved["k"], saved["gated"]
-    sh = layer_shape(x, q, K1, V, k, gated, saved.get("qk_norm", False))
+    sh = layer_shape(x, q, K1, V, k, gated, saved.get("qk_norm", False), dV_dtype)
     T, H = q.shape[0], q.shape[1]
     dev = q.device
     P = T * H * k
@@ -318,7 +320,7 @@ def memory_layer_bwd(dout, x, q, K1, K2, V, W1, W2, saved, dK1=None, dK2=None, w
     if dK2 is None:
         dK2 = torch.zeros(K2.shape, dtype=torch.float32, device=dev)
     rows = buf("rows", (P,), torch.int32)
-    dV = buf("dV", (P, V.shape[1]), torch.float32)
+    dV = buf("dV", (P, V.shape[1]), dV_dtype)
     U = buf("U", (1,), torch.int32)
     dx = buf("dx", x.shape, V.dtype) if gated else None
     dW1 = buf("dW1", W1.shape, torch.float32) if gated else None

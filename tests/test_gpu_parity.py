@@ -567,3 +567,30 @@ def test_out_of_range_index_backward_row0_weight0():
     assert_close(host(dw), rdw, TOL["f32"], "dw")
     y = o.embbag_fwd(dev(V), dev(idx), dev(w))
     assert_close(host(y), obag.embbag_fwd(V, ie, we), TOL["f32"], "y")
+
+
+@pytest.mark.parametrize("N,dv,T,B", [(4096, 256, 300, 64), (1 << 16, 2048, 150, 128),
+                                      (8192, 4096, 40, 128), (2000, 512, 257, 32)])
+def test_bf16_value_gradient_is_rounded_fp32(N, dv, T, B):
+    """grad_dtype = bf16 (memlayer.h): every dV element is the fp32 sum of the
+    fp32 path rounded once to bf16 -> bit-identical to rounding the fp32
+    result; rows, U and dw are unchanged.  Covers both segmented kernels
+    (row slices < 2 KiB and >= 2 KiB), long runs (Zipf) and the consumers
+    (embbag_grad_apply, sparse Adam) of a bf16 dV."""
+    o = ops()
+    V = gen.tensor(22, "V", (N, dv), dtype="bf16")
+    idx = streams.zipf_indices(22, T, B, N, 1.1)
+    w = streams.softmax_free_weights(22, T, B)
+    dy = gen.tensor(22, "dout", (T, dv), dtype="bf16")
+    Vd, idd, wd, dyd = dev(V, "bf16"), dev(idx), dev(w), dev(dy, "bf16")
+    r32, d32, U32, w32 = o.embbag_bwd(Vd, idd, wd, dyd, sync=False)
+    r16, d16, U16, w16 = o.embbag_bwd(Vd, idd, wd, dyd, sync=False, grad_dtype=torch.bfloat16)
+    u = int(U32.item())
+    assert int(U16.item()) == u and d16.dtype == torch.bfloat16
+    assert torch.equal(r16[:u], r32[:u]) and torch.equal(w16, w32)
+    assert torch.equal(d16[:u], d32[:u].to(torch.bfloat16))
+    dense32 = torch.zeros((N, dv), dtype=torch.float32, device="cuda")
+    dense16 = torch.zeros((N, dv), dtype=torch.float32, device="cuda")
+    o.embbag_grad_apply(Vd, idd, r32, d32[:, :].to(torch.bfloat16).contiguous(), U32, dense32)
+    o.embbag_grad_apply(Vd, idd, r16, d16, U16, dense16)
+    assert torch.equal(dense32, dense16)
