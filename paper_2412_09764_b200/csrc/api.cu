@@ -177,9 +177,21 @@ static mlStatus qk_compute(const mlPkmShape& s, const void* q, const void* K1, c
   return ML_OK;
 }
 
-struct PkmFwdBufs { float* scores; int32_t* hI; float* hs; QkBufs qk; };
+struct PkmFwdBufs {
+  float* scores = nullptr; int32_t* hI = nullptr; float* hs = nullptr; QkBufs qk;
+  // fused scoring + filter: candidate lists, their lengths, fallback row list
+  uint64_t* cand = nullptr; int32_t* cnt = nullptr; int32_t* fail_rows = nullptr;
+  int32_t* fail_n = nullptr;
+};
 static void pkm_fwd_carve(Carver& c, const mlPkmShape& s, PkmFwdBufs& b) {
   const int64_t TH = int64_t(s.T) * s.H;
+  if (pkm_select_tc_eligible(s)) {
+    b.cand = c.take<uint64_t>(TH * 2 * pkm_select_cap());
+    b.cnt = c.take<int32_t>(TH * 2);
+    b.fail_rows = c.take<int32_t>(TH * 2);
+    b.fail_n = c.take<int32_t>(1);
+    return;
+  }
   b.scores = c.take<float>(TH * 2 * s.S);
   b.hI = c.take<int32_t>(TH * 2 * s.k);
   b.hs = c.take<float>(TH * 2 * s.k);
@@ -246,6 +258,11 @@ static void bag_bwd_carve(Carver& c, const mlBagShape& s, BagBwdBufs& b) {
 static mlStatus pkm_fwd_core(const mlPkmShape& s, const void* q, const void* K1, const void* K2,
                              int32_t* idx, float* w, float* score, PkmFwdBufs& b, cudaStream_t st) {
   if (s.T == 0) return ML_OK;
+  if (b.cand) {   // fused: scores never leave the SM (pkm_tc.cu)
+    ML_TRY(launch_pkm_select_tc(s, q, K1, K2, b.cand, b.cnt, b.fail_rows, b.fail_n, st));
+    ML_TRY(launch_cand_fallback(s, q, K1, K2, b.cand, b.cnt, b.fail_rows, b.fail_n, st));
+    return launch_combine_cand(s, b.cand, b.cnt, idx, w, score, st);
+  }
   QkNorm qn;
   ML_TRY(qk_compute(s, q, K1, K2, b.qk, &qn, st));
   ML_TRY(launch_pkm_scores(s, q, K1, K2, b.scores, st));

@@ -118,6 +118,24 @@ mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1,
 bool pkm_scores_tc_eligible(const mlPkmShape& sh);
 mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
                               float* scores, cudaStream_t s);
+// fused scoring + half top-k filter (bf16, no qk-norm, S % 256 == 0, S >= 512):
+// per (t, h, half) row a candidate list cand[row][pkm_select_cap()] of 64-bit
+// keys (ord(score) << 32 | ~a) holding the row's k best, cnt[row] its length
+// or -1; rows with -1 are listed in fail_rows[0 .. *fail_n) for the exact
+// fallback (launch_cand_fallback).
+bool pkm_select_tc_eligible(const mlPkmShape& sh);
+int pkm_select_cap();
+mlStatus launch_pkm_select_tc(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
+                              uint64_t* cand, int32_t* cnt, int32_t* fail_rows, int32_t* fail_n,
+                              cudaStream_t s);
+// exact top-k of the listed rows (scores recomputed in fp32), written as k
+// candidates (cnt = k)
+mlStatus launch_cand_fallback(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
+                              uint64_t* cand, int32_t* cnt, const int32_t* fail_rows,
+                              const int32_t* fail_n, cudaStream_t s);
+// exact half top-k of each row's candidates, then the combine + softmax
+mlStatus launch_combine_cand(const mlPkmShape& sh, const uint64_t* cand, const int32_t* cnt,
+                             int32_t* idx, float* w, float* score, cudaStream_t s);
 mlStatus launch_half_topk(const mlPkmShape& sh, const float* scores, int32_t* hI,
                           float* hs, const QkNorm& qn, cudaStream_t s);
 mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const float* hs,

@@ -538,31 +538,18 @@ __device__ __forceinline__ bool combine_fast(const float* s1p, const int32_t* i1
   return true;
 }
 
-// one warp per (t, h): combine the two half lists (k*k Cartesian sums), softmax
-__global__ void __launch_bounds__(256) combine_kernel(const int32_t* hI, const float* hs,
-                                                      int64_t TH, int S, int k, int32_t* idx,
-                                                      float* w, float* score) {
-  __shared__ TopkSmem s_sm[8];
-  __shared__ float s_s1[8][32];
-  __shared__ int32_t s_i1[8][32];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t th = int64_t(blockIdx.x) * 8 + wid;
-  if (th >= TH) return;
-  TopkSmem& sm = s_sm[wid];
-  float s2 = 0.f;
-  uint32_t i2 = 0;
-  if (lane < k) {
-    s_s1[wid][lane] = hs[(th * 2 + 0) * k + lane];
-    s_i1[wid][lane] = hI[(th * 2 + 0) * k + lane];
-    s2 = hs[(th * 2 + 1) * k + lane];
-    i2 = uint32_t(hI[(th * 2 + 1) * k + lane]);
-  }
-  __syncwarp();
+// The combine of one (t, h) given its two half lists: s1/i1 (descending, in
+// this warp's shared memory) and this lane's entry of the second list
+// (lane j < k: s2[j], i2[j]); k*k Cartesian sums, exact top-k, softmax.
+__device__ __forceinline__ void combine_lists(float* s1p, int32_t* i1p, float* s2p, int32_t* i2p,
+                                              float s2, uint32_t i2, int S, int k, TopkSmem& sm,
+                                              int64_t th, int32_t* idx, float* w, float* score) {
+  const int lane = threadIdx.x & 31;
   // lane j owns column j of the k x k grid: c[i][j] = s1[i] + s2[j]
-  if (combine_fast(s_s1[wid], s_i1[wid], s2, i2, S, k, sm.cand, sm.sel, th, idx, w, score)) return;
+  if (combine_fast(s1p, i1p, s2, i2, S, k, sm.cand, sm.sel, th, idx, w, score)) return;
   __syncwarp();
   auto key_of = [&](int i) {
-    return make_key(s_s1[wid][i] + s2, uint32_t(s_i1[wid][i]) * uint32_t(S) + i2);
+    return make_key(s1p[i] + s2, uint32_t(i1p[i]) * uint32_t(S) + i2);
   };
   uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
   if (lane < k)
@@ -578,15 +565,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* hI, const f
   if (count <= kCandCap) {
     key = select_cand(count, k, sm);
   } else {
-    const float* s1p = s_s1[wid];
-    const int32_t* i1p = s_i1[wid];
-    __shared__ float s_s2[8][32];
-    __shared__ int32_t s_i2[8][32];
-    s_s2[wid][lane] = s2;
-    s_i2[wid][lane] = int32_t(i2);
+    s2p[lane] = s2;
+    i2p[lane] = int32_t(i2);
     __syncwarp();
-    const float* s2p = s_s2[wid];
-    const int32_t* i2p = s_i2[wid];
     auto gen = [=](int e) {
       const int i = e / k, j = e - (e / k) * k;
       return make_key(s1p[i] + s2p[j], uint32_t(i1p[i]) * uint32_t(S) + uint32_t(i2p[j]));
@@ -603,6 +584,119 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* hI, const f
     idx[th * k + lane] = int32_t(key_id(key));
     w[th * k + lane] = ex / sum;
     if (score) score[th * k + lane] = sc;
+  }
+}
+
+// one warp per (t, h): combine the two half lists (k*k Cartesian sums), softmax
+__global__ void __launch_bounds__(256) combine_kernel(const int32_t* hI, const float* hs,
+                                                      int64_t TH, int S, int k, int32_t* idx,
+                                                      float* w, float* score) {
+  __shared__ TopkSmem s_sm[8];
+  __shared__ float s_s1[8][32], s_s2[8][32];
+  __shared__ int32_t s_i1[8][32], s_i2[8][32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t th = int64_t(blockIdx.x) * 8 + wid;
+  if (th >= TH) return;
+  float s2 = 0.f;
+  uint32_t i2 = 0;
+  if (lane < k) {
+    s_s1[wid][lane] = hs[(th * 2 + 0) * k + lane];
+    s_i1[wid][lane] = hI[(th * 2 + 0) * k + lane];
+    s2 = hs[(th * 2 + 1) * k + lane];
+    i2 = uint32_t(hI[(th * 2 + 1) * k + lane]);
+  }
+  __syncwarp();
+  combine_lists(s_s1[wid], s_i1[wid], s_s2[wid], s_i2[wid], s2, i2, S, k, s_sm[wid], th, idx, w,
+                score);
+}
+
+// The k best (descending) of a row's n <= 96 unique candidate keys, by
+// counting ranks: lane j < k returns the j-th largest.
+__device__ __forceinline__ uint64_t cand_topk(const uint64_t* keys, int n, int k, TopkSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  uint64_t* c = sm.cand;
+  for (int e = lane; e < n; e += 32) c[e] = keys[e];
+  if ((n & 1) != 0 && lane == 0) c[n] = 0ull;    // pad: ranks nothing
+  __syncwarp();
+  uint64_t mk[3];
+  int rk[3] = {0, 0, 0};
+#pragma unroll
+  for (int r = 0; r < 3; ++r) mk[r] = (lane + 32 * r < n) ? c[lane + 32 * r] : ~0ull;
+  const int pairs = (n + 1) >> 1;
+  for (int l = 0; l < pairs; ++l) {
+    const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(c)[l];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) rk[r] += (kk.x > mk[r] ? 1 : 0) + (kk.y > mk[r] ? 1 : 0);
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    if (lane + 32 * r < n && rk[r] < k) sm.sel[rk[r]] = mk[r];
+  __syncwarp();
+  const uint64_t key = lane < k ? sm.sel[lane] : 0ull;
+  __syncwarp();
+  return key;
+}
+
+// one warp per (t, h): exact half top-k of each half row's candidates (the
+// fused scoring kernel's lists), then the combine + softmax
+__global__ void __launch_bounds__(256) combine_cand_kernel(const uint64_t* cand, const int32_t* cnt,
+                                                           int cap, int64_t TH, int S, int k,
+                                                           int32_t* idx, float* w, float* score) {
+  __shared__ TopkSmem s_sm[8];
+  __shared__ float s_s1[8][32], s_s2[8][32];
+  __shared__ int32_t s_i1[8][32], s_i2[8][32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t th = int64_t(blockIdx.x) * 8 + wid;
+  if (th >= TH) return;
+  TopkSmem& sm = s_sm[wid];
+  const int n1 = cnt[th * 2 + 0], n2 = cnt[th * 2 + 1];
+  const uint64_t k1 = cand_topk(cand + (th * 2 + 0) * cap, n1, k, sm);
+  const uint64_t k2 = cand_topk(cand + (th * 2 + 1) * cap, n2, k, sm);
+  if (lane < k) {
+    s_s1[wid][lane] = key_score(k1);
+    s_i1[wid][lane] = int32_t(key_id(k1));
+  }
+  __syncwarp();
+  combine_lists(s_s1[wid], s_i1[wid], s_s2[wid], s_i2[wid], lane < k ? key_score(k2) : 0.f,
+                lane < k ? key_id(k2) : 0u, S, k, sm, th, idx, w, score);
+}
+
+// Exact fallback for rows whose candidate list overflowed (heavy ties): one
+// warp recomputes the row's S scores (fp32 FMA over the bf16 inputs) into
+// shared memory and selects its k best with the radix select.
+__global__ void __launch_bounds__(32) cand_fallback_kernel(const __nv_bfloat16* q,
+                                                           const __nv_bfloat16* K1,
+                                                           const __nv_bfloat16* K2, int H, int S,
+                                                           int Dk, int k, uint64_t* cand,
+                                                           int32_t* cnt, int cap,
+                                                           const int32_t* fail_rows,
+                                                           const int32_t* fail_n) {
+  extern __shared__ float s_row[];      // [S]
+  __shared__ TopkSmem sm;
+  const int lane = threadIdx.x & 31;
+  const int Dh = Dk / 2;
+  const int nf = *fail_n;
+  for (int f = blockIdx.x; f < nf; f += gridDim.x) {
+    const int64_t row = fail_rows[f];
+    const int64_t th = row >> 1;
+    const int half = int(row & 1);
+    const int h = int(th % H);
+    const __nv_bfloat16* qh = q + th * Dk + half * Dh;
+    const __nv_bfloat16* K = (half ? K2 : K1) + int64_t(h) * S * Dh;
+    for (int a = 0; a < S; ++a) {
+      float part = 0.f;
+      for (int i = lane; i < Dh; i += 32)
+        part = fmaf(__bfloat162float(qh[i]), __bfloat162float(K[int64_t(a) * Dh + i]), part);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+      if (lane == 0) s_row[a] = part;
+    }
+    __syncwarp();
+    auto gen = [](int e) { return make_key(s_row[e], uint32_t(e)); };
+    const uint64_t key = warp_topk(gen, S, k, sm.hist, sm.sel);
+    if (lane < k) cand[row * cap + lane] = key;
+    if (lane == 0) cnt[row] = k;
+    __syncwarp();
   }
 }
 
@@ -728,6 +822,35 @@ mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const f
   const int64_t TH = int64_t(sh.T) * sh.H;
   if (TH <= 0) return ML_OK;
   combine_kernel<<<unsigned((TH + 7) / 8), 256, 0, s>>>(hI, hs, TH, sh.S, sh.k, idx, w, score);
+  ML_LAUNCH_CHECK("combine_softmax");
+  return ML_OK;
+}
+
+mlStatus launch_cand_fallback(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
+                              uint64_t* cand, int32_t* cnt, const int32_t* fail_rows,
+                              const int32_t* fail_n, cudaStream_t s) {
+  const size_t smem = size_t(sh.S) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    ML_CUDA_TRY(cudaFuncSetAttribute(cand_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(16384 * sizeof(float))));
+    attr = true;
+  }
+  if (sh.S > 16384) return fail(ML_ERR_UNSUPPORTED, "cand_fallback: S > 16384");
+  cand_fallback_kernel<<<unsigned(num_sms() * 4), 32, smem, s>>>(
+      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(K1),
+      static_cast<const __nv_bfloat16*>(K2), sh.H, sh.S, sh.Dk, sh.k, cand, cnt,
+      pkm_select_cap(), fail_rows, fail_n);
+  ML_LAUNCH_CHECK("pkm_cand_fallback");
+  return ML_OK;
+}
+
+mlStatus launch_combine_cand(const mlPkmShape& sh, const uint64_t* cand, const int32_t* cnt,
+                             int32_t* idx, float* w, float* score, cudaStream_t s) {
+  const int64_t TH = int64_t(sh.T) * sh.H;
+  if (TH <= 0) return ML_OK;
+  combine_cand_kernel<<<unsigned((TH + 7) / 8), 256, 0, s>>>(cand, cnt, pkm_select_cap(), TH, sh.S,
+                                                             sh.k, idx, w, score);
   ML_LAUNCH_CHECK("combine_softmax");
   return ML_OK;
 }

@@ -20,6 +20,7 @@
 
 #include <cuda.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 
@@ -129,6 +130,73 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ---------------- TMA producer (one thread): the 128-token query tile and the
+// BN-key half-key tile of every K-chunk of every subtile, STAGES-deep ring
+template <int STAGES>
+__device__ __forceinline__ void tc_producer(const CUtensorMap* tmQ, const CUtensorMap* tmK1,
+                                            const CUtensorMap* tmK2, uint8_t* sA, uint8_t* sB,
+                                            uint64_t* full, uint64_t* empty, uint32_t bytes_a,
+                                            uint32_t bytes_b, const TcParams& p) {
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+    const int mt = t % p.m_tiles, hh = t / p.m_tiles;
+    const int h = hh >> 1, half = hh & 1;
+    const CUtensorMap* tmK = half ? tmK2 : tmK1;
+    for (int n = 0; n < p.n_sub; ++n) {
+      for (int kc = 0; kc < p.k_chunks; ++kc) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], bytes_a + bytes_b);
+        tma_load_2d(sA + stage * bytes_a, tmQ, &full[stage], h * p.Dk + half * p.Dh + kc * kBK,
+                    mt * kBM);
+        tma_load_2d(sB + stage * bytes_b, tmK, &full[stage], kc * kBK, h * p.S + n * p.BN);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  }
+}
+
+// ---------------- MMA issuer (one thread): D[acc] = Q_tile x K_tile^T per
+// subtile into a double-buffered TMEM accumulator; commits free smem stages
+template <int STAGES>
+__device__ __forceinline__ void tc_mma(uint8_t* sA, uint8_t* sB, uint64_t* full, uint64_t* empty,
+                                       uint64_t* tfull, uint64_t* tempty, uint32_t bytes_a,
+                                       uint32_t bytes_b, uint32_t tmem_base, const TcParams& p) {
+  int stage = 0;
+  uint32_t phase = 0;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+    for (int n = 0; n < p.n_sub; ++n) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tmem_base + uint32_t(acc * p.BN);
+      for (int kc = 0; kc < p.k_chunks; ++kc) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t ad = sw128_desc(smem_u32(sA + stage * bytes_a));
+        const uint64_t bd = sw128_desc(smem_u32(sB + stage * bytes_b));
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)  // 16 bf16 = 32 bytes = 2 descriptor units
+          umma_f16(dcol, ad + 2 * k, bd + 2 * k, p.idesc, (kc | k) != 0 ? 1u : 0u);
+        umma_commit(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(&tfull[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     pkm_scores_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                          const __grid_constant__ CUtensorMap tmK1,
@@ -179,61 +247,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
-        const int mt = t % p.m_tiles, hh = t / p.m_tiles;
-        const int h = hh >> 1, half = hh & 1;
-        const CUtensorMap* tmK = half ? &tmK2 : &tmK1;
-        for (int n = 0; n < p.n_sub; ++n) {
-          for (int kc = 0; kc < p.k_chunks; ++kc) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], bytes_a + bytes_b);
-            tma_load_2d(sA + stage * bytes_a, &tmQ, &full[stage], h * p.Dk + half * p.Dh + kc * kBK,
-                        mt * kBM);
-            tma_load_2d(sB + stage * bytes_b, tmK, &full[stage], kc * kBK, h * p.S + n * p.BN);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
-      }
-    }
+    if (lane == 0) tc_producer<kStages>(&tmQ, &tmK1, &tmK2, sA, sB, full, empty, bytes_a, bytes_b, p);
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
-        for (int n = 0; n < p.n_sub; ++n) {
-          mbar_wait(&tempty[acc], acc_phase ^ 1);
-          tc_fence_after();
-          const uint32_t dcol = tmem_base + uint32_t(acc * p.BN);
-          for (int kc = 0; kc < p.k_chunks; ++kc) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint64_t ad = sw128_desc(smem_u32(sA + stage * bytes_a));
-            const uint64_t bd = sw128_desc(smem_u32(sB + stage * bytes_b));
-#pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)  // 16 bf16 = 32 bytes = 2 descriptor units
-              umma_f16(dcol, ad + 2 * k, bd + 2 * k, p.idesc, (kc | k) != 0 ? 1u : 0u);
-            umma_commit(&empty[stage]);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-          umma_commit(&tfull[acc]);
-          if (++acc == 2) {
-            acc = 0;
-            acc_phase ^= 1;
-          }
-        }
-      }
-    }
+    if (lane == 0) tc_mma<kStages>(sA, sB, full, empty, tfull, tempty, bytes_a, bytes_b, tmem_base, p);
   } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> fp32 scores
     const int q4 = warp & 3;
     int acc = 0;
@@ -279,6 +295,250 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(p.tmem_cols));
+  }
+}
+
+
+// ============================================================================
+// Scoring fused with the half top-k filter (no score matrix in HBM).
+//
+// The epilogue thread that owns token row r of a 128-token tile (tcgen05.ld
+// 32x32b: thread = TMEM lane = row) sees every score of its (t, h, half) row,
+// S / BN subtiles of BN = 256 keys, and keeps only a small candidate set that
+// provably contains the row's k best ("the top-k indices ... obtained
+// from the respective key sets"; ties resolved later by (score, lower index)):
+//  * subtile 0 is read twice from TMEM: first for the row's mean / standard
+//    deviation, which place a ladder of 32 levels L_j = L_0 + j*delta, then for
+//    a per-thread histogram of its 256 scores over those levels;
+//  * the threshold theta is the highest level with at least k scores counted
+//    at or above it -- a valid lower bound of the row's k-th largest score
+//    whatever the statistics were (they only place the levels; each counted
+//    score is checked against its level with the exact comparison used by the
+//    filter), and it only rises;
+//  * every subtile is filtered with v >= theta; survivors (score, key index)
+//    go to a per-thread list in shared memory and into the histogram, after
+//    which theta is raised; the list is compacted (entries < theta dropped)
+//    when it nears its capacity and at the end of the row.
+// All top-k scores of the row are >= the final theta >= the theta in force
+// when they were seen, so all of them are candidates.  The row's candidates
+// (typically k + a bin, ~40-50) are written as 64-bit keys; rows whose list
+// overflowed are listed for an exact fallback.  The selection among the
+// candidates happens in the combine kernel (pkm.cu).
+constexpr int kSelStages = 3;     // ring depth (shared memory goes to the candidate lists)
+constexpr int kCand = 88;         // candidate list capacity per row
+constexpr int kLevels = 32;       // threshold ladder
+constexpr int kEpi = 128;         // epilogue threads (one per tile row)
+
+struct SelOut {
+  uint64_t* cand;      // [rows][kCand] keys (ord(score) << 32 | ~a), first cnt valid
+  int32_t* cnt;        // [rows]: candidates, or -1 (overflow: exact fallback)
+  int32_t* fail_rows;  // list of rows needing the fallback
+  int32_t* fail_n;     // its length (zeroed before the launch)
+  float z0, dz;        // ladder: L_0 = mean + z0 sd, delta = dz sd
+  int k;
+};
+
+__device__ __forceinline__ uint64_t sel_key(float v, uint32_t a) {
+  return (uint64_t(ord_f32(v)) << 32) | uint64_t(0xFFFFFFFFu - a);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    pkm_scores_select_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                const __grid_constant__ CUtensorMap tmK1,
+                                const __grid_constant__ CUtensorMap tmK2, TcParams p, SelOut o) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t bytes_a = kBM * kBK * 2;
+  const uint32_t bytes_b = uint32_t(p.BN) * kBK * 2;
+  uint8_t* sA = base;
+  uint8_t* sB = base + kSelStages * bytes_a;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kSelStages * bytes_b);
+  uint64_t* empty = full + kSelStages;
+  uint64_t* tfull = empty + kSelStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // per-row lists, [slot][row] so that every lane always hits its own bank
+  float* c_val = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
+  uint16_t* c_key = reinterpret_cast<uint16_t*>(c_val + kCand * kEpi);
+  uint16_t* hist = c_key + kCand * kEpi;                      // [kLevels + 1][row]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSelStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK1)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK2)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) tc_producer<kSelStages>(&tmQ, &tmK1, &tmK2, sA, sB, full, empty, bytes_a, bytes_b, p);
+  } else if (warp == 1) {
+    if (lane == 0) tc_mma<kSelStages>(sA, sB, full, empty, tfull, tempty, bytes_a, bytes_b, tmem_base, p);
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    const int er = q4 * 32 + lane;          // this thread's tile row (= TMEM lane)
+    float* cv = c_val + er;                 // cv[e * kEpi]: e-th candidate score
+    uint16_t* ck = c_key + er;
+    uint16_t* hs = hist + er;               // hs[b * kEpi]
+    const int H2 = 2 * p.H;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      const int mt = t % p.m_tiles, hh = t / p.m_tiles;
+      const int tok = mt * kBM + er;
+      const bool valid = tok < p.T;
+      int cnt = 0, counted = 0;             // list length; entries already in the histogram
+      bool ovf = false;
+      float theta = -INFINITY, L0 = 0.f, delta = 1.f, inv = 1.f;
+#pragma unroll 1
+      for (int b = 0; b <= kLevels; ++b) hs[b * kEpi] = 0;
+      // the bin of v: the highest j with v >= L_j (exact check), -1 below L_0
+      auto bin_of = [&](float v) {
+        const float tt = fminf(fmaxf((v - L0) * inv, -1.f), float(kLevels - 1));
+        int j = int(floorf(tt));
+        if (j >= 0 && v < fmaf(float(j), delta, L0)) --j;
+        return j + 1;
+      };
+      auto raise_theta = [&]() {          // highest level with >= k counted at or above it
+        int c = 0;
+#pragma unroll 1
+        for (int b = kLevels; b >= 1; --b) {
+          c += hs[b * kEpi];
+          if (c >= o.k) {
+            theta = fmaxf(theta, fmaf(float(b - 1), delta, L0));
+            break;
+          }
+        }
+      };
+      auto compact = [&]() {              // drop entries below theta (order kept)
+        int w = 0, cw = 0;
+#pragma unroll 1
+        for (int e = 0; e < cnt; ++e) {
+          const float v = cv[e * kEpi];
+          if (v >= theta) {
+            cv[w * kEpi] = v;
+            ck[w * kEpi] = ck[e * kEpi];
+            cw += e < counted ? 1 : 0;
+            ++w;
+          }
+        }
+        cnt = w;
+        counted = cw;
+      };
+      for (int n = 0; n < p.n_sub; ++n) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t ta = tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN);
+        if (n == 0) {
+          // pass 1: the ladder from the subtile's mean / sd; pass 2: its histogram
+          float sum = 0.f, sq = 0.f;
+          for (int c0 = 0; c0 < p.BN; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(ta + uint32_t(c0), r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float v = __uint_as_float(r[i]);
+              sum += v;
+              sq = fmaf(v, v, sq);
+            }
+          }
+          const float mu = sum / float(p.BN);
+          const float sd = sqrtf(fmaxf(sq / float(p.BN) - mu * mu, 0.f));
+          delta = fmaxf(sd * o.dz, fmaxf(fabsf(mu), 1e-20f) * 1e-6f);
+          inv = 1.f / delta;
+          L0 = fmaf(o.z0, sd, mu);
+          for (int c0 = 0; c0 < p.BN; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(ta + uint32_t(c0), r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int b = bin_of(__uint_as_float(r[i]));
+              hs[b * kEpi] = uint16_t(hs[b * kEpi] + 1);
+            }
+          }
+          raise_theta();
+        }
+        // filter
+        const int col_base = n * p.BN;
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          if (__any_sync(0xffffffffu, cnt > kCand - 32)) {
+            if (cnt > kCand - 32) {
+              compact();
+              if (cnt > kCand - 32) ovf = true;
+            }
+          }
+          uint32_t r[32];
+          tmem_ld32(ta + uint32_t(c0), r);
+          const float th = (ovf || !valid) ? INFINITY : theta;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float v = __uint_as_float(r[i]);
+            if (v >= th) {
+              cv[cnt * kEpi] = v;
+              ck[cnt * kEpi] = uint16_t(col_base + c0 + i);
+              ++cnt;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);          // the accumulator is free for the next subtile
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        if (n == 0) {
+          counted = cnt;                    // subtile 0 is in the histogram already
+        } else {
+#pragma unroll 1
+          for (int e = counted; e < cnt; ++e) {
+            const int b = bin_of(cv[e * kEpi]);
+            hs[b * kEpi] = uint16_t(hs[b * kEpi] + 1);
+          }
+          counted = cnt;
+        }
+        raise_theta();
+      }
+      compact();
+      if (valid) {
+        const int64_t row = int64_t(tok) * H2 + hh;
+        if (ovf || cnt < o.k) {
+          o.cnt[row] = -1;
+          o.fail_rows[atomicAdd(o.fail_n, 1)] = int32_t(row);
+        } else {
+          uint64_t* dst = o.cand + row * kCand;
+#pragma unroll 1
+          for (int e = 0; e < cnt; ++e) dst[e] = sel_key(cv[e * kEpi], ck[e * kEpi]);
+          o.cnt[row] = cnt;
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -390,4 +650,88 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
   return ML_OK;
 }
 
+
+// ---- fused scoring + half top-k filter (pkm_scores_select_tc_kernel)
+bool pkm_select_tc_eligible(const mlPkmShape& sh) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = std::getenv("ML_PKM_FUSED");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  if (off || sh.qk_norm) return false;
+  if (!pkm_scores_tc_eligible(sh)) return false;
+  return sh.S >= 512 && sh.S % 256 == 0 && sh.S <= 65535 && sh.k <= 32;
+}
+
+int pkm_select_cap() { return kCand; }
+
+// upper-tail standard normal quantile z with P(Z > z) = pr (Acklam's rational
+// approximation, |rel err| < 1.2e-9; the ladder needs no more)
+static double normal_isf(double pr) {
+  const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                      1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                      6.680131188771972e+01, -1.328068155288572e+01};
+  const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                      -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  const double d[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                      3.754408661907416e+00};
+  const double q = 1.0 - pr;   // lower-tail probability
+  double x;
+  if (q < 0.02425) {
+    const double u = std::sqrt(-2 * std::log(q));
+    x = (((((c[0] * u + c[1]) * u + c[2]) * u + c[3]) * u + c[4]) * u + c[5]) /
+        ((((d[0] * u + d[1]) * u + d[2]) * u + d[3]) * u + 1);
+  } else if (q > 1 - 0.02425) {
+    const double u = std::sqrt(-2 * std::log(1 - q));
+    x = -(((((c[0] * u + c[1]) * u + c[2]) * u + c[3]) * u + c[4]) * u + c[5]) /
+        ((((d[0] * u + d[1]) * u + d[2]) * u + d[3]) * u + 1);
+  } else {
+    const double u = q - 0.5, r = u * u;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * u /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1);
+  }
+  return x;
+}
+
+mlStatus launch_pkm_select_tc(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
+                              uint64_t* cand, int32_t* cnt, int32_t* fail_rows, int32_t* fail_n,
+                              cudaStream_t s) {
+  const int Dh = sh.Dk / 2;
+  TcParams p;
+  p.scores = nullptr;
+  p.T = sh.T; p.H = sh.H; p.S = sh.S; p.Dh = Dh; p.Dk = sh.Dk;
+  p.BN = 256;
+  p.n_sub = sh.S / p.BN;
+  p.k_chunks = Dh / kBK;
+  p.m_tiles = (sh.T + kBM - 1) / kBM;
+  p.tiles = p.m_tiles * sh.H * 2;
+  p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(p.BN >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+  p.tmem_cols = 512;
+  SelOut o;
+  o.cand = cand; o.cnt = cnt; o.fail_rows = fail_rows; o.fail_n = fail_n; o.k = sh.k;
+  // ladder: from well below subtile 0's k-th largest (so that >= k of its 256
+  // scores are counted at L_0) to above the row's expected k-th largest
+  const double za = normal_isf(double(sh.k) / p.BN) - 1.0;
+  const double zb = normal_isf(double(sh.k) / sh.S) + 0.3;
+  o.z0 = float(za);
+  o.dz = float((zb - za) / (kLevels - 1));
+  CUtensorMap mq, mk1, mk2;
+  ML_TRY(make_map(&mq, q, uint64_t(sh.H) * sh.Dk, uint64_t(sh.T), uint64_t(sh.H) * sh.Dk * 2, kBK, kBM));
+  ML_TRY(make_map(&mk1, K1, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN));
+  ML_TRY(make_map(&mk2, K2, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN));
+  const size_t smem = 1024 + size_t(kSelStages) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 256 +
+                      size_t(kCand) * kEpi * (4 + 2) + size_t(kLevels + 1) * kEpi * 2;
+  static size_t configured = 0;
+  if (smem > configured) {
+    ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_select_tc_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = smem;
+  }
+  ML_CUDA_TRY(cudaMemsetAsync(fail_n, 0, sizeof(int32_t), s));
+  const int grid = std::min(p.tiles, num_sms());
+  pkm_scores_select_tc_kernel<<<grid, kThreads, smem, s>>>(mq, mk1, mk2, p, o);
+  ML_LAUNCH_CHECK("pkm_scores_topk_tc");
+  return ML_OK;
+}
 }  // namespace ml

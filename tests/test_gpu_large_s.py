@@ -92,3 +92,61 @@ def test_pkm_topk_bwd_bf16_large_S(T, H, S, Dk, k):
     assert_close(host(dq), rdq, TOL["f32"], "dq")
     assert_close(host(dK1), rdK1, TOL["f32"], "dK1")
     assert_close(host(dK2), rdK2, TOL["f32"], "dK2")
+
+
+def _unfused_in_subprocess(q, K1, K2, k):
+    """pkm_topk with the fused scoring + filter kernel switched off
+    (ML_PKM_FUSED=0: score matrix + half top-k kernel), in a fresh process."""
+    import os, subprocess, sys, tempfile
+    with tempfile.TemporaryDirectory() as d:
+        np.save(os.path.join(d, "q.npy"), q)
+        np.save(os.path.join(d, "K1.npy"), K1)
+        np.save(os.path.join(d, "K2.npy"), K2)
+        code = (
+            "import numpy as np, torch, sys\n"
+            "from paper_2412_09764_b200 import ops\n"
+            f"d = {d!r}\n"
+            "t = lambda n: torch.from_numpy(np.load(d + '/' + n + '.npy')).cuda().to(torch.bfloat16)\n"
+            f"i, w, s = ops.pkm_topk(t('q'), t('K1'), t('K2'), {k}, with_score=True)\n"
+            "np.save(d + '/i.npy', i.cpu().numpy()); np.save(d + '/w.npy', w.cpu().numpy())\n"
+            "np.save(d + '/s.npy', s.cpu().numpy())\n")
+        env = dict(os.environ, ML_PKM_FUSED="0")
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return (np.load(os.path.join(d, "i.npy")), np.load(os.path.join(d, "w.npy")),
+                np.load(os.path.join(d, "s.npy")))
+
+
+@pytest.mark.parametrize("T,H,S,Dk,k", [(300, 4, 1024, 1024, 32), (260, 2, 8192, 128, 32),
+                                        (200, 2, 512, 128, 8), (130, 2, 2048, 256, 1)])
+def test_fused_select_equals_score_matrix_path(T, H, S, Dk, k):
+    """The fused scoring + threshold filter (no score matrix) selects exactly
+    what the score-matrix path selects from the same tensor-core scores:
+    indices, scores and weights bit-identical."""
+    q, K1, K2 = _inputs(34, T, H, S, Dk, gen.CLS_CONTINUOUS)
+    idx, w, score = ops().pkm_topk(dev(q, "bf16"), dev(K1, "bf16"), dev(K2, "bf16"), k,
+                                   with_score=True)
+    ui, uw, us = _unfused_in_subprocess(q, K1, K2, k)
+    assert np.array_equal(host(idx), ui)
+    assert np.array_equal(host(score), us.astype(np.float64))
+    assert np.array_equal(host(w), uw.astype(np.float64))
+
+
+def test_fused_select_fallback_rows():
+    """Rows whose candidate list overflows (all scores tied: q = 0 on some
+    tokens, heavy ties on the exact class) take the exact fallback: q = 0
+    selects flat indices 0..k-1 with w = 1/k, the other rows match
+    the oracle bit-exactly (exact class)."""
+    T, H, S, Dk, k = 96, 2, 1024, 128, 16
+    q, K1, K2 = _inputs(35, T, H, S, Dk, gen.CLS_EXACT)
+    q[::5] = 0.0
+    idx, w, score = ops().pkm_topk(dev(q, "bf16"), dev(K1, "bf16"), dev(K2, "bf16"), k,
+                                   with_score=True)
+    ridx, rscore, rw = opkm.pkm_lookup(q.astype(np.float64), K1.astype(np.float64),
+                                       K2.astype(np.float64), k, method="two_stage")
+    assert np.array_equal(host(idx)[::5], np.broadcast_to(np.arange(k), (len(q[::5]), H, k)))
+    assert np.array_equal(host(idx), ridx)
+    assert np.array_equal(host(score), rscore)
+    assert_close(host(w), rw, 1e-6, "w")
