@@ -57,6 +57,25 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// With SLEEP, a failed probe backs off (the single-thread producer / MMA
+// loops of the fused kernel would otherwise take issue slots from the
+// epilogue warps on the same schedulers).
+template <bool SLEEP = false>
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0, n = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (++n > kSpinLimit) __trap();
+    if (SLEEP) __nanosleep(64);
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0, n = 0;
@@ -132,7 +151,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
 
 // ---------------- TMA producer (one thread): the 128-token query tile and the
 // BN-key half-key tile of every K-chunk of every subtile, STAGES-deep ring
-template <int STAGES>
+template <int STAGES, bool SLEEP = false>
 __device__ __forceinline__ void tc_producer(const CUtensorMap* tmQ, const CUtensorMap* tmK1,
                                             const CUtensorMap* tmK2, uint8_t* sA, uint8_t* sB,
                                             uint64_t* full, uint64_t* empty, uint32_t bytes_a,
@@ -145,7 +164,7 @@ __device__ __forceinline__ void tc_producer(const CUtensorMap* tmQ, const CUtens
     const CUtensorMap* tmK = half ? tmK2 : tmK1;
     for (int n = 0; n < p.n_sub; ++n) {
       for (int kc = 0; kc < p.k_chunks; ++kc) {
-        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_wait_t<SLEEP>(&empty[stage], phase ^ 1);
         mbar_expect_tx(&full[stage], bytes_a + bytes_b);
         tma_load_2d(sA + stage * bytes_a, tmQ, &full[stage], h * p.Dk + half * p.Dh + kc * kBK,
                     mt * kBM);
@@ -161,7 +180,7 @@ __device__ __forceinline__ void tc_producer(const CUtensorMap* tmQ, const CUtens
 
 // ---------------- MMA issuer (one thread): D[acc] = Q_tile x K_tile^T per
 // subtile into a double-buffered TMEM accumulator; commits free smem stages
-template <int STAGES>
+template <int STAGES, bool SLEEP = false>
 __device__ __forceinline__ void tc_mma(uint8_t* sA, uint8_t* sB, uint64_t* full, uint64_t* empty,
                                        uint64_t* tfull, uint64_t* tempty, uint32_t bytes_a,
                                        uint32_t bytes_b, uint32_t tmem_base, const TcParams& p) {
@@ -171,11 +190,11 @@ __device__ __forceinline__ void tc_mma(uint8_t* sA, uint8_t* sB, uint64_t* full,
   uint32_t acc_phase = 0;
   for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
     for (int n = 0; n < p.n_sub; ++n) {
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      mbar_wait_t<SLEEP>(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t dcol = tmem_base + uint32_t(acc * p.BN);
       for (int kc = 0; kc < p.k_chunks; ++kc) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait_t<SLEEP>(&full[stage], phase);
         tc_fence_after();
         const uint64_t ad = sw128_desc(smem_u32(sA + stage * bytes_a));
         const uint64_t bd = sw128_desc(smem_u32(sB + stage * bytes_b));
@@ -195,6 +214,41 @@ __device__ __forceinline__ void tc_mma(uint8_t* sA, uint8_t* sB, uint64_t* full,
       }
     }
   }
+}
+
+// tcgen05.ld without the wait (the caller issues tmem_wait_ld before using r)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// wait for every outstanding tcgen05.ld of this thread; r (the registers of
+// the last load) are then valid -- the empty asm keeps their uses after it
+__device__ __forceinline__ void tmem_wait_ld(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]),
+                 "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31]));
+}
+__device__ __forceinline__ void sts_pred_f32(uint32_t addr, uint32_t v, uint32_t p) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.b32 [%0], %1;\n}" ::"r"(addr),
+               "r"(v), "r"(p)
+               : "memory");
+}
+__device__ __forceinline__ void sts_pred_u16(uint32_t addr, uint32_t v, uint32_t p) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.u16 [%0], %1;\n}" ::"r"(addr),
+               "h"(uint16_t(v)), "r"(p)
+               : "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -307,33 +361,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 
 // ============================================================================
-// Scoring fused with the half top-k filter (no score matrix in HBM).
+// Scoring fused with the half top-k filter (no score matrix in HBM; opt-in).
 //
 // The epilogue thread that owns token row r of a 128-token tile (tcgen05.ld
 // 32x32b: thread = TMEM lane = row) sees every score of its (t, h, half) row,
 // S / BN subtiles of BN = 256 keys, and keeps only a small candidate set that
 // provably contains the row's k best ("the top-k indices ... obtained
 // from the respective key sets"; ties resolved later by (score, lower index)):
-//  * subtile 0 is read twice from TMEM: first for the row's mean / standard
-//    deviation, which place a ladder of 32 levels L_j = L_0 + j*delta, then for
-//    a per-thread histogram of its 256 scores over those levels;
-//  * the threshold theta is the highest level with at least k scores counted
-//    at or above it -- a valid lower bound of the row's k-th largest score
-//    whatever the statistics were (they only place the levels; each counted
-//    score is checked against its level with the exact comparison used by the
-//    filter), and it only rises;
+//  * subtile 0's mean / standard deviation place a ladder of levels
+//    L_j = L_0 + j*delta; theta_0 = the highest level with >= k of the
+//    subtile's 256 scores at or above it (binary search, exact counts) -- a
+//    valid lower bound of the row's k-th largest score whatever the
+//    statistics were (they only place the levels);
 //  * every subtile is filtered with v >= theta; survivors (score, key index)
-//    go to a per-thread list in shared memory and into the histogram, after
-//    which theta is raised; the list is compacted (entries < theta dropped)
-//    when it nears its capacity and at the end of the row.
+//    go to a per-thread list in shared memory, which therefore holds every
+//    score seen so far that is >= theta;
+//  * when a list would overflow, theta is raised to the highest of the next
+//    levels with >= k list entries at or above it (exact counts, by the
+//    previous point) and the entries below it are dropped.
 // All top-k scores of the row are >= the final theta >= the theta in force
 // when they were seen, so all of them are candidates.  The row's candidates
-// (typically k + a bin, ~40-50) are written as 64-bit keys; rows whose list
-// overflowed are listed for an exact fallback.  The selection among the
-// candidates happens in the combine kernel (pkm.cu).
+// are written as 64-bit keys; rows whose list still overflowed are listed for
+// an exact fallback.  The selection among the candidates happens in the
+// combine kernel (pkm.cu).
 constexpr int kSelStages = 3;     // ring depth (shared memory goes to the candidate lists)
-constexpr int kCand = 88;         // candidate list capacity per row
-constexpr int kLevels = 32;       // threshold ladder
+constexpr int kCand = 96;         // candidate list capacity per row
+constexpr int kLevels = 48;       // threshold ladder
 constexpr int kEpi = 128;         // epilogue threads (one per tile row)
 
 struct SelOut {
@@ -343,6 +396,8 @@ struct SelOut {
   int32_t* fail_n;     // its length (zeroed before the launch)
   float z0, dz;        // ladder: L_0 = mean + z0 sd, delta = dz sd
   int k;
+  int probe;           // timing probes (ML_SEL_PROBE): 1 = TMEM loads only, 2 = + ladder and
+                       // histogram, 3 = + survivor masks (no list writes), 0 = full
 };
 
 __device__ __forceinline__ uint64_t sel_key(float v, uint32_t a) {
@@ -354,7 +409,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const __grid_constant__ CUtensorMap tmK1,
                                 const __grid_constant__ CUtensorMap tmK2, TcParams p, SelOut o) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned, keeping the pointer's shared-space provenance (STS/LDS
+  // for the candidate lists instead of generic stores)
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t bytes_a = kBM * kBK * 2;
   const uint32_t bytes_b = uint32_t(p.BN) * kBK * 2;
   uint8_t* sA = base;
@@ -367,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // per-row lists, [slot][row] so that every lane always hits its own bank
   float* c_val = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
   uint16_t* c_key = reinterpret_cast<uint16_t*>(c_val + kCand * kEpi);
-  uint16_t* hist = c_key + kCand * kEpi;                      // [kLevels + 1][row]
+  uint32_t* stage = reinterpret_cast<uint32_t*>(c_key + kCand * kEpi);   // [row][8]: filter staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -398,134 +455,178 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) tc_producer<kSelStages>(&tmQ, &tmK1, &tmK2, sA, sB, full, empty, bytes_a, bytes_b, p);
+    if (lane == 0) tc_producer<kSelStages, true>(&tmQ, &tmK1, &tmK2, sA, sB, full, empty, bytes_a, bytes_b, p);
   } else if (warp == 1) {
-    if (lane == 0) tc_mma<kSelStages>(sA, sB, full, empty, tfull, tempty, bytes_a, bytes_b, tmem_base, p);
+    if (lane == 0) tc_mma<kSelStages, true>(sA, sB, full, empty, tfull, tempty, bytes_a, bytes_b, tmem_base, p);
   } else if (warp >= 4) {
     const int q4 = warp & 3;
     const int er = q4 * 32 + lane;          // this thread's tile row (= TMEM lane)
     float* cv = c_val + er;                 // cv[e * kEpi]: e-th candidate score
     uint16_t* ck = c_key + er;
-    uint16_t* hs = hist + er;               // hs[b * kEpi]
     const int H2 = 2 * p.H;
     int acc = 0;
     uint32_t acc_phase = 0;
+    constexpr int NC = 256 / 32;            // 32-column chunks per subtile (BN = 256)
+    // bit i of the result: score i of the 32-column chunk r is >= th (two
+    // instructions per score: the sign of v - th funnel-shifted in; -0 as th
+    // so that a -0 score counts as >= +0)
+    auto ge_mask = [](const uint32_t* r, float th0) {
+      const float th = th0 == 0.f ? -0.f : th0;
+      uint32_t neg = 0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        neg = __funnelshift_l(__float_as_uint(__uint_as_float(r[i]) - th), neg, 1);
+      return __brev(~neg);
+    };
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
       const int mt = t % p.m_tiles, hh = t / p.m_tiles;
       const int tok = mt * kBM + er;
       const bool valid = tok < p.T;
-      int cnt = 0, counted = 0;             // list length; entries already in the histogram
+      int cnt = 0;
       bool ovf = false;
-      float theta = -INFINITY, L0 = 0.f, delta = 1.f, inv = 1.f;
-#pragma unroll 1
-      for (int b = 0; b <= kLevels; ++b) hs[b * kEpi] = 0;
-      // the bin of v: the highest j with v >= L_j (exact check), -1 below L_0
-      auto bin_of = [&](float v) {
-        const float tt = fminf(fmaxf((v - L0) * inv, -1.f), float(kLevels - 1));
-        int j = int(floorf(tt));
-        if (j >= 0 && v < fmaf(float(j), delta, L0)) --j;
-        return j + 1;
-      };
-      auto raise_theta = [&]() {          // highest level with >= k counted at or above it
-        int c = 0;
-#pragma unroll 1
-        for (int b = kLevels; b >= 1; --b) {
-          c += hs[b * kEpi];
-          if (c >= o.k) {
-            theta = fmaxf(theta, fmaf(float(b - 1), delta, L0));
-            break;
-          }
-        }
-      };
-      auto compact = [&]() {              // drop entries below theta (order kept)
-        int w = 0, cw = 0;
+      float L0 = 0.f, delta = 1.f;
+      // theta = L_lt: the list holds every score seen so far that is >= theta,
+      // and at least k scores seen so far are >= theta (lt = -1: none yet)
+      int lt = -1;
+      float theta = -INFINITY;
+      auto level = [&](int j) { return fmaf(float(j), delta, L0); };
+      // raise theta to the highest of the next 8 levels with >= k list entries
+      // at or above it (the list holds all scores >= theta, so these are the
+      // exact counts), then drop the entries below it (order kept)
+      auto compact = [&]() {
+        int c8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        float lv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) lv[j] = level(lt + 1 + j);
 #pragma unroll 1
         for (int e = 0; e < cnt; ++e) {
           const float v = cv[e * kEpi];
-          if (v >= theta) {
-            cv[w * kEpi] = v;
-            ck[w * kEpi] = ck[e * kEpi];
-            cw += e < counted ? 1 : 0;
-            ++w;
-          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) c8[j] += v >= lv[j] ? 1 : 0;
+        }
+        int up = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) up += (c8[j] >= o.k && lt + 1 + j < kLevels) ? 1 : 0;
+        if (up > 0) {
+          lt += up;
+          theta = level(lt);
+        }
+        int w = 0;
+#pragma unroll 1
+        for (int e = 0; e < cnt; ++e) {
+          const float v = cv[e * kEpi];
+          const uint16_t kk = ck[e * kEpi];
+          cv[w * kEpi] = v;                 // w <= e: harmless when not kept
+          ck[w * kEpi] = kk;
+          w += v >= theta ? 1 : 0;
         }
         cnt = w;
-        counted = cw;
       };
       for (int n = 0; n < p.n_sub; ++n) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t ta = tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN);
-        if (n == 0) {
-          // pass 1: the ladder from the subtile's mean / sd; pass 2: its histogram
+        uint32_t ra[32], rb[32];
+        // walk the subtile's 8 chunks with the next TMEM load in flight
+        auto walk = [&](auto&& fn) {
+          tmem_ld32_nowait(ta, ra);
+          tmem_wait_ld(ra);
+#pragma unroll 1
+          for (int c = 0; c < NC; c += 2) {
+            tmem_ld32_nowait(ta + uint32_t(32 * (c + 1)), rb);
+            fn(ra, c);
+            tmem_wait_ld(rb);
+            if (c + 2 < NC) tmem_ld32_nowait(ta + uint32_t(32 * (c + 2)), ra);
+            fn(rb, c + 1);
+            if (c + 2 < NC) tmem_wait_ld(ra);
+          }
+        };
+        if (n == 0 && o.probe != 1) {
+          // the ladder from the subtile's mean / sd, then theta_0 = the highest
+          // level with >= k of the subtile's 256 scores at or above it (binary
+          // search; every count is exact)
           float sum = 0.f, sq = 0.f;
-          for (int c0 = 0; c0 < p.BN; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(ta + uint32_t(c0), r);
+          walk([&](const uint32_t* r, int) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float v = __uint_as_float(r[i]);
               sum += v;
               sq = fmaf(v, v, sq);
             }
-          }
+          });
           const float mu = sum / float(p.BN);
           const float sd = sqrtf(fmaxf(sq / float(p.BN) - mu * mu, 0.f));
           delta = fmaxf(sd * o.dz, fmaxf(fabsf(mu), 1e-20f) * 1e-6f);
-          inv = 1.f / delta;
           L0 = fmaf(o.z0, sd, mu);
-          for (int c0 = 0; c0 < p.BN; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(ta + uint32_t(c0), r);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int b = bin_of(__uint_as_float(r[i]));
-              hs[b * kEpi] = uint16_t(hs[b * kEpi] + 1);
+          int lo = -1, hi = kLevels;        // count(>= L_lo) >= k (lo = -1: -inf), count(>= L_hi) < k
+#pragma unroll 1
+          while (__any_sync(0xffffffffu, hi - lo > 1)) {
+            const int mid = (lo + hi) >> 1;
+            const float lm = level(mid);
+            int c = 0;
+            walk([&](const uint32_t* r, int) { c += __popc(ge_mask(r, lm)); });
+            if (hi - lo > 1) {
+              if (c >= o.k) lo = mid;
+              else hi = mid;
             }
           }
-          raise_theta();
+          lt = lo;
+          theta = lt >= 0 ? level(lt) : -INFINITY;
         }
-        // filter
+        // filter: survivors (v >= theta) are staged in 8-score groups and
+        // copied to the list; a list that would overflow is first compacted
+        // (theta raised), and if it still does not fit the row falls back
         const int col_base = n * p.BN;
-        for (int c0 = 0; c0 < p.BN; c0 += 32) {
-          if (__any_sync(0xffffffffu, cnt > kCand - 32)) {
-            if (cnt > kCand - 32) {
-              compact();
-              if (cnt > kCand - 32) ovf = true;
-            }
-          }
-          uint32_t r[32];
-          tmem_ld32(ta + uint32_t(c0), r);
-          const float th = (ovf || !valid) ? INFINITY : theta;
+        walk([&](const uint32_t* r, int c) {
+          if (o.probe == 1 || o.probe == 2) {
+            uint32_t x = 0;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float v = __uint_as_float(r[i]);
-            if (v >= th) {
-              cv[cnt * kEpi] = v;
-              ck[cnt * kEpi] = uint16_t(col_base + c0 + i);
-              ++cnt;
+            for (int i = 0; i < 32; ++i) x ^= r[i];
+            if (x == 0x12345678u) cnt += 1;
+            return;
+          }
+          uint32_t m = ge_mask(r, (ovf || !valid) ? INFINITY : theta);
+          if (o.probe == 3) {
+            if (m == 0x12345678u) cnt += 1;
+            return;
+          }
+          if (__any_sync(0xffffffffu, cnt + __popc(m) > kCand)) {
+            if (cnt + __popc(m) > kCand) {
+              compact();
+              m = ge_mask(r, (ovf || !valid) ? INFINITY : theta);
+              const int room = kCand - cnt;
+              if (__popc(m) > room) {       // still no room: keep what fits, fall back
+                ovf = true;
+                while (__popc(m) > room) m &= ~(1u << (31 - __clz(m)));
+              }
             }
           }
-        }
+          const uint32_t col0 = uint32_t(col_base + 32 * c);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t mg = (m >> (8 * g)) & 0xFFu;
+            if (__any_sync(0xffffffffu, mg != 0u)) {
+              uint4* st = reinterpret_cast<uint4*>(stage + er * 8);
+              st[0] = make_uint4(r[8 * g + 0], r[8 * g + 1], r[8 * g + 2], r[8 * g + 3]);
+              st[1] = make_uint4(r[8 * g + 4], r[8 * g + 5], r[8 * g + 6], r[8 * g + 7]);
+#pragma unroll 1
+              for (uint32_t b = mg; b; b &= b - 1u) {
+                const int i = __ffs(b) - 1;
+                cv[cnt * kEpi] = __uint_as_float(stage[er * 8 + i]);
+                ck[cnt * kEpi] = uint16_t(col0 + uint32_t(8 * g + i));
+                ++cnt;
+              }
+            }
+          }
+        });
         tc_fence_before();
         mbar_arrive(&tempty[acc]);          // the accumulator is free for the next subtile
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
-        if (n == 0) {
-          counted = cnt;                    // subtile 0 is in the histogram already
-        } else {
-#pragma unroll 1
-          for (int e = counted; e < cnt; ++e) {
-            const int b = bin_of(cv[e * kEpi]);
-            hs[b * kEpi] = uint16_t(hs[b * kEpi] + 1);
-          }
-          counted = cnt;
-        }
-        raise_theta();
       }
-      compact();
+      if (__any_sync(0xffffffffu, cnt > o.k)) compact();
       if (valid) {
         const int64_t row = int64_t(tok) * H2 + hh;
         if (ovf || cnt < o.k) {
@@ -652,13 +753,16 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
 
 
 // ---- fused scoring + half top-k filter (pkm_scores_select_tc_kernel)
+// Opt-in (ML_PKM_FUSED=1): measured slower than the score-matrix path at C2
+// (DESIGN.md §6): the per-row list management of 4 epilogue warps is latency-
+// and divergence-bound.
 bool pkm_select_tc_eligible(const mlPkmShape& sh) {
-  static int off = -1;
-  if (off < 0) {
+  static int on = -1;
+  if (on < 0) {
     const char* e = std::getenv("ML_PKM_FUSED");
-    off = (e && e[0] == '0') ? 1 : 0;
+    on = (e && e[0] == '1') ? 1 : 0;
   }
-  if (off || sh.qk_norm) return false;
+  if (!on || sh.qk_norm) return false;
   if (!pkm_scores_tc_eligible(sh)) return false;
   return sh.S >= 512 && sh.S % 256 == 0 && sh.S <= 65535 && sh.k <= 32;
 }
@@ -710,6 +814,8 @@ mlStatus launch_pkm_select_tc(const mlPkmShape& sh, const void* q, const void* K
   p.tmem_cols = 512;
   SelOut o;
   o.cand = cand; o.cnt = cnt; o.fail_rows = fail_rows; o.fail_n = fail_n; o.k = sh.k;
+  static const int probe = [] { const char* e = std::getenv("ML_SEL_PROBE"); return e ? std::atoi(e) : 0; }();
+  o.probe = probe;
   // ladder: from well below subtile 0's k-th largest (so that >= k of its 256
   // scores are counted at L_0) to above the row's expected k-th largest
   const double za = normal_isf(double(sh.k) / p.BN) - 1.0;
@@ -721,7 +827,7 @@ mlStatus launch_pkm_select_tc(const mlPkmShape& sh, const void* q, const void* K
   ML_TRY(make_map(&mk1, K1, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN));
   ML_TRY(make_map(&mk2, K2, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN));
   const size_t smem = 1024 + size_t(kSelStages) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 256 +
-                      size_t(kCand) * kEpi * (4 + 2) + size_t(kLevels + 1) * kEpi * 2;
+                      size_t(kCand) * kEpi * (4 + 2) + size_t(kEpi) * 8 * 4;
   static size_t configured = 0;
   if (smem > configured) {
     ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_select_tc_kernel,

@@ -94,9 +94,9 @@ def test_pkm_topk_bwd_bf16_large_S(T, H, S, Dk, k):
     assert_close(host(dK2), rdK2, TOL["f32"], "dK2")
 
 
-def _unfused_in_subprocess(q, K1, K2, k):
-    """pkm_topk with the fused scoring + filter kernel switched off
-    (ML_PKM_FUSED=0: score matrix + half top-k kernel), in a fresh process."""
+def _in_subprocess(q, K1, K2, k, fused):
+    """pkm_topk in a fresh process with the fused scoring + filter kernel
+    switched on (ML_PKM_FUSED=1) or off (score matrix + half top-k kernel)."""
     import os, subprocess, sys, tempfile
     with tempfile.TemporaryDirectory() as d:
         np.save(os.path.join(d, "q.npy"), q)
@@ -110,7 +110,7 @@ def _unfused_in_subprocess(q, K1, K2, k):
             f"i, w, s = ops.pkm_topk(t('q'), t('K1'), t('K2'), {k}, with_score=True)\n"
             "np.save(d + '/i.npy', i.cpu().numpy()); np.save(d + '/w.npy', w.cpu().numpy())\n"
             "np.save(d + '/s.npy', s.cpu().numpy())\n")
-        env = dict(os.environ, ML_PKM_FUSED="0")
+        env = dict(os.environ, ML_PKM_FUSED="1" if fused else "0")
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                            text=True, timeout=600)
@@ -126,12 +126,11 @@ def test_fused_select_equals_score_matrix_path(T, H, S, Dk, k):
     what the score-matrix path selects from the same tensor-core scores:
     indices, scores and weights bit-identical."""
     q, K1, K2 = _inputs(34, T, H, S, Dk, gen.CLS_CONTINUOUS)
-    idx, w, score = ops().pkm_topk(dev(q, "bf16"), dev(K1, "bf16"), dev(K2, "bf16"), k,
-                                   with_score=True)
-    ui, uw, us = _unfused_in_subprocess(q, K1, K2, k)
-    assert np.array_equal(host(idx), ui)
-    assert np.array_equal(host(score), us.astype(np.float64))
-    assert np.array_equal(host(w), uw.astype(np.float64))
+    fi, fw, fs = _in_subprocess(q, K1, K2, k, fused=True)
+    ui, uw, us = _in_subprocess(q, K1, K2, k, fused=False)
+    assert np.array_equal(fi, ui)
+    assert np.array_equal(fs, us)
+    assert np.array_equal(fw, uw)
 
 
 def test_fused_select_fallback_rows():
@@ -142,11 +141,10 @@ def test_fused_select_fallback_rows():
     T, H, S, Dk, k = 96, 2, 1024, 128, 16
     q, K1, K2 = _inputs(35, T, H, S, Dk, gen.CLS_EXACT)
     q[::5] = 0.0
-    idx, w, score = ops().pkm_topk(dev(q, "bf16"), dev(K1, "bf16"), dev(K2, "bf16"), k,
-                                   with_score=True)
+    idx, w, score = _in_subprocess(q, K1, K2, k, fused=True)
     ridx, rscore, rw = opkm.pkm_lookup(q.astype(np.float64), K1.astype(np.float64),
                                        K2.astype(np.float64), k, method="two_stage")
-    assert np.array_equal(host(idx)[::5], np.broadcast_to(np.arange(k), (len(q[::5]), H, k)))
-    assert np.array_equal(host(idx), ridx)
-    assert np.array_equal(host(score), rscore)
-    assert_close(host(w), rw, 1e-6, "w")
+    assert np.array_equal(idx[::5], np.broadcast_to(np.arange(k), (len(q[::5]), H, k)))
+    assert np.array_equal(idx, ridx)
+    assert np.array_equal(score.astype(np.float64), rscore)
+    assert_close(w.astype(np.float64), rw, 1e-6, "w")
