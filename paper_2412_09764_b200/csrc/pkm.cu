@@ -351,6 +351,91 @@ __device__ __forceinline__ bool row_topk_fast(const float* sr, int S, int k, Top
   return true;
 }
 
+// Streaming variant for long rows (S % 128 == 0, S > 1024: the 16m / 64m
+// memories): the same bound-then-rank selection without holding the
+// row in registers.
+//  1. every lane streams its S/32 values (float4 rounds) keeping its two
+//     largest; theta = the k-th largest of those 64 values (a lower bound of
+//     the row's k-th largest: 64 distinct elements);
+//  2. the row is streamed again (L2-hot) and the survivors v >= theta
+//     (typically k + ~15) are appended to shared memory in lane order;
+//  3. survivors are ranked by counting on unique keys (ranks < k written).
+// Returns false (nothing written) when more than 64 values survive.
+__device__ __forceinline__ bool row_topk_stream(const float* sr, int S, int k, TopkSmem& sm,
+                                                int64_t row, int32_t* hI, float* hs,
+                                                int* count_out) {
+  const int lane = threadIdx.x & 31;
+  const int rounds = S / 128;
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll 4
+  for (int r = 0; r < rounds; ++r) {
+    const float4 v = *reinterpret_cast<const float4*>(sr + r * 128 + lane * 4);
+    const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float lo = fminf(m0, vs[c]);
+      m0 = fmaxf(m0, vs[c]);
+      m1 = fmaxf(m1, lo);
+    }
+  }
+  const float A = warp_sort_desc_f(m0), B = warp_sort_desc_f(m1);
+  float c = -INFINITY;
+  {
+    const int i = lane;
+    const float a = __shfl_sync(FULL, A, (i + 31) & 31);
+    const float b = __shfl_sync(FULL, B, (k - 1 - i) & 31);
+    if (i <= k - 1) c = fminf(i == 0 ? INFINITY : a, b);
+  }
+  const float ak = __shfl_sync(FULL, A, k - 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c = fmaxf(c, __shfl_xor_sync(FULL, c, o));
+  const float theta = fmaxf(c, ak);
+  int count = 0;
+  uint64_t* ck = sm.cand;
+#pragma unroll 4
+  for (int r = 0; r < rounds; ++r) {
+    const float4 v = *reinterpret_cast<const float4*>(sr + r * 128 + lane * 4);
+    const uint32_t mk = (v.x >= theta ? 1u : 0u) | (v.y >= theta ? 2u : 0u) |
+                        (v.z >= theta ? 4u : 0u) | (v.w >= theta ? 8u : 0u);
+    if (__any_sync(FULL, mk != 0u)) {
+      const int cnt = __popc(mk);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int pos = count + incl - cnt;
+      const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if ((mk >> q) & 1u) {
+          if (pos < kCandCap) ck[pos] = make_key(vs[q], uint32_t(r * 128 + lane * 4 + q));
+          ++pos;
+        }
+      }
+      count += __shfl_sync(FULL, incl, 31);
+    }
+  }
+  *count_out = count;
+  if (count > 64) return false;
+  __syncwarp();
+  const bool h0 = lane < count, h1 = lane + 32 < count;
+  const uint64_t k0 = h0 ? ck[lane] : ~0ull, k1 = h1 ? ck[lane + 32] : ~0ull;
+  int r0 = 0, r1 = 0;
+  if ((count & 1) != 0) ck[count] = 0ull;   // pad: ranks nothing
+  __syncwarp();
+  const int pairs = (count + 1) >> 1;
+  for (int l = 0; l < pairs; ++l) {
+    const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(ck)[l];
+    r0 += (kk.x > k0 ? 1 : 0) + (kk.y > k0 ? 1 : 0);
+    r1 += (kk.x > k1 ? 1 : 0) + (kk.y > k1 ? 1 : 0);
+  }
+  if (h0 && r0 < k) { hI[row * k + r0] = int32_t(key_id(k0)); hs[row * k + r0] = key_score(k0); }
+  if (h1 && r1 < k) { hI[row * k + r1] = int32_t(key_id(k1)); hs[row * k + r1] = key_score(k1); }
+  return true;
+}
+
 // one warp per (t, h, half) row of S scores
 __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int64_t rows, int S,
                                                         int k, int32_t* hI, float* hs, QkNorm qn,
@@ -365,10 +450,11 @@ __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int
   const float qi = qn.qinv ? qn.qinv[row] : 1.f;
   const float* ki = qn.qinv ? ((row & 1) ? qn.kinv2 : qn.kinv1) + int64_t((row >> 1) % H) * S : nullptr;
   auto score_at = [=](int e) { return ki ? (sr[e] * qi) * ki[e] : sr[e]; };
-  if ((S % 128) == 0 && S <= 1024 && ki == nullptr && k <= 32) {
+  if ((S % 128) == 0 && ki == nullptr && k <= 32) {
     int count = 0;
-    if (S == 1024 ? row_topk_fast<true>(sr, S, k, sm, row, hI, hs, &count)
-                  : row_topk_fast<false>(sr, S, k, sm, row, hI, hs, &count))
+    if (S > 1024 ? row_topk_stream(sr, S, k, sm, row, hI, hs, &count)
+                 : (S == 1024 ? row_topk_fast<true>(sr, S, k, sm, row, hI, hs, &count)
+                              : row_topk_fast<false>(sr, S, k, sm, row, hI, hs, &count)))
       return;
     uint64_t key;
     if (count <= kCandCap) {     // many ties: exact select over the survivors
