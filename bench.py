@@ -156,55 +156,45 @@ def respawn_under_torchrun(n):
 
 
 # ------------------------------------------------------------- comm wrappers
-class TimedComm:
-    """Wraps a communicator; records CUDA events around each collective while
-    `on` so the bench can report per-collective NVLink GB/s (bytes a rank
-    sends and receives over the link / time)."""
+class CGroup:
+    """Marks the C-ABI memory group (ops.Group over NCCL) for build_step."""
 
-    def __init__(self, inner):
-        self.inner, self.size, self.rank = inner, inner.size, inner.rank
-        self.on, self.rec = False, []
+    def __init__(self, grp):
+        self.grp = grp
 
-    def _run(self, kind, fn, out, inp, link_bytes):
-        import torch
-        if not self.on:
-            return fn(out, inp)
-        s = torch.cuda.current_stream()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s)
-        r = fn(out, inp)
-        b.record(s)
-        self.rec.append((kind, a, b, link_bytes))
-        return r
 
-    def all_gather(self, out, inp):
-        nb = out.numel() * out.element_size() * (self.size - 1) // self.size
-        return self._run("all_gather", self.inner.all_gather, out, inp, nb)
+def coll_bytes(cfg, G, T_loc, mode):
+    """Bytes one rank sends over NVLink per step, per collective kind of the
+    C-ABI group (include/memlayer.h memory_layer_*_group)."""
+    e = 2 if cfg["dtype"] == "bf16" else 4
+    B = cfg["H"] * cfg["k"]
+    dvG = cfg["dv"] // G
+    blk = T_loc * dvG * e
+    out = {"nccl_all_gather": (G - 1) * T_loc * 2 * B * 4,         # packed (idx, w)
+           "nccl_all_to_all": (G - 1) * blk,                      # dy slices
+           "nccl_reduce_scatter": (G - 1) * T_loc * B * 4}        # partial dw
+    if mode == "alltoall":
+        out["nccl_sendrecv"] = (G - 1) * blk                      # the forward's blocks
+    else:
+        out["nccl_all_gather"] += G * (G - 1) * blk               # every block to everyone
+    return out
 
-    def all_to_all(self, out, inp):
-        nb = inp.numel() * inp.element_size() * (self.size - 1) // self.size
-        return self._run("all_to_all", self.inner.all_to_all, out, inp, nb)
 
-    def reduce_scatter(self, out, inp):
-        nb = inp.numel() * inp.element_size() * (self.size - 1) // self.size
-        return self._run("reduce_scatter", self.inner.reduce_scatter, out, inp, nb)
-
-    def report(self, steps):
-        agg = {}
-        for kind, a, b, nb in self.rec:
-            t = a.elapsed_time(b)
-            e = agg.setdefault(kind, [0, 0.0, 0])
-            e[0] += 1
-            e[1] += t
-            e[2] += nb
-        out = {}
-        for kind, (cnt, ms, nb) in agg.items():
-            gbs = nb / (ms / 1e3) / 1e9 if ms > 0 else None
-            out[kind] = {"calls_per_step": cnt / steps, "ms_per_step": round(ms / steps, 4),
-                         "link_bytes_per_step": nb // steps,
-                         "GBps": round(gbs, 1) if gbs else None,
-                         "frac_of_peer_copy": round(gbs / NVLINK_PEER_GBS, 4) if gbs else None}
-        return out
+def coll_report(kern, steps, cfg, G, T_loc, mode):
+    nb = coll_bytes(cfg, G, T_loc, mode)
+    out = {}
+    for kind, b in nb.items():
+        if kind not in kern:
+            continue
+        cnt, tot = kern[kind]
+        ms = tot / steps
+        gbs = b / (ms / 1e3) / 1e9 if ms > 0 else None
+        out[kind] = {"calls_per_step": cnt / steps, "ms_per_step": round(ms, 4),
+                     "link_bytes_per_step": b, "GBps": round(gbs, 1) if gbs else None,
+                     "frac_of_peer_copy": round(gbs / NVLINK_PEER_GBS, 4) if gbs else None}
+    out["note"] = ("per-rank bytes sent over NVLink / collective time (serialised measurement pass); "
+                   f"peer-copy reference {NVLINK_PEER_GBS} GB/s per direction (B200_PROFILING.md)")
+    return out
 
 
 class LoopbackComm:
@@ -310,7 +300,20 @@ def build_step(args, cfg, t, ops, torch, comm=None):
     dK2 = torch.zeros(t["K2"].shape, dtype=torch.float32, device=t["q"].device)
     bufs = {}
     dV_dtype = torch.bfloat16 if args.dv_dtype == "bf16" else torch.float32
-    if comm is not None:
+    if isinstance(comm, CGroup):
+        # the product path for N > 1: the memory group behind the C ABI
+        # (exchange, overlap and local kernels inside libmemlayer, NCCL)
+        from paper_2412_09764_b200 import group
+        layer = group.CGroupMemoryLayer(comm.grp, k=k, mode=args.mode, dV_dtype=dV_dtype)
+
+        def step(inp=t):
+            dK1.zero_()
+            dK2.zero_()
+            out, saved = layer.forward(inp["x"], inp["q"], t["K1"], t["K2"], t["V"], t["W1"], t["W2"])
+            g = layer.backward(inp["dout"], saved, dK1, dK2)
+            step.last_saved = saved
+            return out, g
+    elif comm is not None:
         from paper_2412_09764_b200 import group
         layer = group.GroupMemoryLayer(comm, k=k, mode=args.mode,
                                        local=group.CudaLocal(dV_dtype=dV_dtype))
@@ -383,11 +386,11 @@ def run_ours(args, cfg, world, rank, local):
     if world > 1 or args.force_group:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-        from paper_2412_09764_b200.group import TorchComm
-        comm = TimedComm(TorchComm(dist.group.WORLD))
+        from paper_2412_09764_b200.group import nccl_group
+        comm = CGroup(nccl_group(dist.group.WORLD))
     t = make_inputs(cfg, dev, G, rank if world > 1 else 0, ops, torch, group_path)
     if per_rank > 1:
-        comm = TimedComm(LoopbackComm(G, 0, group_others(cfg, G, 0, t, ops, torch)))
+        comm = LoopbackComm(G, 0, group_others(cfg, G, 0, t, ops, torch))
     step = build_step(args, cfg, t, ops, torch, comm)
     T_loc = tokens_per_rank(cfg, G)
 
@@ -411,19 +414,13 @@ def run_ours(args, cfg, world, rank, local):
     ops.set_serial(True)
     ops.timing_reset()
     ops.timing_enable(True)
-    if comm is not None:
-        comm.on = True
     for _ in range(kern_steps):
         step()
     torch.cuda.synchronize()
     ops.timing_enable(False)
     ops.set_serial(False)
     kern = ops.timing_report()
-    coll = None
-    if comm is not None:
-        comm.on = False
-        coll = comm.report(kern_steps) if world > 1 else None
-        comm.rec = []
+    coll = coll_report(kern, kern_steps, cfg, G, T_loc, args.mode) if isinstance(comm, CGroup) else None
 
     # ---- variant: the compact value gradient stored as bf16 (memlayer.h
     # grad_dtype; fp32 sums rounded once) -- same step otherwise
@@ -447,6 +444,8 @@ def run_ours(args, cfg, world, rank, local):
     if world > 1:
         saved = step.last_saved
         others = {str(torch.int32): saved["idx_all"].clone(), str(torch.float32): saved["w_all"].clone()}
+        # t_ref(G): the same kernels through the Python protocol with the
+        # collectives replaced by local copies
         ref_step = build_step(args, cfg, t, ops, torch, LoopbackComm(world, rank, others))
         for _ in range(max(2, args.warmup // 2)):
             ref_step()

@@ -53,6 +53,7 @@ typedef enum {
   ML_ERR_INDEX = 3,        /* out-of-range index seen (ML_CHECK_INDICES=1)      */
   ML_ERR_WORKSPACE = 4,    /* workspace smaller than the *_workspace() size     */
   ML_ERR_CUDA = 5,         /* CUDA runtime / launch error (text in last_error)  */
+  ML_ERR_NCCL = 6,         /* NCCL error or libnccl.so.2 missing (group calls)  */
   ML_ERR_UNSUPPORTED = 7   /* legal per the paper but not supported by v1       */
 } mlStatus;
 
@@ -315,8 +316,8 @@ mlStatus peer_bwd(const mlPeerShape* shape, const void* dy, const void* x, const
  * sharded along the embedding dim over the G ranks of a memory group; the
  * exchange (all-gather of (idx, w), all-to-all of the partial embeddings,
  * reverse all-to-all of dy, reduce-scatter of the partial dw) is issued by
- * the caller (paper_2412_09764_b200/group.py, NCCL).  These calls do the
- * on-device layout work around it:
+ * the group entry points below (or by a caller running its own exchange).
+ * These calls do the on-device layout work around it:
  *   ml_group_unpack: recv [G][T_loc][dv/G] (rank g's slice of this rank's
  *     tokens) -> y [T_loc][dv], y[t][g*dv/G + c] = recv[g][t][c]; if gate !=
  *     NULL also z = y ⊙ silu(gate) (Eq. 2) into z [T_loc][dv] (y nullable then).
@@ -338,6 +339,101 @@ mlStatus ml_gate_bwd(const void* dz, const void* g, const void* y, void* z, void
 mlStatus ml_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                  const void* B, int64_t ldb, void* C, int64_t ldc, mlDtype ab, int c_f32, void* ws,
                  size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------ memory group (a7, a12)
+ * The dim-sharded memory group of PAPER.md §3.1.2 (Fig. 2)
+ * behind the C ABI: rank g of G owns V[:, g*dv/G : (g+1)*dv/G] as a
+ * contiguous [N, dv/G] table; tokens are data-parallel (T_loc per rank, equal
+ * on every rank: reading Q19).
+ *
+ * A group owns its transport and its streams (one outstanding forward /
+ * backward pair at a time per group; calls on one group are not
+ * thread-safe).  ml_group_init: NCCL on the current device -- one rank of an
+ * ncclUniqueId (128 bytes) that the caller creates on one rank with
+ * ml_group_unique_id and broadcasts (torch.distributed).  NCCL is resolved
+ * at run time (libnccl.so.2); without it these two return ML_ERR_NCCL and
+ * the rest of the library is unaffected.  ml_group_init_hub: G ranks as host
+ * threads of one process on one device sharing a hub (ml_group_hub_create);
+ * collectives are host-synchronised device copies (test harness of the same
+ * protocol on one GPU; no kernel waits on another).
+ *
+ * Output modes (reading Q13): ML_OUT_ALLTOALL (the paper: "each
+ * worker gathers the partial embeddings corresponding to its own portion of
+ * the indices": y [T_loc, dv] of the rank's own tokens) and ML_OUT_ALLGATHER
+ * (north-star wording: every rank receives y [G*T_loc, dv] of all tokens). */
+typedef struct mlGroup_* mlGroup;
+typedef enum { ML_OUT_ALLTOALL = 0, ML_OUT_ALLGATHER = 1 } mlOutMode;
+mlStatus ml_group_unique_id(void* id128);
+mlStatus ml_group_init(const void* id128, int G, int rank, mlGroup* out);
+mlStatus ml_group_hub_create(int G, void** hub);
+mlStatus ml_group_hub_destroy(void* hub);
+mlStatus ml_group_init_hub(void* hub, int rank, mlGroup* out);
+mlStatus ml_group_destroy(mlGroup g);
+mlStatus ml_group_info(mlGroup g, int* G, int* rank);
+
+/* Bag level.  shape: N, dv = the FULL value dim, T = T_loc, B, dtype
+ * (grad_dtype for dV_shard).  Forward: idx_local/w_local [T_loc, B] ->
+ * idx_all/w_all [G*T_loc, B] (outputs: one packed all-gather; keep them for
+ * the backward), the bag over all G*T_loc tokens on V_shard [N, dv/G] (block
+ * by block, each block sent to its owner while the next is computed), then
+ * y: ML_OUT_ALLTOALL [T_loc, dv], ML_OUT_ALLGATHER [G*T_loc, dv].
+ * Backward: dy ML_OUT_ALLTOALL [T_loc, dv] (this rank's tokens; the dv/G
+ * slices go back by one all-to-all) or ML_OUT_ALLGATHER [G*T_loc, dv]
+ * (replicated; the rank reads its column slice, no exchange); the sorted
+ * segmented reduction on the slice gives rows [<= G*T_loc*B] ascending,
+ * dV_shard [cap G*T_loc*B, dv/G] (dV never leaves the rank), *U; the partial
+ * dw (a dot over dv/G columns) is reduce-scattered: dw_local [T_loc, B] =
+ * the full dw of this rank's tokens.  state (nullable): the inverse index
+ * map of idx_all built early by embbag_bwd_group_prepare (group stream; the
+ * backward waits for it), embbag_bwd_group_state_bytes bytes. */
+mlStatus embbag_fwd_group_workspace(mlGroup g, const mlBagShape* shape, mlOutMode mode, size_t* bytes);
+mlStatus embbag_fwd_group(mlGroup g, const mlBagShape* shape, const void* V_shard,
+                          const int32_t* idx_local, const float* w_local, int32_t* idx_all,
+                          float* w_all, mlOutMode mode, void* y, void* ws, size_t ws_bytes,
+                          void* stream);
+mlStatus embbag_bwd_group_state_bytes(mlGroup g, const mlBagShape* shape, size_t* bytes);
+mlStatus embbag_bwd_group_prepare(mlGroup g, const mlBagShape* shape, const int32_t* idx_all,
+                                  void* state, size_t state_bytes, void* stream);
+mlStatus embbag_bwd_group_workspace(mlGroup g, const mlBagShape* shape, mlOutMode mode, size_t* bytes);
+mlStatus embbag_bwd_group(mlGroup g, const mlBagShape* shape, const void* V_shard,
+                          const int32_t* idx_all, const float* w_all, const void* dy,
+                          mlOutMode mode, const void* state, size_t state_bytes, int32_t* rows,
+                          void* dV_shard, int32_t* U, float* dw_local, void* ws, size_t ws_bytes,
+                          void* stream);
+
+/* Layer level (the gated Memory+ layer, Eq. 1 + Eq. 2, over the group).
+ * shape: pkm.T = T_loc, N, dv = FULL value dim, D, gated = 1.  Forward: own
+ * tokens' pkm_topk -> idx_saved/w_saved [T_loc,H,k]; g_saved = x W1 (library
+ * side stream); the bag forward of embbag_fwd_group (idx_all/w_all
+ * [G*T_loc,H,k] outputs); own rows y_saved [T_loc, dv] and z = y ⊙ silu(g)
+ * in the unpack; out = z W2 [T_loc, D].  ML_OUT_ALLGATHER also fills y_all
+ * [G*T_loc, dv].  state (nullable, embbag_bwd_group_state_bytes of the bag
+ * shape [T_loc, H*k]): the backward's inverse map, built during the forward.
+ * Backward (gate on own tokens, then embbag_bwd_group in the all-to-all form
+ * -- the layer's dy exists for own tokens only -- then pkm_topk_bwd on own
+ * tokens with the reduce-scattered dw): dx [T_loc, D] (gate path), dq
+ * [T_loc,H,Dk], dK1/dK2 ACCUMULATE (this rank's tokens' part; the caller
+ * all-reduces them like any replicated weight gradient), dV_rows / dV_shard /
+ * U as embbag_bwd_group, dW1/dW2 fp32 (this rank's part), dw_out
+ * [T_loc,H,k] nullable. */
+mlStatus memory_layer_fwd_group_workspace(mlGroup g, const mlLayerShape* shape, mlOutMode mode,
+                                          size_t* bytes);
+mlStatus memory_layer_fwd_group(mlGroup g, const mlLayerShape* shape, mlOutMode mode, const void* x,
+                                const void* q, const void* K1, const void* K2, const void* V_shard,
+                                const void* W1, const void* W2, void* out, int32_t* idx_saved,
+                                float* w_saved, int32_t* idx_all, float* w_all, void* g_saved,
+                                void* y_saved, void* y_all, void* state, size_t state_bytes,
+                                void* ws, size_t ws_bytes, void* stream);
+mlStatus memory_layer_bwd_group_workspace(mlGroup g, const mlLayerShape* shape, size_t* bytes);
+mlStatus memory_layer_bwd_group(mlGroup g, const mlLayerShape* shape, const void* dout,
+                                const void* x, const void* q, const void* K1, const void* K2,
+                                const void* V_shard, const void* W1, const void* W2,
+                                const int32_t* idx_saved, const float* w_saved,
+                                const int32_t* idx_all, const float* w_all, const void* g_saved,
+                                const void* y_saved, const void* state, size_t state_bytes, void* dx,
+                                float* dq, float* dK1, float* dK2, int32_t* dV_rows, void* dV_shard,
+                                int32_t* U, float* dW1, float* dW2, float* dw_out, void* ws,
+                                size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

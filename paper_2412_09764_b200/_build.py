@@ -59,7 +59,7 @@ def build(verbose=False, extra=()):
     if os.path.exists(OUT) and os.path.getmtime(OUT) >= _newest(objs):
         return OUT
     cmd = [NVCC, "-shared", "-o", OUT] + objs + ARCH + [
-        "-L/usr/local/cuda/lib64", "-lcublasLt",
+        "-L/usr/local/cuda/lib64", "-lcublasLt", "-ldl",
         "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), flush=True)

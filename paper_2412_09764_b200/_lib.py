@@ -11,10 +11,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmemlayer.so")
 
 ML_OK, ML_ERR_ARG, ML_ERR_CONFIG, ML_ERR_INDEX, ML_ERR_WORKSPACE, ML_ERR_CUDA = 0, 1, 2, 3, 4, 5
-ML_ERR_UNSUPPORTED = 7
+ML_ERR_NCCL, ML_ERR_UNSUPPORTED = 6, 7
 ML_F32, ML_BF16 = 0, 1
 STATUS_NAMES = {0: "ML_OK", 1: "ML_ERR_ARG", 2: "ML_ERR_CONFIG", 3: "ML_ERR_INDEX",
-                4: "ML_ERR_WORKSPACE", 5: "ML_ERR_CUDA", 7: "ML_ERR_UNSUPPORTED"}
+                4: "ML_ERR_WORKSPACE", 5: "ML_ERR_CUDA", 6: "ML_ERR_NCCL", 7: "ML_ERR_UNSUPPORTED"}
 
 
 class PkmShape(C.Structure):
@@ -93,8 +93,26 @@ SIGNATURES = {
     "ml_group_pack": [P, C.c_int32, C.c_int32, C.c_int32, P, C.c_int, P],
     "ml_gate_bwd": [P, P, P, P, P, P, I64, C.c_int, P],
     "ml_gemm": [C.c_int, C.c_int, I64, I64, I64, P, I64, P, I64, P, I64, C.c_int, C.c_int, P, SZ, P],
+    # memory group (a7 / a12)
+    "ml_group_unique_id": [P],
+    "ml_group_init": [P, C.c_int, C.c_int, C.POINTER(P)],
+    "ml_group_hub_create": [C.c_int, C.POINTER(P)],
+    "ml_group_hub_destroy": [P],
+    "ml_group_init_hub": [P, C.c_int, C.POINTER(P)],
+    "ml_group_destroy": [P],
+    "ml_group_info": [P, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "embbag_fwd_group_workspace": [P, C.POINTER(BagShape), C.c_int, C.POINTER(SZ)],
+    "embbag_fwd_group": [P, C.POINTER(BagShape), P, P, P, P, P, C.c_int, P, P, SZ, P],
+    "embbag_bwd_group_state_bytes": [P, C.POINTER(BagShape), C.POINTER(SZ)],
+    "embbag_bwd_group_prepare": [P, C.POINTER(BagShape), P, P, SZ, P],
+    "embbag_bwd_group_workspace": [P, C.POINTER(BagShape), C.c_int, C.POINTER(SZ)],
+    "embbag_bwd_group": [P, C.POINTER(BagShape), P, P, P, P, C.c_int, P, SZ, P, P, P, P, P, SZ, P],
+    "memory_layer_fwd_group_workspace": [P, C.POINTER(LayerShape), C.c_int, C.POINTER(SZ)],
+    "memory_layer_fwd_group": [P, C.POINTER(LayerShape), C.c_int] + [P] * 16 + [SZ, P, SZ, P],
+    "memory_layer_bwd_group_workspace": [P, C.POINTER(LayerShape), C.POINTER(SZ)],
+    "memory_layer_bwd_group": [P, C.POINTER(LayerShape)] + [P] * 15 + [SZ] + [P] * 11 + [SZ, P],
 }
-_RESTYPES = {"ml_last_error": C.c_char_p, "ml_version": C.c_int, "ml_launch_count": C.c_uint64,
+_RESTYPES = {"ml_group_hub_destroy": C.c_int, "ml_last_error": C.c_char_p, "ml_version": C.c_int, "ml_launch_count": C.c_uint64,
              "ml_device_info": C.c_int, "ml_timing_enable": None, "ml_set_serial": None, "ml_timing_reset": None,
              "ml_timing_report": C.c_size_t, "embbag_bwd_lock_count": C.c_int64}
 

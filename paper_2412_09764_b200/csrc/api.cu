@@ -65,6 +65,7 @@ static mlStatus state_event(const void* state, cudaEvent_t* ev) {
 // the per-kernel measurement pass of bench.py; the headline timing runs with
 // the concurrent streams.
 static std::atomic<int> g_serial{0};
+bool serial_mode() { return g_serial.load() != 0; }
 static mlStatus aux_for(cudaStream_t caller, Aux** out) {
   static std::mutex mu;
   static std::map<cudaStream_t, Aux*> m, m_serial;

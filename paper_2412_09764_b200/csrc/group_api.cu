@@ -1,0 +1,796 @@
+// The dim-sharded memory group behind the C ABI (§3.1.2, P:159-167,
+// Fig. 2): "The memory values are sharded across the embedding
+// dimension.  At each step, the indices are gathered from the process group,
+// each worker does a lookup and then aggregates the portion of embeddings in
+// its own shard.  After this, each worker gathers the partial embeddings
+// corresponding to its own portion of the indices."
+//
+// A group owns its transport: NCCL (ml_group_init; one process per GPU, the
+// 128-byte unique id broadcast by the caller) or an in-process hub whose G
+// ranks are host threads on one device (ml_group_init_hub; the collectives
+// are host-synchronised copies, so no kernel ever waits on another -- the
+// single-GPU test harness of exactly this protocol code).
+//
+// Forward (mode P, the paper's): (idx, w) packed into one all-gather; the
+// bag forward over all group tokens on this rank's [N, dv/G] slice runs one
+// token block (one source rank's tokens) at a time and each finished block
+// is sent to its owner on a communication stream while the next block is
+// computed (point-to-point ring steps), so NVLink traffic overlaps the
+// HBM-bound gather; the owner interleaves the G slices (+ the silu gate).
+// Mode N (north-star wording): the blocks are all-gathered instead and every
+// rank holds every token's full row.
+// Backward (reading Q14): the dy slices travel back by one all-to-all, the
+// sorted segmented reduction runs on the local slice (dV never leaves the
+// rank), and the partial dw (a dot over dv/G columns) is reduce-scattered to
+// the token owners.
+#include "internal.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#define ML_API_BEGIN_X try {
+#define ML_API_END_X                                                            \
+  }                                                                             \
+  catch (const std::exception& e) {                                             \
+    return ::ml::fail(ML_ERR_CUDA, std::string("internal exception: ") + e.what()); \
+  }                                                                             \
+  catch (...) {                                                                 \
+    return ::ml::fail(ML_ERR_CUDA, "internal exception");                       \
+  }
+
+namespace ml {
+namespace {
+
+// ------------------------------------------------------------ NCCL (dlopen)
+// NCCL is resolved at run time (the process's libnccl.so.2 -- torch's, when
+// torch.distributed loaded it), so the library loads without it and only
+// the NCCL group calls fail (ML_ERR_NCCL) when it is absent.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*reduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    auto sym = [h](const char* n) { return dlsym(h, n); };
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(sym("ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(sym("ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(sym("ncclAllGather"));
+    api.reduceScatter = reinterpret_cast<decltype(api.reduceScatter)>(sym("ncclReduceScatter"));
+    api.send = reinterpret_cast<decltype(api.send)>(sym("ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(sym("ncclRecv"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(sym("ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(sym("ncclGroupEnd"));
+    api.errorString = reinterpret_cast<decltype(api.errorString)>(sym("ncclGetErrorString"));
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allGather &&
+             api.reduceScatter && api.send && api.recv && api.groupStart && api.groupEnd &&
+             api.errorString;
+  });
+  return api;
+}
+
+#define ML_NCCL_TRY(expr)                                                              \
+  do {                                                                                 \
+    ncclResult_t _r = (expr);                                                          \
+    if (_r != ncclSuccess)                                                             \
+      return ::ml::fail(ML_ERR_NCCL, std::string(#expr) + ": " + nccl().errorString(_r)); \
+  } while (0)
+
+// ------------------------------------------------------------ transports
+struct Transport {
+  int G = 1, rank = 0;
+  virtual ~Transport() {}
+  // recv [G][bytes] <- every rank's send [bytes]
+  virtual mlStatus all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+  // recv[g] <- rank g's send[rank] (send, recv: [G][bytes])
+  virtual mlStatus all_to_all(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+  // recv [count] = sum over ranks of their send[rank] (send: [G][count] fp32)
+  virtual mlStatus reduce_scatter_f32(const float* send, float* recv, size_t count,
+                                      cudaStream_t s) = 0;
+  // one ring step: send -> rank `to`, recv <- rank `from` (bytes each)
+  virtual bool has_p2p() const { return false; }
+  virtual mlStatus sendrecv(const void*, int, void*, int, size_t, cudaStream_t) {
+    return fail(ML_ERR_UNSUPPORTED, "transport: no point-to-point steps");
+  }
+};
+
+struct NcclTransport : Transport {
+  ncclComm_t comm = nullptr;
+  ~NcclTransport() override {
+    if (comm) nccl().commDestroy(comm);
+  }
+  mlStatus all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    ML_NCCL_TRY(nccl().allGather(send, recv, bytes, ncclUint8, comm, s));
+    timing_mark("nccl_all_gather", s);
+    return ML_OK;
+  }
+  mlStatus all_to_all(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    ML_NCCL_TRY(nccl().groupStart());
+    for (int g = 0; g < G; ++g) {
+      ML_NCCL_TRY(nccl().send(static_cast<const char*>(send) + g * bytes, bytes, ncclUint8, g, comm, s));
+      ML_NCCL_TRY(nccl().recv(static_cast<char*>(recv) + g * bytes, bytes, ncclUint8, g, comm, s));
+    }
+    ML_NCCL_TRY(nccl().groupEnd());
+    timing_mark("nccl_all_to_all", s);
+    return ML_OK;
+  }
+  mlStatus reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) override {
+    ML_NCCL_TRY(nccl().reduceScatter(send, recv, count, ncclFloat32, ncclSum, comm, s));
+    timing_mark("nccl_reduce_scatter", s);
+    return ML_OK;
+  }
+  bool has_p2p() const override { return true; }
+  mlStatus sendrecv(const void* send, int to, void* recv, int from, size_t bytes,
+                    cudaStream_t s) override {
+    ML_NCCL_TRY(nccl().groupStart());
+    ML_NCCL_TRY(nccl().send(send, bytes, ncclUint8, to, comm, s));
+    ML_NCCL_TRY(nccl().recv(recv, bytes, ncclUint8, from, comm, s));
+    ML_NCCL_TRY(nccl().groupEnd());
+    timing_mark("nccl_sendrecv", s);
+    return ML_OK;
+  }
+};
+
+__global__ void add_f32_kernel(float* dst, const float* src, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] += src[i];
+}
+
+// G ranks as host threads of one process on one device.  Each collective:
+// the caller's stream is drained, every rank publishes its buffers, a
+// barrier, each rank copies what it receives (in rank order), a barrier.
+struct Hub {
+  int G;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> send;
+  explicit Hub(int g) : G(g), send(size_t(g), nullptr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t my = gen;
+    if (++arrived == G) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != my; });
+    }
+  }
+};
+
+struct HubTransport : Transport {
+  Hub* hub = nullptr;
+  mlStatus publish(const void* p, cudaStream_t s) {
+    ML_CUDA_TRY(cudaStreamSynchronize(s));
+    hub->send[size_t(rank)] = p;
+    hub->barrier();
+    return ML_OK;
+  }
+  mlStatus done(cudaStream_t s) {
+    ML_CUDA_TRY(cudaStreamSynchronize(s));
+    hub->barrier();
+    return ML_OK;
+  }
+  mlStatus all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    ML_TRY(publish(send, s));
+    for (int g = 0; g < G; ++g)
+      ML_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv) + g * bytes, hub->send[size_t(g)], bytes,
+                                  cudaMemcpyDeviceToDevice, s));
+    return done(s);
+  }
+  mlStatus all_to_all(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    ML_TRY(publish(send, s));
+    for (int g = 0; g < G; ++g)
+      ML_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv) + g * bytes,
+                                  static_cast<const char*>(hub->send[size_t(g)]) + size_t(rank) * bytes,
+                                  bytes, cudaMemcpyDeviceToDevice, s));
+    return done(s);
+  }
+  mlStatus reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) override {
+    ML_TRY(publish(send, s));
+    ML_CUDA_TRY(cudaMemcpyAsync(recv, static_cast<const float*>(hub->send[0]) + size_t(rank) * count,
+                                count * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    for (int g = 1; g < G; ++g) {     // fixed order -> deterministic
+      add_f32_kernel<<<256, 256, 0, s>>>(recv, static_cast<const float*>(hub->send[size_t(g)]) +
+                                                   size_t(rank) * count, int64_t(count));
+      ML_LAUNCH_CHECK("group_hub_add");
+    }
+    return done(s);
+  }
+};
+
+// ------------------------------------------------------------ layout kernels
+// (idx, w) of T rows of B -> one packed [T][2B] int32 block (w as bits)
+__global__ void pack_iw_kernel(const int32_t* idx, const float* w, int64_t T, int B, int32_t* out) {
+  const int64_t n = T * B;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / B, j = i - t * B;
+    out[t * 2 * B + j] = idx[i];
+    out[t * 2 * B + B + j] = __float_as_int(w[i]);
+  }
+}
+__global__ void unpack_iw_kernel(const int32_t* in, int64_t T, int B, int32_t* idx, float* w) {
+  const int64_t n = T * B;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / B, j = i - t * B;
+    idx[i] = in[t * 2 * B + j];
+    w[i] = __int_as_float(in[t * 2 * B + B + j]);
+  }
+}
+
+unsigned grid_for(int64_t n) {
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8)));
+}
+
+}  // namespace
+}  // namespace ml
+
+using namespace ml;
+
+// ------------------------------------------------------------ the group
+struct mlGroup_ {
+  Transport* tr = nullptr;
+  int device = 0;
+  cudaStream_t comm = nullptr, aux = nullptr, prep = nullptr;
+  cudaEvent_t ev[8] = {};
+  std::vector<cudaEvent_t> blk;     // per-block events of the pipelined forward
+  cudaEvent_t state_ready = nullptr;
+};
+
+namespace ml {
+namespace {
+
+mlStatus group_make(mlGroup_* g) {
+  ML_CUDA_TRY(cudaGetDevice(&g->device));
+  int lo = 0, hi = 0;
+  ML_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  ML_CUDA_TRY(cudaStreamCreateWithPriority(&g->comm, cudaStreamNonBlocking, hi));
+  ML_CUDA_TRY(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
+  ML_CUDA_TRY(cudaStreamCreateWithFlags(&g->prep, cudaStreamNonBlocking));
+  for (auto& e : g->ev) ML_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  g->blk.resize(size_t(g->tr->G));
+  for (auto& e : g->blk) ML_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ML_CUDA_TRY(cudaEventCreateWithFlags(&g->state_ready, cudaEventDisableTiming));
+  return ML_OK;
+}
+
+mlStatus dep(cudaStream_t from, cudaStream_t to, cudaEvent_t e) {
+  ML_CUDA_TRY(cudaEventRecord(e, from));
+  ML_CUDA_TRY(cudaStreamWaitEvent(to, e, 0));
+  return ML_OK;
+}
+
+mlStatus check_group_shape(const mlGroup_* g, const mlBagShape* s, mlOutMode mode) {
+  if (!g || !g->tr) return fail(ML_ERR_ARG, "null group");
+  if (!s) return fail(ML_ERR_ARG, "null shape");
+  if (mode != ML_OUT_ALLTOALL && mode != ML_OUT_ALLGATHER) return fail(ML_ERR_ARG, "unknown output mode");
+  const int G = g->tr->G;
+  if (s->dv % G) return fail(ML_ERR_CONFIG, "group: G must divide dv (SPEC S:401)");
+  if ((int64_t(s->dv / G) * int64_t(dtype_size(s->dtype))) % 16)
+    return fail(ML_ERR_CONFIG, "group: (dv/G)*e must be a multiple of 16 bytes");
+  if (int64_t(G) * s->T * s->B >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "group: G*T*B must be < 2^31");
+  return ML_OK;
+}
+
+// the local bag over all group tokens on the [N, dv/G] shard
+mlBagShape shard_shape(const mlGroup_* g, const mlBagShape& s) {
+  mlBagShape b = s;
+  b.dv = s.dv / g->tr->G;
+  b.T = s.T * g->tr->G;
+  return b;
+}
+
+struct FwdBufs { int32_t* iw_send; int32_t* iw_recv; void* y_part; void* recv; };
+void fwd_carve(Carver& c, const mlGroup_* g, const mlBagShape& s, mlOutMode mode, FwdBufs& b) {
+  const int G = g->tr->G;
+  const int64_t e = int64_t(dtype_size(s.dtype));
+  const int64_t slice = int64_t(s.T) * (s.dv / G);   // one block of one slice
+  b.iw_send = c.take<int32_t>(int64_t(s.T) * 2 * s.B);
+  b.iw_recv = c.take<int32_t>(int64_t(G) * s.T * 2 * s.B);
+  b.y_part = c.take<char>(int64_t(G) * slice * e);
+  b.recv = c.take<char>((mode == ML_OUT_ALLGATHER ? int64_t(G) * G : int64_t(G)) * slice * e);
+}
+
+// (idx, w) all-gather: the caller's [T_loc, B] -> idx_all / w_all [G*T_loc, B]
+mlStatus gather_iw(mlGroup_* g, const mlBagShape& s, const int32_t* idx, const float* w,
+                   int32_t* idx_all, float* w_all, FwdBufs& b, cudaStream_t st) {
+  const int G = g->tr->G;
+  const int64_t n = int64_t(s.T) * s.B;
+  pack_iw_kernel<<<grid_for(n), 256, 0, st>>>(idx, w, s.T, s.B, b.iw_send);
+  count_launch();
+  ML_CUDA_TRY(cudaGetLastError());
+  ML_TRY(g->tr->all_gather(b.iw_send, b.iw_recv, size_t(n) * 2 * sizeof(int32_t), st));
+  unpack_iw_kernel<<<grid_for(n * G), 256, 0, st>>>(b.iw_recv, int64_t(s.T) * G, s.B, idx_all, w_all);
+  count_launch();
+  ML_CUDA_TRY(cudaGetLastError());
+  return ML_OK;
+}
+
+// the bag forward block by block, each finished block leaving on the
+// communication stream while the next one is computed.  Mode P: block of
+// rank `to` goes to `to` (ring step i: to = rank+1+i, from = rank-1-i; own
+// block last); recv [G][T_loc][dv/G] from every rank.  Mode N: blocks in rank
+// order, each all-gathered: recv [block][G src][T_loc][dv/G].
+mlStatus bag_blocks(mlGroup_* g, const mlBagShape& s, mlOutMode mode, const void* V_shard,
+                    const int32_t* idx_all, const float* w_all, FwdBufs& b, cudaStream_t st) {
+  const int G = g->tr->G, r = g->tr->rank;
+  const int dvG = s.dv / G;
+  const int64_t e = int64_t(dtype_size(s.dtype));
+  const size_t blk_bytes = size_t(s.T) * dvG * e;
+  const mlBagShape bs{s.N, dvG, s.T, s.B, s.dtype, ML_F32};
+  const bool p2p = mode == ML_OUT_ALLTOALL && g->tr->has_p2p();
+  const bool pipelined = p2p || mode == ML_OUT_ALLGATHER;
+  // measurement mode (ml_set_serial): the exchange runs on the caller's
+  // stream, so each collective's timing event brackets it alone
+  cudaStream_t cs = serial_mode() ? st : g->comm;
+  if (pipelined) ML_TRY(dep(st, cs, g->ev[0]));    // inputs of the exchange are ready
+  for (int i = 0; i < G; ++i) {
+    const int blk = mode == ML_OUT_ALLTOALL ? (r + 1 + i) % G : i;
+    char* yp = static_cast<char*>(b.y_part) + size_t(blk) * blk_bytes;
+    ML_TRY((embbag_fwd(&bs, V_shard, idx_all + int64_t(blk) * s.T * s.B,
+                                   w_all + int64_t(blk) * s.T * s.B, nullptr, yp, nullptr, st)));
+    if (!pipelined) continue;
+    ML_CUDA_TRY(cudaEventRecord(g->blk[size_t(i)], st));
+    ML_CUDA_TRY(cudaStreamWaitEvent(cs, g->blk[size_t(i)], 0));
+    if (p2p) {
+      const int from = ((r - 1 - i) % G + G) % G;
+      ML_TRY(g->tr->sendrecv(yp, blk, static_cast<char*>(b.recv) + size_t(from) * blk_bytes, from,
+                             blk_bytes, cs));
+    } else {
+      ML_TRY(g->tr->all_gather(yp, static_cast<char*>(b.recv) + size_t(blk) * G * blk_bytes,
+                               blk_bytes, cs));
+    }
+  }
+  if (pipelined) return dep(cs, st, g->ev[1]);
+  return g->tr->all_to_all(b.y_part, b.recv, blk_bytes, st);
+}
+
+}  // namespace
+}  // namespace ml
+
+extern "C" {
+
+mlStatus ml_group_unique_id(void* id) {
+  ML_API_BEGIN_X
+  if (!id) return fail(ML_ERR_ARG, "null id");
+  if (!nccl().ok) return fail(ML_ERR_NCCL, "libnccl.so.2 not found");
+  ncclUniqueId u;
+  ML_NCCL_TRY(nccl().getUniqueId(&u));
+  memcpy(id, &u, sizeof(u));
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus ml_group_init(const void* id, int G, int rank, mlGroup* out) {
+  ML_API_BEGIN_X
+  if (!id || !out) return fail(ML_ERR_ARG, "null argument");
+  if (G < 1 || rank < 0 || rank >= G) return fail(ML_ERR_CONFIG, "group: need 0 <= rank < G");
+  if (!nccl().ok) return fail(ML_ERR_NCCL, "libnccl.so.2 not found");
+  auto* t = new NcclTransport();
+  t->G = G;
+  t->rank = rank;
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof(u));
+  const ncclResult_t r = nccl().commInitRank(&t->comm, G, u, rank);
+  if (r != ncclSuccess) {
+    delete t;
+    return fail(ML_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().errorString(r));
+  }
+  auto* g = new mlGroup_();
+  g->tr = t;
+  const mlStatus st = group_make(g);
+  if (st != ML_OK) return st;
+  *out = g;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus ml_group_hub_create(int G, void** hub) {
+  ML_API_BEGIN_X
+  if (!hub || G < 1) return fail(ML_ERR_ARG, "hub: need G >= 1");
+  *hub = new Hub(G);
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus ml_group_hub_destroy(void* hub) {
+  delete static_cast<Hub*>(hub);
+  return ML_OK;
+}
+
+mlStatus ml_group_init_hub(void* hub, int rank, mlGroup* out) {
+  ML_API_BEGIN_X
+  if (!hub || !out) return fail(ML_ERR_ARG, "null argument");
+  Hub* h = static_cast<Hub*>(hub);
+  if (rank < 0 || rank >= h->G) return fail(ML_ERR_CONFIG, "group: need 0 <= rank < G");
+  auto* t = new HubTransport();
+  t->G = h->G;
+  t->rank = rank;
+  t->hub = h;
+  auto* g = new mlGroup_();
+  g->tr = t;
+  ML_TRY(group_make(g));
+  *out = g;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus ml_group_destroy(mlGroup g) {
+  ML_API_BEGIN_X
+  if (!g) return ML_OK;
+  cudaStreamSynchronize(g->comm);
+  cudaStreamSynchronize(g->aux);
+  cudaStreamSynchronize(g->prep);
+  for (auto e : g->ev) cudaEventDestroy(e);
+  for (auto e : g->blk) cudaEventDestroy(e);
+  cudaEventDestroy(g->state_ready);
+  cudaStreamDestroy(g->comm);
+  cudaStreamDestroy(g->aux);
+  cudaStreamDestroy(g->prep);
+  delete g->tr;
+  delete g;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus ml_group_info(mlGroup g, int* G, int* rank) {
+  if (!g) return fail(ML_ERR_ARG, "null group");
+  if (G) *G = g->tr->G;
+  if (rank) *rank = g->tr->rank;
+  return ML_OK;
+}
+
+// ------------------------------------------------------------ bag level
+mlStatus embbag_fwd_group_workspace(mlGroup g, const mlBagShape* shape, mlOutMode mode, size_t* bytes) {
+  ML_API_BEGIN_X
+  ML_TRY(check_group_shape(g, shape, mode));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  FwdBufs b;
+  fwd_carve(c, g, *shape, mode, b);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus embbag_fwd_group(mlGroup g, const mlBagShape* shape, const void* V_shard,
+                          const int32_t* idx_local, const float* w_local, int32_t* idx_all,
+                          float* w_all, mlOutMode mode, void* y, void* ws, size_t ws_bytes,
+                          void* stream) {
+  ML_API_BEGIN_X
+  ML_TRY(check_group_shape(g, shape, mode));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int G = g->tr->G;
+  if (shape->T == 0) return ML_OK;
+  if (!V_shard || !idx_local || !w_local || !idx_all || !w_all || !y || !ws)
+    return fail(ML_ERR_ARG, "null pointer argument");
+  size_t need = 0;
+  ML_TRY(embbag_fwd_group_workspace(g, shape, mode, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_fwd_group: workspace too small");
+  Carver c(ws);
+  FwdBufs b;
+  fwd_carve(c, g, *shape, mode, b);
+  ML_TRY(gather_iw(g, *shape, idx_local, w_local, idx_all, w_all, b, st));
+  ML_TRY(bag_blocks(g, *shape, mode, V_shard, idx_all, w_all, b, st));
+  const size_t blk_bytes = size_t(shape->T) * (shape->dv / G) * dtype_size(shape->dtype);
+  if (mode == ML_OUT_ALLTOALL)
+    return ml_group_unpack(b.recv, G, shape->T, shape->dv, nullptr, y, nullptr, shape->dtype, st);
+  for (int blk = 0; blk < G; ++blk)
+    ML_TRY((ml_group_unpack(static_cast<char*>(b.recv) + size_t(blk) * G * blk_bytes, G,
+                                        shape->T, shape->dv, nullptr,
+                                        static_cast<char*>(y) + size_t(blk) * G * blk_bytes, nullptr,
+                                        shape->dtype, st)));
+  return ML_OK;
+  ML_API_END_X
+}
+
+struct BwdGroupBufs { void* dy_send; void* dy_recv; float* dw_part; void* state; void* bag_ws; };
+static mlStatus bwd_carve(Carver& c, const mlGroup_* g, const mlBagShape& s, BwdGroupBufs& b,
+                          bool own_state) {
+  const int G = g->tr->G;
+  const int64_t e = int64_t(dtype_size(s.dtype));
+  const mlBagShape bs = shard_shape(g, s);
+  b.dy_send = c.take<char>(int64_t(s.T) * s.dv * e);
+  b.dy_recv = c.take<char>(int64_t(G) * s.T * (s.dv / G) * e);
+  b.dw_part = c.take<float>(int64_t(G) * s.T * s.B);
+  size_t sb = 0, wb = 0;
+  ML_TRY((embbag_bwd_state_bytes(&bs, &sb)));
+  ML_TRY((embbag_bwd_workspace(&bs, &wb)));
+  b.state = own_state ? c.take<char>(sb) : nullptr;
+  b.bag_ws = c.take<char>(wb);
+  return ML_OK;
+}
+
+mlStatus embbag_bwd_group_workspace(mlGroup g, const mlBagShape* shape, mlOutMode mode, size_t* bytes) {
+  ML_API_BEGIN_X
+  ML_TRY(check_group_shape(g, shape, mode));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  BwdGroupBufs b;
+  ML_TRY(bwd_carve(c, g, *shape, b, true));
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus embbag_bwd_group_state_bytes(mlGroup g, const mlBagShape* shape, size_t* bytes) {
+  ML_API_BEGIN_X
+  ML_TRY(check_group_shape(g, shape, ML_OUT_ALLTOALL));
+  const mlBagShape bs = shard_shape(g, *shape);
+  return embbag_bwd_state_bytes(&bs, bytes);
+  ML_API_END_X
+}
+
+mlStatus embbag_bwd_group(mlGroup g, const mlBagShape* shape, const void* V_shard,
+                          const int32_t* idx_all, const float* w_all, const void* dy,
+                          mlOutMode mode, const void* state, size_t state_bytes, int32_t* rows,
+                          void* dV_shard, int32_t* U, float* dw_local, void* ws, size_t ws_bytes,
+                          void* stream) {
+  ML_API_BEGIN_X
+  ML_TRY(check_group_shape(g, shape, mode));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int G = g->tr->G, r = g->tr->rank;
+  if (!U) return fail(ML_ERR_ARG, "null U");
+  if (shape->T == 0) {
+    ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
+    return ML_OK;
+  }
+  if (!V_shard || !idx_all || !w_all || !dy || !rows || !dV_shard || !dw_local || !ws)
+    return fail(ML_ERR_ARG, "null pointer argument");
+  size_t need = 0;
+  ML_TRY(embbag_bwd_group_workspace(g, shape, mode, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_bwd_group: workspace too small");
+  Carver c(ws);
+  BwdGroupBufs b;
+  ML_TRY(bwd_carve(c, g, *shape, b, true));
+  const mlBagShape bs = shard_shape(g, *shape);
+  const int dvG = shape->dv / G;
+  const size_t e = dtype_size(shape->dtype);
+  if (mode == ML_OUT_ALLTOALL) {
+    // dy of this rank's tokens -> [G][T_loc][dv/G] -> slice g to rank g
+    ML_TRY((ml_group_pack(dy, G, shape->T, shape->dv, b.dy_send, shape->dtype, st)));
+    ML_TRY(g->tr->all_to_all(b.dy_send, b.dy_recv, size_t(shape->T) * dvG * e, st));
+  } else {
+    // dy replicated [G*T_loc, dv]: this rank's column slice
+    ML_CUDA_TRY(cudaMemcpy2DAsync(b.dy_recv, size_t(dvG) * e, static_cast<const char*>(dy) + size_t(r) * dvG * e,
+                                  size_t(shape->dv) * e, size_t(dvG) * e, size_t(G) * shape->T,
+                                  cudaMemcpyDeviceToDevice, st));
+  }
+  size_t wb = 0, sb = 0;
+  ML_TRY((embbag_bwd_workspace(&bs, &wb)));
+  ML_TRY((embbag_bwd_state_bytes(&bs, &sb)));
+  if (state) {
+    if (state_bytes < sb) return fail(ML_ERR_WORKSPACE, "embbag_bwd_group: state too small");
+    ML_CUDA_TRY(cudaStreamWaitEvent(st, g->state_ready, 0));
+  } else {
+    ML_TRY((embbag_bwd_prepare(&bs, idx_all, b.state, sb, st)));
+    state = b.state;
+  }
+  ML_TRY((embbag_bwd_state(&bs, V_shard, w_all, b.dy_recv, state, sb, rows, dV_shard, U,
+                                       b.dw_part, b.bag_ws, wb, st)));
+  // partial dw (a dot over this rank's dv/G columns) summed over the shards
+  return g->tr->reduce_scatter_f32(b.dw_part, dw_local, size_t(shape->T) * shape->B, st);
+  ML_API_END_X
+}
+
+// the backward's inverse index map of idx_all, on the group's preparation
+// stream (ordered after the caller's work so far); embbag_bwd_group /
+// memory_layer_bwd_group wait for it
+mlStatus embbag_bwd_group_prepare(mlGroup g, const mlBagShape* shape, const int32_t* idx_all,
+                                  void* state, size_t state_bytes, void* stream) {
+  ML_API_BEGIN_X
+  ML_TRY(check_group_shape(g, shape, ML_OUT_ALLTOALL));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const mlBagShape bs = shard_shape(g, *shape);
+  cudaStream_t ps = serial_mode() ? st : g->prep;
+  ML_TRY(dep(st, ps, g->ev[2]));
+  ML_TRY((embbag_bwd_prepare(&bs, idx_all, state, state_bytes, ps)));
+  ML_CUDA_TRY(cudaEventRecord(g->state_ready, ps));
+  return ML_OK;
+  ML_API_END_X
+}
+
+// ------------------------------------------------------------ layer level
+static mlStatus check_layer_group(const mlGroup_* g, const mlLayerShape* s, mlOutMode mode) {
+  if (!s) return fail(ML_ERR_ARG, "null shape");
+  if (!s->gated) return fail(ML_ERR_UNSUPPORTED, "memory_layer_*_group: the gated (Memory+) layer only");
+  const mlBagShape b{s->N, s->dv, s->pkm.T, s->pkm.H * s->pkm.k, s->pkm.dtype, s->grad_dtype};
+  return check_group_shape(g, &b, mode);
+}
+static mlBagShape bag_of_layer(const mlLayerShape& s) {
+  return mlBagShape{s.N, s.dv, s.pkm.T, s.pkm.H * s.pkm.k, s.pkm.dtype, s.grad_dtype};
+}
+
+struct LayerFwdGroupBufs { FwdBufs f; void* pkm_ws; size_t pkm_bytes; void* z; void* gemm_ws; };
+static mlStatus layer_fwd_group_carve(Carver& c, const mlGroup_* g, const mlLayerShape& s,
+                                      mlOutMode mode, LayerFwdGroupBufs& b) {
+  fwd_carve(c, g, bag_of_layer(s), mode, b.f);
+  ML_TRY((pkm_topk_workspace(&s.pkm, &b.pkm_bytes)));
+  b.pkm_ws = c.take<char>(b.pkm_bytes);
+  b.z = c.take<char>(int64_t(s.pkm.T) * s.dv * int64_t(dtype_size(s.pkm.dtype)));
+  b.gemm_ws = c.take<char>(kGemmWs);
+  return ML_OK;
+}
+
+mlStatus memory_layer_fwd_group_workspace(mlGroup g, const mlLayerShape* shape, mlOutMode mode,
+                                          size_t* bytes) {
+  ML_API_BEGIN_X
+  ML_TRY(check_layer_group(g, shape, mode));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  LayerFwdGroupBufs b;
+  ML_TRY(layer_fwd_group_carve(c, g, *shape, mode, b));
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus memory_layer_fwd_group(mlGroup g, const mlLayerShape* shape, mlOutMode mode, const void* x,
+                                const void* q, const void* K1, const void* K2, const void* V_shard,
+                                const void* W1, const void* W2, void* out, int32_t* idx_saved,
+                                float* w_saved, int32_t* idx_all, float* w_all, void* g_saved,
+                                void* y_saved, void* y_all, void* state, size_t state_bytes,
+                                void* ws, size_t ws_bytes, void* stream) {
+  ML_API_BEGIN_X
+  ML_TRY(check_layer_group(g, shape, mode));
+  const mlLayerShape& s = *shape;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int G = g->tr->G, r = g->tr->rank;
+  const int T = s.pkm.T;
+  if (T == 0) return ML_OK;
+  if (!x || !q || !K1 || !K2 || !V_shard || !W1 || !W2 || !out || !idx_saved || !w_saved ||
+      !idx_all || !w_all || !g_saved || !y_saved || !ws)
+    return fail(ML_ERR_ARG, "null pointer argument");
+  if (mode == ML_OUT_ALLGATHER && !y_all) return fail(ML_ERR_ARG, "mode N needs y_all");
+  size_t need = 0;
+  ML_TRY(memory_layer_fwd_group_workspace(g, shape, mode, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "memory_layer_fwd_group: workspace too small");
+  Carver c(ws);
+  LayerFwdGroupBufs b;
+  ML_TRY(layer_fwd_group_carve(c, g, s, mode, b));
+  const mlBagShape bag = bag_of_layer(s);
+  const mlDtype dt = s.pkm.dtype;
+  // g = x W1 on the aux stream, concurrent with the lookup and the exchange
+  cudaStream_t as = serial_mode() ? st : g->aux;
+  ML_TRY(dep(st, as, g->ev[3]));
+  ML_TRY((ml_gemm(0, 0, T, s.dv, s.D, x, s.D, W1, s.dv, g_saved, s.dv, dt, 0, b.gemm_ws,
+                              kGemmWs, as)));
+  // own tokens' product-key lookup, then the (idx, w) all-gather
+  ML_TRY((pkm_topk(&s.pkm, q, K1, K2, idx_saved, w_saved, nullptr, b.pkm_ws, b.pkm_bytes, st)));
+  ML_TRY(gather_iw(g, bag, idx_saved, w_saved, idx_all, w_all, b.f, st));
+  if (state) ML_TRY(embbag_bwd_group_prepare(g, &bag, idx_all, state, state_bytes, st));
+  ML_TRY(bag_blocks(g, bag, mode, V_shard, idx_all, w_all, b.f, st));
+  ML_TRY(dep(as, st, g->ev[4]));                   // g ready
+  const size_t blk_bytes = size_t(T) * (s.dv / G) * dtype_size(dt);
+  const void* own = mode == ML_OUT_ALLTOALL ? b.f.recv
+                                            : static_cast<const char*>(b.f.recv) + size_t(r) * G * blk_bytes;
+  ML_TRY((ml_group_unpack(own, G, T, s.dv, g_saved, y_saved, b.z, dt, st)));
+  if (mode == ML_OUT_ALLGATHER)
+    for (int blk = 0; blk < G; ++blk)
+      ML_TRY((ml_group_unpack(static_cast<char*>(b.f.recv) + size_t(blk) * G * blk_bytes, G, T,
+                                          s.dv, nullptr, static_cast<char*>(y_all) + size_t(blk) * G * blk_bytes,
+                                          nullptr, dt, st)));
+  return ml_gemm(0, 0, T, s.D, s.dv, b.z, s.dv, W2, s.D, out, s.D, dt, 0, b.gemm_ws, kGemmWs, st);
+  ML_API_END_X
+}
+
+struct LayerBwdGroupBufs {
+  BwdGroupBufs bag; void *dz, *z, *dy, *dg, *gemm_ws, *gemm_ws2, *pkm_ws; size_t pkm_bytes;
+  float* dw_local;
+};
+static mlStatus layer_bwd_group_carve(Carver& c, const mlGroup_* g, const mlLayerShape& s,
+                                      LayerBwdGroupBufs& b) {
+  const int64_t act = int64_t(s.pkm.T) * s.dv * int64_t(dtype_size(s.pkm.dtype));
+  ML_TRY(bwd_carve(c, g, bag_of_layer(s), b.bag, true));
+  b.dz = c.take<char>(act);
+  b.z = c.take<char>(act);
+  b.dy = c.take<char>(act);
+  b.dg = c.take<char>(act);
+  b.gemm_ws = c.take<char>(kGemmWs);
+  b.gemm_ws2 = c.take<char>(kGemmWs);
+  ML_TRY((pkm_topk_bwd_workspace(&s.pkm, &b.pkm_bytes)));
+  b.pkm_ws = c.take<char>(b.pkm_bytes);
+  b.dw_local = c.take<float>(int64_t(s.pkm.T) * s.pkm.H * s.pkm.k);
+  return ML_OK;
+}
+
+mlStatus memory_layer_bwd_group_workspace(mlGroup g, const mlLayerShape* shape, size_t* bytes) {
+  ML_API_BEGIN_X
+  ML_TRY(check_layer_group(g, shape, ML_OUT_ALLTOALL));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  LayerBwdGroupBufs b;
+  ML_TRY(layer_bwd_group_carve(c, g, *shape, b));
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus memory_layer_bwd_group(mlGroup g, const mlLayerShape* shape, const void* dout,
+                                const void* x, const void* q, const void* K1, const void* K2,
+                                const void* V_shard, const void* W1, const void* W2,
+                                const int32_t* idx_saved, const float* w_saved,
+                                const int32_t* idx_all, const float* w_all, const void* g_saved,
+                                const void* y_saved, const void* state, size_t state_bytes, void* dx,
+                                float* dq, float* dK1, float* dK2, int32_t* dV_rows, void* dV_shard,
+                                int32_t* U, float* dW1, float* dW2, float* dw_out, void* ws,
+                                size_t ws_bytes, void* stream) {
+  ML_API_BEGIN_X
+  ML_TRY(check_layer_group(g, shape, ML_OUT_ALLTOALL));
+  const mlLayerShape& s = *shape;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int T = s.pkm.T;
+  if (!U) return fail(ML_ERR_ARG, "null U");
+  if (T == 0) {
+    ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
+    return ML_OK;
+  }
+  if (!dout || !x || !q || !K1 || !K2 || !V_shard || !W1 || !W2 || !idx_saved || !w_saved ||
+      !idx_all || !w_all || !g_saved || !y_saved || !dx || !dq || !dK1 || !dK2 || !dV_rows ||
+      !dV_shard || !dW1 || !dW2 || !ws)
+    return fail(ML_ERR_ARG, "null pointer argument");
+  size_t need = 0;
+  ML_TRY(memory_layer_bwd_group_workspace(g, shape, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "memory_layer_bwd_group: workspace too small");
+  Carver c(ws);
+  LayerBwdGroupBufs b;
+  ML_TRY(layer_bwd_group_carve(c, g, s, b));
+  const mlDtype dt = s.pkm.dtype;
+  // gate backward (Eq. 2) on own tokens; weight gradients on the aux stream
+  ML_TRY((ml_gemm(0, 1, T, s.dv, s.D, dout, s.D, W2, s.D, b.dz, s.dv, dt, 0, b.gemm_ws,
+                              kGemmWs, st)));
+  ML_TRY((ml_gate_bwd(b.dz, g_saved, y_saved, b.z, b.dy, b.dg, int64_t(T) * s.dv, dt, st)));
+  cudaStream_t as = serial_mode() ? st : g->aux;
+  ML_TRY(dep(st, as, g->ev[5]));
+  ML_TRY((ml_gemm(1, 0, s.dv, s.D, T, b.z, s.dv, dout, s.D, dW2, s.D, dt, 1, b.gemm_ws2,
+                              kGemmWs, as)));
+  ML_TRY((ml_gemm(1, 0, s.D, s.dv, T, x, s.D, b.dg, s.dv, dW1, s.dv, dt, 1, b.gemm_ws2,
+                              kGemmWs, as)));
+  ML_TRY((ml_gemm(0, 1, T, s.D, s.dv, b.dg, s.dv, W1, s.dv, dx, s.D, dt, 0, b.gemm_ws2,
+                              kGemmWs, as)));
+  // bag backward over the group: dy slices all-to-all, local sorted
+  // reduction (dV stays here), reduce-scatter of the partial dw
+  const mlBagShape bag = bag_of_layer(s);
+  size_t bw = 0;
+  ML_TRY(embbag_bwd_group_workspace(g, &bag, ML_OUT_ALLTOALL, &bw));
+  // b.bag was carved first from ws by the same bwd_carve, so the bag-level
+  // call re-carves exactly that region from its start (b.bag.dy_send)
+  ML_TRY((embbag_bwd_group(g, &bag, V_shard, idx_all, w_all, b.dy, ML_OUT_ALLTOALL, state,
+                                       state_bytes, dV_rows, dV_shard, U, b.dw_local, b.bag.dy_send,
+                                       bw, st)));
+  ML_TRY((pkm_topk_bwd(&s.pkm, q, K1, K2, idx_saved, w_saved, b.dw_local, dq, dK1, dK2,
+                                   b.pkm_ws, b.pkm_bytes, st)));
+  if (dw_out)
+    ML_CUDA_TRY(cudaMemcpyAsync(dw_out, b.dw_local, sizeof(float) * size_t(T) * s.pkm.H * s.pkm.k,
+                                cudaMemcpyDeviceToDevice, st));
+  return dep(as, st, g->ev[6]);                    // join the weight gradients
+  ML_API_END_X
+}
+
+}  // extern "C"

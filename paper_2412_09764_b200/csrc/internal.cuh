@@ -4,6 +4,9 @@
 
 namespace ml {
 
+// ml_set_serial(1) in force: every library stream is the caller's stream
+bool serial_mode();
+
 // ------------------------------------------------------------ bag forward
 // out[b, out_col0 + c] = sum_{j<B} w[b,j] * V[idx[b,j], c]   for c < dv
 // (optionally gated: out = y * silu(gate[b, c]); y_ungated gets y).

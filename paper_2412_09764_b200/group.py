@@ -234,3 +234,40 @@ class GroupMemoryLayer:
             L.join(dW1, dW2, dx, z, dg)
         return dict(dx=dx, dq=dq, dK1=dK1, dK2=dK2, dW1=dW1, dW2=dW2, rows=rows, dV=dV, U=U,
                     dw=dw.view(T_loc, H, k))
+
+
+# --------------------------------------------------------------- C-ABI group
+def nccl_group(pg=None):
+    """Bootstraps the library's NCCL memory group (include/memlayer.h
+    ml_group_init) over a torch.distributed process group: rank 0 creates the
+    128-byte ncclUniqueId, torch.distributed broadcasts it."""
+    import torch.distributed as dist
+    from . import ops
+    rank, G = dist.get_rank(pg), dist.get_world_size(pg)
+    obj = [ops.group_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(pg, 0) if pg is not None else 0, group=pg)
+    return ops.Group.nccl(obj[0], G, rank)
+
+
+class CGroupMemoryLayer:
+    """The memory group through the C ABI (memory_layer_fwd_group /
+    memory_layer_bwd_group): the exchange, its overlap with the bag forward
+    and all local kernels run inside the library."""
+
+    def __init__(self, grp, k, mode="alltoall", dV_dtype=torch.float32):
+        if mode not in ("alltoall", "allgather"):
+            raise ValueError(mode)
+        self.grp, self.k, self.mode, self.dV_dtype = grp, k, mode, dV_dtype
+
+    def forward(self, x, q, K1, K2, V_shard, W1, W2):
+        from . import ops
+        out, saved = ops.memory_layer_fwd_group(self.grp, x, q, K1, K2, V_shard, W1, W2, self.k,
+                                                mode=self.mode)
+        saved.update(x=x, q=q, K1=K1, K2=K2, V=V_shard, W1=W1, W2=W2)
+        return out, saved
+
+    def backward(self, dout, saved, dK1=None, dK2=None):
+        from . import ops
+        return ops.memory_layer_bwd_group(self.grp, dout, saved["x"], saved["q"], saved["K1"],
+                                          saved["K2"], saved["V"], saved["W1"], saved["W2"], saved,
+                                          dK1=dK1, dK2=dK2, dV_dtype=self.dV_dtype, want_dw=True)

@@ -468,3 +468,164 @@ for _name in ("synth_fill", "pkm_topk", "pkm_topk_bwd", "embbag_fwd", "embbag_bw
               "peer_bwd", "group_unpack", "group_pack", "gate_bwd", "gemm", "embbag_bwd_pool"):
     globals()[_name] = _on_device(globals()[_name])
 del _name
+
+
+# ------------------------------------------------------------ memory group (C ABI)
+MODES = {"alltoall": 0, "allgather": 1}
+
+
+class Group:
+    """A memory group handle (include/memlayer.h mlGroup): NCCL (one process
+    per GPU; `unique_id` from group_unique_id() on one rank, broadcast by the
+    caller) or an in-process hub (G ranks as host threads on one device)."""
+
+    def __init__(self, handle):
+        self.h = C.c_void_p(handle)
+        G, r = C.c_int(), C.c_int()
+        check(lib().ml_group_info(self.h, C.byref(G), C.byref(r)))
+        self.size, self.rank = G.value, r.value
+
+    @classmethod
+    def nccl(cls, unique_id, G, rank):
+        out = C.c_void_p()
+        check(lib().ml_group_init(C.c_char_p(bytes(unique_id)), G, rank, C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def from_hub(cls, hub, rank):
+        out = C.c_void_p()
+        check(lib().ml_group_init_hub(C.c_void_p(hub), rank, C.byref(out)))
+        return cls(out.value)
+
+    def close(self):
+        if self.h:
+            check(lib().ml_group_destroy(self.h))
+            self.h = None
+
+
+def group_unique_id():
+    buf = C.create_string_buffer(128)
+    check(lib().ml_group_unique_id(buf))
+    return buf.raw
+
+
+def group_hub(G):
+    out = C.c_void_p()
+    check(lib().ml_group_hub_create(G, C.byref(out)))
+    return out.value
+
+
+def group_hub_destroy(hub):
+    lib().ml_group_hub_destroy(C.c_void_p(hub))
+
+
+def memory_layer_fwd_group(grp, x, q, K1, K2, V_shard, W1, W2, k, mode="alltoall", keep_state=True):
+    """Eq. 1 + Eq. 2 over a dim-sharded memory group (§3.1.2):
+    x/q of this rank's T_loc tokens, V_shard [N, dv/G].  Returns out [T_loc, D]
+    and the saved tensors (idx/w of own and all tokens, g, y, y_all, state)."""
+    G = grp.size
+    T, H, Dk = q.shape
+    dv = V_shard.shape[1] * G
+    sh = LayerShape(PkmShape(T, H, K1.shape[1], Dk, k, _dt(q), 0), V_shard.shape[0], dv, x.shape[1],
+                    1, _lib.ML_F32)
+    dev = q.device
+    md = MODES[mode]
+    out = torch.empty((T, x.shape[1]), dtype=q.dtype, device=dev)
+    idx = torch.empty((T, H, k), dtype=torch.int32, device=dev)
+    w = torch.empty((T, H, k), dtype=torch.float32, device=dev)
+    idx_all = torch.empty((G * T, H, k), dtype=torch.int32, device=dev)
+    w_all = torch.empty((G * T, H, k), dtype=torch.float32, device=dev)
+    g = torch.empty((T, dv), dtype=q.dtype, device=dev)
+    y = torch.empty((T, dv), dtype=q.dtype, device=dev)
+    y_all = torch.empty((G * T, dv), dtype=q.dtype, device=dev) if md == 1 else None
+    state, nst = None, 0
+    if keep_state:
+        bs = BagShape(V_shard.shape[0], dv, T, H * k, _dt(q), _lib.ML_F32)
+        nst = _size(lambda b, p: lib().embbag_bwd_group_state_bytes(grp.h, b, p), bs)
+        state = torch.empty((max(nst, 1),), dtype=torch.uint8, device=dev)
+    n = _size(lambda b, p: lib().memory_layer_fwd_group_workspace(grp.h, b, md, p), sh)
+    ws = workspace(n, dev, tag="group_fwd")
+    check(lib().memory_layer_fwd_group(grp.h, C.byref(sh), md, _p(x), _p(q), _p(K1), _p(K2),
+                                       _p(V_shard), _p(W1), _p(W2), _p(out), _p(idx), _p(w),
+                                       _p(idx_all), _p(w_all), _p(g), _p(y), _p(y_all), _p(state),
+                                       nst, _p(ws), n, _stream()))
+    return out, dict(idx=idx, w=w, idx_all=idx_all, w_all=w_all, g=g, y=y, y_all=y_all, k=k,
+                     state=state, state_bytes=nst, mode=mode)
+
+
+def memory_layer_bwd_group(grp, dout, x, q, K1, K2, V_shard, W1, W2, saved, dK1=None, dK2=None,
+                           dV_dtype=torch.float32, want_dw=False):
+    """Backward of memory_layer_fwd_group: dx, dq, dK1/dK2 (accumulate; this
+    rank's tokens' part), compact dV of the shard (rows[:U], dV[:U]), dW1,
+    dW2 (this rank's part), dw of own tokens (want_dw)."""
+    G = grp.size
+    T, H, Dk = q.shape
+    k = saved["k"]
+    dv = V_shard.shape[1] * G
+    sh = LayerShape(PkmShape(T, H, K1.shape[1], Dk, k, _dt(q), 0), V_shard.shape[0], dv, x.shape[1],
+                    1, _DT[dV_dtype])
+    dev = q.device
+    P = G * T * H * k
+    dx = torch.empty_like(x)
+    dq = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    if dK1 is None:
+        dK1 = torch.zeros(K1.shape, dtype=torch.float32, device=dev)
+    if dK2 is None:
+        dK2 = torch.zeros(K2.shape, dtype=torch.float32, device=dev)
+    rows = torch.empty(P, dtype=torch.int32, device=dev)
+    dV = torch.empty((P, V_shard.shape[1]), dtype=dV_dtype, device=dev)
+    U = torch.empty(1, dtype=torch.int32, device=dev)
+    dW1 = torch.empty(W1.shape, dtype=torch.float32, device=dev)
+    dW2 = torch.empty(W2.shape, dtype=torch.float32, device=dev)
+    dw = torch.empty((T, H, k), dtype=torch.float32, device=dev) if want_dw else None
+    n = _size(lambda b, p: lib().memory_layer_bwd_group_workspace(grp.h, b, p), sh)
+    ws = workspace(n, dev, tag="group_bwd")
+    check(lib().memory_layer_bwd_group(
+        grp.h, C.byref(sh), _p(dout), _p(x), _p(q), _p(K1), _p(K2), _p(V_shard), _p(W1), _p(W2),
+        _p(saved["idx"]), _p(saved["w"]), _p(saved["idx_all"]), _p(saved["w_all"]), _p(saved["g"]),
+        _p(saved["y"]), _p(saved["state"]), saved["state_bytes"], _p(dx), _p(dq), _p(dK1), _p(dK2),
+        _p(rows), _p(dV), _p(U), _p(dW1), _p(dW2), _p(dw), _p(ws), n, _stream()))
+    return LayerGrads(dx=dx, dq=dq, dK1=dK1, dK2=dK2, rows=rows, dV=dV, U=U, dW1=dW1, dW2=dW2, dw=dw)
+
+
+def embbag_fwd_group(grp, V_shard, idx, w, mode="alltoall"):
+    """Bag level: returns y (alltoall: [T_loc, dv]; allgather: [G*T_loc, dv]),
+    idx_all, w_all [G*T_loc, B]."""
+    G = grp.size
+    T, B = idx.shape
+    dv = V_shard.shape[1] * G
+    sh = BagShape(V_shard.shape[0], dv, T, B, _dt(V_shard), _lib.ML_F32)
+    md = MODES[mode]
+    y = torch.empty(((G if md == 1 else 1) * T, dv), dtype=V_shard.dtype, device=V_shard.device)
+    idx_all = torch.empty((G * T, B), dtype=torch.int32, device=V_shard.device)
+    w_all = torch.empty((G * T, B), dtype=torch.float32, device=V_shard.device)
+    n = _size(lambda b, p: lib().embbag_fwd_group_workspace(grp.h, b, md, p), sh)
+    ws = workspace(n, V_shard.device, tag="group_fwd")
+    check(lib().embbag_fwd_group(grp.h, C.byref(sh), _p(V_shard), _p(idx), _p(w), _p(idx_all),
+                                 _p(w_all), md, _p(y), _p(ws), n, _stream()))
+    return y, idx_all, w_all
+
+
+def embbag_bwd_group(grp, V_shard, idx_all, w_all, dy, mode="alltoall", grad_dtype=torch.float32):
+    """Bag level backward: rows, dV_shard (capacity), device U, dw_local [T_loc, B]."""
+    G = grp.size
+    TG, B = idx_all.shape
+    T = TG // G
+    dv = V_shard.shape[1] * G
+    sh = BagShape(V_shard.shape[0], dv, T, B, _dt(V_shard), _DT[grad_dtype])
+    md = MODES[mode]
+    rows = torch.empty(TG * B, dtype=torch.int32, device=V_shard.device)
+    dV = torch.empty((TG * B, V_shard.shape[1]), dtype=grad_dtype, device=V_shard.device)
+    U = torch.empty(1, dtype=torch.int32, device=V_shard.device)
+    dw = torch.empty((T, B), dtype=torch.float32, device=V_shard.device)
+    n = _size(lambda b, p: lib().embbag_bwd_group_workspace(grp.h, b, md, p), sh)
+    ws = workspace(n, V_shard.device, tag="group_bwd")
+    check(lib().embbag_bwd_group(grp.h, C.byref(sh), _p(V_shard), _p(idx_all), _p(w_all), _p(dy),
+                                 md, None, 0, _p(rows), _p(dV), _p(U), _p(dw), _p(ws), n, _stream()))
+    return rows, dV, U, dw
+
+
+for _name in ("memory_layer_fwd_group", "memory_layer_bwd_group", "embbag_fwd_group",
+              "embbag_bwd_group"):
+    globals()[_name] = _on_device(globals()[_name])
+del _name

@@ -24,7 +24,9 @@ def test_header_parsed():
               "memory_layer_bwd", "memory_layer_state_bytes", "memory_layer_fwd_state",
               "memory_layer_bwd_state", "peer_fwd", "peer_bwd", "embbag_bwd_prepare",
               "embbag_bwd_state", "ml_last_error",
-              "ml_synth_fill"):
+              "ml_synth_fill", "ml_group_init", "ml_group_destroy", "ml_group_unique_id",
+              "embbag_fwd_group", "embbag_bwd_group", "memory_layer_fwd_group",
+              "memory_layer_bwd_group"):
         assert n in names
 
 
@@ -120,3 +122,21 @@ def test_state_and_peer_queries_and_validation():
                                 None)
     assert st == _lib.ML_ERR_WORKSPACE
     assert lib.memory_layer_state_wait(None, None) == _lib.ML_ERR_ARG
+
+
+def test_group_bootstrap_on_host():
+    """The NCCL unique id (the group bootstrap, P:167's process group) is made
+    without a GPU, or ML_ERR_NCCL names a missing libnccl; the in-process hub
+    is created and destroyed on the host."""
+    lib = _lib.lib()
+    buf = C.create_string_buffer(128)
+    st = lib.ml_group_unique_id(buf)
+    assert st in (_lib.ML_OK, _lib.ML_ERR_NCCL), st
+    if st == _lib.ML_OK:
+        assert any(buf.raw)
+    hub = C.c_void_p()
+    assert lib.ml_group_hub_create(2, C.byref(hub)) == _lib.ML_OK and hub.value
+    assert lib.ml_group_hub_destroy(hub) == _lib.ML_OK
+    assert lib.ml_group_hub_create(0, C.byref(hub)) == _lib.ML_ERR_ARG
+    out = C.c_void_p()
+    assert lib.ml_group_init(buf, 2, 5, C.byref(out)) in (_lib.ML_ERR_CONFIG, _lib.ML_ERR_NCCL)
