@@ -98,6 +98,11 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            # first queries outside the timed region (the first NVML query of a
+            # process can stall the driver for tens of milliseconds)
+            for _ in range(3):
+                pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+                pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         except Exception:
             self.nv = None
 
@@ -394,13 +399,14 @@ def run_ours(args, cfg, world, rank, local):
     step = build_step(args, cfg, t, ops, torch, comm)
     T_loc = tokens_per_rank(cfg, G)
 
+    clk = ClockSampler(local)          # NVML initialised and queried before the warm-up
     for _ in range(args.warmup):
         out, g = step()
     torch.cuda.synchronize()
 
     # ---- headline: device events around K steps, library timing OFF
     launches0 = ops.launch_count()
-    with ClockSampler(local) as clk:
+    with clk:
         ms, out, g = time_steps(step, args.steps, world, torch, dev)
     launches = ops.launch_count() - launches0
     U = int((g["U"] if isinstance(g, dict) else g.U).item())
