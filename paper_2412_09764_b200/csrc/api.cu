@@ -237,11 +237,9 @@ static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
     if (!c.base) b.ds_dense = reinterpret_cast<__nv_bfloat16*>(1);  // measuring: mark dense
     return;
   }
-  if (s.qk_norm) {
-    b.ds1w = c.take<float>(P);
-    b.ds2w = c.take<float>(P);
-  }
-  sort_carve(c, P, ceil_log2(int64_t(s.H) * s.S), b.sort);
+  b.ds1w = c.take<float>(P);
+  b.ds2w = c.take<float>(P);
+  sort_carve(c, P, ceil_log2(int64_t(s.H) * s.S + 1), b.sort);
   runs_carve(c, P, b.runs);
   seg_carve(c, P, s.Dk / 2, s.dtype, &b.partial, &b.counters);
 }
@@ -315,21 +313,19 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
                              true, b.gemm_ws, kGemmWs, st, 1.f));
     }
   } else {
+    // sparse: per (t, h, half) the selected sub-keys deduplicated (ds summed
+    // per distinct sub-key, the other slots get the sentinel key H*S)
     ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, nullptr, qn,
                               b.ds1w, b.ds2w, st));
-    const int bits = ceil_log2(HS);
+    // dq_half[t,h] = sum_a ds_half[a] K_half[h, a]   (one warp per (t, h))
+    float* dq_target = dq;
+    ML_TRY(launch_pkm_dq(s, b.key1, b.key2, b.ds1w, b.ds2w, K1, K2, dq_target, st));
+    const int bits = ceil_log2(HS + 1);
     for (int half = 0; half < 2; ++half) {
-      const void* K = half ? K2 : K1;
       const int32_t* key = half ? b.key2 : b.key1;
-      const float* wts = s.qk_norm ? (half ? b.ds2w : b.ds1w) : b.ds;
-      // dq_half[t,h] = sum_j ds_j K_half[h, a_j]  (a bag over the [H*S, Dh] table)
-      BagFwdArgs a;
-      a.V = K; a.ldv = Dh; a.N = HS;
-      a.idx = key; a.w = wts; a.B = s.k; a.nbags = s.T * s.H; a.dv = Dh;
-      a.out = dq; a.ldo = s.Dk; a.out_col0 = half * Dh; a.out_f32 = true; a.dtype = s.dtype;
-      a.name = "pkm_dq_bag";
-      ML_TRY(launch_bag_fwd(a, st));
-      // dK_half[h, a] += sum ds * q_half[t,h]  (sorted segments, dense accumulate)
+      const float* wts = half ? b.ds2w : b.ds1w;
+      // dK_half[h, a] += sum ds * q_half[t,h]  (sorted segments, dense
+      // accumulate; the sentinel slots sort last and are skipped)
       int32_t *skey, *spos;
       ML_TRY(sort_pairs(key, P, bits, b.sort, &skey, &spos, st));
       ML_TRY(find_runs(skey, P, b.runs, nullptr, nullptr, st));
@@ -337,6 +333,7 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
       g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = wts;
       g.src = q; g.lds = s.Dk; g.src_col0 = half * Dh; g.B = s.k;
       g.out = half ? dKo2 : dKo1; g.ldo = Dh; g.dense_accumulate = true;
+      g.row_limit = int32_t(HS);
       g.partial = b.partial; g.counters = b.counters; g.dv = Dh; g.dtype = s.dtype;
       g.name = "pkm_dK_segreduce";
       ML_TRY(launch_segreduce(g, st));

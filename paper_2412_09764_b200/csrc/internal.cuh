@@ -94,6 +94,7 @@ struct SegArgs {
   float* dw_part = nullptr;
   float* out = nullptr; int64_t ldo = 0; bool dense_accumulate = false;
   bool out_bf16 = false;             // out holds bf16 rows (grad_dtype ML_BF16)
+  int32_t row_limit = INT32_MAX;     // dense form: keys >= row_limit are sentinels (skipped)
   float* partial = nullptr; int32_t* counters = nullptr;
   int32_t dv = 0; mlDtype dtype = ML_BF16;
   const char* name = "segreduce";  // timing / profiling label
@@ -136,6 +137,10 @@ mlStatus launch_pkm_select_tc(const mlPkmShape& sh, const void* q, const void* K
 mlStatus launch_cand_fallback(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
                               uint64_t* cand, int32_t* cnt, const int32_t* fail_rows,
                               const int32_t* fail_n, cudaStream_t s);
+// dq from the deduplicated (key, ds) slots of softmax_bwd's sparse form
+mlStatus launch_pkm_dq(const mlPkmShape& sh, const int32_t* key1, const int32_t* key2,
+                       const float* ds1, const float* ds2, const void* K1, const void* K2,
+                       float* dq, cudaStream_t s);
 // exact half top-k of each row's candidates, then the combine + softmax
 mlStatus launch_combine_cand(const mlPkmShape& sh, const uint64_t* cand, const int32_t* cnt,
                              int32_t* idx, float* w, float* score, cudaStream_t s);

@@ -820,13 +820,23 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
     sc1 = qn.qinv[th * 2 + 0] * qn.kinv1[int64_t(h) * S + ix / S];
     sc2 = qn.qinv[th * 2 + 1] * qn.kinv2[int64_t(h) * S + ix % S];
   }
-  if (lane < k) {
-    ds[o] = dsv;
-    key1[o] = h * S + ix / S;
-    key2[o] = h * S + ix % S;
-    if (ds1w) {
-      ds1w[o] = dsv * sc1;
-      ds2w[o] = dsv * sc2;
+  if (lane < k) ds[o] = dsv;
+  if (!ds_dense) {
+    // sparse form: per half, the lanes selecting the same sub-key are summed
+    // by the lowest one (lane order: deterministic); the others get the
+    // sentinel key H*S and weight 0 (sorted last, skipped by the reduction)
+    const int sub1 = lane < k ? ix / S : -1 - lane, sub2 = lane < k ? ix % S : -1 - lane;
+    const float v1 = dsv * sc1, v2 = dsv * sc2;
+    const unsigned g1 = __match_any_sync(FULL, sub1), g2 = __match_any_sync(FULL, sub2);
+    float s1 = 0.f, s2 = 0.f;
+    for (unsigned m = g1; m; m &= m - 1) s1 += __shfl_sync(g1, v1, __ffs(m) - 1);
+    for (unsigned m = g2; m; m &= m - 1) s2 += __shfl_sync(g2, v2, __ffs(m) - 1);
+    const bool l1 = (__ffs(g1) - 1) == lane, l2 = (__ffs(g2) - 1) == lane;
+    if (lane < k) {
+      key1[o] = l1 ? h * S + sub1 : H * S;
+      key2[o] = l2 ? h * S + sub2 : H * S;
+      ds1w[o] = l1 ? s1 : 0.f;
+      ds2w[o] = l2 ? s2 : 0.f;
     }
   }
   if (ds_dense) {
@@ -869,6 +879,76 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
       __syncwarp();
       uint4* dst = reinterpret_cast<uint4*>(ds_dense + th * 2 * S);
       for (int c = lane; c < (2 * S) / 8; c += 32) dst[c] = reinterpret_cast<const uint4*>(rows)[c];
+    }
+  }
+}
+
+// dq[t, h, half] = sum over the distinct selected sub-keys a of
+// ds_half[t,h,a] * K_half[h, a, :] (the deduplicated slots of softmax_bwd:
+// sentinel slots skipped), one warp per (t, h), fp32 accumulation in slot
+// order.  Each lane owns 16-byte column vectors; 4 rows in flight.
+template <typename T>
+__global__ void __launch_bounds__(256) pkm_dq_kernel(const int32_t* key1, const int32_t* key2,
+                                                     const float* ds1, const float* ds2,
+                                                     const T* K1, const T* K2, int64_t TH, int HS,
+                                                     int Dh, int k, float* dq) {
+  constexpr int VEC = Vec<T>::N;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t th = int64_t(blockIdx.x) * 8 + wid;
+  if (th >= TH) return;
+  const int nv = Dh / VEC;                 // 16-byte vectors per key row
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const int32_t* key = half ? key2 : key1;
+    const float* dsw = half ? ds2 : ds1;
+    const T* K = half ? K2 : K1;
+    int32_t kk = HS;
+    float wv = 0.f;
+    if (lane < k) {
+      kk = key[th * k + lane];
+      wv = dsw[th * k + lane];
+    }
+    const unsigned valid = __ballot_sync(FULL, kk < HS);
+    float* out = dq + (th * 2 + half) * int64_t(Dh);
+#pragma unroll 1
+    for (int v0 = lane; v0 < ((nv + 31) & ~31); v0 += 32) {
+      float acc[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
+      const bool act = v0 < nv;
+      unsigned m = valid;
+      while (m) {
+        int ls[4];
+        int n = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ls[u] = m ? __ffs(m) - 1 : -1;
+          if (m) { m &= m - 1; ++n; }
+        }
+        uint4 raw[4];
+        float wg[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int src = ls[u] < 0 ? 0 : ls[u];
+          const int32_t row = __shfl_sync(FULL, kk, src);
+          wg[u] = __shfl_sync(FULL, wv, src);
+          raw[u] = (act && u < n) ? ldg_nc_v4(K + int64_t(row) * Dh + int64_t(v0) * VEC)
+                                  : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (u >= n) break;
+          float f[VEC];
+          Vec<T>::load(raw[u], f);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[e] = fmaf(wg[u], f[e], acc[e]);
+        }
+      }
+      if (act) {
+        float4* o4 = reinterpret_cast<float4*>(out + int64_t(v0) * VEC);
+#pragma unroll
+        for (int e = 0; e < VEC; e += 4) o4[e / 4] = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+      }
     }
   }
 }
@@ -964,4 +1044,25 @@ mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const floa
   return ML_OK;
 }
 
+}  // namespace ml
+
+namespace ml {
+mlStatus launch_pkm_dq(const mlPkmShape& sh, const int32_t* key1, const int32_t* key2,
+                       const float* ds1, const float* ds2, const void* K1, const void* K2,
+                       float* dq, cudaStream_t s) {
+  const int64_t TH = int64_t(sh.T) * sh.H;
+  if (TH <= 0) return ML_OK;
+  const int Dh = sh.Dk / 2;
+  const int HS = sh.H * sh.S;
+  if (sh.dtype == ML_BF16)
+    pkm_dq_kernel<__nv_bfloat16><<<unsigned((TH + 7) / 8), 256, 0, s>>>(
+        key1, key2, ds1, ds2, static_cast<const __nv_bfloat16*>(K1),
+        static_cast<const __nv_bfloat16*>(K2), TH, HS, Dh, sh.k, dq);
+  else
+    pkm_dq_kernel<float><<<unsigned((TH + 7) / 8), 256, 0, s>>>(
+        key1, key2, ds1, ds2, static_cast<const float*>(K1), static_cast<const float*>(K2), TH, HS,
+        Dh, sh.k, dq);
+  ML_LAUNCH_CHECK("pkm_dq");
+  return ML_OK;
+}
 }  // namespace ml

@@ -55,6 +55,7 @@ struct SegParams {
   float* partial; int32_t* counters; int64_t nslots_cap;
   int32_t* ticket;   // work-item counter of the persistent kernel (zeroed)
   int32_t vec_units;  // 16-byte vectors per row (whole dv)
+  int32_t row_limit;  // keys >= row_limit (sorted last) are skipped (sentinels)
 };
 
 constexpr int kChunk = 64;                   // positions whose pieces a team owns
@@ -273,6 +274,8 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int slice = blockIdx.y;
   const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+  // sentinel keys sort last: a chunk that starts on one has nothing to do
+  if (c0 < p.P && p.skey[c0] >= p.row_limit) return;
   if (tid == 0) {
     s_range[0] = 0x7fffffff;
     s_range[1] = -1;
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
     const int64_t i = c0 + k;
     int fl = 0, t = 0, key = 0, pos = 0, r = 0, rb = 0, re = 0;
     float w = 0.f;
-    if (i < p.P) {
+    if (i < p.P && p.skey[i] < p.row_limit) {
       pos = p.spos[i];
       const bool clamped = pos < 0;   // index outside [0, N): row 0, weight 0
       pos &= ~kClampedPos;
@@ -815,6 +818,9 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
   p.partial = a.partial; p.counters = a.counters; p.nslots_cap = nslots_cap(a.P);
   p.ticket = a.counters + 2 * int64_t(ns) * p.nslots_cap;
   p.vec_units = int32_t(vu);
+  p.row_limit = a.row_limit;
+  if (a.row_limit != INT32_MAX && !a.dense_accumulate)
+    return fail(ML_ERR_UNSUPPORTED, "segreduce: sentinel keys need the dense-accumulating form");
   timing_mark(nullptr, s);
   ML_CUDA_TRY(cudaMemsetAsync(a.counters, 0, sizeof(int32_t) * (2 * size_t(ns) * size_t(p.nslots_cap) + 1), s));
   timing_mark("memset", s);
