@@ -45,7 +45,7 @@ step = ks[a:b]
 tot = sum(t for _, t in step)
 out = io.StringIO()
 out.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none (cold cache, serialised)\n")
-out.write(f"# command: python bench.py --steps 2 --warmup 3 --no-cpu-baseline ; {len(ks)} launches\n")
+out.write(f"# command: python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-variants ; {len(ks)} launches\n")
 out.write(f"# one steady-state step = launches {a}..{b - 1}: {len(step)} launches, {tot:.1f} us serialised\n")
 out.write("# us        share  kernel\n")
 for n, t in step:
@@ -97,6 +97,30 @@ for x in r[2:]:
     for key, lab in LABEL.items():
         if name.startswith(key):
             traffic[lab] = int(rd + wr)
+# tensor-pipe utilisation of the tcgen05 scoring kernel (a1)
+tmets = ["sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+         "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+         "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]
+rawt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rt = list(csv.reader(io.StringIO(rawt)))
+tutil = {}
+for x in rt[2:]:
+    nm = short(x[rt[0].index("Kernel Name")])
+    if nm.startswith("pkm_scores_tc"):
+        vals = {}
+        for m in tmets:
+            if m in rt[0]:
+                try:
+                    vals[m.split(".", 2)[-1] if m.startswith("TPC") else m] = float(
+                        x[rt[0].index(m)].replace(",", ""))
+                except ValueError:
+                    pass
+        tutil["pkm_scores_tc"] = vals
+        out.write(f"\n# {nm}: tensor pipe " + ", ".join(f"{k} = {v:.1f} %" for k, v in vals.items()) + "\n")
+if tutil:
+    tu = os.path.join(ROOT, "profiles", "tensor_util.json")
+    json.dump({"_note": f"ncu --set full (profiles/{tag}_ncu_summary.txt), C2", "c2": tutil},
+              open(tu, "w"), indent=1, sort_keys=True)
 open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt"), "w").write(out.getvalue())
 tf = os.path.join(ROOT, "profiles", "traffic.json")
 allt = json.load(open(tf)) if os.path.exists(tf) else {}
