@@ -469,6 +469,32 @@ def run_ours(args, cfg, world, rank, local):
                 variants=variants)
 
 
+def pin_to_gpu_numa_node(index):
+    """Run this process on the CPUs local to the GPU (its PCI device's
+    local_cpulist) so the pinned staging buffers allocated next are first
+    touched -- and placed -- on the GPU's NUMA node.  Best effort."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        bus = pynvml.nvmlDeviceGetPciInfo(pynvml.nvmlDeviceGetHandleByIndex(index)).busId
+        bus = bus.decode() if isinstance(bus, bytes) else bus
+        bus = bus.lower()
+        if bus.count(":") == 2 and len(bus.split(":")[0]) == 8:   # 00000000:1b:00.0
+            bus = bus[4:]
+        txt = open(f"/sys/bus/pci/devices/{bus}/local_cpulist").read().strip()
+        cpus = set()
+        for part in txt.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        pass
+    return None
+
+
 def run_e2e(args, t, step, torch, tokens_per_step, world):
     """End to end through the public API with HOST buffers: every step copies
     its inputs (q, x, dout) from pinned host memory and copies the result
@@ -477,7 +503,10 @@ def run_e2e(args, t, step, torch, tokens_per_step, world):
     layer); all of it is inside the timed region."""
     stream = torch.cuda.current_stream()
     names = ("q", "x", "dout")
+    aff = os.sched_getaffinity(0)
+    numa_cpus = pin_to_gpu_numa_node(t["q"].device.index)
     hostbufs = {n: t[n].cpu().pin_memory() for n in names}
+    os.sched_setaffinity(0, aff)           # the pages stay where they were first touched
     h2d = sum(hostbufs[n].numel() * hostbufs[n].element_size() for n in names)
     dbuf = [{n: torch.empty_like(t[n]) for n in names} for _ in range(2)]
     copy = torch.cuda.Stream()      # uploads
@@ -532,6 +561,9 @@ def run_e2e(args, t, step, torch, tokens_per_step, world):
     return {"value": tokens_per_step / (ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
             "note": "pinned host inputs uploaded on a copy stream, double-buffered against compute; "
+                    "results downloaded on a second copy stream; host buffers on the GPU's NUMA "
+                    f"node ({numa_cpus} local CPUs)" if numa_cpus else
+                    "pinned host inputs uploaded on a copy stream, double-buffered against compute; "
                     "results downloaded on a second copy stream"}
 
 
