@@ -41,6 +41,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the caching allocator grows by mapping pages into expandable segments
+# instead of cudaMalloc-ing new ones (a 10-200 ms host stall when it happens
+# inside a timed step with tens of GB of per-step buffers, C5)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 CONFIGS = {
     # T: tokens per rank (weak scaling); T_global: fixed global batch split over the ranks
@@ -119,6 +123,8 @@ class ClockSampler:
             time.sleep(0.02)
 
     def __enter__(self):
+        if os.environ.get("BENCH_NO_CLOCKS") == "1":
+            self.nv = None
         if self.nv:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
@@ -360,12 +366,28 @@ def time_steps(step, steps, world, torch, dev):
     gc.collect()
     gc.disable()         # no collector pause between launches inside the timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    diag = os.environ.get("BENCH_STEP_TIMES") == "1"
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)] if diag else None
+    if diag:
+        m0 = torch.cuda.memory_stats()
+    h0 = time.perf_counter()
     e0.record(stream)
-    for _ in range(steps):
+    for i in range(steps):
+        if diag:
+            ev[i].record(stream)
         out, g = step()
+    if diag:
+        ev[steps].record(stream)
     e1.record(stream)
+    h1 = time.perf_counter()
     torch.cuda.synchronize()
     gc.enable()
+    if diag:
+        m1 = torch.cuda.memory_stats()
+        keys = ("segment.all.allocated", "num_alloc_retries", "num_device_alloc", "num_device_free")
+        print("step ms:", [round(ev[i].elapsed_time(ev[i + 1]), 3) for i in range(steps)],
+              f"host enqueue {1e3 * (h1 - h0) / steps:.3f} ms/step",
+              {k: m1.get(k, 0) - m0.get(k, 0) for k in keys}, file=sys.stderr)
     barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
@@ -400,9 +422,14 @@ def run_ours(args, cfg, world, rank, local):
     T_loc = tokens_per_rank(cfg, G)
 
     clk = ClockSampler(local)          # NVML initialised and queried before the warm-up
-    for _ in range(args.warmup):
-        out, g = step()
-    torch.cuda.synchronize()
+    # the memory-group paths allocate per step on several streams: more
+    # warm-up steps until the caching allocator's pool is settled
+    n_warm = args.warmup if comm is None else max(args.warmup, 8)
+    for _ in range(n_warm):            # same pattern as the timed loop: the previous
+        out, g = step()                # step's results alive while the next one runs
+    del out, g                         # ... but none across the timed region: one more live
+    torch.cuda.synchronize()           # generation made the allocator grow (a cudaMalloc,
+                                       # up to tens of ms) inside the timed steps
 
     # ---- headline: device events around K steps, library timing OFF
     launches0 = ops.launch_count()
@@ -437,7 +464,8 @@ def run_ours(args, cfg, world, rank, local):
         a2.dv_dtype = "bf16"
         vstep = build_step(a2, cfg, t, ops, torch, comm)
         for _ in range(args.warmup):
-            vstep()
+            o_, g_ = vstep()
+        del o_, g_
         ms_v, _, _ = time_steps(vstep, args.steps, world, torch, dev)
         variants = {"dV_bf16": {"ms_per_step": round(ms_v / args.steps, 4),
                                 "value": tokens_per_step / (ms_v / args.steps / 1e3),
@@ -454,7 +482,8 @@ def run_ours(args, cfg, world, rank, local):
         # collectives replaced by local copies
         ref_step = build_step(args, cfg, t, ops, torch, LoopbackComm(world, rank, others))
         for _ in range(max(2, args.warmup // 2)):
-            ref_step()
+            o_, g_ = ref_step()
+        del o_, g_
         ms_ref, _, _ = time_steps(ref_step, args.steps, world, torch, dev)
         eff = {"t_G_ms": round(ms_step, 4), "t_ref_ms": round(ms_ref / args.steps, 4),
                "E": round((ms_ref / args.steps) / ms_step, 4),

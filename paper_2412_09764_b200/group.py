@@ -101,13 +101,14 @@ class CudaLocal:
             return state, ev
         if getattr(self, "_bg", None) is None:
             self._bg = torch.cuda.Stream(device=idx.device)
-        self._bg.wait_stream(cur)
+        self._bg.wait_stream(cur)           # also orders it after the previous backward
         with torch.cuda.stream(self._bg):
-            state = self.ops.embbag_bwd_prepare(N, dv, idx, dtype)
+            # one persistent state buffer (allocated once, on this stream)
+            state = self.ops.embbag_bwd_prepare(N, dv, idx, dtype, out=getattr(self, "_state", None))
+            self._state = state
             ev = torch.cuda.Event()
             ev.record(self._bg)
         idx.record_stream(self._bg)
-        state.record_stream(cur)
         return state, ev
 
     def wait(self, ev):
@@ -120,8 +121,12 @@ class CudaLocal:
         return self.ops.embbag_fwd(V, idx, w)
 
     def embbag_bwd(self, V, idx, w, dy, state=None):
+        # outputs reused across calls (valid until the next backward): the
+        # capacity-sized dV is the largest allocation of the step
+        if not hasattr(self, "_bufs"):
+            self._bufs = {}
         rows, dV, U, dw = self.ops.embbag_bwd(V, idx, w, dy, sync=False, state=state,
-                                              grad_dtype=self.dV_dtype)
+                                              grad_dtype=self.dV_dtype, bufs=self._bufs)
         return rows, dV, U, dw
 
     def pkm_topk_bwd(self, q, K1, K2, idx, w, dw, dK1, dK2):
@@ -258,6 +263,7 @@ class CGroupMemoryLayer:
         if mode not in ("alltoall", "allgather"):
             raise ValueError(mode)
         self.grp, self.k, self.mode, self.dV_dtype = grp, k, mode, dV_dtype
+        self.bufs = {}      # backward outputs, reused across steps (valid until the next one)
 
     def forward(self, x, q, K1, K2, V_shard, W1, W2):
         from . import ops
@@ -270,4 +276,5 @@ class CGroupMemoryLayer:
         from . import ops
         return ops.memory_layer_bwd_group(self.grp, dout, saved["x"], saved["q"], saved["K1"],
                                           saved["K2"], saved["V"], saved["W1"], saved["W2"], saved,
-                                          dK1=dK1, dK2=dK2, dV_dtype=self.dV_dtype, want_dw=True)
+                                          dK1=dK1, dK2=dK2, dV_dtype=self.dV_dtype, want_dw=True,
+                                          bufs=self.bufs)

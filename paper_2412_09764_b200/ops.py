@@ -162,7 +162,18 @@ def embbag_fwd(V, idx, w, gate_pre=None, return_ungated=False):
     return (y, yu) if return_ungated else y
 
 
-def embbag_bwd(V, idx, w, dy, sync=True, state=None, grad_dtype=torch.float32):
+def _buf(bufs, name, shape, dtype, device):
+    """A reusable output buffer (bufs: a caller-owned dict; None -> fresh)."""
+    if bufs is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    t = bufs.get(name)
+    if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != device:
+        t = torch.empty(shape, dtype=dtype, device=device)
+        bufs[name] = t
+    return t
+
+
+def embbag_bwd(V, idx, w, dy, sync=True, state=None, grad_dtype=torch.float32, bufs=None):
     """"reverse_indices" backward.  Returns rows [U] int32 (ascending),
     dV [U, dv] (grad_dtype: fp32, or bf16 for a bf16 table), dw [T,B] fp32
     (sync=True trims to U on the host); with sync=False returns the
@@ -170,10 +181,10 @@ def embbag_bwd(V, idx, w, dy, sync=True, state=None, grad_dtype=torch.float32):
     state: from embbag_bwd_prepare(N, dv, idx) (skips the sort)."""
     sh = bag_shape(V, idx, grad_dtype)
     P = idx.numel()
-    rows = torch.empty(P, dtype=torch.int32, device=V.device)
-    dV = torch.empty((P, V.shape[1]), dtype=grad_dtype, device=V.device)
-    U = torch.empty(1, dtype=torch.int32, device=V.device)
-    dw = torch.empty(idx.shape, dtype=torch.float32, device=V.device)
+    rows = _buf(bufs, "rows", (P,), torch.int32, V.device)
+    dV = _buf(bufs, "dV", (P, V.shape[1]), grad_dtype, V.device)
+    U = _buf(bufs, "U", (1,), torch.int32, V.device)
+    dw = _buf(bufs, "dw", tuple(idx.shape), torch.float32, V.device)
     n = _size(lib().embbag_bwd_workspace, sh)
     ws = workspace(n, V.device)
     if state is not None:
@@ -188,13 +199,15 @@ def embbag_bwd(V, idx, w, dy, sync=True, state=None, grad_dtype=torch.float32):
     return rows[:u], dV[:u], dw
 
 
-def embbag_bwd_prepare(N, dv, idx, dtype=torch.bfloat16):
+def embbag_bwd_prepare(N, dv, idx, dtype=torch.bfloat16, out=None):
     """The inverse index map of embbag_bwd for indices idx [T,B] into an
     N-row table of width dv (include/memlayer.h embbag_bwd_prepare); returns
-    the state tensor for embbag_bwd(..., state=)."""
+    the state tensor for embbag_bwd(..., state=) (`out`, if large enough, is
+    reused)."""
     sh = BagShape(N, dv, idx.shape[0], idx.shape[1], _DT[dtype])
     n = _size(lib().embbag_bwd_state_bytes, sh)
-    state = torch.empty((max(n, 1),), dtype=torch.uint8, device=idx.device)
+    state = out if (out is not None and out.numel() >= n) else \
+        torch.empty((max(n, 1),), dtype=torch.uint8, device=idx.device)
     check(lib().embbag_bwd_prepare(C.byref(sh), _p(idx), _p(state), n, _stream()))
     return state
 
@@ -554,7 +567,7 @@ def memory_layer_fwd_group(grp, x, q, K1, K2, V_shard, W1, W2, k, mode="alltoall
 
 
 def memory_layer_bwd_group(grp, dout, x, q, K1, K2, V_shard, W1, W2, saved, dK1=None, dK2=None,
-                           dV_dtype=torch.float32, want_dw=False):
+                           dV_dtype=torch.float32, want_dw=False, bufs=None):
     """Backward of memory_layer_fwd_group: dx, dq, dK1/dK2 (accumulate; this
     rank's tokens' part), compact dV of the shard (rows[:U], dV[:U]), dW1,
     dW2 (this rank's part), dw of own tokens (want_dw)."""
@@ -566,18 +579,18 @@ def memory_layer_bwd_group(grp, dout, x, q, K1, K2, V_shard, W1, W2, saved, dK1=
                     1, _DT[dV_dtype])
     dev = q.device
     P = G * T * H * k
-    dx = torch.empty_like(x)
-    dq = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    dx = _buf(bufs, "dx", tuple(x.shape), x.dtype, dev)
+    dq = _buf(bufs, "dq", tuple(q.shape), torch.float32, dev)
     if dK1 is None:
         dK1 = torch.zeros(K1.shape, dtype=torch.float32, device=dev)
     if dK2 is None:
         dK2 = torch.zeros(K2.shape, dtype=torch.float32, device=dev)
-    rows = torch.empty(P, dtype=torch.int32, device=dev)
-    dV = torch.empty((P, V_shard.shape[1]), dtype=dV_dtype, device=dev)
-    U = torch.empty(1, dtype=torch.int32, device=dev)
-    dW1 = torch.empty(W1.shape, dtype=torch.float32, device=dev)
-    dW2 = torch.empty(W2.shape, dtype=torch.float32, device=dev)
-    dw = torch.empty((T, H, k), dtype=torch.float32, device=dev) if want_dw else None
+    rows = _buf(bufs, "rows", (P,), torch.int32, dev)
+    dV = _buf(bufs, "dV", (P, V_shard.shape[1]), dV_dtype, dev)
+    U = _buf(bufs, "U", (1,), torch.int32, dev)
+    dW1 = _buf(bufs, "dW1", tuple(W1.shape), torch.float32, dev)
+    dW2 = _buf(bufs, "dW2", tuple(W2.shape), torch.float32, dev)
+    dw = _buf(bufs, "dw", (T, H, k), torch.float32, dev) if want_dw else None
     n = _size(lambda b, p: lib().memory_layer_bwd_group_workspace(grp.h, b, p), sh)
     ws = workspace(n, dev, tag="group_bwd")
     check(lib().memory_layer_bwd_group(
