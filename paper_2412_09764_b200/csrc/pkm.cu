@@ -886,13 +886,15 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
 // dq[t, h, half] = sum over the distinct selected sub-keys a of
 // ds_half[t,h,a] * K_half[h, a, :] (the deduplicated slots of softmax_bwd:
 // sentinel slots skipped), one warp per (t, h), fp32 accumulation in slot
-// order.  Each lane owns 16-byte column vectors; 4 rows in flight.
-template <typename T>
+// order.  Lane l owns the 16-byte column vectors l, l + 32, ... (NV of them);
+// 8 key rows are loaded per batch (8 * NV vectors in flight per lane).
+template <typename T, int NV>
 __global__ void __launch_bounds__(256) pkm_dq_kernel(const int32_t* key1, const int32_t* key2,
                                                      const float* ds1, const float* ds2,
                                                      const T* K1, const T* K2, int64_t TH, int HS,
                                                      int Dh, int k, float* dq) {
   constexpr int VEC = Vec<T>::N;
+  constexpr int BATCH = 8;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t th = int64_t(blockIdx.x) * 8 + wid;
   if (th >= TH) return;
@@ -908,47 +910,53 @@ __global__ void __launch_bounds__(256) pkm_dq_kernel(const int32_t* key1, const 
       kk = key[th * k + lane];
       wv = dsw[th * k + lane];
     }
-    const unsigned valid = __ballot_sync(FULL, kk < HS);
-    float* out = dq + (th * 2 + half) * int64_t(Dh);
-#pragma unroll 1
-    for (int v0 = lane; v0 < ((nv + 31) & ~31); v0 += 32) {
-      float acc[VEC];
+    unsigned m = __ballot_sync(FULL, kk < HS);
+    float acc[NV][VEC];
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
-      const bool act = v0 < nv;
-      unsigned m = valid;
-      while (m) {
-        int ls[4];
-        int n = 0;
+    for (int c = 0; c < NV; ++c)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          ls[u] = m ? __ffs(m) - 1 : -1;
-          if (m) { m &= m - 1; ++n; }
+      for (int e = 0; e < VEC; ++e) acc[c][e] = 0.f;
+    while (m) {
+      int32_t row[BATCH];
+      float wg[BATCH];
+      int n = 0;
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        const int src = m ? __ffs(m) - 1 : 0;
+        row[u] = __shfl_sync(FULL, kk, src);
+        wg[u] = __shfl_sync(FULL, wv, src);
+        if (m) { m &= m - 1; ++n; }
+      }
+      uint4 raw[BATCH][NV];
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+          const int v = lane + 32 * c;
+          raw[u][c] = (u < n && v < nv) ? ldg_nc_v4(K + int64_t(row[u]) * Dh + int64_t(v) * VEC)
+                                        : make_uint4(0, 0, 0, 0);
         }
-        uint4 raw[4];
-        float wg[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int src = ls[u] < 0 ? 0 : ls[u];
-          const int32_t row = __shfl_sync(FULL, kk, src);
-          wg[u] = __shfl_sync(FULL, wv, src);
-          raw[u] = (act && u < n) ? ldg_nc_v4(K + int64_t(row) * Dh + int64_t(v0) * VEC)
-                                  : make_uint4(0, 0, 0, 0);
-        }
+      for (int u = 0; u < BATCH; ++u) {
+        if (u >= n) break;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (u >= n) break;
+        for (int c = 0; c < NV; ++c) {
           float f[VEC];
-          Vec<T>::load(raw[u], f);
+          Vec<T>::load(raw[u][c], f);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[e] = fmaf(wg[u], f[e], acc[e]);
+          for (int e = 0; e < VEC; ++e) acc[c][e] = fmaf(wg[u], f[e], acc[c][e]);
         }
       }
-      if (act) {
-        float4* o4 = reinterpret_cast<float4*>(out + int64_t(v0) * VEC);
+    }
+    float* out = dq + (th * 2 + half) * int64_t(Dh);
 #pragma unroll
-        for (int e = 0; e < VEC; e += 4) o4[e / 4] = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
-      }
+    for (int c = 0; c < NV; ++c) {
+      const int v = lane + 32 * c;
+      if (v >= nv) continue;
+      float4* o4 = reinterpret_cast<float4*>(out + int64_t(v) * VEC);
+#pragma unroll
+      for (int e = 0; e < VEC; e += 4)
+        o4[e / 4] = make_float4(acc[c][e], acc[c][e + 1], acc[c][e + 2], acc[c][e + 3]);
     }
   }
 }
@@ -1054,14 +1062,24 @@ mlStatus launch_pkm_dq(const mlPkmShape& sh, const int32_t* key1, const int32_t*
   if (TH <= 0) return ML_OK;
   const int Dh = sh.Dk / 2;
   const int HS = sh.H * sh.S;
-  if (sh.dtype == ML_BF16)
-    pkm_dq_kernel<__nv_bfloat16><<<unsigned((TH + 7) / 8), 256, 0, s>>>(
-        key1, key2, ds1, ds2, static_cast<const __nv_bfloat16*>(K1),
-        static_cast<const __nv_bfloat16*>(K2), TH, HS, Dh, sh.k, dq);
-  else
-    pkm_dq_kernel<float><<<unsigned((TH + 7) / 8), 256, 0, s>>>(
-        key1, key2, ds1, ds2, static_cast<const float*>(K1), static_cast<const float*>(K2), TH, HS,
-        Dh, sh.k, dq);
+  const unsigned grid = unsigned((TH + 7) / 8);
+  if (sh.dtype == ML_BF16) {
+    const auto* k1 = static_cast<const __nv_bfloat16*>(K1);
+    const auto* k2 = static_cast<const __nv_bfloat16*>(K2);
+    const int nvl = (Dh / 8 + 31) / 32;
+    if (nvl <= 1) pkm_dq_kernel<__nv_bfloat16, 1><<<grid, 256, 0, s>>>(key1, key2, ds1, ds2, k1, k2, TH, HS, Dh, sh.k, dq);
+    else if (nvl <= 2) pkm_dq_kernel<__nv_bfloat16, 2><<<grid, 256, 0, s>>>(key1, key2, ds1, ds2, k1, k2, TH, HS, Dh, sh.k, dq);
+    else if (nvl <= 4) pkm_dq_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(key1, key2, ds1, ds2, k1, k2, TH, HS, Dh, sh.k, dq);
+    else return fail(ML_ERR_UNSUPPORTED, "pkm_dq: Dk/2 > 1024");
+  } else {
+    const auto* k1 = static_cast<const float*>(K1);
+    const auto* k2 = static_cast<const float*>(K2);
+    const int nvl = (Dh / 4 + 31) / 32;
+    if (nvl <= 1) pkm_dq_kernel<float, 1><<<grid, 256, 0, s>>>(key1, key2, ds1, ds2, k1, k2, TH, HS, Dh, sh.k, dq);
+    else if (nvl <= 2) pkm_dq_kernel<float, 2><<<grid, 256, 0, s>>>(key1, key2, ds1, ds2, k1, k2, TH, HS, Dh, sh.k, dq);
+    else if (nvl <= 4) pkm_dq_kernel<float, 4><<<grid, 256, 0, s>>>(key1, key2, ds1, ds2, k1, k2, TH, HS, Dh, sh.k, dq);
+    else return fail(ML_ERR_UNSUPPORTED, "pkm_dq: Dk/2 > 512 (fp32)");
+  }
   ML_LAUNCH_CHECK("pkm_dq");
   return ML_OK;
 }
