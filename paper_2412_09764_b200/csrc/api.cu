@@ -297,6 +297,10 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
     }
     ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, b.ds_dense, qn,
                               nullptr, nullptr, st));
+    if (pkm_bwd_tc_eligible(s)) {
+      // hand-written tcgen05 contractions (pkm_tc_bwd.cu)
+      ML_TRY(launch_pkm_bwd_tc(s, b.ds_dense, q, K1, K2, dq, dKo1, dKo2, st));
+    } else {
     const int64_t lds = int64_t(s.H) * 2 * s.S;  // row pitch of ds_dense per token
     for (int half = 0; half < 2; ++half) {        // one strided-batched GEMM over heads each
       const __nv_bfloat16* A = b.ds_dense + int64_t(half) * s.S;
@@ -311,6 +315,7 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
       ML_TRY(gemm_rm_batched(true, false, s.S, Dh, s.T, A, lds, 2 * int64_t(s.S), qh,
                              int64_t(s.H) * s.Dk, s.Dk, dKh, Dh, int64_t(s.S) * Dh, s.H, ML_BF16,
                              true, b.gemm_ws, kGemmWs, st, 1.f));
+    }
     }
   } else {
     // sparse: per (t, h, half) the selected sub-keys deduplicated (ds summed

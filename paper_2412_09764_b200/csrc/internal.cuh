@@ -137,6 +137,12 @@ mlStatus launch_pkm_select_tc(const mlPkmShape& sh, const void* q, const void* K
 mlStatus launch_cand_fallback(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
                               uint64_t* cand, int32_t* cnt, const int32_t* fail_rows,
                               const int32_t* fail_n, cudaStream_t s);
+// key / query backward contractions on tcgen05 (pkm_tc_bwd.cu): dq = ds K
+// (overwrite), dK1/dK2 += ds^T q, ds the bf16 [T, H, 2, S] matrix
+bool pkm_bwd_tc_eligible(const mlPkmShape& sh);
+mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const void* q,
+                           const void* K1, const void* K2, float* dq, float* dK1, float* dK2,
+                           cudaStream_t s);
 // dq from the deduplicated (key, ds) slots of softmax_bwd's sparse form
 mlStatus launch_pkm_dq(const mlPkmShape& sh, const int32_t* key1, const int32_t* key2,
                        const float* ds1, const float* ds2, const void* K1, const void* K2,
