@@ -218,7 +218,7 @@ static bool pkm_bwd_dense(const mlPkmShape& s) {
 struct PkmBwdBufs {
   float* ds; int32_t* key1; int32_t* key2;
   SortBufs sort; RunBufs runs; float* partial; int32_t* counters;
-  __nv_bfloat16* ds_dense; void* gemm_ws;
+  __nv_bfloat16* ds_dense; __nv_bfloat16* ds_lo; void* gemm_ws;
   QkBufs qk; float* dK_tmp; float* ds1w; float* ds2w;
 };
 static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
@@ -226,7 +226,7 @@ static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
   b.ds = c.take<float>(P);
   b.key1 = c.take<int32_t>(P);
   b.key2 = c.take<int32_t>(P);
-  b.ds_dense = nullptr;
+  b.ds_dense = b.ds_lo = nullptr;
   b.gemm_ws = nullptr;
   b.dK_tmp = b.ds1w = b.ds2w = nullptr;
   qk_carve(c, s, b.qk);
@@ -234,7 +234,11 @@ static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
   if (pkm_bwd_dense(s)) {
     b.ds_dense = c.take<__nv_bfloat16>(int64_t(s.T) * s.H * 2 * s.S);
     b.gemm_ws = c.take<char>(kGemmWs);
-    if (!c.base) b.ds_dense = reinterpret_cast<__nv_bfloat16*>(1);  // measuring: mark dense
+    if (pkm_bwd_split(s)) b.ds_lo = c.take<__nv_bfloat16>(int64_t(s.T) * s.H * 2 * s.S);
+    if (!c.base) {   // measuring: mark dense / split
+      b.ds_dense = reinterpret_cast<__nv_bfloat16*>(1);
+      if (b.ds_lo) b.ds_lo = b.ds_dense;
+    }
     return;
   }
   b.ds1w = c.take<float>(P);
@@ -296,10 +300,11 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
       timing_mark("memset", st);
     }
     ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, b.ds_dense, qn,
-                              nullptr, nullptr, st));
+                              nullptr, nullptr, st, b.ds_lo));
     if (pkm_bwd_tc_eligible(s)) {
-      // hand-written tcgen05 contractions (pkm_tc_bwd.cu)
-      ML_TRY(launch_pkm_bwd_tc(s, b.ds_dense, q, K1, K2, dq, dKo1, dKo2, st));
+      // hand-written tcgen05 contractions (pkm_tc_bwd.cu); with ds_lo the
+      // operand is the bf16 pair hi + lo (two MMAs per k-step)
+      ML_TRY(launch_pkm_bwd_tc(s, b.ds_dense, b.ds_lo, q, K1, K2, dq, dKo1, dKo2, st));
     } else {
     const int64_t lds = int64_t(s.H) * 2 * s.S;  // row pitch of ds_dense per token
     for (int half = 0; half < 2; ++half) {        // one strided-batched GEMM over heads each

@@ -140,7 +140,11 @@ mlStatus launch_cand_fallback(const mlPkmShape& sh, const void* q, const void* K
 // key / query backward contractions on tcgen05 (pkm_tc_bwd.cu): dq = ds K
 // (overwrite), dK1/dK2 += ds^T q, ds the bf16 [T, H, 2, S] matrix
 bool pkm_bwd_tc_eligible(const mlPkmShape& sh);
-mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const void* q,
+// opt-in (ML_PKM_BWD_SPLIT=1): ds carried as a bf16 hi/lo pair into the
+// tcgen05 key backward (needs the tcgen05 path and whole ds rows)
+bool pkm_bwd_split(const mlPkmShape& sh);
+mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const __nv_bfloat16* ds_lo,
+                           const void* q,
                            const void* K1, const void* K2, float* dq, float* dK1, float* dK2,
                            cudaStream_t s);
 // dq from the deduplicated (key, ds) slots of softmax_bwd's sparse form
@@ -164,7 +168,8 @@ bool softmax_bwd_full_rows(const mlPkmShape& sh);
 mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
                             const float* dw_part, int nslices, int64_t slice_stride,
                             float* ds, int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,
-                            const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s);
+                            const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s,
+                            __nv_bfloat16* ds_lo = nullptr);
 
 // ------------------------------------------------------------ gate
 // z = y*silu(g); dy = dz*silu(g); dg = dz*y*silu'(g)   (elementwise, n elems)

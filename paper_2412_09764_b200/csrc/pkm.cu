@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
                                                           int S, int k, float* ds, int32_t* key1,
                                                           int32_t* key2, __nv_bfloat16* ds_dense,
                                                           QkNorm qn, float* ds1w, float* ds2w,
-                                                          int full_rows) {
+                                                          int full_rows, __nv_bfloat16* ds_lo) {
   __shared__ int s_sub[8][2][32];
   __shared__ float s_ds[8][32];
   __shared__ float s_sc[8][2][32];
@@ -852,9 +852,14 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
     s_sc[wid][1][lane] = sc2;
     extern __shared__ __align__(16) __nv_bfloat16 s_rows[];   // [8 warps][2][S] when full_rows
     __nv_bfloat16* rows = s_rows + int64_t(wid) * 2 * S;
+    // split form (ds_lo != NULL, full rows only): ds = hi + lo, both bf16,
+    // hi = RN(ds), lo = RN(ds - hi): the pair carries ~16 significant bits
+    __nv_bfloat16* rows_lo = s_rows + int64_t(8 + wid) * 2 * S;
     if (full_rows) {
       const uint4 z = make_uint4(0, 0, 0, 0);
       for (int c = lane; c < (2 * S) / 8; c += 32) reinterpret_cast<uint4*>(rows)[c] = z;
+      if (ds_lo)
+        for (int c = lane; c < (2 * S) / 8; c += 32) reinterpret_cast<uint4*>(rows_lo)[c] = z;
     }
     __syncwarp();
 #pragma unroll
@@ -871,14 +876,23 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
         }
       }
       if (leader) {
-        if (full_rows) rows[half * S + a] = __float2bfloat16_rn(sum);
-        else ds_dense[(th * 2 + half) * S + a] = __float2bfloat16_rn(sum);
+        const __nv_bfloat16 hi = __float2bfloat16_rn(sum);
+        if (full_rows) {
+          rows[half * S + a] = hi;
+          if (ds_lo) rows_lo[half * S + a] = __float2bfloat16_rn(sum - __bfloat162float(hi));
+        } else {
+          ds_dense[(th * 2 + half) * S + a] = hi;
+        }
       }
     }
     if (full_rows) {
       __syncwarp();
       uint4* dst = reinterpret_cast<uint4*>(ds_dense + th * 2 * S);
       for (int c = lane; c < (2 * S) / 8; c += 32) dst[c] = reinterpret_cast<const uint4*>(rows)[c];
+      if (ds_lo) {
+        uint4* dl = reinterpret_cast<uint4*>(ds_lo + th * 2 * S);
+        for (int c = lane; c < (2 * S) / 8; c += 32) dl[c] = reinterpret_cast<const uint4*>(rows_lo)[c];
+      }
     }
   }
 }
@@ -1034,20 +1048,22 @@ bool softmax_bwd_full_rows(const mlPkmShape& sh) { return sh.S % 8 == 0 && sh.S 
 mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const float* w,
                             const float* dw_part, int nslices, int64_t slice_stride, float* ds,
                             int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,
-                            const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s) {
+                            const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s,
+                            __nv_bfloat16* ds_lo) {
   const int64_t TH = int64_t(sh.T) * sh.H;
   if (TH <= 0) return ML_OK;
   const bool full = ds_dense && softmax_bwd_full_rows(sh);
-  const size_t smem = full ? size_t(8) * 2 * sh.S * sizeof(__nv_bfloat16) : 0;
+  if (ds_lo && !full) return fail(ML_ERR_UNSUPPORTED, "softmax_bwd: the split ds needs full rows");
+  const size_t smem = full ? size_t(ds_lo ? 16 : 8) * 2 * sh.S * sizeof(__nv_bfloat16) : 0;
   static bool attr = false;
   if (full && !attr) {
     ML_CUDA_TRY(cudaFuncSetAttribute(softmax_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(8 * 2 * 2048 * sizeof(__nv_bfloat16))));
+                                     int(16 * 2 * 2048 * sizeof(__nv_bfloat16))));
     attr = true;
   }
   softmax_bwd_kernel<<<unsigned((TH + 7) / 8), 256, smem, s>>>(
       idx, w, dw_part, nslices, slice_stride, TH, sh.H, sh.S, sh.k, ds, key1, key2, ds_dense, qn,
-      ds1w, ds2w, full ? 1 : 0);
+      ds1w, ds2w, full ? 1 : 0, ds_lo);
   ML_LAUNCH_CHECK("softmax_bwd");
   return ML_OK;
 }

@@ -29,6 +29,7 @@ enum Mode { MODE_DQ = 0, MODE_DK = 1 };
 struct BwdParams {
   int T, H, S, Dh, Dk;
   int BN, n_tiles, m_tiles, k_chunks, tiles;
+  int split, stages;         // split: A = hi + lo (two bf16 tiles per stage)
   uint32_t idesc, tmem_cols;
   float* dq;                 // MODE_DQ: [T, H*Dk]
   float* dK1; float* dK2;    // MODE_DK: [H*S, Dh] each, accumulate
@@ -52,14 +53,16 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreadsB, 1)
     pkm_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB1,
                       const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmD,
-                      BwdParams p) {
+                      const __grid_constant__ CUtensorMap tmAlo, BwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t bytes_a = kBM * kBK * 2;
+  const uint32_t bytes_as = bytes_a << p.split;     // A bytes per stage (hi [+ lo])
   const uint32_t bytes_b = uint32_t(p.BN) * kBK * 2;
+  const int stages = p.stages;
   uint8_t* sA = base;
-  uint8_t* sB = base + kStagesB * bytes_a;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStagesB * bytes_b);
+  uint8_t* sB = base + stages * bytes_as;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + stages * bytes_b);
   uint64_t* empty = full + kStagesB;
   uint64_t* tfull = empty + kStagesB;
   uint64_t* tempty = tfull + 2;
@@ -70,7 +73,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStagesB; ++i) {
+    for (int i = 0; i < stages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -84,6 +87,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB1)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
+    if (p.split) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmAlo)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -116,12 +120,13 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         const CUtensorMap* tmB = half ? &tmB2 : &tmB1;
         for (int kc = 0; kc < p.k_chunks; ++kc) {
           mbar_wait_t<true>(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], bytes_a + bytes_b);
-          uint8_t* a = sA + stage * bytes_a;
+          mbar_expect_tx(&full[stage], bytes_as + bytes_b);
+          uint8_t* a = sA + stage * bytes_as;
           uint8_t* b = sB + stage * bytes_b;
           if constexpr (MODE == MODE_DQ) {
             // A = ds (K-major): keys [pr*S + kc*64, +64) x tokens [mt*128, +128)
             tma_load_2d(a, &tmA, &full[stage], pr * p.S + kc * kBK, mt * kBM);
+            if (p.split) tma_load_2d(a + bytes_a, &tmAlo, &full[stage], pr * p.S + kc * kBK, mt * kBM);
             // B = K_half[h] (MN-major): head-dim boxes x keys [h*S + kc*64, +64)
             for (int j = 0; j < nb; ++j)
               tma_load_2d(b + j * 8192, tmB, &full[stage], nt * p.BN + j * 64, h * p.S + kc * kBK);
@@ -129,12 +134,16 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             // A = ds (MN-major): keys [pr*S + mt*128 + j*64, +64) x tokens [kc*64, +64)
             for (int j = 0; j < 2; ++j)
               tma_load_2d(a + j * 8192, &tmA, &full[stage], pr * p.S + mt * kBM + j * 64, kc * kBK);
+            if (p.split)
+              for (int j = 0; j < 2; ++j)
+                tma_load_2d(a + bytes_a + j * 8192, &tmAlo, &full[stage], pr * p.S + mt * kBM + j * 64,
+                            kc * kBK);
             // B = q (MN-major): head-dim boxes of (h, half) x tokens [kc*64, +64)
             for (int j = 0; j < nb; ++j)
               tma_load_2d(b + j * 8192, &tmB1, &full[stage], h * p.Dk + half * p.Dh + nt * p.BN + j * 64,
                           kc * kBK);
           }
-          if (++stage == kStagesB) {
+          if (++stage == stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -154,7 +163,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         for (int kc = 0; kc < p.k_chunks; ++kc) {
           mbar_wait_t<true>(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * bytes_a), b0 = smem_u32(sB + stage * bytes_b);
+          const uint32_t a0 = smem_u32(sA + stage * bytes_as), b0 = smem_u32(sB + stage * bytes_b);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             // K-major: the next 16 K = 32 bytes along the row; MN-major: the
@@ -163,9 +172,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                                                 : desc_sw128(a0 + 2048 * k, 8192, 1024);
             const uint64_t bd = desc_sw128(b0 + 2048 * k, 8192, 1024);
             umma_f16(dcol, ad, bd, p.idesc, (kc | k) != 0 ? 1u : 0u);
+            if (p.split) umma_f16(dcol, ad + ((bytes_a >> 4) & 0x3FFFu), bd, p.idesc, 1u);  // + lo x B
           }
           umma_commit(&empty[stage]);
-          if (++stage == kStagesB) {
+          if (++stage == stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -272,8 +282,19 @@ bool pkm_bwd_tc_eligible(const mlPkmShape& sh) {
   return !off && sh.dtype == ML_BF16 && sh.S % 128 == 0 && Dh % 64 == 0 && sh.T > 0;
 }
 
+bool pkm_bwd_split(const mlPkmShape& sh) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("ML_PKM_BWD_SPLIT");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on && pkm_bwd_tc_eligible(sh) && softmax_bwd_full_rows(sh);
+}
+
 // dq (overwrite) and dK1/dK2 (accumulate) from ds [T, H, 2, S] bf16
-mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const void* q,
+// (ds + ds_lo when ds_lo != NULL)
+mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const __nv_bfloat16* ds_lo,
+                           const void* q,
                            const void* K1, const void* K2, float* dq, float* dK1, float* dK2,
                            cudaStream_t s) {
   const int Dh = sh.Dk / 2;
@@ -285,16 +306,20 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
   p.tmem_cols = 32;
   while (p.tmem_cols < uint32_t(2 * p.BN)) p.tmem_cols <<= 1;
   p.dq = dq; p.dK1 = dK1; p.dK2 = dK2;
+  p.split = ds_lo ? 1 : 0;
+  p.stages = ds_lo ? 3 : kStagesB;
   const uint32_t base_idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(p.BN >> 3) << 17) |
                               (uint32_t(kBM >> 4) << 24);
-  const size_t smem = 1024 + size_t(kStagesB) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 1024 +
+  const size_t smem = 1024 + size_t(p.stages) * ((kBM * kBK * 2 << p.split) + size_t(p.BN) * kBK * 2) + 1024 +
                       size_t(4) * 2 * 1024 * sizeof(float);
   static size_t configured[2] = {0, 0};
   const int grid_max = num_sms();
   // ---- dq = ds K: A K-major (ds rows), B MN-major (key table)
   {
-    CUtensorMap ma, mb1, mb2;
+    CUtensorMap ma, mb1, mb2, mlo;
     ML_TRY(make_map(&ma, ds, uint64_t(HS2), uint64_t(sh.T), uint64_t(HS2) * 2, kBK, kBM));
+    mlo = ma;
+    if (ds_lo) ML_TRY(make_map(&mlo, ds_lo, uint64_t(HS2), uint64_t(sh.T), uint64_t(HS2) * 2, kBK, kBM));
     ML_TRY(make_map(&mb1, K1, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, 64, kBK));
     ML_TRY(make_map(&mb2, K2, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, 64, kBK));
     BwdParams pq = p;
@@ -320,13 +345,15 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return fail(ML_ERR_CUDA, "cuTensorMapEncodeTiled (dq) failed: " + std::to_string(int(r)));
     }
-    pkm_bwd_tc_kernel<MODE_DQ><<<std::min(pq.tiles, grid_max), kThreadsB, smem, s>>>(ma, mb1, mb2, md, pq);
+    pkm_bwd_tc_kernel<MODE_DQ><<<std::min(pq.tiles, grid_max), kThreadsB, smem, s>>>(ma, mb1, mb2, md, mlo, pq);
     ML_LAUNCH_CHECK("pkm_dq_tc");
   }
   // ---- dK += ds^T q: A MN-major (ds, keys along M), B MN-major (q)
   {
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mlo;
     ML_TRY(make_map(&ma, ds, uint64_t(HS2), uint64_t(sh.T), uint64_t(HS2) * 2, 64, kBK));
+    mlo = ma;
+    if (ds_lo) ML_TRY(make_map(&mlo, ds_lo, uint64_t(HS2), uint64_t(sh.T), uint64_t(HS2) * 2, 64, kBK));
     ML_TRY(make_map(&mb, q, uint64_t(sh.H) * sh.Dk, uint64_t(sh.T), uint64_t(sh.H) * sh.Dk * 2, 64, kBK));
     BwdParams pk = p;
     pk.m_tiles = sh.S / kBM;
@@ -338,7 +365,7 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       configured[1] = smem;
     }
-    pkm_bwd_tc_kernel<MODE_DK><<<std::min(pk.tiles, grid_max), kThreadsB, smem, s>>>(ma, mb, mb, mb, pk);
+    pkm_bwd_tc_kernel<MODE_DK><<<std::min(pk.tiles, grid_max), kThreadsB, smem, s>>>(ma, mb, mb, mb, mlo, pk);
     ML_LAUNCH_CHECK("pkm_dK_tc");
   }
   return ML_OK;

@@ -24,7 +24,7 @@ U_BF16 = 2.0 ** -8      # unit roundoff of bf16 storage (8 significant bits, RNE
 KAPPA = 4.0             # bf16 roundings along one element's chain (rounding model)
 
 
-def assert_close(got, ref, rtol, name="", floor=None, mag=None):
+def assert_close(got, ref, rtol, name="", floor=None, mag=None, u=U_BF16):
     """Reading Q17: max|got-ref| <= rtol * max|ref| per tensor (the north_star
     relative tolerance), and elementwise |got-ref| <= rtol * (|ref| +
     floor * max|ref|), floor = 1e-2 for fp32 tolerances and 0.1 for bf16 ones
@@ -44,8 +44,9 @@ def assert_close(got, ref, rtol, name="", floor=None, mag=None):
     if mag is not None:
         # rounding model: an element whose terms cancel carries the bf16
         # rounding of its terms, |err| <= KAPPA * u * sum|terms| (mag = that
-        # sum, from the oracle on absolute values)
-        bound = bound + KAPPA * U_BF16 * np.asarray(mag, np.float64)
+        # sum, from the oracle on absolute values); u = the unit
+        # roundoff of the narrowest intermediate (2^-16 for a bf16 hi/lo pair)
+        bound = bound + KAPPA * u * np.asarray(mag, np.float64)
     bad = err > bound
     assert not bad.any(), f"{name}: {bad.sum()} elements beyond elementwise bound; worst {err[bad].max():.3e}"
 
@@ -133,9 +134,24 @@ def layer_magnitudes(h, rs, rb, gated=True):
         for j in range(B):
             mdV[pos[int(idx[t, j])]] += w[t, j] * mdy[t]
     m["dV"] = mdV
-    mw = mdw.reshape(T, H, k)
-    wk = A(rs["w"])
+    m["dq"], m["dK1"], m["dK2"] = key_magnitudes(h["q"], h["K1"], h["K2"], rs["idx"], rs["w"],
+                                                 mdw.reshape(T, H, k))
+    return m
+
+
+def key_magnitudes(q, K1, K2, idx, w, mdw):
+    """sum|terms| of dq, dK1, dK2 (PAPER.md P:145 key backward) given the
+    selection (idx, w) and the magnitudes of dw: ds magnitudes
+    |w| (|dw| + sum_j |w_j||dw_j|), then the two contractions on absolute
+    values."""
+    A = np.abs
+    T, H, k = idx.shape
+    S, Dh = K1.shape[1], K1.shape[2]
+    mw = A(mdw)
+    wk = A(w)
     mds = wk * (mw + (wk * mw).sum(-1, keepdims=True))
+    h = {"q": q, "K1": K1, "K2": K2}
+    rs = {"idx": idx}
     mdq = np.zeros((T, H, 2 * Dh))
     mdK1 = np.zeros(h["K1"].shape)
     mdK2 = np.zeros(h["K2"].shape)
@@ -147,5 +163,4 @@ def layer_magnitudes(h, rs, rb, gated=True):
             mdq[:, hh, Dh:] += mds[:, hh, j, None] * A(h["K2"][hh, b[:, hh, j]])
             np.add.at(mdK1[hh], a[:, hh, j], mds[:, hh, j, None] * q[:, hh, :Dh])
             np.add.at(mdK2[hh], b[:, hh, j], mds[:, hh, j, None] * q[:, hh, Dh:])
-    m["dq"], m["dK1"], m["dK2"] = mdq, mdK1, mdK2
-    return m
+    return mdq, mdK1, mdK2
