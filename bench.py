@@ -218,9 +218,13 @@ class LoopbackComm:
     def __init__(self, G, rank, others):
         self.size, self.rank, self.others = G, rank, others
 
+    @staticmethod
+    def key(t):
+        return (str(t.dtype), tuple(t.shape[1:]))
+
     def all_gather(self, out, inp):
         n = inp.shape[0]
-        src = self.others.get(str(inp.dtype))
+        src = self.others.get(self.key(inp))
         if src is not None and src.shape[1:] == inp.shape[1:] and src.shape[0] == out.shape[0]:
             if self.rank > 0:
                 out[:self.rank * n].copy_(src[:self.rank * n])
@@ -294,13 +298,17 @@ def group_others(cfg, G, rank, t, ops, torch):
     T = tokens_per_rank(cfg, G)
     idx_all = torch.empty((G * T, H, k), dtype=torch.int32, device=t["q"].device)
     w_all = torch.empty((G * T, H, k), dtype=torch.float32, device=t["q"].device)
+    lists = torch.empty((G, 2, T * H * k), dtype=torch.int32, device=t["q"].device)
     q = torch.empty_like(t["q"])
     for g in range(G):
         ops.synth_fill(q, SEED, gen.TAGS["q"], row0=g * T * H)
         i, w = ops.pkm_topk(q, t["K1"], t["K2"], k)
         idx_all[g * T:(g + 1) * T].copy_(i)
         w_all[g * T:(g + 1) * T].copy_(w)
-    return {str(torch.int32): idx_all, str(torch.float32): w_all}
+        # rank g's sorted share of the group's inverse map
+        ops.group_sort_local(cfg["S"] ** 2, i.view(T, H * k), g, out=lists[g])
+    key = LoopbackComm.key
+    return {key(idx_all): idx_all, key(w_all): w_all, key(lists): lists}
 
 
 def build_step(args, cfg, t, ops, torch, comm=None):
@@ -477,7 +485,14 @@ def run_ours(args, cfg, world, rank, local):
     eff = None
     if world > 1:
         saved = step.last_saved
-        others = {str(torch.int32): saved["idx_all"].clone(), str(torch.float32): saved["w_all"].clone()}
+        idx_all, w_all = saved["idx_all"].clone(), saved["w_all"].clone()
+        P_loc = idx_all[0].numel() * (idx_all.shape[0] // world)
+        lists = torch.empty((world, 2, P_loc), dtype=torch.int32, device=dev)
+        for g in range(world):   # every rank's sorted share of the inverse map
+            ops.group_sort_local(cfg["S"] ** 2, idx_all.view(world, -1)[g].view(-1, idx_all[0].numel()), g,
+                                 out=lists[g])
+        key = LoopbackComm.key
+        others = {key(idx_all): idx_all, key(w_all): w_all, key(lists): lists}
         # t_ref(G): the same kernels through the Python protocol with the
         # collectives replaced by local copies
         ref_step = build_step(args, cfg, t, ops, torch, LoopbackComm(world, rank, others))

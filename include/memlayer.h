@@ -385,7 +385,13 @@ mlStatus ml_group_info(mlGroup g, int* G, int* rank);
  * dw (a dot over dv/G columns) is reduce-scattered: dw_local [T_loc, B] =
  * the full dw of this rank's tokens.  state (nullable): the inverse index
  * map of idx_all built early by embbag_bwd_group_prepare (group stream; the
- * backward waits for it), embbag_bwd_group_state_bytes bytes. */
+ * backward waits for it), embbag_bwd_group_state_bytes bytes.
+ * embbag_bwd_group_prepare is a COLLECTIVE (every rank calls it, in the same
+ * order relative to the other group calls): the inverse map is built once per
+ * group, not G times -- each rank stably sorts only its own T_loc*B positions
+ * (embbag_bwd_group_sort_local), the G sorted lists are all-gathered and
+ * merged (embbag_bwd_group_merge); the result is bit-identical to
+ * embbag_bwd_prepare of idx_all on the shard shape. */
 mlStatus embbag_fwd_group_workspace(mlGroup g, const mlBagShape* shape, mlOutMode mode, size_t* bytes);
 mlStatus embbag_fwd_group(mlGroup g, const mlBagShape* shape, const void* V_shard,
                           const int32_t* idx_local, const float* w_local, int32_t* idx_all,
@@ -394,6 +400,25 @@ mlStatus embbag_fwd_group(mlGroup g, const mlBagShape* shape, const void* V_shar
 mlStatus embbag_bwd_group_state_bytes(mlGroup g, const mlBagShape* shape, size_t* bytes);
 mlStatus embbag_bwd_group_prepare(mlGroup g, const mlBagShape* shape, const int32_t* idx_all,
                                   void* state, size_t state_bytes, void* stream);
+/* The two local halves of embbag_bwd_group_prepare, usable with any
+ * transport (every rank needs the inverse map of all gathered
+ * indices).  sort_local: local = this rank's bag shape [T_loc, B]; idx_local
+ * its [T_loc, B] indices; list [2][T_loc*B] int32 (device) receives the
+ * positions sorted stably by row: list[0..P) the rows (an index outside
+ * [0, N) sorts as row 0 and sets the sticky index flag), list[P..2P) the
+ * GLOBAL positions rank*T_loc*B + p (bit 31 set on an out-of-range index,
+ * which the backward then ignores); needs (rank+1)*T_loc*B < 2^31; idx_local
+ * and list 4-byte aligned, ws 16-byte aligned, of
+ * embbag_bwd_group_sort_local_workspace bytes.  merge: shard = the bag shape
+ * over all group tokens (T = G*T_loc, dv = dv/G); lists [G][2][T_loc*B] the
+ * G ranks' lists in rank order; state of embbag_bwd_state_bytes(shard) bytes
+ * receives the merged map (ties to the lower rank: the stable order) and its
+ * run table, for embbag_bwd_state. */
+mlStatus embbag_bwd_group_sort_local_workspace(const mlBagShape* local, size_t* bytes);
+mlStatus embbag_bwd_group_sort_local(const mlBagShape* local, int rank, const int32_t* idx_local,
+                                     int32_t* list, void* ws, size_t ws_bytes, void* stream);
+mlStatus embbag_bwd_group_merge(const mlBagShape* shard, int G, const int32_t* lists, void* state,
+                                size_t state_bytes, void* stream);
 mlStatus embbag_bwd_group_workspace(mlGroup g, const mlBagShape* shape, mlOutMode mode, size_t* bytes);
 mlStatus embbag_bwd_group(mlGroup g, const mlBagShape* shape, const void* V_shard,
                           const int32_t* idx_all, const float* w_all, const void* dy,

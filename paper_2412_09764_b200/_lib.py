@@ -105,6 +105,9 @@ SIGNATURES = {
     "embbag_fwd_group": [P, C.POINTER(BagShape), P, P, P, P, P, C.c_int, P, P, SZ, P],
     "embbag_bwd_group_state_bytes": [P, C.POINTER(BagShape), C.POINTER(SZ)],
     "embbag_bwd_group_prepare": [P, C.POINTER(BagShape), P, P, SZ, P],
+    "embbag_bwd_group_sort_local_workspace": [C.POINTER(BagShape), C.POINTER(SZ)],
+    "embbag_bwd_group_sort_local": [C.POINTER(BagShape), C.c_int, P, P, P, SZ, P],
+    "embbag_bwd_group_merge": [C.POINTER(BagShape), C.c_int, P, P, SZ, P],
     "embbag_bwd_group_workspace": [P, C.POINTER(BagShape), C.c_int, C.POINTER(SZ)],
     "embbag_bwd_group": [P, C.POINTER(BagShape), P, P, P, P, C.c_int, P, SZ, P, P, P, P, P, SZ, P],
     "memory_layer_fwd_group_workspace": [P, C.POINTER(LayerShape), C.c_int, C.POINTER(SZ)],

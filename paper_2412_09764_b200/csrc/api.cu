@@ -722,6 +722,79 @@ mlStatus embbag_bwd_prepare(const mlBagShape* shape, const int32_t* idx, void* s
   ML_API_END
 }
 
+// ---- the memory group's state, built once per group (merge.cu)
+mlStatus embbag_bwd_group_sort_local_workspace(const mlBagShape* local, size_t* bytes) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(local));
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  SortBufs sb;
+  sort_carve(c, int64_t(local->T) * local->B, ceil_log2(local->N), sb);
+  *bytes = c.used;
+  return ML_OK;
+  ML_API_END
+}
+
+mlStatus embbag_bwd_group_sort_local(const mlBagShape* local, int rank, const int32_t* idx_local,
+                                     int32_t* list, void* ws, size_t ws_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(local));
+  const int64_t P = int64_t(local->T) * local->B;
+  if (rank < 0) return fail(ML_ERR_ARG, "embbag_bwd_group_sort_local: rank < 0");
+  if (int64_t(rank + 1) * P >= (int64_t(1) << 31))
+    return fail(ML_ERR_CONFIG, "embbag_bwd_group_sort_local: (rank+1)*T*B must be < 2^31");
+  if (P == 0) return ML_OK;
+  ML_TRY(check_ptrs({ws}));
+  // element-wise int32 access: 4-byte alignment suffices (a rank's chunk of
+  // a gathered index array need not start on 16 bytes)
+  if (!idx_local || !list) return fail(ML_ERR_ARG, "null pointer argument");
+  if ((reinterpret_cast<uintptr_t>(idx_local) | reinterpret_cast<uintptr_t>(list)) % 4)
+    return fail(ML_ERR_ARG, "pointer not 4-byte aligned");
+  size_t need = 0;
+  ML_TRY(embbag_bwd_group_sort_local_workspace(local, &need));
+  if (ws_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_bwd_group_sort_local: workspace too small");
+  Carver c(ws);
+  SortBufs sb;
+  sort_carve(c, P, ceil_log2(local->N), sb);
+  int32_t *sk = nullptr, *sp = nullptr;
+  timing_mark(nullptr, S(stream));
+  ML_TRY(sort_pairs(idx_local, P, ceil_log2(local->N), sb, &sk, &sp, S(stream), local->N));
+  ML_TRY(tag_global_positions(sk, sp, P, int64_t(rank) * P, list, S(stream)));
+  return check_index_flag(S(stream));
+  ML_API_END
+}
+
+mlStatus embbag_bwd_group_merge(const mlBagShape* shard, int G, const int32_t* lists, void* state,
+                                size_t state_bytes, void* stream) {
+  ML_API_BEGIN
+  ML_TRY(check_bag(shard));
+  if (G < 1) return fail(ML_ERR_ARG, "embbag_bwd_group_merge: G < 1");
+  if (shard->T % G) return fail(ML_ERR_CONFIG, "embbag_bwd_group_merge: G must divide shard T");
+  size_t need = 0;
+  ML_TRY(embbag_bwd_state_bytes(shard, &need));
+  if (state_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_bwd_group_merge: state too small");
+  ML_TRY(check_ptrs({state}));
+  cudaStream_t st = S(stream);
+  const int64_t P = int64_t(shard->T) * shard->B;
+  Carver sc(state);
+  BagPrepState ps;
+  state_carve(sc, *shard, ps);
+  if (P == 0) {
+    ML_CUDA_TRY(cudaMemsetAsync(ps.U, 0, sizeof(int32_t), st));
+    return ML_OK;
+  }
+  if (!lists || reinterpret_cast<uintptr_t>(lists) % 4) return fail(ML_ERR_ARG, "lists: null or not 4-byte aligned");
+  const int bits = ceil_log2(shard->N);
+  int32_t *fk = nullptr, *fp = nullptr;
+  ML_TRY(sorted_result(P, bits, ps.sort, &fk, &fp));
+  const int other = fk == ps.sort.k[0] ? 1 : 0;
+  timing_mark(nullptr, st);
+  ML_TRY(merge_sorted_lists(lists, G, P / G, fk, fp, ps.sort.k[other], ps.sort.v[other], st));
+  ML_TRY(find_runs(fk, P, ps.runs, ps.rows, ps.U, st));
+  return ML_OK;
+  ML_API_END
+}
+
 mlStatus embbag_bwd_state(const mlBagShape* shape, const void* V, const float* w, const void* dy,
                           const void* state, size_t state_bytes, int32_t* rows, void* dV,
                           int32_t* U, float* dw, void* ws, size_t ws_bytes, void* stream) {

@@ -371,6 +371,49 @@ mlStatus bag_blocks(mlGroup_* g, const mlBagShape& s, mlOutMode mode, const void
   return g->tr->all_to_all(b.y_part, b.recv, blk_bytes, st);
 }
 
+// The group's backward state: the bag-level state of
+// the shard shape (the merged inverse map of all G*T_loc tokens) followed by
+// this rank's sorted list, the G gathered lists and the local sort's
+// workspace.  Built once per group: each rank sorts only its own positions,
+// the sorted lists are all-gathered and merged (merge.cu), instead of every
+// rank sorting all G*T_loc*B positions.
+struct GroupState { void* bag; size_t bag_bytes; int32_t* send; int32_t* recv; void* sort_ws; size_t sort_bytes; };
+mlStatus group_state_carve(Carver& c, const mlGroup_* g, const mlBagShape& s, GroupState& gs) {
+  const mlBagShape bs = shard_shape(g, s);
+  const int64_t P_loc = int64_t(s.T) * s.B;
+  ML_TRY((embbag_bwd_state_bytes(&bs, &gs.bag_bytes)));
+  ML_TRY((embbag_bwd_group_sort_local_workspace(&s, &gs.sort_bytes)));
+  gs.bag = c.take<char>(int64_t(gs.bag_bytes));
+  gs.send = c.take<int32_t>(2 * P_loc);
+  gs.recv = c.take<int32_t>(int64_t(g->tr->G) * 2 * P_loc);
+  gs.sort_ws = c.take<char>(int64_t(gs.sort_bytes));
+  return ML_OK;
+}
+
+// phase A (preparation stream): sort this rank's own positions
+mlStatus group_state_local(mlGroup_* g, const mlBagShape& s, const int32_t* idx_own, GroupState& gs,
+                           cudaStream_t st) {
+  cudaStream_t ps = serial_mode() ? st : g->prep;
+  ML_TRY(dep(st, ps, g->ev[2]));
+  ML_TRY((embbag_bwd_group_sort_local(&s, g->tr->rank, idx_own, gs.send, gs.sort_ws, gs.sort_bytes, ps)));
+  return ML_OK;
+}
+
+// phase B: the lists' all-gather on the communication stream, then the merge
+// and the run table on the preparation stream -> state_ready
+mlStatus group_state_merge(mlGroup_* g, const mlBagShape& s, GroupState& gs, cudaStream_t st) {
+  cudaStream_t ps = serial_mode() ? st : g->prep;
+  cudaStream_t cs = serial_mode() ? st : g->comm;
+  const int64_t P_loc = int64_t(s.T) * s.B;
+  ML_TRY(dep(ps, cs, g->ev[7]));
+  ML_TRY(g->tr->all_gather(gs.send, gs.recv, size_t(2 * P_loc) * sizeof(int32_t), cs));
+  ML_TRY(dep(cs, ps, g->ev[7]));
+  const mlBagShape bs = shard_shape(g, s);
+  ML_TRY((embbag_bwd_group_merge(&bs, g->tr->G, gs.recv, gs.bag, gs.bag_bytes, ps)));
+  ML_CUDA_TRY(cudaEventRecord(g->state_ready, ps));
+  return ML_OK;
+}
+
 }  // namespace
 }  // namespace ml
 
@@ -542,8 +585,12 @@ mlStatus embbag_bwd_group_workspace(mlGroup g, const mlBagShape* shape, mlOutMod
 mlStatus embbag_bwd_group_state_bytes(mlGroup g, const mlBagShape* shape, size_t* bytes) {
   ML_API_BEGIN_X
   ML_TRY(check_group_shape(g, shape, ML_OUT_ALLTOALL));
-  const mlBagShape bs = shard_shape(g, *shape);
-  return embbag_bwd_state_bytes(&bs, bytes);
+  if (!bytes) return fail(ML_ERR_ARG, "null bytes");
+  Carver c(nullptr);
+  GroupState gs;
+  ML_TRY(group_state_carve(c, g, *shape, gs));
+  *bytes = c.used;
+  return ML_OK;
   ML_API_END_X
 }
 
@@ -599,20 +646,26 @@ mlStatus embbag_bwd_group(mlGroup g, const mlBagShape* shape, const void* V_shar
   ML_API_END_X
 }
 
-// the backward's inverse index map of idx_all, on the group's preparation
-// stream (ordered after the caller's work so far); embbag_bwd_group /
+// the backward's inverse index map of idx_all (a collective: every rank
+// calls it): this rank's own positions sorted on the group's preparation
+// stream, the G sorted lists all-gathered on the communication stream and
+// merged (ordered after the caller's work so far); embbag_bwd_group /
 // memory_layer_bwd_group wait for it
 mlStatus embbag_bwd_group_prepare(mlGroup g, const mlBagShape* shape, const int32_t* idx_all,
                                   void* state, size_t state_bytes, void* stream) {
   ML_API_BEGIN_X
   ML_TRY(check_group_shape(g, shape, ML_OUT_ALLTOALL));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const mlBagShape bs = shard_shape(g, *shape);
-  cudaStream_t ps = serial_mode() ? st : g->prep;
-  ML_TRY(dep(st, ps, g->ev[2]));
-  ML_TRY((embbag_bwd_prepare(&bs, idx_all, state, state_bytes, ps)));
-  ML_CUDA_TRY(cudaEventRecord(g->state_ready, ps));
-  return ML_OK;
+  size_t need = 0;
+  ML_TRY(embbag_bwd_group_state_bytes(g, shape, &need));
+  if (!state || state_bytes < need) return fail(ML_ERR_WORKSPACE, "embbag_bwd_group_prepare: state too small");
+  if (shape->T > 0 && !idx_all) return fail(ML_ERR_ARG, "null idx_all");
+  Carver c(state);
+  GroupState gs;
+  ML_TRY(group_state_carve(c, g, *shape, gs));
+  const int64_t P_loc = int64_t(shape->T) * shape->B;
+  ML_TRY(group_state_local(g, *shape, idx_all + int64_t(g->tr->rank) * P_loc, gs, st));
+  return group_state_merge(g, *shape, gs, st);
   ML_API_END_X
 }
 
@@ -683,9 +736,20 @@ mlStatus memory_layer_fwd_group(mlGroup g, const mlLayerShape* shape, mlOutMode 
                               kGemmWs, as)));
   // own tokens' product-key lookup, then the (idx, w) all-gather
   ML_TRY((pkm_topk(&s.pkm, q, K1, K2, idx_saved, w_saved, nullptr, b.pkm_ws, b.pkm_bytes, st)));
+  // the backward's state: own positions sorted beside the exchange and the
+  // bag forward, the sorted lists exchanged and merged after the blocks
+  GroupState gs{};
+  if (state) {
+    size_t sneed = 0;
+    ML_TRY(embbag_bwd_group_state_bytes(g, &bag, &sneed));
+    if (state_bytes < sneed) return fail(ML_ERR_WORKSPACE, "memory_layer_fwd_group: state too small");
+    Carver sc(state);
+    ML_TRY(group_state_carve(sc, g, bag, gs));
+    ML_TRY(group_state_local(g, bag, idx_saved, gs, st));
+  }
   ML_TRY(gather_iw(g, bag, idx_saved, w_saved, idx_all, w_all, b.f, st));
-  if (state) ML_TRY(embbag_bwd_group_prepare(g, &bag, idx_all, state, state_bytes, st));
   ML_TRY(bag_blocks(g, bag, mode, V_shard, idx_all, w_all, b.f, st));
+  if (state) ML_TRY(group_state_merge(g, bag, gs, st));
   ML_TRY(dep(as, st, g->ev[4]));                   // g ready
   const size_t blk_bytes = size_t(T) * (s.dv / G) * dtype_size(dt);
   const void* own = mode == ML_OUT_ALLTOALL ? b.f.recv

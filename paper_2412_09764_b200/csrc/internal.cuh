@@ -65,17 +65,23 @@ mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t
 // --------------------------------------------------- runs of sorted keys
 constexpr int kPieceLen = 32;  // positions per reduction piece (L)
 struct RunBufs {
-  int32_t* flags = nullptr;      // [n]
-  int32_t* excl = nullptr;       // [n] run id of each position (exclusive scan of heads)
-  int32_t* run_begin = nullptr;  // [n+1]
-  int32_t* pieces = nullptr;     // [n] npieces at heads
-  int32_t* piece_base = nullptr; // [n] exclusive scan of pieces
-  int32_t* n_slots = nullptr;    // device scalar
-  int32_t* scan_tmp = nullptr;
-  int32_t* lb = nullptr;         // single-pass mode: look-back status words + tickets
+  int32_t* rid = nullptr;        // [n] run id of each position
+  int32_t* run_begin = nullptr;  // [U+1] first position of each run, then n
+  int32_t* piece_base = nullptr; // [n] at the first position of each run longer than
+                                 //     kPieceLen: exclusive scan of those runs' pieces
+  int32_t* n_slots = nullptr;    // device scalar: total pieces
+  int32_t* lb = nullptr;         // look-back status words + tile tickets
 };
 void runs_carve(Carver& c, int64_t n, RunBufs& r);
 // rows_out (nullable) [n]: distinct keys ascending; U (device int) count.
+// ---- group state (merge.cu): list [2][n] = sorted keys | global positions
+// (pos + offset, kClampedPos kept); merge_sorted_lists merges G such lists
+// (lists + g*2*n_each) stably (ties to the lower list) into out_k / out_p,
+// using scratch_k / scratch_p (n_each*G each) between rounds.
+mlStatus tag_global_positions(const int32_t* sk, const int32_t* sp, int64_t n, int64_t offset,
+                              int32_t* list, cudaStream_t s);
+mlStatus merge_sorted_lists(const int32_t* lists, int G, int64_t n_each, int32_t* out_k,
+                            int32_t* out_p, int32_t* scratch_k, int32_t* scratch_p, cudaStream_t s);
 mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out,
                    int32_t* U, cudaStream_t s);
 

@@ -45,7 +45,7 @@ namespace {
 
 struct SegParams {
   const int32_t* skey; const int32_t* spos; int64_t P;
-  const int32_t* flags; const int32_t* excl; const int32_t* run_begin; const int32_t* piece_base;
+  const int32_t* rid; const int32_t* run_begin; const int32_t* piece_base;
   const float* w;
   const char* src; int64_t lds_bytes; int32_t src_col0; int32_t B;
   const char* V; int64_t ldv_bytes; int32_t v_col0;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
       const bool clamped = pos < 0;   // index outside [0, N): row 0, weight 0
       pos &= ~kClampedPos;
       key = p.skey[i];
-      r = p.excl[i] - 1 + p.flags[i];
+      r = p.rid[i];
       w = clamped ? 0.f : p.w[pos];
       t = pos / p.B;
       rb = p.run_begin[r];
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
           const bool clamped = m.pos < 0;   // index outside [0, N): row 0, weight 0
           m.pos &= ~kClampedPos;
           m.key = p.skey[i];
-          m.rr = p.excl[i] - 1 + p.flags[i];
+          m.rr = p.rid[i];
           m.w = clamped ? 0.f : p.w[m.pos];
           m.t = m.pos / p.B;
           m.rb = p.run_begin[m.rr];
@@ -804,7 +804,7 @@ mlStatus launch_segreduce(const SegArgs& a, cudaStream_t s) {
     return fail(ML_ERR_UNSUPPORTED, "segreduce: source row pitch too large");
   SegParams p;
   p.skey = a.skey; p.spos = a.spos; p.P = a.P;
-  p.flags = a.runs->flags; p.excl = a.runs->excl; p.run_begin = a.runs->run_begin;
+  p.rid = a.runs->rid; p.run_begin = a.runs->run_begin;
   p.piece_base = a.runs->piece_base;
   p.w = a.w;
   const int64_t es = int64_t(dtype_size(a.dtype));

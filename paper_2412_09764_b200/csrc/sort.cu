@@ -187,15 +187,16 @@ __global__ void __launch_bounds__(256) sort_hist_kernel(SortPassParams p, bool f
 // then writes every digit's run contiguously (coalesced) at its global offset.
 // dynamic smem: s_cnt[kSortWarps][nbins], s_dstart[nbins], s_goff[nbins],
 //               s_key[kSortTile], s_val[kSortTile]
-template <bool ONESWEEP>
+template <bool ONESWEEP, int ROUNDS = kSortRounds>
 __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, bool first) {
+  constexpr int TILE = kSortWarps * ROUNDS * 32;
   extern __shared__ int s_dyn[];
   const int nbins = 1 << p.dbits;
   int* s_cnt = s_dyn;
   int* s_dstart = s_cnt + kSortWarps * nbins;
   int* s_goff = s_dstart + nbins;
   int32_t* s_key = s_goff + nbins;
-  int32_t* s_val = s_key + kSortTile;
+  int32_t* s_val = s_key + TILE;
   __shared__ int s_warp[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t mask = uint32_t(nbins - 1);
@@ -206,14 +207,14 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
   }
   __syncthreads();
   const int tile = ONESWEEP ? s_tile : int(blockIdx.x);
-  const int64_t bbase = int64_t(tile) * kSortTile;
-  const int64_t wbase = bbase + int64_t(wid) * kSortRounds * 32;
-  const int nvalid = int(p.n - bbase < kSortTile ? p.n - bbase : kSortTile);
-  int32_t key[kSortRounds], val[kSortRounds];
-  uint32_t dig[kSortRounds];
-  unsigned peers[kSortRounds];
+  const int64_t bbase = int64_t(tile) * TILE;
+  const int64_t wbase = bbase + int64_t(wid) * ROUNDS * 32;
+  const int nvalid = int(p.n - bbase < TILE ? p.n - bbase : TILE);
+  int32_t key[ROUNDS], val[ROUNDS];
+  uint32_t dig[ROUNDS];
+  unsigned peers[ROUNDS];
 #pragma unroll
-  for (int r = 0; r < kSortRounds; ++r) {
+  for (int r = 0; r < ROUNDS; ++r) {
     const int64_t i = wbase + r * 32 + lane;
     const bool valid = i < p.n;
     bool clamped = false;
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
     val[r] = valid ? (p.vin ? p.vin[i] : (int32_t(i) | (clamped ? kClampedPos : 0))) : 0;
   }
 #pragma unroll
-  for (int r = 0; r < kSortRounds; ++r) {
+  for (int r = 0; r < ROUNDS; ++r) {
     const int64_t i = wbase + r * 32 + lane;
     const bool valid = i < p.n;
     dig[r] = valid ? ((uint32_t(key[r]) >> p.shift) & mask) : 0x10000u;
@@ -260,35 +261,46 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
     // all of this thread's digits walk back together: one round of independent
     // status loads per predecessor tile, until every digit found an inclusive
     // prefix (tile 0 publishes inclusive values)
+    // kLB predecessors per digit per round of loads (all independent), so a
+    // walk over aggregate-only predecessors takes 1/kLB of the round trips
+    constexpr int kLB = 4;
     uint32_t excl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int ptj[8];
     uint32_t open = 0;
-    for (int j = 0; j < per; ++j)
-      if (threadIdx.x * per + j < nbins) open |= 1u << j;
+    for (int j = 0; j < 8; ++j) {
+      ptj[j] = tile - 1;
+      if (j < per && threadIdx.x * per + j < nbins && tile > 0) open |= 1u << j;
+    }
     uint32_t spins = 0;
-    for (int pt = tile - 1; pt >= 0 && open; ) {
-      const volatile uint32_t* row = p.status + int64_t(pt) * nbins + threadIdx.x * per;
-      uint32_t v[8];
-      bool ready = true;
+    const volatile uint32_t* stp = p.status;
+    while (open) {
+      uint32_t v[8][kLB];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+          v[j][q] = 2u << 30;    // before tile 0: an inclusive prefix of 0
+          if ((open >> j & 1u) && ptj[j] - q >= 0)
+            v[j][q] = stp[int64_t(ptj[j] - q) * nbins + threadIdx.x * per + j];
+        }
+      bool progress = false;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        v[j] = 0;
-        if (j < per && (open >> j & 1u)) {
-          v[j] = row[j];
-          ready = ready && (v[j] >> 30) != 0;
-        }
-      }
-      if (!ready) {              // some predecessor has not published yet
-        if (++spins > kSortSpin) __trap();
-        continue;
-      }
+        if (!(open >> j & 1u)) continue;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j < per && (open >> j & 1u)) {
-          excl[j] += v[j] & kStMask;
-          if ((v[j] >> 30) == 2) open &= ~(1u << j);
+        for (int q = 0; q < kLB; ++q) {
+          const uint32_t f = v[j][q] >> 30;
+          if (f == 0) break;                 // not published yet: retry from here
+          excl[j] += v[j][q] & kStMask;
+          --ptj[j];
+          progress = true;
+          if (f == 2) {
+            open &= ~(1u << j);
+            break;
+          }
         }
       }
-      --pt;
+      if (!progress && ++spins > kSortSpin) __trap();
     }
     for (int j = 0; j < per; ++j) {
       const int d = threadIdx.x * per + j;
@@ -317,7 +329,7 @@ __global__ void __launch_bounds__(256) sort_scatter_kernel(SortPassParams p, boo
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-  for (int r = 0; r < kSortRounds; ++r) {
+  for (int r = 0; r < ROUNDS; ++r) {
     const int64_t i = wbase + r * 32 + lane;
     const bool valid = i < p.n;
     int dst = 0;
@@ -390,37 +402,9 @@ __global__ void __launch_bounds__(1024) sort_gscan_kernel(int32_t* ghist, int pa
 }
 
 // ------------------------------------------------------------ runs
-__global__ void run_flags_kernel(const int32_t* skey, int64_t n, int32_t* flags) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) flags[i] = (i == 0 || skey[i] != skey[i - 1]) ? 1 : 0;
-}
-
-__global__ void run_fill_kernel(const int32_t* skey, int64_t n, const int32_t* flags,
-                                const int32_t* excl, int32_t* run_begin, int32_t* rows_out) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (flags[i]) {
-    const int32_t r = excl[i];
-    run_begin[r] = int32_t(i);
-    if (rows_out) rows_out[r] = skey[i];
-  }
-  if (i == n - 1) run_begin[excl[i] + flags[i]] = int32_t(n);
-}
-
-__global__ void run_pieces_kernel(int64_t n, const int32_t* flags, const int32_t* excl,
-                                  const int32_t* run_begin, int32_t* pieces) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int np = 0;
-  if (flags[i]) {
-    const int32_t len = run_begin[excl[i] + 1] - int32_t(i);
-    np = len > kPieceLen ? (len + kPieceLen - 1) / kPieceLen : 0;
-  }
-  pieces[i] = np;
-}
-
-// ---- runs in two single-pass kernels (tiles of kScanTile positions, ticket
-// order, decoupled look-back over one status word per tile)
+// Two single-pass kernels (tiles of kScanTile, ticket order, decoupled
+// look-back over one status word per tile); every array is read and written
+// coalesced (tiles staged in shared memory, scanned blocked).
 __device__ __forceinline__ uint32_t lookback_prefix(uint32_t* status, int tile, uint32_t total) {
   // thread 0 of the tile: publish, walk back, publish the inclusive prefix
   volatile uint32_t* st = status;
@@ -441,91 +425,151 @@ __device__ __forceinline__ uint32_t lookback_prefix(uint32_t* status, int tile, 
   return excl;
 }
 
-// heads, run ids (exclusive scan of heads), run_begin, rows, U
+// Warp 0 of the tile: publish the tile's count, then walk back 32
+// predecessors at a time (one status word per lane, the nearest one with an
+// inclusive prefix ends the walk), publish the inclusive prefix.
+constexpr int kRunItems = 4;
+constexpr int kRunTile = kScanThreads * kRunItems;   // 2048 positions per tile
+__device__ __forceinline__ uint32_t lookback_prefix_warp(uint32_t* status, int tile, uint32_t total,
+                                                         int lane) {
+  volatile uint32_t* st = status;
+  if (lane == 0) {
+    st[tile] = (tile == 0 ? kStInc : kStAgg) | total;
+    __threadfence();
+  }
+  __syncwarp();
+  uint32_t excl = 0;
+  for (int pt = tile - 1; pt >= 0; pt -= 32) {
+    const int idx = pt - lane;
+    uint32_t v = 2u << 30;          // before tile 0: an inclusive prefix of 0
+    if (idx >= 0) v = st[idx];
+    uint32_t spins = 0;
+    while ((v >> 30) == 0) {
+      if (++spins > kSortSpin) __trap();
+      v = st[idx];
+    }
+    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 30) == 2);
+    const int lim = inc ? __ffs(inc) - 1 : 31;     // lanes 0..lim contribute
+    uint32_t c = lane <= lim ? (v & kStMask) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    excl += c;
+    if (inc) break;
+  }
+  if (lane == 0 && tile > 0) st[tile] = kStInc | (excl + total);
+  return excl;
+}
+
+// run id of every position (rid), run_begin, rows (the distinct keys), *U
 __global__ void __launch_bounds__(kScanThreads) run_scan1_kernel(const int32_t* skey, int64_t n,
-                                                                 int32_t* flags, int32_t* excl,
-                                                                 int32_t* run_begin,
+                                                                 int32_t* rid, int32_t* run_begin,
                                                                  int32_t* rows_out, int32_t* U,
                                                                  uint32_t* status, int32_t* ticket) {
   __shared__ int s_warp[32];
   __shared__ int s_tile;
   __shared__ uint32_t s_prefix;
+  __shared__ int32_t s_k[kRunTile + 1];   // s_k[0]: the key before the tile
+  __shared__ int32_t s_r[kRunTile];
+  __shared__ int32_t s_w[kRunTile];
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
   __syncthreads();
   const int tile = s_tile;
-  const int64_t base = int64_t(tile) * kScanTile + threadIdx.x * kScanItems;
-  int32_t key[kScanItems];
-  int f[kScanItems], sum = 0;
+  const int64_t t0 = int64_t(tile) * kRunTile;
+  for (int x = threadIdx.x; x < kRunTile; x += kScanThreads)
+    s_k[1 + x] = t0 + x < n ? skey[t0 + x] : 0;
+  if (threadIdx.x == 0) s_k[0] = tile > 0 ? skey[t0 - 1] : 0;
+  __syncthreads();
+  const int x0 = threadIdx.x * kRunItems;
+  int f[kRunItems], sum = 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int64_t ix = base + i;
-    key[i] = ix < n ? skey[ix] : 0;
-    f[i] = (ix < n && (ix == 0 || key[i] != skey[ix - 1])) ? 1 : 0;
+  for (int i = 0; i < kRunItems; ++i) {
+    const int64_t ix = t0 + x0 + i;
+    f[i] = (ix < n && (ix == 0 || s_k[1 + x0 + i] != s_k[x0 + i])) ? 1 : 0;
     sum += f[i];
   }
   int total;
-  int ex = block_excl_scan(sum, s_warp, &total);
-  if (threadIdx.x == 0) s_prefix = lookback_prefix(status, tile, uint32_t(total));
+  const int ex = block_excl_scan(sum, s_warp, &total);
+  if (threadIdx.x < 32) {
+    const uint32_t pre = lookback_prefix_warp(status, tile, uint32_t(total), threadIdx.x);
+    if (threadIdx.x == 0) s_prefix = pre;
+  }
   __syncthreads();
-  int e = int(s_prefix) + ex;
+  const int pre = int(s_prefix);
+  int e = pre + ex;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int64_t ix = base + i;
-    if (ix < n) {
-      flags[ix] = f[i];
-      excl[ix] = e;
-      if (f[i]) {
-        run_begin[e] = int32_t(ix);
-        if (rows_out) rows_out[e] = key[i];
-      }
-      e += f[i];
-      if (ix == n - 1) {
-        run_begin[e] = int32_t(n);
-        if (U) *U = e;
-      }
+  for (int i = 0; i < kRunItems; ++i) {
+    e += f[i];
+    s_r[x0 + i] = e - 1;
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < kRunTile; x += kScanThreads)
+    if (t0 + x < n) rid[t0 + x] = s_r[x];
+  __syncthreads();
+  // the tile's runs have the contiguous ids [pre, pre + total): stage their
+  // first positions and keys, then store both coalesced
+  e = ex;
+#pragma unroll
+  for (int i = 0; i < kRunItems; ++i) {
+    if (f[i]) {
+      s_r[e] = int32_t(t0 + x0 + i);
+      s_w[e] = s_k[1 + x0 + i];
     }
+    e += f[i];
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < total; x += kScanThreads) {
+    run_begin[pre + x] = s_r[x];
+    if (rows_out) rows_out[pre + x] = s_w[x];
+  }
+  if (t0 + kRunTile >= n && threadIdx.x == 0) {   // the last tile
+    run_begin[pre + total] = int32_t(n);
+    *U = pre + total;
   }
 }
 
-// pieces of runs longer than kPieceLen and their exclusive scan (piece_base), n_slots
-__global__ void __launch_bounds__(kScanThreads) run_scan2_kernel(int64_t n, const int32_t* flags,
-                                                                 const int32_t* excl,
-                                                                 const int32_t* run_begin,
-                                                                 int32_t* piece_base,
-                                                                 int32_t* n_slots, uint32_t* status,
-                                                                 int32_t* ticket) {
+// pieces of the runs longer than kPieceLen: their exclusive scan over runs,
+// written at each long run's first position (piece_base), and n_slots
+__global__ void __launch_bounds__(kScanThreads) run_scan2_kernel(const int32_t* run_begin,
+                                                                 const int32_t* U, int32_t* piece_base,
+                                                                 int32_t* n_slots, int ntiles,
+                                                                 uint32_t* status, int32_t* ticket) {
   __shared__ int s_warp[32];
   __shared__ int s_tile;
   __shared__ uint32_t s_prefix;
+  __shared__ int32_t s_b[kRunTile + 1];
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
   __syncthreads();
   const int tile = s_tile;
-  const int64_t base = int64_t(tile) * kScanTile + threadIdx.x * kScanItems;
-  int np[kScanItems], sum = 0;
+  const int64_t r0 = int64_t(tile) * kRunTile;
+  const int64_t u = *U;
+  for (int x = threadIdx.x; x <= kRunTile; x += kScanThreads)
+    s_b[x] = r0 + x <= u ? run_begin[r0 + x] : 0;
+  __syncthreads();
+  const int x0 = threadIdx.x * kRunItems;
+  int np[kRunItems], sum = 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int64_t ix = base + i;
+  for (int i = 0; i < kRunItems; ++i) {
     np[i] = 0;
-    if (ix < n && flags[ix]) {
-      const int32_t len = run_begin[excl[ix] + 1] - int32_t(ix);
+    if (r0 + x0 + i < u) {
+      const int32_t len = s_b[x0 + i + 1] - s_b[x0 + i];
       np[i] = len > kPieceLen ? (len + kPieceLen - 1) / kPieceLen : 0;
     }
     sum += np[i];
   }
   int total;
-  int ex = block_excl_scan(sum, s_warp, &total);
-  if (threadIdx.x == 0) s_prefix = lookback_prefix(status, tile, uint32_t(total));
+  const int ex = block_excl_scan(sum, s_warp, &total);
+  if (threadIdx.x < 32) {
+    const uint32_t pre = lookback_prefix_warp(status, tile, uint32_t(total), threadIdx.x);
+    if (threadIdx.x == 0) s_prefix = pre;
+  }
   __syncthreads();
   int e = int(s_prefix) + ex;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int64_t ix = base + i;
-    if (ix < n) {
-      piece_base[ix] = e;
-      e += np[i];
-      if (ix == n - 1 && n_slots) *n_slots = e;
-    }
+  for (int i = 0; i < kRunItems; ++i) {
+    if (np[i]) piece_base[s_b[x0 + i]] = e;
+    e += np[i];
   }
+  if (tile == ntiles - 1 && threadIdx.x == kScanThreads - 1 && n_slots) *n_slots = e;
 }
 
 }  // namespace
@@ -550,6 +594,7 @@ mlStatus scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* tmp
 }
 
 static int sort_nblocks(int64_t n) { return int((n + kSortTile - 1) / kSortTile); }
+
 
 void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b) {
   (void)bits;
@@ -677,13 +722,10 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
 }
 
 void runs_carve(Carver& c, int64_t n, RunBufs& r) {
-  r.flags = c.take<int32_t>(n);
-  r.excl = c.take<int32_t>(n);
+  r.rid = c.take<int32_t>(n);
   r.run_begin = c.take<int32_t>(n + 1);
-  r.pieces = c.take<int32_t>(n);
   r.piece_base = c.take<int32_t>(n);
   r.n_slots = c.take<int32_t>(1);
-  r.scan_tmp = c.take<int32_t>(scan_tmp_elems(n));
   r.lb = c.take<int32_t>(2 * scan_tmp_elems(n) + 4);
 }
 
@@ -693,35 +735,19 @@ mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out
     if (U) ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), s));
     return ML_OK;
   }
-  static const bool single = [] {
-    const char* e = std::getenv("ML_SORT_ONESWEEP");
-    return !(e && e[0] == '0');
-  }();
-  // two single-pass kernels pay off only for large n (measured: 0.39 vs 0.46 ms
-  // at 16.8M positions, 69 vs 60 us at 2.1M)
-  if (single && n >= (int64_t(1) << 23) && n < (int64_t(1) << 30)) {
-    const int64_t nt = (n + kScanTile - 1) / kScanTile;
-    uint32_t* st1 = reinterpret_cast<uint32_t*>(r.lb);
-    uint32_t* st2 = st1 + nt;
-    int32_t* tickets = r.lb + 2 * nt;
-    ML_CUDA_TRY(cudaMemsetAsync(r.lb, 0, sizeof(int32_t) * size_t(2 * nt + 2), s));
-    run_scan1_kernel<<<unsigned(nt), kScanThreads, 0, s>>>(skey, n, r.flags, r.excl, r.run_begin,
-                                                           rows_out, U, st1, tickets);
-    ML_LAUNCH_CHECK("run_flags");
-    run_scan2_kernel<<<unsigned(nt), kScanThreads, 0, s>>>(n, r.flags, r.excl, r.run_begin,
-                                                           r.piece_base, r.n_slots, st2, tickets + 1);
-    ML_LAUNCH_CHECK("run_pieces");
-    return ML_OK;
-  }
-  const unsigned g = unsigned((n + 255) / 256);
-  run_flags_kernel<<<g, 256, 0, s>>>(skey, n, r.flags);
+  if (n >= (int64_t(1) << 30)) return fail(ML_ERR_CONFIG, "runs: n must be < 2^30");
+  const int64_t nt = (n + kRunTile - 1) / kRunTile;
+  uint32_t* st1 = reinterpret_cast<uint32_t*>(r.lb);
+  uint32_t* st2 = st1 + nt;
+  int32_t* tickets = r.lb + 2 * nt;     // [0], [1]: tile tickets; [2]: U when the caller passes none
+  int32_t* u = U ? U : tickets + 2;
+  ML_CUDA_TRY(cudaMemsetAsync(r.lb, 0, sizeof(int32_t) * size_t(2 * nt + 2), s));
+  run_scan1_kernel<<<unsigned(nt), kScanThreads, 0, s>>>(skey, n, r.rid, r.run_begin, rows_out, u,
+                                                         st1, tickets);
   ML_LAUNCH_CHECK("run_flags");
-  ML_TRY(scan_exclusive(r.flags, r.excl, n, r.scan_tmp, U, s));
-  run_fill_kernel<<<g, 256, 0, s>>>(skey, n, r.flags, r.excl, r.run_begin, rows_out);
-  ML_LAUNCH_CHECK("run_fill");
-  run_pieces_kernel<<<g, 256, 0, s>>>(n, r.flags, r.excl, r.run_begin, r.pieces);
+  run_scan2_kernel<<<unsigned(nt), kScanThreads, 0, s>>>(r.run_begin, u, r.piece_base, r.n_slots,
+                                                         int(nt), st2, tickets + 1);
   ML_LAUNCH_CHECK("run_pieces");
-  ML_TRY(scan_exclusive(r.pieces, r.piece_base, n, r.scan_tmp, r.n_slots, s));
   return ML_OK;
 }
 

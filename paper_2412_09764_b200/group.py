@@ -111,6 +111,49 @@ class CudaLocal:
         idx.record_stream(self._bg)
         return state, ev
 
+    # ---- the group's inverse map, built once per group (include/memlayer.h
+    # embbag_bwd_group_sort_local / _merge): own positions sorted on the
+    # background stream during the forward, the G sorted lists exchanged at
+    # the end of the forward, merged on the background stream
+    def _bg_stream(self, like):
+        cur = torch.cuda.current_stream(like.device)
+        if self.ops.SERIAL:       # measurement mode: one in-order stream
+            return cur
+        if getattr(self, "_bg", None) is None:
+            self._bg = torch.cuda.Stream(device=like.device)
+        self._bg.wait_stream(cur)
+        return self._bg
+
+    def group_sort_local(self, N, idx, rank):
+        bg = self._bg_stream(idx)
+        with torch.cuda.stream(bg):
+            lst = getattr(self, "_lst", None)
+            if lst is None or lst.shape[1] != idx.numel():
+                lst = self._lst = torch.empty((2, idx.numel()), dtype=torch.int32, device=idx.device)
+                self._lst_ws = None
+            self.ops.group_sort_local(N, idx, rank, out=lst, ws=getattr(self, "_lst_ws", None))
+            self._sorted_ev = torch.cuda.Event()
+            self._sorted_ev.record(bg)
+        if bg is not torch.cuda.current_stream(idx.device):
+            idx.record_stream(bg)
+        return lst
+
+    def group_lists(self, G, lst):
+        buf = getattr(self, "_lists", None)
+        if buf is None or buf.shape != (G,) + tuple(lst.shape):
+            buf = self._lists = torch.empty((G,) + tuple(lst.shape), dtype=lst.dtype, device=lst.device)
+        torch.cuda.current_stream(lst.device).wait_event(self._sorted_ev)
+        return buf
+
+    def group_merge(self, N, dv, lists, dtype):
+        bg = self._bg_stream(lists)
+        with torch.cuda.stream(bg):
+            state = self.ops.group_merge(N, dv, lists, dtype, out=getattr(self, "_state", None))
+            self._state = state
+            ev = torch.cuda.Event()
+            ev.record(bg)
+        return state, ev
+
     def wait(self, ev):
         torch.cuda.current_stream().wait_event(ev)
 
@@ -171,13 +214,14 @@ class GroupMemoryLayer:
         dvG = V_shard.shape[1]
         dv = dvG * G
         idx, w = L.pkm_topk(q, K1, K2, k)                              # 1
+        # the backward's inverse map, built once per group: own positions
+        # sorted now (beside the exchange and the bag forward), the G sorted
+        # lists exchanged and merged at the end of the forward
+        lst = L.group_sort_local(V_shard.shape[0], idx.view(T_loc, B), rank) \
+            if hasattr(L, "group_sort_local") else None
         idx_all = L.empty((G * T_loc, H, k), idx.dtype, idx)
         w_all = L.empty((G * T_loc, H, k), w.dtype, w)
         C.all_gather(idx_all, idx)                                      # 2
-        state = state_ev = None
-        if hasattr(L, "embbag_bwd_prepare"):      # the backward's inverse map, concurrently
-            state, state_ev = L.embbag_bwd_prepare(V_shard.shape[0], dvG,
-                                                   idx_all.view(G * T_loc, B), V_shard.dtype)
         C.all_gather(w_all, w)
         y_part = L.embbag_fwd(V_shard, idx_all.view(G * T_loc, B), w_all.view(G * T_loc, B))  # 3
         gpre = L.gemm(x, W1)
@@ -193,6 +237,11 @@ class GroupMemoryLayer:
             y = y_all[rank * T_loc:(rank + 1) * T_loc]
             _, z = L.unpack(y.reshape(1, T_loc, dv), 1, T_loc, dv, gate=gpre, want_y=False)
         out = L.gemm(z, W2)                                             # 5
+        state = state_ev = None
+        if lst is not None:
+            lists = L.group_lists(G, lst)
+            C.all_gather(lists, lst.unsqueeze(0))                      # [G, 2, T_loc*B]
+            state, state_ev = L.group_merge(V_shard.shape[0], dvG, lists, V_shard.dtype)
         saved = dict(x=x, q=q, K1=K1, K2=K2, V=V_shard, W1=W1, W2=W2, idx=idx, w=w,
                      idx_all=idx_all, w_all=w_all, g=gpre, y=y, y_all=y_all, state=state,
                      state_ev=state_ev)

@@ -212,6 +212,35 @@ def embbag_bwd_prepare(N, dv, idx, dtype=torch.bfloat16, out=None):
     return state
 
 
+def group_sort_local(N, idx, rank, out=None, ws=None):
+    """This rank's share of the memory group's inverse map
+    (include/memlayer.h embbag_bwd_group_sort_local): its positions [T_loc*B]
+    sorted stably by row, tagged with global positions; returns the int32
+    list [2, T_loc*B] (rows | positions)."""
+    sh = BagShape(N, 8, idx.shape[0], idx.shape[1], _DT[torch.bfloat16])   # dv unused
+    P = idx.numel()
+    lst = out if out is not None else torch.empty((2, P), dtype=torch.int32, device=idx.device)
+    n = _size(lib().embbag_bwd_group_sort_local_workspace, sh)
+    ws = ws if (ws is not None and ws.numel() >= n) else workspace(n, idx.device)
+    check(lib().embbag_bwd_group_sort_local(C.byref(sh), int(rank), _p(idx), _p(lst), _p(ws), n,
+                                            _stream()))
+    return lst
+
+
+def group_merge(N, dv, lists, dtype=torch.bfloat16, out=None):
+    """The G ranks' sorted lists [G, 2, T_loc*B] (rank order) -> the state of
+    the bag over all G*T_loc tokens (embbag_bwd_group_merge), for
+    embbag_bwd(..., state=) on the [N, dv] shard."""
+    G, _, P_loc = lists.shape
+    sh = BagShape(N, dv, G * P_loc, 1, _DT[dtype])
+    # the state layout depends on P = T*B only: carve it as [G*P_loc, 1]
+    n = _size(lib().embbag_bwd_state_bytes, sh)
+    state = out if (out is not None and out.numel() >= n) else \
+        torch.empty((max(n, 1),), dtype=torch.uint8, device=lists.device)
+    check(lib().embbag_bwd_group_merge(C.byref(sh), int(G), _p(lists), _p(state), n, _stream()))
+    return state
+
+
 def embbag_bwd_dv_only(N, idx, w, dy, sync=True):
     """"reverse_indices" value gradient only (no V, no dw): rows, dV (compact)."""
     sh = BagShape(N, dy.shape[1], idx.shape[0], idx.shape[1], _dt(dy))

@@ -24,7 +24,32 @@ class OracleLocal:
     def embbag_fwd(self, V, idx, w):
         return torch.from_numpy(obag.embbag_fwd(_np(V), _np(idx), _np(w)))
 
-    def embbag_bwd(self, V, idx, w, dy):
+    # the group's inverse map (include/memlayer.h embbag_bwd_group_sort_local
+    # / _merge): own positions stably sorted by row with global positions,
+    # then a G-way merge of the gathered lists (ties to the lower rank)
+    def group_sort_local(self, N, idx, rank):
+        flat = _np(idx).reshape(-1).astype(np.int64)
+        order = np.argsort(flat, kind="stable")
+        return torch.from_numpy(np.stack([flat[order], order + rank * flat.size]).astype(np.int32))
+
+    def group_lists(self, G, lst):
+        return torch.empty((G,) + tuple(lst.shape), dtype=lst.dtype)
+
+    def group_merge(self, N, dv, lists, dtype):
+        import heapq
+        L = _np(lists)
+        runs = [[(int(L[g, 0, i]), g, int(L[g, 1, i])) for i in range(L.shape[2])] for g in range(L.shape[0])]
+        merged = list(heapq.merge(*runs, key=lambda e: (e[0], e[1])))
+        return np.array([[e[0] for e in merged], [e[2] for e in merged]], dtype=np.int64), None
+
+    def wait(self, ev):
+        pass
+
+    def embbag_bwd(self, V, idx, w, dy, state=None):
+        if state is not None:    # the merged map is the stable sort of all gathered positions
+            flat = _np(idx).reshape(-1).astype(np.int64)
+            order = np.argsort(flat, kind="stable")
+            assert np.array_equal(state[1], order) and np.array_equal(state[0], flat[order])
         rows, dV, dw = obag.embbag_bwd(_np(V), _np(idx), _np(w), _np(dy))
         return (torch.from_numpy(rows.astype(np.int32)), torch.from_numpy(dV),
                 torch.tensor([rows.size], dtype=torch.int32), torch.from_numpy(dw))

@@ -216,3 +216,39 @@ def test_capi_group_nccl_single_rank_equals_hub():
     for n in ("dx", "dq", "dK1", "dK2", "dW1", "dW2", "dw"):
         assert torch.equal(g[n], ref[2][n]), n
     assert torch.equal(g["dV"][:u], ref[2]["dV"][:u]) and torch.equal(g["rows"][:u], ref[2]["rows"][:u])
+
+
+@pytest.mark.parametrize("G,T_loc,B,N", [(2, 300, 32, 4096), (3, 257, 64, 1 << 20), (4, 64, 128, 512),
+                                         (8, 77, 128, 1 << 26), (5, 1, 7, 3)])
+def test_group_state_merge_bit_identical(G, T_loc, B, N):
+    """The group's inverse map built once per group (each rank sorts its own
+    positions, the sorted lists are merged: embbag_bwd_group_sort_local /
+    _merge) equals one sort of all G*T_loc*B gathered positions
+    (embbag_bwd_prepare): the bag backward from either state is
+    bit-identical.  Skewed indices (many equal rows across ranks, so the merge's
+    tie rule decides the order), G not a power of two, ragged tiles."""
+    from paper_2412_09764_b200 import ops
+    dv = 64
+    rng = np.random.default_rng(G * 1000 + T_loc)
+    hot = rng.integers(0, N, size=max(1, min(N, 50)))
+    raw = np.where(rng.random((G * T_loc, B)) < 0.5, rng.choice(hot, size=(G * T_loc, B)),
+                   rng.integers(0, N, size=(G * T_loc, B)))
+    idx = torch.from_numpy(raw.astype(np.int32)).cuda()
+    w = torch.from_numpy(rng.standard_normal((G * T_loc, B)).astype(np.float32)).cuda()
+    dy = torch.from_numpy(rng.standard_normal((G * T_loc, dv)).astype(np.float32)).cuda().to(torch.bfloat16)
+    V = torch.from_numpy(rng.standard_normal((N, dv)).astype(np.float32)).cuda().to(torch.bfloat16)
+    ref_state = ops.embbag_bwd_prepare(N, dv, idx)
+    lists = torch.empty((G, 2, T_loc * B), dtype=torch.int32, device="cuda")
+    for g in range(G):
+        ops.group_sort_local(N, idx[g * T_loc:(g + 1) * T_loc], g, out=lists[g])
+    # each list: rows ascending, positions stable (ascending within a row) and global
+    L = lists.cpu().numpy()
+    for g in range(G):
+        flat = raw[g * T_loc:(g + 1) * T_loc].reshape(-1)
+        order = np.argsort(flat, kind="stable")
+        assert np.array_equal(L[g, 0], flat[order]) and np.array_equal(L[g, 1], order + g * flat.size)
+    state = ops.group_merge(N, dv, lists)
+    a = ops.embbag_bwd(V, idx, w, dy, state=ref_state)
+    b = ops.embbag_bwd(V, idx, w, dy, state=state)
+    for x, y, n in zip(a, b, ("rows", "dV", "dw")):
+        assert torch.equal(x, y), n
