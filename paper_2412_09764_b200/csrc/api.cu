@@ -180,6 +180,7 @@ static mlStatus qk_compute(const mlPkmShape& s, const void* q, const void* K1, c
 
 struct PkmFwdBufs {
   float* scores = nullptr; int32_t* hI = nullptr; float* hs = nullptr; QkBufs qk;
+  float* cmax = nullptr;   // chunk maxima for the chunk-filtered half top-k (long rows)
   // fused scoring + filter: candidate lists, their lengths, fallback row list
   uint64_t* cand = nullptr; int32_t* cnt = nullptr; int32_t* fail_rows = nullptr;
   int32_t* fail_n = nullptr;
@@ -194,6 +195,7 @@ static void pkm_fwd_carve(Carver& c, const mlPkmShape& s, PkmFwdBufs& b) {
     return;
   }
   b.scores = c.take<float>(TH * 2 * s.S);
+  if (half_topk_chunked(s)) b.cmax = c.take<float>(TH * 2 * (s.S / 32));
   b.hI = c.take<int32_t>(TH * 2 * s.k);
   b.hs = c.take<float>(TH * 2 * s.k);
   qk_carve(c, s, b.qk);
@@ -268,8 +270,8 @@ static mlStatus pkm_fwd_core(const mlPkmShape& s, const void* q, const void* K1,
   }
   QkNorm qn;
   ML_TRY(qk_compute(s, q, K1, K2, b.qk, &qn, st));
-  ML_TRY(launch_pkm_scores(s, q, K1, K2, b.scores, st));
-  ML_TRY(launch_half_topk(s, b.scores, b.hI, b.hs, qn, st));
+  ML_TRY(launch_pkm_scores(s, q, K1, K2, b.scores, st, b.cmax));
+  ML_TRY(launch_half_topk(s, b.scores, b.hI, b.hs, qn, st, b.cmax));
   ML_TRY(launch_combine_softmax(s, b.hI, b.hs, idx, w, score, st));
   return ML_OK;
 }

@@ -122,12 +122,16 @@ mlStatus launch_row_inv_norm(const void* x, int64_t rows, int Dh, mlDtype dt, fl
 // out (=|+=) G - x_hat (x_hat . G) per row (or G where ||x|| <= eps)
 mlStatus launch_qk_proj(const void* x, int64_t rows, int Dh, mlDtype dt, const float* G, float* out,
                         bool accumulate, cudaStream_t s);
+// cmax (nullable; tcgen05 path): [T*H*2][S/32] maxima of every 32 consecutive
+// scores, written by the scoring epilogue for the half top-k's chunk filter
 mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1,
-                           const void* K2, float* scores, cudaStream_t s);
+                           const void* K2, float* scores, cudaStream_t s, float* cmax = nullptr);
+// the chunk-filtered half top-k applies (and the scoring should write cmax)
+bool half_topk_chunked(const mlPkmShape& sh);
 // tcgen05 path (bf16, Dk/2 % 64 == 0, S = 32..256 power of two or multiple of 256)
 bool pkm_scores_tc_eligible(const mlPkmShape& sh);
 mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
-                              float* scores, cudaStream_t s);
+                              float* scores, cudaStream_t s, float* cmax = nullptr);
 // fused scoring + half top-k filter (bf16, no qk-norm, S % 256 == 0, S >= 512):
 // per (t, h, half) row a candidate list cand[row][pkm_select_cap()] of 64-bit
 // keys (ord(score) << 32 | ~a) holding the row's k best, cnt[row] its length
@@ -161,7 +165,7 @@ mlStatus launch_pkm_dq(const mlPkmShape& sh, const int32_t* key1, const int32_t*
 mlStatus launch_combine_cand(const mlPkmShape& sh, const uint64_t* cand, const int32_t* cnt,
                              int32_t* idx, float* w, float* score, cudaStream_t s);
 mlStatus launch_half_topk(const mlPkmShape& sh, const float* scores, int32_t* hI,
-                          float* hs, const QkNorm& qn, cudaStream_t s);
+                          float* hs, const QkNorm& qn, cudaStream_t s, const float* cmax = nullptr);
 mlStatus launch_combine_softmax(const mlPkmShape& sh, const int32_t* hI, const float* hs,
                                 int32_t* idx, float* w, float* score, cudaStream_t s);
 // ds = w (dw - sum w dw) with dw = sum over nslices partials; also writes the

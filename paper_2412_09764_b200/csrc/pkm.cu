@@ -436,10 +436,127 @@ __device__ __forceinline__ bool row_topk_stream(const float* sr, int S, int k, T
   return true;
 }
 
+// Chunk-filtered variant for long rows (S % 1024 == 0, S >= 2048) when the
+// scoring epilogue wrote cm = the maxima of the row's S/32 chunks of 32
+// consecutive scores:
+//  1. every lane keeps the two largest of its S/1024 chunk maxima; theta =
+//     the k-th largest of those 64 values (distinct elements of the row, so a
+//     lower bound of its k-th largest score);
+//  2. only the chunks whose maximum reaches theta (typically ~k of S/32) are
+//     read, one coalesced 128-byte row segment each, and their scores
+//     v >= theta appended to shared memory;
+//  3. survivors ranked by counting as in row_topk_stream.
+// Reads ~k * 128 B of scores per row instead of streaming the row twice.
+__device__ __forceinline__ bool row_topk_chunks(const float* sr, const float* cm, int S, int k,
+                                                TopkSmem& sm, int64_t row, int32_t* hI, float* hs,
+                                                int* count_out) {
+  constexpr int NJ = 8;                        // chunk maxima per lane held in registers (S <= 8192)
+  const int lane = threadIdx.x & 31;
+  const int nj = S >> 10;
+  float x[NJ];
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    x[j] = j < nj ? cm[j * 32 + lane] : -INFINITY;
+    const float lo = fminf(m0, x[j]);
+    m0 = fmaxf(m0, x[j]);
+    m1 = fmaxf(m1, lo);
+  }
+  for (int j = NJ; j < nj; ++j) {              // S > 8192
+    const float v = cm[j * 32 + lane];
+    const float lo = fminf(m0, v);
+    m0 = fmaxf(m0, v);
+    m1 = fmaxf(m1, lo);
+  }
+  const float A = warp_sort_desc_f(m0), B = warp_sort_desc_f(m1);
+  float c = -INFINITY;
+  {
+    const int i = lane;
+    const float a = __shfl_sync(FULL, A, (i + 31) & 31);
+    const float b = __shfl_sync(FULL, B, (k - 1 - i) & 31);
+    if (i <= k - 1) c = fminf(i == 0 ? INFINITY : a, b);
+  }
+  const float ak = __shfl_sync(FULL, A, k - 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c = fmaxf(c, __shfl_xor_sync(FULL, c, o));
+  const float theta = fmaxf(c, ak);
+  // qualifying chunk ids (max >= theta) -> sm.hist, in chunk order
+  uint32_t* qlist = sm.hist;
+  int nq = 0;
+  auto list_chunks = [&](float xm, int j) {
+    const unsigned qm = __ballot_sync(FULL, xm >= theta);
+    if (xm >= theta) {
+      const int pos = nq + __popc(qm & ((1u << lane) - 1u));
+      if (pos < 256) qlist[pos] = uint32_t(j * 32 + lane);
+    }
+    nq += __popc(qm);
+  };
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+    if (j < nj) list_chunks(x[j], j);
+  for (int j = NJ; j < nj; ++j) list_chunks(cm[j * 32 + lane], j);
+  if (nq > 256) {           // heavy ties at theta: leave it to the exact fallback
+    *count_out = kCandCap + 1;
+    return false;
+  }
+  __syncwarp();
+  // four chunks per warp load (lane: chunk l/8, scores 4(l%8)..+3), two loads in flight
+  int count = 0;
+  uint64_t* ckw = sm.cand;
+  auto take = [&](float4 v, int ci) {
+    const int base = ci < nq ? int(qlist[ci]) * 32 + (lane & 7) * 4 : 0;
+    const float vs[4] = {v.x, v.y, v.z, v.w};
+    uint32_t mk = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mk |= (ci < nq && vs[q] >= theta ? 1u : 0u) << q;
+    const int cnt = __popc(mk);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos = count + incl - cnt;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if ((mk >> q) & 1u) {
+        if (pos < kCandCap) ckw[pos] = make_key(vs[q], uint32_t(base + q));
+        ++pos;
+      }
+    count += __shfl_sync(FULL, incl, 31);
+  };
+  const float4 ninf = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+  for (int g = 0; g < nq; g += 8) {
+    const int ca = g + (lane >> 3), cb = g + 4 + (lane >> 3);
+    const float4 va = ca < nq ? *reinterpret_cast<const float4*>(sr + qlist[ca] * 32 + (lane & 7) * 4) : ninf;
+    const float4 vb = cb < nq ? *reinterpret_cast<const float4*>(sr + qlist[cb] * 32 + (lane & 7) * 4) : ninf;
+    take(va, ca);
+    if (g + 4 < nq) take(vb, cb);
+  }
+  *count_out = count;
+  if (count > 64) return false;
+  __syncwarp();
+  uint64_t* ck = sm.cand;
+  const bool h0 = lane < count, h1 = lane + 32 < count;
+  const uint64_t k0 = h0 ? ck[lane] : ~0ull, k1 = h1 ? ck[lane + 32] : ~0ull;
+  int r0 = 0, r1 = 0;
+  if ((count & 1) != 0) ck[count] = 0ull;   // pad: ranks nothing
+  __syncwarp();
+  const int pairs = (count + 1) >> 1;
+  for (int l = 0; l < pairs; ++l) {
+    const ulonglong2 kk = reinterpret_cast<const ulonglong2*>(ck)[l];
+    r0 += (kk.x > k0 ? 1 : 0) + (kk.y > k0 ? 1 : 0);
+    r1 += (kk.x > k1 ? 1 : 0) + (kk.y > k1 ? 1 : 0);
+  }
+  if (h0 && r0 < k) { hI[row * k + r0] = int32_t(key_id(k0)); hs[row * k + r0] = key_score(k0); }
+  if (h1 && r1 < k) { hI[row * k + r1] = int32_t(key_id(k1)); hs[row * k + r1] = key_score(k1); }
+  return true;
+}
+
 // one warp per (t, h, half) row of S scores
 __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int64_t rows, int S,
                                                         int k, int32_t* hI, float* hs, QkNorm qn,
-                                                        int H) {
+                                                        int H, const float* cmax) {
   __shared__ TopkSmem s_sm[8];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = int64_t(blockIdx.x) * 8 + wid;
@@ -452,7 +569,8 @@ __global__ void __launch_bounds__(256) half_topk_kernel(const float* scores, int
   auto score_at = [=](int e) { return ki ? (sr[e] * qi) * ki[e] : sr[e]; };
   if ((S % 128) == 0 && ki == nullptr && k <= 32) {
     int count = 0;
-    if (S > 1024 ? row_topk_stream(sr, S, k, sm, row, hI, hs, &count)
+    if (cmax ? row_topk_chunks(sr, cmax + row * (S >> 5), S, k, sm, row, hI, hs, &count)
+        : S > 1024 ? row_topk_stream(sr, S, k, sm, row, hI, hs, &count)
                  : (S == 1024 ? row_topk_fast<true>(sr, S, k, sm, row, hI, hs, &count)
                               : row_topk_fast<false>(sr, S, k, sm, row, hI, hs, &count)))
       return;
@@ -977,10 +1095,21 @@ __global__ void __launch_bounds__(256) pkm_dq_kernel(const int32_t* key1, const 
 
 }  // namespace
 
+bool half_topk_chunked(const mlPkmShape& sh) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = std::getenv("ML_TOPK_CHUNKS");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  return !off && pkm_scores_tc_eligible(sh) && !sh.qk_norm && sh.S >= 2048 && sh.S % 1024 == 0 &&
+         sh.k <= 32;
+}
+
 mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
-                           float* scores, cudaStream_t s) {
+                           float* scores, cudaStream_t s, float* cmax) {
   if (sh.T <= 0) return ML_OK;
-  if (pkm_scores_tc_eligible(sh)) return launch_pkm_scores_tc(sh, q, K1, K2, scores, s);
+  if (pkm_scores_tc_eligible(sh)) return launch_pkm_scores_tc(sh, q, K1, K2, scores, s, cmax);
+  if (cmax) return fail(ML_ERR_UNSUPPORTED, "chunk maxima need the tcgen05 scoring path");
   dim3 grid{unsigned((sh.T + 63) / 64), unsigned((sh.S + 63) / 64), unsigned(sh.H * 2)};
   if (sh.dtype == ML_BF16)
     pkm_scores_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
@@ -996,11 +1125,11 @@ mlStatus launch_pkm_scores(const mlPkmShape& sh, const void* q, const void* K1, 
 }
 
 mlStatus launch_half_topk(const mlPkmShape& sh, const float* scores, int32_t* hI, float* hs,
-                          const QkNorm& qn, cudaStream_t s) {
+                          const QkNorm& qn, cudaStream_t s, const float* cmax) {
   const int64_t rows = int64_t(sh.T) * sh.H * 2;
   if (rows <= 0) return ML_OK;
   half_topk_kernel<<<unsigned((rows + 7) / 8), 256, 0, s>>>(scores, rows, sh.S, sh.k, hI, hs, qn,
-                                                            sh.H);
+                                                            sh.H, cmax);
   ML_LAUNCH_CHECK("half_topk");
   return ML_OK;
 }

@@ -38,6 +38,7 @@ constexpr int kThreads = 256;
 
 struct TcParams {
   float* scores;
+  float* cmax;      // nullable: [T][H*2][S/32] chunk maxima
   int T, H, S, Dh, Dk;
   int BN, n_sub, k_chunks, m_tiles, tiles;
   uint32_t idesc;
@@ -176,9 +177,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int n = 0; n < p.n_sub; ++n) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        float cm[8];          // this row's chunk maxima of the subtile (BN / 32 <= 8)
         for (int c0 = 0; c0 < p.BN; c0 += 32, ++it) {
           uint32_t r[32];
           tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
+          if (p.cmax) {
+            float m = __uint_as_float(r[0]);
+#pragma unroll
+            for (int j = 1; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]));
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j == (c0 >> 5)) cm[j] = m;
+          }
           float* stg = stg0 + (it % kStageBufs) * kStageFloats;
           // the store issued from this buffer kStageBufs chunks ago must have read it
           if (lane == 0) {
@@ -201,6 +211,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
+        if (p.cmax && row0 + lane < p.T) {    // 32 contiguous bytes per row (BN = 256)
+          float* dst = p.cmax + (int64_t(row0 + lane) * p.H * 2 + hh) * (p.S >> 5) + (n * p.BN >> 5);
+          if (p.BN == 256) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(cm[0], cm[1], cm[2], cm[3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(cm[4], cm[5], cm[6], cm[7]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < (p.BN >> 5)) dst[j] = cm[j];
+          }
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -531,10 +552,11 @@ bool pkm_scores_tc_eligible(const mlPkmShape& sh) {
 }
 
 mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K1, const void* K2,
-                              float* scores, cudaStream_t s) {
+                              float* scores, cudaStream_t s, float* cmax) {
   const int Dh = sh.Dk / 2;
   TcParams p;
   p.scores = scores;
+  p.cmax = cmax;
   p.T = sh.T; p.H = sh.H; p.S = sh.S; p.Dh = Dh; p.Dk = sh.Dk;
   p.BN = tc_bn(sh.S);
   p.n_sub = sh.S / p.BN;
@@ -631,6 +653,7 @@ mlStatus launch_pkm_select_tc(const mlPkmShape& sh, const void* q, const void* K
   const int Dh = sh.Dk / 2;
   TcParams p;
   p.scores = nullptr;
+  p.cmax = nullptr;
   p.T = sh.T; p.H = sh.H; p.S = sh.S; p.Dh = Dh; p.Dk = sh.Dk;
   p.BN = 256;
   p.n_sub = sh.S / p.BN;

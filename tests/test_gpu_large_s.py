@@ -94,9 +94,10 @@ def test_pkm_topk_bwd_bf16_large_S(T, H, S, Dk, k):
     assert_close(host(dK2), rdK2, TOL["f32"], "dK2")
 
 
-def _in_subprocess(q, K1, K2, k, fused):
+def _in_subprocess(q, K1, K2, k, fused, env_extra=None):
     """pkm_topk in a fresh process with the fused scoring + filter kernel
-    switched on (ML_PKM_FUSED=1) or off (score matrix + half top-k kernel)."""
+    switched on (ML_PKM_FUSED=1) or off (score matrix + half top-k kernel);
+    env_extra: further switches (e.g. ML_TOPK_CHUNKS)."""
     import os, subprocess, sys, tempfile
     with tempfile.TemporaryDirectory() as d:
         np.save(os.path.join(d, "q.npy"), q)
@@ -110,7 +111,7 @@ def _in_subprocess(q, K1, K2, k, fused):
             f"i, w, s = ops.pkm_topk(t('q'), t('K1'), t('K2'), {k}, with_score=True)\n"
             "np.save(d + '/i.npy', i.cpu().numpy()); np.save(d + '/w.npy', w.cpu().numpy())\n"
             "np.save(d + '/s.npy', s.cpu().numpy())\n")
-        env = dict(os.environ, ML_PKM_FUSED="1" if fused else "0")
+        env = dict(os.environ, ML_PKM_FUSED="1" if fused else "0", **(env_extra or {}))
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                            text=True, timeout=600)
@@ -148,3 +149,20 @@ def test_fused_select_fallback_rows():
     assert np.array_equal(idx, ridx)
     assert np.array_equal(score.astype(np.float64), rscore)
     assert_close(w.astype(np.float64), rw, 1e-6, "w")
+
+
+@pytest.mark.parametrize("T,H,S,Dk,k,cls", [(300, 2, 4096, 128, 32, gen.CLS_CONTINUOUS),
+                                            (260, 2, 8192, 128, 32, gen.CLS_CONTINUOUS),
+                                            (130, 2, 2048, 256, 8, gen.CLS_CONTINUOUS),
+                                            (200, 2, 4096, 128, 32, gen.CLS_EXACT)])
+def test_chunk_filtered_half_topk_equals_streaming(T, H, S, Dk, k, cls):
+    """Long rows: the half top-k that reads only the 32-score chunks whose
+    maximum (written by the scoring epilogue) reaches the bound selects
+    exactly what the two-pass streaming top-k selects: indices, scores and
+    weights bit-identical (exact class: heavy ties at the bound)."""
+    q, K1, K2 = _inputs(36, T, H, S, Dk, cls)
+    ci, cw, cs = _in_subprocess(q, K1, K2, k, fused=False, env_extra={"ML_TOPK_CHUNKS": "1"})
+    si, sw, ss = _in_subprocess(q, K1, K2, k, fused=False, env_extra={"ML_TOPK_CHUNKS": "0"})
+    assert np.array_equal(ci, si)
+    assert np.array_equal(cs, ss)
+    assert np.array_equal(cw, sw)
