@@ -22,7 +22,8 @@ LABEL = OrderedDict([("seg_pipe_kernel", "embbag_bwd_segreduce"),
                      ("bag_fwd_kernel", "embbag_fwd_gate"),
                      ("pkm_scores_tc_kernel", "pkm_scores_tc"),
                      ("half_topk_kernel", "half_topk"),
-                     ("combine_kernel", "combine_softmax")])
+                     ("combine_kernel", "combine_softmax"),
+                     ("pkm_bwd_tc_kernel", "pkm_dq_tc / pkm_dK_tc")])
 
 
 def short(name):
