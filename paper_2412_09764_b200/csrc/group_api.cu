@@ -405,7 +405,10 @@ mlStatus group_state_merge(mlGroup_* g, const mlBagShape& s, GroupState& gs, cud
   cudaStream_t ps = serial_mode() ? st : g->prep;
   cudaStream_t cs = serial_mode() ? st : g->comm;
   const int64_t P_loc = int64_t(s.T) * s.B;
+  // after the local sort AND after every collective already issued on the
+  // caller's stream (one device order for all of the group's NCCL calls)
   ML_TRY(dep(ps, cs, g->ev[7]));
+  if (cs != st) ML_TRY(dep(st, cs, g->ev[5]));
   ML_TRY(g->tr->all_gather(gs.send, gs.recv, size_t(2 * P_loc) * sizeof(int32_t), cs));
   ML_TRY(dep(cs, ps, g->ev[7]));
   const mlBagShape bs = shard_shape(g, s);
@@ -619,6 +622,17 @@ mlStatus embbag_bwd_group(mlGroup g, const mlBagShape* shape, const void* V_shar
   const mlBagShape bs = shard_shape(g, *shape);
   const int dvG = shape->dv / G;
   const size_t e = dtype_size(shape->dtype);
+  size_t wb = 0, sb = 0;
+  ML_TRY((embbag_bwd_workspace(&bs, &wb)));
+  ML_TRY((embbag_bwd_state_bytes(&bs, &sb)));
+  // the state's list all-gather ran on the communication stream: wait for the
+  // state BEFORE this call's collectives, so that every NCCL operation of the
+  // group is ordered on the device exactly as it was issued (no two in flight
+  // on different streams)
+  if (state) {
+    if (state_bytes < sb) return fail(ML_ERR_WORKSPACE, "embbag_bwd_group: state too small");
+    ML_CUDA_TRY(cudaStreamWaitEvent(st, g->state_ready, 0));
+  }
   if (mode == ML_OUT_ALLTOALL) {
     // dy of this rank's tokens -> [G][T_loc][dv/G] -> slice g to rank g
     ML_TRY((ml_group_pack(dy, G, shape->T, shape->dv, b.dy_send, shape->dtype, st)));
@@ -629,13 +643,7 @@ mlStatus embbag_bwd_group(mlGroup g, const mlBagShape* shape, const void* V_shar
                                   size_t(shape->dv) * e, size_t(dvG) * e, size_t(G) * shape->T,
                                   cudaMemcpyDeviceToDevice, st));
   }
-  size_t wb = 0, sb = 0;
-  ML_TRY((embbag_bwd_workspace(&bs, &wb)));
-  ML_TRY((embbag_bwd_state_bytes(&bs, &sb)));
-  if (state) {
-    if (state_bytes < sb) return fail(ML_ERR_WORKSPACE, "embbag_bwd_group: state too small");
-    ML_CUDA_TRY(cudaStreamWaitEvent(st, g->state_ready, 0));
-  } else {
+  if (!state) {
     ML_TRY((embbag_bwd_prepare(&bs, idx_all, b.state, sb, st)));
     state = b.state;
   }
