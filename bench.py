@@ -423,6 +423,8 @@ def run_ours(args, cfg, world, rank, local):
         dist.init_process_group("nccl", device_id=dev)
         from paper_2412_09764_b200.group import nccl_group
         comm = CGroup(nccl_group(dist.group.WORLD))
+        if args.p2p:
+            comm.grp.set_p2p(True)
     t = make_inputs(cfg, dev, G, rank if world > 1 else 0, ops, torch, group_path)
     if per_rank > 1:
         comm = LoopbackComm(G, 0, group_others(cfg, G, 0, t, ops, torch))
@@ -847,6 +849,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None)
     ap.add_argument("--mode", default="alltoall", choices=["alltoall", "allgather"])
+    ap.add_argument("--p2p", action="store_true",
+                    help="N > 1, mode alltoall: the fused peer-memory forward exchange "
+                         "(ml_group_set_p2p: bag kernels store into the owners' regions) instead "
+                         "of NCCL point-to-point steps")
     ap.add_argument("--per-rank", type=int, default=0,
                     help="on one GPU: time one rank's work of a G-rank group (collectives removed)")
     ap.add_argument("--cpu-tokens", type=int, default=1024)
@@ -896,7 +902,8 @@ def main():
         cb = cpu_baseline(cfg, args.cpu_tokens if cfg_name != "c1" else cfg["T"])
     bb = bag_bytes(cfg, G, res["T_loc"], res["U"])
     if world > 1:
-        par = f"memory-group dim-shard G={G} ({args.mode}), NCCL"
+        par = f"memory-group dim-shard G={G} ({args.mode}), NCCL" + (
+            " + fused peer-memory forward exchange" if args.p2p and args.mode == "alltoall" else "")
     elif args.per_rank > 1:
         par = (f"one rank of a G={G} memory group on one GPU (collectives replaced by local "
                f"copies: SURVEY §8(e) t_ref(G)), {args.mode}")

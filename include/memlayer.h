@@ -370,6 +370,19 @@ mlStatus ml_group_hub_destroy(void* hub);
 mlStatus ml_group_init_hub(void* hub, int rank, mlGroup* out);
 mlStatus ml_group_destroy(mlGroup g);
 mlStatus ml_group_info(mlGroup g, int* G, int* rank);
+/* Fused forward exchange (mode ML_OUT_ALLTOALL; "each worker gathers
+ * the partial embeddings corresponding to its own portion of the indices"):
+ * on = 1 makes the bag forward of every token block store its output rows
+ * straight into the owning rank's exchange region over peer memory (NCCL
+ * transport: a cudaMalloc'd region per rank mapped into the others with CUDA
+ * IPC, which needs peer access between the group's GPUs -- NVLink/NVSwitch;
+ * hub transport: plain device pointers) instead of point-to-point sends,
+ * followed by one flag barrier (epoch flags stored with release semantics at
+ * system scope, waited on with acquire).  The region (2 x G x T_loc x dv/G
+ * elements + 4 KiB of flags per rank) is allocated by the group on first use
+ * -- a collective: every rank must make the same calls.  Default off, or on
+ * when the environment sets ML_GROUP_P2P=1 at group creation. */
+mlStatus ml_group_set_p2p(mlGroup g, int on);
 
 /* Bag level.  shape: N, dv = the FULL value dim, T = T_loc, B, dtype
  * (grad_dtype for dV_shard).  Forward: idx_local/w_local [T_loc, B] ->

@@ -101,6 +101,7 @@ SIGNATURES = {
     "ml_group_init_hub": [P, C.c_int, C.POINTER(P)],
     "ml_group_destroy": [P],
     "ml_group_info": [P, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "ml_group_set_p2p": [P, C.c_int],
     "embbag_fwd_group_workspace": [P, C.POINTER(BagShape), C.c_int, C.POINTER(SZ)],
     "embbag_fwd_group": [P, C.POINTER(BagShape), P, P, P, P, P, C.c_int, P, P, SZ, P],
     "embbag_bwd_group_state_bytes": [P, C.POINTER(BagShape), C.POINTER(SZ)],

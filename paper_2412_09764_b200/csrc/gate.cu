@@ -183,7 +183,9 @@ mlStatus gemm_rm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t
       ck(cublasLtMatmulAlgoGetHeuristic(h, desc, l1, l2, lc, lc, pref, kCand, all, &nres), "heuristic");
       if (nres > 0) heur = all[0];
       if (st == ML_OK && tune && nres > 1 && beta == 0.f) {
-        static cudaEvent_t e0 = nullptr, e1 = nullptr;
+        // per host thread: concurrent callers (one thread per rank of a hub
+        // group) must not record into each other's timing events
+        thread_local cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (!e0) {
           ML_CUDA_TRY(cudaEventCreate(&e0));
           ML_CUDA_TRY(cudaEventCreate(&e1));

@@ -113,12 +113,129 @@ struct Transport {
   virtual mlStatus sendrecv(const void*, int, void*, int, size_t, cudaStream_t) {
     return fail(ML_ERR_UNSUPPORTED, "transport: no point-to-point steps");
   }
+  // Peer memory (the fused exchange): every rank owns an exchange region that
+  // the other ranks' kernels store into directly.  peer_setup is collective
+  // (all ranks, same bytes); peer_region(g) = rank g's region as addressed by
+  // this rank; peer_barrier: every peer-memory store issued on s so far is
+  // visible to its target, and every peer's stores to this rank are visible
+  // to the work that follows on s.
+  virtual bool has_peer_mem() const { return false; }
+  virtual mlStatus peer_setup(size_t, cudaStream_t) {
+    return fail(ML_ERR_UNSUPPORTED, "transport: no peer memory");
+  }
+  virtual char* peer_region(int) { return nullptr; }
+  virtual mlStatus peer_barrier(cudaStream_t) {
+    return fail(ML_ERR_UNSUPPORTED, "transport: no peer memory");
+  }
 };
+
+constexpr size_t kPeerFlagBytes = 4096;    // head of every exchange region: G epoch flags
+
+// one warp: release this rank's stores (epoch flag written into every peer's
+// region), then acquire every peer's (wait for their flags); bounded spin
+__global__ void p2p_barrier_kernel(uint64_t* const* peer_flags, uint64_t* my_flags, int G, int rank,
+                                   uint64_t epoch) {
+  const int g = threadIdx.x;
+  const bool peer = g < G && g != rank;
+  if (peer) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_flags[g] + rank), "l"(epoch)
+                 : "memory");
+  }
+  __syncwarp();
+  if (peer) {
+    uint64_t v = 0;
+    for (uint32_t spins = 0;; ++spins) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + g) : "memory");
+      if (v >= epoch) break;
+      if (spins > (1u << 26)) __trap();     // ~7 s: a peer never arrived
+      __nanosleep(100);
+    }
+  }
+  __syncwarp();
+}
 
 struct NcclTransport : Transport {
   ncclComm_t comm = nullptr;
+  // peer memory: a cudaMalloc'd region per rank, mapped into the other ranks
+  // with CUDA IPC (NVLink / NVSwitch peer access); epoch flags at its head
+  bool peer_on = false;
+  char* region = nullptr;
+  size_t region_bytes = 0;
+  std::vector<char*> peers;
+  uint64_t** d_peer_flags = nullptr;
+  uint64_t epoch = 0;
+  uint8_t* d_sync = nullptr;      // [G] bytes: a 1-byte all-gather as a barrier
   ~NcclTransport() override {
+    release_peers();
+    if (d_sync) cudaFree(d_sync);
     if (comm) nccl().commDestroy(comm);
+  }
+  mlStatus nccl_barrier(cudaStream_t s) {
+    if (!d_sync) ML_CUDA_TRY(cudaMalloc(&d_sync, size_t(G)));
+    ML_NCCL_TRY(nccl().allGather(d_sync + rank, d_sync, 1, ncclUint8, comm, s));
+    ML_CUDA_TRY(cudaStreamSynchronize(s));
+    return ML_OK;
+  }
+  void release_peers() {
+    for (int g = 0; g < int(peers.size()); ++g)
+      if (g != rank && peers[size_t(g)]) cudaIpcCloseMemHandle(peers[size_t(g)]);
+    peers.clear();
+    if (region) cudaFree(region);
+    if (d_peer_flags) cudaFree(d_peer_flags);
+    region = nullptr;
+    d_peer_flags = nullptr;
+    region_bytes = 0;
+  }
+  bool has_peer_mem() const override { return peer_on && G > 1; }
+  char* peer_region(int g) override { return peers[size_t(g)]; }
+  mlStatus peer_setup(size_t bytes, cudaStream_t s) override {
+    if (bytes <= region_bytes) return ML_OK;      // every rank decides alike (same shapes)
+    ML_CUDA_TRY(cudaStreamSynchronize(s));
+    // nobody may still write into the old regions: a collective as a barrier
+    if (region) {
+      ML_CUDA_TRY(cudaDeviceSynchronize());
+      ML_TRY(nccl_barrier(s));
+    }
+    release_peers();
+    ML_CUDA_TRY(cudaMalloc(&region, bytes));
+    ML_CUDA_TRY(cudaMemset(region, 0, kPeerFlagBytes));
+    region_bytes = bytes;
+    cudaIpcMemHandle_t mine;
+    ML_CUDA_TRY(cudaIpcGetMemHandle(&mine, region));
+    char* d_handles = nullptr;
+    ML_CUDA_TRY(cudaMalloc(&d_handles, sizeof(cudaIpcMemHandle_t) * size_t(G)));
+    ML_CUDA_TRY(cudaMemcpyAsync(d_handles + sizeof(mine) * size_t(rank), &mine, sizeof(mine),
+                                cudaMemcpyHostToDevice, s));
+    ML_NCCL_TRY(nccl().allGather(d_handles + sizeof(mine) * size_t(rank), d_handles, sizeof(mine),
+                                 ncclUint8, comm, s));
+    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(G));
+    ML_CUDA_TRY(cudaMemcpyAsync(all.data(), d_handles, sizeof(mine) * size_t(G), cudaMemcpyDeviceToHost, s));
+    ML_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(d_handles);
+    peers.assign(size_t(G), nullptr);
+    std::vector<uint64_t*> flags(static_cast<size_t>(G));
+    for (int g = 0; g < G; ++g) {
+      if (g == rank) {
+        peers[size_t(g)] = region;
+      } else {
+        void* p = nullptr;
+        ML_CUDA_TRY(cudaIpcOpenMemHandle(&p, all[size_t(g)], cudaIpcMemLazyEnablePeerAccess));
+        peers[size_t(g)] = static_cast<char*>(p);
+      }
+      flags[size_t(g)] = reinterpret_cast<uint64_t*>(peers[size_t(g)]);
+    }
+    ML_CUDA_TRY(cudaMalloc(&d_peer_flags, sizeof(uint64_t*) * size_t(G)));
+    ML_CUDA_TRY(cudaMemcpy(d_peer_flags, flags.data(), sizeof(uint64_t*) * size_t(G), cudaMemcpyHostToDevice));
+    // every rank mapped every region before the first store into one
+    return nccl_barrier(s);
+  }
+  mlStatus peer_barrier(cudaStream_t s) override {
+    ++epoch;
+    p2p_barrier_kernel<<<1, 32, 0, s>>>(d_peer_flags, reinterpret_cast<uint64_t*>(region), G, rank, epoch);
+    ML_CUDA_TRY(cudaGetLastError());
+    timing_mark("p2p_barrier", s);
+    return ML_OK;
   }
   mlStatus all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
     ML_NCCL_TRY(nccl().allGather(send, recv, bytes, ncclUint8, comm, s));
@@ -184,6 +301,37 @@ struct Hub {
 
 struct HubTransport : Transport {
   Hub* hub = nullptr;
+  // peer memory of G threads on one device: plain device pointers, the
+  // barrier a host one after draining the stream (no kernel ever waits on
+  // another rank's kernel)
+  bool peer_on = false;
+  char* region = nullptr;
+  size_t region_bytes = 0;
+  std::vector<char*> peers;
+  ~HubTransport() override {
+    if (region) cudaFree(region);
+  }
+  bool has_peer_mem() const override { return peer_on && G > 1; }
+  char* peer_region(int g) override { return peers[size_t(g)]; }
+  mlStatus peer_setup(size_t bytes, cudaStream_t s) override {
+    if (bytes <= region_bytes) return ML_OK;
+    ML_CUDA_TRY(cudaStreamSynchronize(s));
+    hub->barrier();                        // nobody still uses the old regions
+    if (region) cudaFree(region);
+    ML_CUDA_TRY(cudaMalloc(&region, bytes));
+    region_bytes = bytes;
+    hub->send[size_t(rank)] = region;
+    hub->barrier();
+    peers.assign(size_t(G), nullptr);
+    for (int g = 0; g < G; ++g) peers[size_t(g)] = static_cast<char*>(const_cast<void*>(hub->send[size_t(g)]));
+    hub->barrier();
+    return ML_OK;
+  }
+  mlStatus peer_barrier(cudaStream_t s) override {
+    ML_CUDA_TRY(cudaStreamSynchronize(s));
+    hub->barrier();
+    return ML_OK;
+  }
   mlStatus publish(const void* p, cudaStream_t s) {
     ML_CUDA_TRY(cudaStreamSynchronize(s));
     hub->send[size_t(rank)] = p;
@@ -261,10 +409,18 @@ struct mlGroup_ {
   cudaEvent_t ev[8] = {};
   std::vector<cudaEvent_t> blk;     // per-block events of the pipelined forward
   cudaEvent_t state_ready = nullptr;
+  uint64_t p2p_steps = 0;           // fused forward exchanges so far (double-buffer parity)
 };
 
 namespace ml {
 namespace {
+
+// ML_GROUP_P2P=1: the fused peer-memory forward exchange by default (else
+// ml_group_set_p2p)
+bool p2p_env() {
+  const char* e = std::getenv("ML_GROUP_P2P");
+  return e && e[0] == '1';
+}
 
 mlStatus group_make(mlGroup_* g) {
   ML_CUDA_TRY(cudaGetDevice(&g->device));
@@ -338,12 +494,35 @@ mlStatus gather_iw(mlGroup_* g, const mlBagShape& s, const int32_t* idx, const f
 // block last); recv [G][T_loc][dv/G] from every rank.  Mode N: blocks in rank
 // order, each all-gathered: recv [block][G src][T_loc][dv/G].
 mlStatus bag_blocks(mlGroup_* g, const mlBagShape& s, mlOutMode mode, const void* V_shard,
-                    const int32_t* idx_all, const float* w_all, FwdBufs& b, cudaStream_t st) {
+                    const int32_t* idx_all, const float* w_all, FwdBufs& b, cudaStream_t st,
+                    const void** recv_out) {
   const int G = g->tr->G, r = g->tr->rank;
   const int dvG = s.dv / G;
   const int64_t e = int64_t(dtype_size(s.dtype));
   const size_t blk_bytes = size_t(s.T) * dvG * e;
   const mlBagShape bs{s.N, dvG, s.T, s.B, s.dtype, ML_F32};
+  *recv_out = b.recv;
+  if (mode == ML_OUT_ALLTOALL && g->tr->has_peer_mem()) {
+    // Fused exchange (peer memory): the bag kernel of block `to` stores its
+    // output rows straight into rank `to`'s exchange region, slot `r`, over
+    // NVLink -- the transfer rides inside the HBM-bound gather, no separate
+    // collective.  Regions are double-buffered by step parity: a writer
+    // reuses a half only two steps later, after the barrier of the step in
+    // between, which the receiver passes only after unpacking this one.
+    const size_t half_bytes = size_t(G) * blk_bytes;
+    ML_TRY(g->tr->peer_setup(kPeerFlagBytes + 2 * half_bytes, st));
+    const size_t off = kPeerFlagBytes + size_t(g->p2p_steps & 1) * half_bytes;
+    ++g->p2p_steps;
+    for (int i = 0; i < G; ++i) {
+      const int to = (r + 1 + i) % G;      // own block last
+      char* dst = g->tr->peer_region(to) + off + size_t(r) * blk_bytes;
+      ML_TRY((embbag_fwd(&bs, V_shard, idx_all + int64_t(to) * s.T * s.B,
+                         w_all + int64_t(to) * s.T * s.B, nullptr, dst, nullptr, st)));
+    }
+    ML_TRY(g->tr->peer_barrier(st));
+    *recv_out = g->tr->peer_region(r) + off;
+    return ML_OK;
+  }
   const bool p2p = mode == ML_OUT_ALLTOALL && g->tr->has_p2p();
   const bool pipelined = p2p || mode == ML_OUT_ALLGATHER;
   // measurement mode (ml_set_serial): the exchange runs on the caller's
@@ -441,6 +620,7 @@ mlStatus ml_group_init(const void* id, int G, int rank, mlGroup* out) {
   auto* t = new NcclTransport();
   t->G = G;
   t->rank = rank;
+  t->peer_on = p2p_env();
   ncclUniqueId u;
   memcpy(&u, id, sizeof(u));
   const ncclResult_t r = nccl().commInitRank(&t->comm, G, u, rank);
@@ -478,6 +658,7 @@ mlStatus ml_group_init_hub(void* hub, int rank, mlGroup* out) {
   auto* t = new HubTransport();
   t->G = h->G;
   t->rank = rank;
+  t->peer_on = p2p_env();
   t->hub = h;
   auto* g = new mlGroup_();
   g->tr = t;
@@ -501,6 +682,15 @@ mlStatus ml_group_destroy(mlGroup g) {
   cudaStreamDestroy(g->prep);
   delete g->tr;
   delete g;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus ml_group_set_p2p(mlGroup g, int on) {
+  ML_API_BEGIN_X
+  if (!g) return fail(ML_ERR_ARG, "null group");
+  if (auto* t = dynamic_cast<NcclTransport*>(g->tr)) t->peer_on = on != 0;
+  else if (auto* h = dynamic_cast<HubTransport*>(g->tr)) h->peer_on = on != 0;
   return ML_OK;
   ML_API_END_X
 }
@@ -543,10 +733,11 @@ mlStatus embbag_fwd_group(mlGroup g, const mlBagShape* shape, const void* V_shar
   FwdBufs b;
   fwd_carve(c, g, *shape, mode, b);
   ML_TRY(gather_iw(g, *shape, idx_local, w_local, idx_all, w_all, b, st));
-  ML_TRY(bag_blocks(g, *shape, mode, V_shard, idx_all, w_all, b, st));
+  const void* recv = nullptr;
+  ML_TRY(bag_blocks(g, *shape, mode, V_shard, idx_all, w_all, b, st, &recv));
   const size_t blk_bytes = size_t(shape->T) * (shape->dv / G) * dtype_size(shape->dtype);
   if (mode == ML_OUT_ALLTOALL)
-    return ml_group_unpack(b.recv, G, shape->T, shape->dv, nullptr, y, nullptr, shape->dtype, st);
+    return ml_group_unpack(recv, G, shape->T, shape->dv, nullptr, y, nullptr, shape->dtype, st);
   for (int blk = 0; blk < G; ++blk)
     ML_TRY((ml_group_unpack(static_cast<char*>(b.recv) + size_t(blk) * G * blk_bytes, G,
                                         shape->T, shape->dv, nullptr,
@@ -756,11 +947,12 @@ mlStatus memory_layer_fwd_group(mlGroup g, const mlLayerShape* shape, mlOutMode 
     ML_TRY(group_state_local(g, bag, idx_saved, gs, st));
   }
   ML_TRY(gather_iw(g, bag, idx_saved, w_saved, idx_all, w_all, b.f, st));
-  ML_TRY(bag_blocks(g, bag, mode, V_shard, idx_all, w_all, b.f, st));
+  const void* recv = nullptr;
+  ML_TRY(bag_blocks(g, bag, mode, V_shard, idx_all, w_all, b.f, st, &recv));
   if (state) ML_TRY(group_state_merge(g, bag, gs, st));
   ML_TRY(dep(as, st, g->ev[4]));                   // g ready
   const size_t blk_bytes = size_t(T) * (s.dv / G) * dtype_size(dt);
-  const void* own = mode == ML_OUT_ALLTOALL ? b.f.recv
+  const void* own = mode == ML_OUT_ALLTOALL ? recv
                                             : static_cast<const char*>(b.f.recv) + size_t(r) * G * blk_bytes;
   ML_TRY((ml_group_unpack(own, G, T, s.dv, g_saved, y_saved, b.z, dt, st)));
   if (mode == ML_OUT_ALLGATHER)

@@ -539,6 +539,12 @@ class Group:
         check(lib().ml_group_init_hub(C.c_void_p(hub), rank, C.byref(out)))
         return cls(out.value)
 
+    def set_p2p(self, on=True):
+        """The fused peer-memory forward exchange (ml_group_set_p2p); every
+        rank of the group must make the same choice."""
+        check(lib().ml_group_set_p2p(self.h, 1 if on else 0))
+        return self
+
     def close(self):
         if self.h:
             check(lib().ml_group_destroy(self.h))

@@ -42,7 +42,7 @@ def _inputs(seed, T, H, S, Dk, dv, D, dt="bf16"):
                 W2=f("W2", (dv, D), gen.scale_for("W2", dv=dv)), dout=f("dout", (T, D)))
 
 
-def _run_hub(t, G, T_loc, dv, k, mode):
+def _run_hub(t, G, T_loc, dv, k, mode, p2p=False):
     from paper_2412_09764_b200 import ops
     hub = ops.group_hub(G)
     res, errs = [None] * G, []
@@ -50,7 +50,7 @@ def _run_hub(t, G, T_loc, dv, k, mode):
     def worker(r):
         try:
             torch.cuda.set_device(0)
-            grp = ops.Group.from_hub(hub, r)
+            grp = ops.Group.from_hub(hub, r).set_p2p(p2p)
             with torch.cuda.stream(torch.cuda.Stream()):
                 sl = slice(r * T_loc, (r + 1) * T_loc)
                 lo, hi = r * dv // G, (r + 1) * dv // G
@@ -76,9 +76,13 @@ def _run_hub(t, G, T_loc, dv, k, mode):
     return res
 
 
-@pytest.mark.parametrize("G", [1, 2, 4])
-@pytest.mark.parametrize("mode", ["alltoall", "allgather"])
-def test_capi_group_layer_vs_oracle(G, mode):
+@pytest.mark.parametrize("G,mode,p2p", [(1, "alltoall", False), (2, "alltoall", False),
+                                         (4, "alltoall", False), (1, "allgather", False),
+                                         (2, "allgather", False), (4, "allgather", False),
+                                         (2, "alltoall", True), (4, "alltoall", True)])
+def test_capi_group_layer_vs_oracle(G, mode, p2p):
+    """p2p: the fused forward exchange (ml_group_set_p2p), the bag kernel of
+    every block storing straight into the owner's exchange region."""
     from paper_2412_09764_b200 import ops
     T_loc, H, S, Dk, k, dv, D = 96, 4, 64, 128, 8, 512, 256
     T = G * T_loc
@@ -89,7 +93,7 @@ def test_capi_group_layer_vs_oracle(G, mode):
     ref_u = ops.memory_layer_bwd(t["dout"], t["x"], t["q"], t["K1"], t["K2"], t["V"], t["W1"],
                                  t["W2"], saved_u, want_dw=True)
     U_u = int(ref_u["U"].item())
-    res = _run_hub(t, G, T_loc, dv, k, mode)
+    res = _run_hub(t, G, T_loc, dv, k, mode, p2p=p2p)
 
     h64 = {n: a.astype(np.float64) for n, a in h.items()}
     rout, rs = olayer.memory_layer_fwd(h64["x"], h64["q"], h64["K1"], h64["K2"], h64["V"],
@@ -252,3 +256,58 @@ def test_group_state_merge_bit_identical(G, T_loc, B, N):
     b = ops.embbag_bwd(V, idx, w, dy, state=state)
     for x, y, n in zip(a, b, ("rows", "dV", "dw")):
         assert torch.equal(x, y), n
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_capi_group_p2p_equals_sendrecv(G):
+    """The fused peer-memory forward exchange produces exactly the point-to-
+    point path's results (same kernels, same arithmetic; only where the bag
+    kernel stores its rows differs), over three steps (both halves of the
+    double-buffered exchange region, reused)."""
+    from paper_2412_09764_b200 import ops
+    T_loc, H, S, Dk, k, D = 64, 2, 64, 128, 8, 128
+    # the full row and every rank's slice must pass the row-width rule
+    # (bytes/16 a power of two or a multiple of 256)
+    dv = 6144 if G == 3 else 128 * G
+    h = _inputs(7, G * T_loc, H, S, Dk, dv, D)
+    t = {n: torch.from_numpy(a).to(torch.bfloat16).cuda() for n, a in h.items()}
+    hub = {p: ops.group_hub(G) for p in (False, True)}
+    res = {False: [None] * G, True: [None] * G}
+    errs = []
+
+    def worker(r, p2p):
+        try:
+            torch.cuda.set_device(0)
+            grp = ops.Group.from_hub(hub[p2p], r).set_p2p(p2p)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                sl = slice(r * T_loc, (r + 1) * T_loc)
+                lo, hi = r * dv // G, (r + 1) * dv // G
+                Vs = t["V"][:, lo:hi].contiguous()
+                x, q, dout = (t[n][sl].contiguous() for n in ("x", "q", "dout"))
+                outs = []
+                for step in range(3):
+                    xs = x * (1 + step)        # a different forward every step
+                    out, sv = ops.memory_layer_fwd_group(grp, xs, q, t["K1"], t["K2"], Vs, t["W1"],
+                                                         t["W2"], k, mode="alltoall")
+                    g = ops.memory_layer_bwd_group(grp, dout, xs, q, t["K1"], t["K2"], Vs, t["W1"],
+                                                   t["W2"], sv, want_dw=True)
+                    torch.cuda.current_stream().synchronize()
+                    outs.append((out.clone(), sv["y"].clone(), g["dw"].clone(), g["dq"].clone(),
+                                 g["dx"].clone()))
+                res[p2p][r] = outs
+            grp.close()
+        except Exception as e:  # surface thread failures
+            errs.append(e)
+
+    for p2p in (False, True):
+        ths = [threading.Thread(target=worker, args=(r, p2p)) for r in range(G)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        ops.group_hub_destroy(hub[p2p])
+    assert not errs, errs
+    for r in range(G):
+        for a, b in zip(res[False][r], res[True][r]):
+            for x, y in zip(a, b):
+                assert torch.equal(x, y)
