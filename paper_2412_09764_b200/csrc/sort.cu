@@ -432,41 +432,45 @@ __device__ __forceinline__ uint32_t lookback_prefix(uint32_t* status, int tile, 
 // inclusive prefix ends the walk), publish the inclusive prefix.
 constexpr int kRunItems = 4;
 constexpr int kRunTile = kScanThreads * kRunItems;   // 2048 positions per tile
-__device__ __forceinline__ uint32_t lookback_prefix_warp(uint32_t* status, int tile, uint32_t total,
+__device__ __forceinline__ uint32_t lookback_prefix_warp(uint64_t* status, int tile, uint32_t total,
                                                          int lane) {
-  volatile uint32_t* st = status;
+  // 64-bit status words: flag in bits 62-63 (1 = aggregate, 2 = inclusive),
+  // the count below (any n < 2^31)
+  constexpr uint64_t kAgg = uint64_t(1) << 62, kInc = uint64_t(2) << 62;
+  constexpr uint64_t kMask = kAgg - 1;
+  volatile uint64_t* st = status;
   if (lane == 0) {
-    st[tile] = (tile == 0 ? kStInc : kStAgg) | total;
+    st[tile] = (tile == 0 ? kInc : kAgg) | total;
     __threadfence();
   }
   __syncwarp();
-  uint32_t excl = 0;
+  uint64_t excl = 0;
   for (int pt = tile - 1; pt >= 0; pt -= 32) {
     const int idx = pt - lane;
-    uint32_t v = 2u << 30;          // before tile 0: an inclusive prefix of 0
+    uint64_t v = kInc;              // before tile 0: an inclusive prefix of 0
     if (idx >= 0) v = st[idx];
     uint32_t spins = 0;
-    while ((v >> 30) == 0) {
+    while ((v >> 62) == 0) {
       if (++spins > kSortSpin) __trap();
       v = st[idx];
     }
-    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 30) == 2);
+    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
     const int lim = inc ? __ffs(inc) - 1 : 31;     // lanes 0..lim contribute
-    uint32_t c = lane <= lim ? (v & kStMask) : 0u;
+    uint64_t c = lane <= lim ? (v & kMask) : 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     excl += c;
     if (inc) break;
   }
-  if (lane == 0 && tile > 0) st[tile] = kStInc | (excl + total);
-  return excl;
+  if (lane == 0 && tile > 0) st[tile] = kInc | (excl + total);
+  return uint32_t(excl);
 }
 
 // run id of every position (rid), run_begin, rows (the distinct keys), *U
 __global__ void __launch_bounds__(kScanThreads) run_scan1_kernel(const int32_t* skey, int64_t n,
                                                                  int32_t* rid, int32_t* run_begin,
                                                                  int32_t* rows_out, int32_t* U,
-                                                                 uint32_t* status, int32_t* ticket) {
+                                                                 uint64_t* status, int32_t* ticket) {
   __shared__ int s_warp[32];
   __shared__ int s_tile;
   __shared__ uint32_t s_prefix;
@@ -534,7 +538,7 @@ __global__ void __launch_bounds__(kScanThreads) run_scan1_kernel(const int32_t* 
 __global__ void __launch_bounds__(kScanThreads) run_scan2_kernel(const int32_t* run_begin,
                                                                  const int32_t* U, int32_t* piece_base,
                                                                  int32_t* n_slots, int ntiles,
-                                                                 uint32_t* status, int32_t* ticket) {
+                                                                 uint64_t* status, int32_t* ticket) {
   __shared__ int s_warp[32];
   __shared__ int s_tile;
   __shared__ uint32_t s_prefix;
@@ -728,7 +732,7 @@ void runs_carve(Carver& c, int64_t n, RunBufs& r) {
   r.run_begin = c.take<int32_t>(n + 1);
   r.piece_base = c.take<int32_t>(n);
   r.n_slots = c.take<int32_t>(1);
-  r.lb = c.take<int32_t>(2 * scan_tmp_elems(n) + 4);
+  r.lb = c.take<int32_t>(4 * ((n + 2047) / 2048) + 8);   // 2 x tiles 64-bit status + tickets
 }
 
 mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out, int32_t* U,
@@ -737,13 +741,13 @@ mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out
     if (U) ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), s));
     return ML_OK;
   }
-  if (n >= (int64_t(1) << 30)) return fail(ML_ERR_CONFIG, "runs: n must be < 2^30");
+  if (n >= (int64_t(1) << 31)) return fail(ML_ERR_CONFIG, "runs: n must be < 2^31");
   const int64_t nt = (n + kRunTile - 1) / kRunTile;
-  uint32_t* st1 = reinterpret_cast<uint32_t*>(r.lb);
-  uint32_t* st2 = st1 + nt;
-  int32_t* tickets = r.lb + 2 * nt;     // [0], [1]: tile tickets; [2]: U when the caller passes none
+  uint64_t* st1 = reinterpret_cast<uint64_t*>(r.lb);   // r.lb is 8-byte aligned (carver)
+  uint64_t* st2 = st1 + nt;
+  int32_t* tickets = r.lb + 4 * nt;     // [0], [1]: tile tickets; [2]: U when the caller passes none
   int32_t* u = U ? U : tickets + 2;
-  ML_CUDA_TRY(cudaMemsetAsync(r.lb, 0, sizeof(int32_t) * size_t(2 * nt + 2), s));
+  ML_CUDA_TRY(cudaMemsetAsync(r.lb, 0, sizeof(int32_t) * size_t(4 * nt + 2), s));
   run_scan1_kernel<<<unsigned(nt), kScanThreads, 0, s>>>(skey, n, r.rid, r.run_begin, rows_out, u,
                                                          st1, tickets);
   ML_LAUNCH_CHECK("run_flags");
