@@ -37,6 +37,8 @@
 //    group their partial sums by thread width (equal up to rounding).
 #include "internal.cuh"
 
+#include <type_traits>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -127,11 +129,17 @@ __device__ __forceinline__ void store_vec(float* o, const float* acc, bool dense
 
 // One finished output row slice: fp32 (optionally added into a dense table),
 // or rounded once to bf16 (grad_dtype = ML_BF16; half the dV bytes).
-template <int VEC, bool WIDE = true>
+template <int VEC, bool WIDE = true, bool OBF = false, bool MAYBE_DENSE = true>
 __device__ __forceinline__ void store_out(const SegParams& p, int64_t row, int64_t col,
                                           const float* acc) {
-  if constexpr (VEC % 8 == 0) {
-    if (p.out_bf16) {
+  // MAYBE_DENSE = false (the pipelined kernel, never launched in dense mode):
+  // the dense read-add-write path is compiled out (with a runtime p.dense the
+  // 1-2 KiB-row kernel measured 1.66 vs 1.35 ms)
+  // OBF is a template parameter: the fp32 kernels carry no trace of the bf16
+  // path (a runtime branch cost the 1-2 KiB-row pipelined kernel 27 %: spills)
+  static_assert(!OBF || VEC % 8 == 0, "bf16 rows are stored 8 elements at a time");
+  if constexpr (OBF) {
+    {
       __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + col;
 #pragma unroll
       for (int h = 0; h < VEC; h += 8) {
@@ -146,7 +154,7 @@ __device__ __forceinline__ void store_out(const SegParams& p, int64_t row, int64
       return;
     }
   }
-  store_vec<VEC, WIDE>(p.out + row * p.ldo + col, acc, p.dense != 0);
+  store_vec<VEC, WIDE>(p.out + row * p.ldo + col, acc, MAYBE_DENSE && p.dense != 0);
 }
 
 // Piece of a run longer than kPieceLen: park the partial; pieces are combined
@@ -190,7 +198,7 @@ __device__ __forceinline__ int team_tid() {
   else return int(threadIdx.x);
 }
 
-template <int VEC, int SYNC = 0>
+template <int VEC, int SYNC = 0, bool OBF = false, bool MAYBE_DENSE = true>
 __device__ __forceinline__ void finish_long_piece(const SegParams& p, const FVec<VEC> accv, bool act,
                                                int64_t col, int slice, int32_t row, int32_t rbb,
                                                int32_t re, int32_t ps, int* s_flag, int team) {
@@ -223,7 +231,7 @@ __device__ __forceinline__ void finish_long_piece(const SegParams& p, const FVec
     float tot[VEC];
     sum_slots<VEC>(p, slice, slice_w, base + g0, gn, 1, act, tot, ttid);
     if (ngroups == 1) {
-      if (act) store_out<VEC, false>(p, row, col, tot);
+      if (act) store_out<VEC, false, OBF, MAYBE_DENSE>(p, row, col, tot);
     } else {
       team_sync<SYNC>(team);                 // every thread has read the group's slots
       float* gp = p.partial + (int64_t(slice) * p.nslots_cap + base + g0) * slice_w + ttid * VEC;
@@ -239,7 +247,7 @@ __device__ __forceinline__ void finish_long_piece(const SegParams& p, const FVec
       if (*s_flag) {                   // last group: sum the group partials in order
         __threadfence();
         sum_slots<VEC>(p, slice, slice_w, base, ngroups, GRP, act, tot, ttid);
-        if (act) store_out<VEC, false>(p, row, col, tot);
+        if (act) store_out<VEC, false, OBF, MAYBE_DENSE>(p, row, col, tot);
       }
     }
   }
@@ -250,16 +258,16 @@ __device__ __forceinline__ void finish_long_piece(const SegParams& p, const FVec
 // out of its hot loop leaves the consumer's registers to the batch (measured:
 // 2.50 ms out of line vs 2.58 ms inlined at C2); the one-CTA-per-chunk kernel
 // inlines it (2.65 vs 2.81 ms at the 8-way group shape).
-template <typename T, int VEC, int SYNC>
+template <typename T, int VEC, int SYNC, bool OBF = false>
 __device__ __noinline__ void finish_long_piece_ool(const SegParams& p, const FVec<VEC> accv,
                                                    bool act, int64_t col, int slice, int32_t row,
                                                    int32_t rbb, int32_t re, int32_t ps, int* s_flag,
                                                    int team) {
-  finish_long_piece<VEC, SYNC>(p, accv, act, col, slice, row, rbb, re, ps, s_flag, team);
+  finish_long_piece<VEC, SYNC, OBF, false>(p, accv, act, col, slice, row, rbb, re, ps, s_flag, team);
 }
 
 // blockDim.x = row vectors of one column slice (32..256); one CTA per chunk.
-template <typename T, bool DW>
+template <typename T, bool DW, bool OBF = false>
 __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
   constexpr int VEC = Vec<T>::N;
   constexpr int NB = 8;                  // positions per batch
@@ -374,14 +382,14 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
         const int32_t row = p.dense ? s_key[k] : rr;
         const float* accf = reinterpret_cast<const float*>(acc);
         if (re - rb <= L) {
-          if (act) store_out<VEC>(p, row, col, accf);
+          if (act) store_out<VEC, true, OBF>(p, row, col, accf);
         } else {
           const int32_t i = int32_t(c0) + k;
           const int32_t ps = rb + ((i - rb) / L) * L;
           FVec<VEC> av;
 #pragma unroll
           for (int v = 0; v < VEC; ++v) av.v[v] = accf[v];
-          finish_long_piece<VEC>(p, av, act, col, slice, row, rb, re, ps, &s_flag, blockDim.x);
+          finish_long_piece<VEC, 0, OBF>(p, av, act, col, slice, row, rb, re, ps, &s_flag, blockDim.x);
         }
       }
     }
@@ -470,7 +478,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // dynamic smem: [2*nslots] mbarriers (full, empty), pad to 128, nslots x (dy, V) row slots.
 // UPT = 16-byte row vectors per consumer thread, NB = positions per batch / stage.
-template <typename T, bool DW, int UPT, int NB, int CT, int TEAM>
+template <typename T, bool DW, int UPT, int NB, int CT, int TEAM, bool OBF = false>
 __global__ void __launch_bounds__(TEAM + 64, CT)
     seg_pipe_kernel(SegParams p, int nslots, int64_t nchunks, int nslices) {
   constexpr int VEC = Vec<T>::N;
@@ -672,14 +680,14 @@ __global__ void __launch_bounds__(TEAM + 64, CT)
           const int32_t rr = M[k].rr, rb = M[k].rb, re = M[k].re;
           const float* accf = reinterpret_cast<const float*>(acc);
           if (re - rb <= L) {
-            if (act) store_out<TV>(p, rr, col, accf);
+            if (act) store_out<TV, true, OBF, false>(p, rr, col, accf);
           } else {
             const int32_t i = int32_t(c0) + k;
             const int32_t ps = rb + ((i - rb) / L) * L;
             FVec<TV> av;
 #pragma unroll
             for (int v = 0; v < TV; ++v) av.v[v] = accf[v];
-            finish_long_piece_ool<T, TV, 1>(p, av, act, col, slice, rr, rb, re, ps, &s_flag, team);
+            finish_long_piece_ool<T, TV, 1, OBF>(p, av, act, col, slice, rr, rb, re, ps, &s_flag, team);
           }
 #pragma unroll
           for (int v = 0; v < V2; ++v) acc[v] = make_float2(0.f, 0.f);
@@ -727,6 +735,14 @@ int team_threads(int64_t vu) {
 template <typename T>
 mlStatus dispatch_seg(int threads, bool dw, dim3 grid, const SegParams& p, cudaStream_t s,
                       const char* name) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (p.out_bf16) {
+      if (dw) seg_kernel<T, true, true><<<grid, threads, 0, s>>>(p);
+      else seg_kernel<T, false, true><<<grid, threads, 0, s>>>(p);
+      ML_LAUNCH_CHECK(name);
+      return ML_OK;
+    }
+  }
   if (dw) seg_kernel<T, true><<<grid, threads, 0, s>>>(p);
   else seg_kernel<T, false><<<grid, threads, 0, s>>>(p);
   ML_LAUNCH_CHECK(name);
@@ -740,7 +756,7 @@ static int env_int(const char* name, int dflt) {
 
 // pipelined kernel. cfg 2 (default): 2 CTAs per SM, 32 bytes per consumer
 // thread, batches of 4; cfg 1: 1 CTA per SM, 16 bytes per thread, batches of 8.
-template <typename T, bool DW, int UPT, int NB, int CT, int TEAM>
+template <typename T, bool DW, int UPT, int NB, int CT, int TEAM, bool OBF = false>
 mlStatus launch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, cudaStream_t s,
                      const char* name, int ctas, size_t budget) {
   const int team = threads / UPT;
@@ -753,13 +769,13 @@ mlStatus launch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p, c
   const size_t smem = ((2 * size_t(nslots) * 8 + 127) / 128) * 128 + size_t(nslots) * stage + pad;
   static bool attr = false;
   if (!attr) {
-    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW, UPT, NB, CT, TEAM>,
+    ML_CUDA_TRY(cudaFuncSetAttribute(seg_pipe_kernel<T, DW, UPT, NB, CT, TEAM, OBF>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(210 * 1024)));
     attr = true;
   }
   const int64_t items = nchunks * ns;
   const unsigned grid = unsigned(std::min<int64_t>(items, int64_t(num_sms()) * ctas));
-  seg_pipe_kernel<T, DW, UPT, NB, CT, TEAM><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
+  seg_pipe_kernel<T, DW, UPT, NB, CT, TEAM, OBF><<<grid, team + 64, smem, s>>>(p, nslots, nchunks, ns);
   ML_LAUNCH_CHECK(name);
   return ML_OK;
 }
@@ -770,6 +786,13 @@ mlStatus dispatch_pipe(int threads, int ns, int64_t nchunks, const SegParams& p,
   // 4 KiB row slices: 4 consumer warps of 32-byte threads, 2 CTAs/SM;
   // 1-2 KiB rows: 16-byte threads, 3 CTAs/SM (more rows in flight per SM)
   // both configurations run kDwWarps = 4 consumer warps (one dw partial each)
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (p.out_bf16) {
+      if (threads >= 256)
+        return launch_pipe<T, DW, 2, 4, 2, 128, true>(threads, ns, nchunks, p, s, name, 2, 100 * 1024);
+      return launch_pipe<T, DW, 1, 4, 3, 128, true>(threads, ns, nchunks, p, s, name, 3, 62 * 1024);
+    }
+  }
   if (threads >= 256)
     return launch_pipe<T, DW, 2, 4, 2, 128>(threads, ns, nchunks, p, s, name, 2, 100 * 1024);
   return launch_pipe<T, DW, 1, 4, 3, 128>(threads, ns, nchunks, p, s, name, 3, 62 * 1024);

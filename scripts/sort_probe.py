@@ -10,7 +10,7 @@ import torch  # noqa: E402
 from paper_2412_09764_b200 import ops  # noqa: E402
 
 dev = torch.device("cuda", 0)
-N, dv, T, B = 1 << 20, 2048, 16384, 128
+N, dv, T, B = 1 << 20, int(os.environ.get("DV", "2048")), 16384, 128
 g = torch.Generator(device=dev).manual_seed(0)
 idx = torch.randint(0, N, (T, B), dtype=torch.int32, device=dev, generator=g)
 w = torch.rand((T, B), device=dev, generator=g)
