@@ -359,6 +359,27 @@ def build_step(args, cfg, t, ops, torch, comm=None):
     return step
 
 
+class Throttle:
+    """Keeps at most two steps in flight: before enqueueing step i the host
+    waits for step i-2's end event (the GPU still has step i-1 queued, so it
+    never idles).  Without it the host runs ahead of the device by many steps
+    on the memory-group paths, whose side-stream tensors stay reserved by the
+    caching allocator until their streams catch up -- and the pool then grows
+    (a device allocation, tens of ms) inside the timed region."""
+
+    def __init__(self, torch):
+        self.torch, self.ev = torch, []
+
+    def before(self):
+        if len(self.ev) >= 2:
+            self.ev.pop(0).synchronize()
+
+    def after(self):
+        e = self.torch.cuda.Event()
+        e.record()
+        self.ev.append(e)
+
+
 def time_steps(step, steps, world, torch, dev):
     """Device time of `steps` steps on the launch stream (barrier + sync on
     both sides, max over ranks)."""
@@ -379,11 +400,18 @@ def time_steps(step, steps, world, torch, dev):
     if diag:
         m0 = torch.cuda.memory_stats()
     h0 = time.perf_counter()
+    thr = Throttle(torch)
+    # pre-roll (outside the timed region): ~1 ms of GPU spin so that the
+    # first timed step's kernels are already queued when e0 fires -- otherwise
+    # step 1 also times the host's launch latency on an idle GPU
+    torch.cuda._sleep(2_000_000)
     e0.record(stream)
     for i in range(steps):
+        thr.before()
         if diag:
             ev[i].record(stream)
         out, g = step()
+        thr.after()
     if diag:
         ev[steps].record(stream)
     e1.record(stream)
@@ -435,8 +463,11 @@ def run_ours(args, cfg, world, rank, local):
     # the memory-group paths allocate per step on several streams: more
     # warm-up steps until the caching allocator's pool is settled
     n_warm = args.warmup if comm is None else max(args.warmup, 8)
+    thr = Throttle(torch)
     for _ in range(n_warm):            # same pattern as the timed loop: the previous
-        out, g = step()                # step's results alive while the next one runs
+        thr.before()                   # step's results alive while the next one runs,
+        out, g = step()                # at most two steps in flight
+        thr.after()
     del out, g                         # ... but none across the timed region: one more live
     torch.cuda.synchronize()           # generation made the allocator grow (a cudaMalloc,
                                        # up to tens of ms) inside the timed steps

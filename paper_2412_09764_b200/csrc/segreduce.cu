@@ -267,7 +267,10 @@ __device__ __noinline__ void finish_long_piece_ool(const SegParams& p, const FVe
 }
 
 // blockDim.x = row vectors of one column slice (32..256); one CTA per chunk.
-template <typename T, bool DW, bool OBF = false>
+// DENSE: rows added into a dense table (the key gradient, sentinel keys
+// >= row_limit skipped); else compact rows (the value gradient) -- a compile-
+// time split so the value path carries neither the dense nor the sentinel code
+template <typename T, bool DW, bool OBF = false, bool DENSE = false>
 __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
   constexpr int VEC = Vec<T>::N;
   constexpr int NB = 8;                  // positions per batch
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
   const int slice = blockIdx.y;
   const int64_t c0 = int64_t(blockIdx.x) * kChunk;
   // sentinel keys sort last: a chunk that starts on one has nothing to do
-  if (c0 < p.P && p.skey[c0] >= p.row_limit) return;
+  if (DENSE && c0 < p.P && p.skey[c0] >= p.row_limit) return;
   if (tid == 0) {
     s_range[0] = 0x7fffffff;
     s_range[1] = -1;
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
     const int64_t i = c0 + k;
     int fl = 0, t = 0, key = 0, pos = 0, r = 0, rb = 0, re = 0;
     float w = 0.f;
-    if (i < p.P && p.skey[i] < p.row_limit) {
+    if (i < p.P && (!DENSE || p.skey[i] < p.row_limit)) {
       pos = p.spos[i];
       const bool clamped = pos < 0;   // index outside [0, N): row 0, weight 0
       pos &= ~kClampedPos;
@@ -379,17 +382,17 @@ __global__ void __launch_bounds__(256, 2) seg_kernel(SegParams p) {
       for (int v = 0; v < V2; ++v) acc[v] = ffma2(w2, f[v], acc[v]);
       if (fl[j] & 2) {                       // last position of a piece
         const int32_t rr = s_rr[k], rb = s_rb[k], re = s_re[k];
-        const int32_t row = p.dense ? s_key[k] : rr;
+        const int32_t row = DENSE ? s_key[k] : rr;
         const float* accf = reinterpret_cast<const float*>(acc);
         if (re - rb <= L) {
-          if (act) store_out<VEC, true, OBF>(p, row, col, accf);
+          if (act) store_out<VEC, true, OBF, DENSE>(p, row, col, accf);
         } else {
           const int32_t i = int32_t(c0) + k;
           const int32_t ps = rb + ((i - rb) / L) * L;
           FVec<VEC> av;
 #pragma unroll
           for (int v = 0; v < VEC; ++v) av.v[v] = accf[v];
-          finish_long_piece<VEC, 0, OBF>(p, av, act, col, slice, row, rb, re, ps, &s_flag, blockDim.x);
+          finish_long_piece<VEC, 0, OBF, DENSE>(p, av, act, col, slice, row, rb, re, ps, &s_flag, blockDim.x);
         }
       }
     }
@@ -743,8 +746,13 @@ mlStatus dispatch_seg(int threads, bool dw, dim3 grid, const SegParams& p, cudaS
       return ML_OK;
     }
   }
-  if (dw) seg_kernel<T, true><<<grid, threads, 0, s>>>(p);
-  else seg_kernel<T, false><<<grid, threads, 0, s>>>(p);
+  if (p.dense) {
+    if (dw) seg_kernel<T, true, false, true><<<grid, threads, 0, s>>>(p);
+    else seg_kernel<T, false, false, true><<<grid, threads, 0, s>>>(p);
+  } else {
+    if (dw) seg_kernel<T, true><<<grid, threads, 0, s>>>(p);
+    else seg_kernel<T, false><<<grid, threads, 0, s>>>(p);
+  }
   ML_LAUNCH_CHECK(name);
   return ML_OK;
 }
