@@ -380,6 +380,22 @@ class Throttle:
         self.ev.append(e)
 
 
+def warm_up(step, n, torch):
+    """n untimed steps in the timed loop's pattern (the previous step's
+    results alive while the next one runs, at most two steps in flight), so
+    the caching allocator's pool is settled before timing; none of them live
+    across the timed region (one more live generation made the pool grow --
+    a device allocation of up to tens of ms -- inside the timed steps)."""
+    thr = Throttle(torch)
+    out = g = None
+    for _ in range(n):
+        thr.before()
+        out, g = step()
+        thr.after()
+    del out, g
+    torch.cuda.synchronize()
+
+
 def time_steps(step, steps, world, torch, dev):
     """Device time of `steps` steps on the launch stream (barrier + sync on
     both sides, max over ranks)."""
@@ -463,14 +479,7 @@ def run_ours(args, cfg, world, rank, local):
     # the memory-group paths allocate per step on several streams: more
     # warm-up steps until the caching allocator's pool is settled
     n_warm = args.warmup if comm is None else max(args.warmup, 8)
-    thr = Throttle(torch)
-    for _ in range(n_warm):            # same pattern as the timed loop: the previous
-        thr.before()                   # step's results alive while the next one runs,
-        out, g = step()                # at most two steps in flight
-        thr.after()
-    del out, g                         # ... but none across the timed region: one more live
-    torch.cuda.synchronize()           # generation made the allocator grow (a cudaMalloc,
-                                       # up to tens of ms) inside the timed steps
+    warm_up(step, n_warm, torch)
 
     # ---- headline: device events around K steps, library timing OFF
     launches0 = ops.launch_count()
@@ -504,9 +513,7 @@ def run_ours(args, cfg, world, rank, local):
         a2 = copy.copy(args)
         a2.dv_dtype = "bf16"
         vstep = build_step(a2, cfg, t, ops, torch, comm)
-        for _ in range(args.warmup):
-            o_, g_ = vstep()
-        del o_, g_
+        warm_up(vstep, n_warm, torch)
         ms_v, _, _ = time_steps(vstep, args.steps, world, torch, dev)
         variants = {"dV_bf16": {"ms_per_step": round(ms_v / args.steps, 4),
                                 "value": tokens_per_step / (ms_v / args.steps / 1e3),
@@ -529,9 +536,7 @@ def run_ours(args, cfg, world, rank, local):
         # t_ref(G): the same kernels through the Python protocol with the
         # collectives replaced by local copies
         ref_step = build_step(args, cfg, t, ops, torch, LoopbackComm(world, rank, others))
-        for _ in range(max(2, args.warmup // 2)):
-            o_, g_ = ref_step()
-        del o_, g_
+        warm_up(ref_step, max(args.warmup, 8), torch)
         ms_ref, _, _ = time_steps(ref_step, args.steps, world, torch, dev)
         eff = {"t_G_ms": round(ms_step, 4), "t_ref_ms": round(ms_ref / args.steps, 4),
                "E": round((ms_ref / args.steps) / ms_step, 4),

@@ -1,12 +1,12 @@
 # round-2 final config sweep (current tree): every config once, with the bf16-dV variant
 mkdir -p gpurun_out
-for cfg in "c2_dv1024" "c2_dv4096" "c3" "c4 --per-rank 8" "c5 --per-rank 8"; do
+for cfg in "c2" "c2_dv1024" "c2_dv4096" "c3" "c4 --per-rank 8" "c5 --per-rank 8"; do
   tag=$(echo $cfg | cut -d' ' -f1)
   timeout 900 python bench.py --config $cfg --steps 10 --no-cpu-baseline > gpurun_out/r2z_$tag.log 2>gpurun_out/r2z_$tag.err; echo $tag=$?
 done
 python - <<'PY'
 import json
-for t in ("c2_dv1024", "c2_dv4096", "c3", "c4", "c5"):
+for t in ("c2", "c2_dv1024", "c2_dv4096", "c3", "c4", "c5"):
     f = f"gpurun_out/r2z_{t}.log"
     try:
         d = json.loads([x for x in open(f) if x.startswith('{')][-1])
