@@ -208,42 +208,6 @@ def coll_report(kern, steps, cfg, G, T_loc, mode):
     return out
 
 
-class LoopbackComm:
-    """The collectives of rank `rank` of a G-rank group with the network
-    removed (SURVEY §8(e) t_ref(G)): this rank's own chunk is copied into
-    place and the other ranks' chunks come from `others` (captured from a real
-    exchange, or computed once before timing), so the local work sees the
-    data -- and the index distribution -- of a real G-rank step."""
-
-    def __init__(self, G, rank, others):
-        self.size, self.rank, self.others = G, rank, others
-
-    @staticmethod
-    def key(t):
-        return (str(t.dtype), tuple(t.shape[1:]))
-
-    def all_gather(self, out, inp):
-        n = inp.shape[0]
-        src = self.others.get(self.key(inp))
-        if src is not None and src.shape[1:] == inp.shape[1:] and src.shape[0] == out.shape[0]:
-            if self.rank > 0:
-                out[:self.rank * n].copy_(src[:self.rank * n])
-            if self.rank < self.size - 1:
-                out[(self.rank + 1) * n:].copy_(src[(self.rank + 1) * n:])
-        else:   # no captured data of this kind: replicate this rank's chunk
-            out.view(self.size, *inp.shape).copy_(inp.unsqueeze(0).expand(self.size, *inp.shape))
-        out[self.rank * n:(self.rank + 1) * n].copy_(inp)
-
-    def all_to_all(self, out, inp):
-        n = inp.shape[0] // self.size
-        chunk = inp[self.rank * n:(self.rank + 1) * n]
-        out.view(self.size, n, *inp.shape[1:]).copy_(chunk.unsqueeze(0).expand(self.size, *chunk.shape))
-
-    def reduce_scatter(self, out, inp):
-        n = out.shape[0]
-        out.copy_(inp[self.rank * n:(self.rank + 1) * n])
-
-
 # ------------------------------------------------------------- our arm
 def synth_value_shard(N, dv, G, rank, dt, dev, ops, torch):
     """This rank's [N, dv/G] column shard of the synthetic value table,
@@ -307,8 +271,17 @@ def group_others(cfg, G, rank, t, ops, torch):
         w_all[g * T:(g + 1) * T].copy_(w)
         # rank g's sorted share of the group's inverse map
         ops.group_sort_local(cfg["S"] ** 2, i.view(T, H * k), g, out=lists[g])
-    key = LoopbackComm.key
-    return {key(idx_all): idx_all, key(w_all): w_all, key(lists): lists}
+    return {"idx_all": idx_all, "w_all": w_all, "lists": lists}
+
+
+def loopback_group(G, rank, others, ops, torch):
+    """The C-ABI loopback group of one rank (include/memlayer.h
+    ml_group_init_loopback) from the other ranks' captured data: the packed
+    (idx, w) [G*T_loc, 2B] int32 (w as bits) and the sorted lists."""
+    idx_all, w_all = others["idx_all"], others["w_all"]
+    n = idx_all.shape[0]
+    iw = torch.cat([idx_all.reshape(n, -1), w_all.reshape(n, -1).view(torch.int32)], 1).contiguous()
+    return ops.Group.loopback(G, rank, [iw, others["lists"].contiguous()])
 
 
 def build_step(args, cfg, t, ops, torch, comm=None):
@@ -471,7 +444,9 @@ def run_ours(args, cfg, world, rank, local):
             comm.grp.set_p2p(True)
     t = make_inputs(cfg, dev, G, rank if world > 1 else 0, ops, torch, group_path)
     if per_rank > 1:
-        comm = LoopbackComm(G, 0, group_others(cfg, G, 0, t, ops, torch))
+        # one rank's work through the library's own group path (C ABI), the
+        # collectives replaced by local copies (ml_group_init_loopback)
+        comm = CGroup(loopback_group(G, 0, group_others(cfg, G, 0, t, ops, torch), ops, torch))
     step = build_step(args, cfg, t, ops, torch, comm)
     T_loc = tokens_per_rank(cfg, G)
 
@@ -503,7 +478,8 @@ def run_ours(args, cfg, world, rank, local):
     ops.timing_enable(False)
     ops.set_serial(False)
     kern = ops.timing_report()
-    coll = coll_report(kern, kern_steps, cfg, G, T_loc, args.mode) if isinstance(comm, CGroup) else None
+    coll = coll_report(kern, kern_steps, cfg, G, T_loc, args.mode) \
+        if (isinstance(comm, CGroup) and world > 1) else None
 
     # ---- variant: the compact value gradient stored as bf16 (memlayer.h
     # grad_dtype; fp32 sums rounded once) -- same step otherwise
@@ -531,11 +507,11 @@ def run_ours(args, cfg, world, rank, local):
         for g in range(world):   # every rank's sorted share of the inverse map
             ops.group_sort_local(cfg["S"] ** 2, idx_all.view(world, -1)[g].view(-1, idx_all[0].numel()), g,
                                  out=lists[g])
-        key = LoopbackComm.key
-        others = {key(idx_all): idx_all, key(w_all): w_all, key(lists): lists}
-        # t_ref(G): the same kernels through the Python protocol with the
-        # collectives replaced by local copies
-        ref_step = build_step(args, cfg, t, ops, torch, LoopbackComm(world, rank, others))
+        others = {"idx_all": idx_all, "w_all": w_all, "lists": lists}
+        # t_ref(G): the same rank's work through the same library group path
+        # with the collectives replaced by local copies
+        ref_step = build_step(args, cfg, t, ops, torch,
+                              CGroup(loopback_group(world, rank, others, ops, torch)))
         warm_up(ref_step, max(args.warmup, 8), torch)
         ms_ref, _, _ = time_steps(ref_step, args.steps, world, torch, dev)
         eff = {"t_G_ms": round(ms_step, 4), "t_ref_ms": round(ms_ref / args.steps, 4),

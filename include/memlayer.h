@@ -368,6 +368,18 @@ mlStatus ml_group_init(const void* id128, int G, int rank, mlGroup* out);
 mlStatus ml_group_hub_create(int G, void** hub);
 mlStatus ml_group_hub_destroy(void* hub);
 mlStatus ml_group_init_hub(void* hub, int rank, mlGroup* out);
+/* ml_group_init_loopback: rank `rank` of a G-rank group with the network
+ * removed (SURVEY §8(e) t_ref(G): this rank's work, collectives replaced by
+ * local copies), running the group's own code path on one GPU.  All-gathers
+ * copy this rank's chunk into place and the other ranks' chunks from the
+ * caller's captures (device buffers, not copied: they must outlive the
+ * group): the next capture, cyclically, whose size is G x the chunk -- in a
+ * layer step the packed (idx, w) [G][T_loc][2B] int32 (w as bits) and the
+ * sorted lists [G][2][T_loc*B] of embbag_bwd_group_sort_local; without a
+ * match the own chunk is replicated.  Other exchanges move this rank's own
+ * data. */
+mlStatus ml_group_init_loopback(int G, int rank, const void* const* sources, const size_t* bytes,
+                                int n_sources, mlGroup* out);
 mlStatus ml_group_destroy(mlGroup g);
 mlStatus ml_group_info(mlGroup g, int* G, int* rank);
 /* Fused forward exchange (mode ML_OUT_ALLTOALL; "each worker gathers

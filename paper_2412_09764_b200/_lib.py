@@ -99,6 +99,7 @@ SIGNATURES = {
     "ml_group_hub_create": [C.c_int, C.POINTER(P)],
     "ml_group_hub_destroy": [P],
     "ml_group_init_hub": [P, C.c_int, C.POINTER(P)],
+    "ml_group_init_loopback": [C.c_int, C.c_int, P, P, C.c_int, C.POINTER(P)],
     "ml_group_destroy": [P],
     "ml_group_info": [P, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "ml_group_set_p2p": [P, C.c_int],

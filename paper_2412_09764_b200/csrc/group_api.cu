@@ -371,6 +371,55 @@ struct HubTransport : Transport {
   }
 };
 
+// One rank of a G-rank group with the network removed (t_ref(G)
+// = this rank's work with the collectives replaced by local copies), running
+// exactly the group's code path on one GPU.  An all-gather copies this rank's
+// chunk into place and the other ranks' chunks from a caller capture: the
+// next capture (cyclically) whose size is G x the chunk -- per step: the
+// packed (idx, w), then the sorted lists of the inverse map; without a match
+// the own chunk is replicated.  Every other exchange moves this rank's own
+// data (shapes right; values do not change the work).
+struct LoopbackTransport : Transport {
+  std::vector<const char*> src;
+  std::vector<size_t> src_bytes;
+  size_t next = 0;
+  mlStatus all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    const char* from = nullptr;
+    for (size_t k = 0; k < src.size() && !from; ++k) {
+      const size_t c = (next + k) % src.size();
+      if (src_bytes[c] == size_t(G) * bytes) {
+        from = src[c];
+        next = c + 1;
+      }
+    }
+    char* r = static_cast<char*>(recv);
+    for (int g = 0; g < G; ++g) {
+      const void* piece = (g == rank || !from) ? send : static_cast<const void*>(from + size_t(g) * bytes);
+      if (piece != r + size_t(g) * bytes)
+        ML_CUDA_TRY(cudaMemcpyAsync(r + size_t(g) * bytes, piece, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    timing_mark("loopback_all_gather", s);
+    return ML_OK;
+  }
+  mlStatus all_to_all(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    ML_CUDA_TRY(cudaMemcpyAsync(recv, send, size_t(G) * bytes, cudaMemcpyDeviceToDevice, s));
+    timing_mark("loopback_all_to_all", s);
+    return ML_OK;
+  }
+  mlStatus reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) override {
+    ML_CUDA_TRY(cudaMemcpyAsync(recv, send + size_t(rank) * count, count * sizeof(float),
+                                cudaMemcpyDeviceToDevice, s));
+    timing_mark("loopback_reduce_scatter", s);
+    return ML_OK;
+  }
+  bool has_p2p() const override { return true; }
+  mlStatus sendrecv(const void* send, int, void* recv, int, size_t bytes, cudaStream_t s) override {
+    ML_CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s));
+    timing_mark("loopback_sendrecv", s);
+    return ML_OK;
+  }
+};
+
 // ------------------------------------------------------------ layout kernels
 // (idx, w) of T rows of B -> one packed [T][2B] int32 block (w as bits)
 __global__ void pack_iw_kernel(const int32_t* idx, const float* w, int64_t T, int B, int32_t* out) {
@@ -660,6 +709,27 @@ mlStatus ml_group_init_hub(void* hub, int rank, mlGroup* out) {
   t->rank = rank;
   t->peer_on = p2p_env();
   t->hub = h;
+  auto* g = new mlGroup_();
+  g->tr = t;
+  ML_TRY(group_make(g));
+  *out = g;
+  return ML_OK;
+  ML_API_END_X
+}
+
+mlStatus ml_group_init_loopback(int G, int rank, const void* const* sources, const size_t* bytes,
+                                int n_sources, mlGroup* out) {
+  ML_API_BEGIN_X
+  if (!out) return fail(ML_ERR_ARG, "null argument");
+  if (G < 1 || rank < 0 || rank >= G) return fail(ML_ERR_CONFIG, "group: need 0 <= rank < G");
+  if (n_sources < 0 || (n_sources > 0 && (!sources || !bytes))) return fail(ML_ERR_ARG, "bad sources");
+  auto* t = new LoopbackTransport();
+  t->G = G;
+  t->rank = rank;
+  for (int k = 0; k < n_sources; ++k) {
+    t->src.push_back(static_cast<const char*>(sources[k]));
+    t->src_bytes.push_back(bytes[k]);
+  }
   auto* g = new mlGroup_();
   g->tr = t;
   ML_TRY(group_make(g));

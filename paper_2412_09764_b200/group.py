@@ -313,11 +313,12 @@ class CGroupMemoryLayer:
             raise ValueError(mode)
         self.grp, self.k, self.mode, self.dV_dtype = grp, k, mode, dV_dtype
         self.bufs = {}      # backward outputs, reused across steps (valid until the next one)
+        self.fbufs = {}     # forward outputs / saved tensors, likewise
 
     def forward(self, x, q, K1, K2, V_shard, W1, W2):
         from . import ops
         out, saved = ops.memory_layer_fwd_group(self.grp, x, q, K1, K2, V_shard, W1, W2, self.k,
-                                                mode=self.mode)
+                                                mode=self.mode, bufs=self.fbufs)
         saved.update(x=x, q=q, K1=K1, K2=K2, V=V_shard, W1=W1, W2=W2)
         return out, saved
 

@@ -539,6 +539,21 @@ class Group:
         check(lib().ml_group_init_hub(C.c_void_p(hub), rank, C.byref(out)))
         return cls(out.value)
 
+    @classmethod
+    def loopback(cls, G, rank, captures=()):
+        """One rank of a G-rank group with the network removed
+        (ml_group_init_loopback): `captures` are device tensors (kept alive by
+        the group object) the all-gathers take the other ranks' chunks from."""
+        caps = [c.contiguous() for c in captures]
+        n = len(caps)
+        ptrs = (C.c_void_p * max(n, 1))(*[c.data_ptr() for c in caps])
+        sizes = (C.c_size_t * max(n, 1))(*[c.numel() * c.element_size() for c in caps])
+        out = C.c_void_p()
+        check(lib().ml_group_init_loopback(G, rank, ptrs, sizes, n, C.byref(out)))
+        g = cls(out.value)
+        g._captures = caps
+        return g
+
     def set_p2p(self, on=True):
         """The fused peer-memory forward exchange (ml_group_set_p2p); every
         rank of the group must make the same choice."""
@@ -567,10 +582,13 @@ def group_hub_destroy(hub):
     lib().ml_group_hub_destroy(C.c_void_p(hub))
 
 
-def memory_layer_fwd_group(grp, x, q, K1, K2, V_shard, W1, W2, k, mode="alltoall", keep_state=True):
+def memory_layer_fwd_group(grp, x, q, K1, K2, V_shard, W1, W2, k, mode="alltoall", keep_state=True,
+                           bufs=None):
     """Eq. 1 + Eq. 2 over a dim-sharded memory group (§3.1.2):
     x/q of this rank's T_loc tokens, V_shard [N, dv/G].  Returns out [T_loc, D]
-    and the saved tensors (idx/w of own and all tokens, g, y, y_all, state)."""
+    and the saved tensors (idx/w of own and all tokens, g, y, y_all, state).
+    bufs (a caller-owned dict): outputs and saved tensors reused across calls
+    (valid until the next forward with the same dict)."""
     G = grp.size
     T, H, Dk = q.shape
     dv = V_shard.shape[1] * G
@@ -578,19 +596,19 @@ def memory_layer_fwd_group(grp, x, q, K1, K2, V_shard, W1, W2, k, mode="alltoall
                     1, _lib.ML_F32)
     dev = q.device
     md = MODES[mode]
-    out = torch.empty((T, x.shape[1]), dtype=q.dtype, device=dev)
-    idx = torch.empty((T, H, k), dtype=torch.int32, device=dev)
-    w = torch.empty((T, H, k), dtype=torch.float32, device=dev)
-    idx_all = torch.empty((G * T, H, k), dtype=torch.int32, device=dev)
-    w_all = torch.empty((G * T, H, k), dtype=torch.float32, device=dev)
-    g = torch.empty((T, dv), dtype=q.dtype, device=dev)
-    y = torch.empty((T, dv), dtype=q.dtype, device=dev)
-    y_all = torch.empty((G * T, dv), dtype=q.dtype, device=dev) if md == 1 else None
+    out = _buf(bufs, "out", (T, x.shape[1]), q.dtype, dev)
+    idx = _buf(bufs, "idx", (T, H, k), torch.int32, dev)
+    w = _buf(bufs, "w", (T, H, k), torch.float32, dev)
+    idx_all = _buf(bufs, "idx_all", (G * T, H, k), torch.int32, dev)
+    w_all = _buf(bufs, "w_all", (G * T, H, k), torch.float32, dev)
+    g = _buf(bufs, "g", (T, dv), q.dtype, dev)
+    y = _buf(bufs, "y", (T, dv), q.dtype, dev)
+    y_all = _buf(bufs, "y_all", (G * T, dv), q.dtype, dev) if md == 1 else None
     state, nst = None, 0
     if keep_state:
         bs = BagShape(V_shard.shape[0], dv, T, H * k, _dt(q), _lib.ML_F32)
         nst = _size(lambda b, p: lib().embbag_bwd_group_state_bytes(grp.h, b, p), bs)
-        state = torch.empty((max(nst, 1),), dtype=torch.uint8, device=dev)
+        state = _buf(bufs, "state", (max(nst, 1),), torch.uint8, dev)
     n = _size(lambda b, p: lib().memory_layer_fwd_group_workspace(grp.h, b, md, p), sh)
     ws = workspace(n, dev, tag="group_fwd")
     check(lib().memory_layer_fwd_group(grp.h, C.byref(sh), md, _p(x), _p(q), _p(K1), _p(K2),

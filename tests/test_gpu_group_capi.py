@@ -311,3 +311,40 @@ def test_capi_group_p2p_equals_sendrecv(G):
         for a, b in zip(res[False][r], res[True][r]):
             for x, y in zip(a, b):
                 assert torch.equal(x, y)
+
+
+def test_loopback_group_uses_captures():
+    """ml_group_init_loopback (t_ref(G) through the library's group path):
+    rank 0 of a G = 2 group on one GPU, the other rank's (idx, w) and sorted
+    lists taken from a hub run's captures -- the gathered indices, the
+    inverse map (distinct rows U, the rows) and rank 0's own outputs that do
+    not depend on the other rank's data (idx, w of its own tokens) match the
+    hub run exactly."""
+    from paper_2412_09764_b200 import ops
+    G, T_loc, H, S, Dk, k, D = 2, 64, 2, 64, 128, 8, 128
+    dv = 256
+    h = _inputs(9, G * T_loc, H, S, Dk, dv, D)
+    t = {n: torch.from_numpy(a).to(torch.bfloat16).cuda() for n, a in h.items()}
+    res = _run_hub(t, G, T_loc, dv, k, "alltoall")
+    out0, sv0, g0 = res[0]
+    B = H * k
+    idx_all, w_all = sv0["idx_all"], sv0["w_all"]
+    lists = torch.empty((G, 2, T_loc * B), dtype=torch.int32, device="cuda")
+    for r in range(G):
+        ops.group_sort_local(S * S, idx_all[r * T_loc:(r + 1) * T_loc].reshape(T_loc, B), r, out=lists[r])
+    n = idx_all.shape[0]
+    iw = torch.cat([idx_all.reshape(n, -1), w_all.reshape(n, -1).view(torch.int32)], 1).contiguous()
+    grp = ops.Group.loopback(G, 0, [iw, lists])
+    sl = slice(0, T_loc)
+    Vs = t["V"][:, :dv // G].contiguous()
+    x, q, dout = (t[nm][sl].contiguous() for nm in ("x", "q", "dout"))
+    out, sv = ops.memory_layer_fwd_group(grp, x, q, t["K1"], t["K2"], Vs, t["W1"], t["W2"], k)
+    g = ops.memory_layer_bwd_group(grp, dout, x, q, t["K1"], t["K2"], Vs, t["W1"], t["W2"], sv,
+                                   want_dw=True)
+    torch.cuda.synchronize()
+    assert torch.equal(sv["idx"], sv0["idx"]) and torch.equal(sv["w"], sv0["w"])
+    assert torch.equal(sv["idx_all"], idx_all) and torch.equal(sv["w_all"], w_all)
+    u, u0 = int(g["U"].item()), int(g0["U"].item())
+    assert u == u0 and torch.equal(g["rows"][:u], g0["rows"][:u0])
+    assert torch.isfinite(out.float()).all() and torch.isfinite(g["dq"]).all()
+    grp.close()
