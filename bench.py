@@ -447,6 +447,8 @@ def run_ours(args, cfg, world, rank, local):
         # one rank's work through the library's own group path (C ABI), the
         # collectives replaced by local copies (ml_group_init_loopback)
         comm = CGroup(loopback_group(G, 0, group_others(cfg, G, 0, t, ops, torch), ops, torch))
+        if args.p2p:
+            comm.grp.set_p2p(True)
     step = build_step(args, cfg, t, ops, torch, comm)
     T_loc = tokens_per_rank(cfg, G)
 
@@ -510,8 +512,10 @@ def run_ours(args, cfg, world, rank, local):
         others = {"idx_all": idx_all, "w_all": w_all, "lists": lists}
         # t_ref(G): the same rank's work through the same library group path
         # with the collectives replaced by local copies
-        ref_step = build_step(args, cfg, t, ops, torch,
-                              CGroup(loopback_group(world, rank, others, ops, torch)))
+        lb = loopback_group(world, rank, others, ops, torch)
+        if args.p2p:
+            lb.set_p2p(True)
+        ref_step = build_step(args, cfg, t, ops, torch, CGroup(lb))
         warm_up(ref_step, max(args.warmup, 8), torch)
         ms_ref, _, _ = time_steps(ref_step, args.steps, world, torch, dev)
         eff = {"t_G_ms": round(ms_step, 4), "t_ref_ms": round(ms_ref / args.steps, 4),
@@ -918,7 +922,8 @@ def main():
             " + fused peer-memory forward exchange" if args.p2p and args.mode == "alltoall" else "")
     elif args.per_rank > 1:
         par = (f"one rank of a G={G} memory group on one GPU (collectives replaced by local "
-               f"copies: SURVEY §8(e) t_ref(G)), {args.mode}")
+               f"copies: SURVEY §8(e) t_ref(G)), {args.mode}" +
+               (", fused peer-store exchange" if args.p2p and args.mode == "alltoall" else ""))
     elif args.force_group:
         par = f"memory-group path G=1 ({args.mode}), NCCL"
     else:

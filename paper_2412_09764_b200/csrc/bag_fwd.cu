@@ -54,13 +54,17 @@ struct BagParams {
   char* out; int64_t ldo; int32_t out_col0;
   const char* gate; char* y_ungated;
   int* flag;
+  // blocked output (BLK): bag b's row goes to block b / block_rows, row
+  // b % block_rows -- e.g. each token block straight into its owner rank's
+  // exchange region over peer memory (memory group, fused exchange)
+  char* blocks[kMaxOutBlocks]; int32_t block_rows;
 };
 
 // UNROLL = 8 rows per thread in flight at 4 CTAs/SM (<= 64 registers): 32
 // resident warps per SM keep 128 KiB of row loads outstanding (measured
 // 1.28 ms at C2 vs 1.33-1.34 for 16 rows at 1-2 CTAs/SM)
-template <typename Tin, bool OUT_F32, int NT, int UNROLL, bool GATE, int MINB>
-__global__ void __launch_bounds__(256, MINB) bag_fwd_kernel(BagParams p) {
+template <typename Tin, bool OUT_F32, int NT, int UNROLL, bool GATE, int MINB, bool BLK = false>
+__global__ void __launch_bounds__(256, MINB) bag_fwd_kernel(const __grid_constant__ BagParams p) {
   constexpr int VEC = Vec<Tin>::N;
   constexpr int TPC = 256 / NT;
   extern __shared__ int2 s_iw[];  // [TPC][B] (row, weight bits)
@@ -132,17 +136,21 @@ __global__ void __launch_bounds__(256, MINB) bag_fwd_kernel(BagParams p) {
     for (int v = 0; v < VEC; v += 4)
       stg_v4(o + v, make_uint4(__float_as_uint(acc[v]), __float_as_uint(acc[v + 1]),
                                __float_as_uint(acc[v + 2]), __float_as_uint(acc[v + 3])));
+  } else if constexpr (BLK) {
+    const int32_t blk = int32_t(bag / p.block_rows);
+    const int64_t o = (bag - int64_t(blk) * p.block_rows) * p.ldo + p.out_col0 + col;
+    stg_v4(p.blocks[blk] + o * int64_t(sizeof(Tin)), Vec<Tin>::pack(acc));
   } else {
     stg_v4(p.out + oelem * int64_t(sizeof(Tin)), Vec<Tin>::pack(acc));
   }
 }
 
-template <typename Tin, bool OUT_F32, bool GATE>
+template <typename Tin, bool OUT_F32, bool GATE, bool BLK = false>
 mlStatus dispatch_nt(int nt, dim3 grid, size_t smem, const BagParams& p, cudaStream_t s,
                      const char* name) {
 #define ML_BAG_CASE(NTV)                                                              \
   case NTV: {                                                                         \
-    auto k = bag_fwd_kernel<Tin, OUT_F32, NTV, 8, GATE, 4>;                           \
+    auto k = bag_fwd_kernel<Tin, OUT_F32, NTV, 8, GATE, 4, BLK>;                      \
     if (smem > 48 * 1024)                                                             \
       ML_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                        int(smem)));                                   \
@@ -199,9 +207,20 @@ mlStatus launch_bag_fwd(const BagFwdArgs& a, cudaStream_t s) {
   p.gate = static_cast<const char*>(a.gate);
   p.y_ungated = static_cast<char*>(a.y_ungated);
   p.flag = index_flag_ptr();
+  p.block_rows = 0;
   dim3 grid{unsigned(nblk), unsigned(slices), 1u};
   const bool gate = a.gate != nullptr;
   if (gate && a.out_f32) return fail(ML_ERR_UNSUPPORTED, "bag: gated output must be of the value dtype");
+  if (a.out_blocks) {
+    if (gate || a.out_f32 || a.y_ungated || a.block_rows <= 0 ||
+        (int64_t(a.nbags) + a.block_rows - 1) / a.block_rows > kMaxOutBlocks)
+      return fail(ML_ERR_UNSUPPORTED, "bag: blocked output is ungated, of the value dtype, <= 64 blocks");
+    const int nblocks = int((int64_t(a.nbags) + a.block_rows - 1) / a.block_rows);
+    for (int b = 0; b < nblocks; ++b) p.blocks[b] = static_cast<char*>(a.out_blocks[b]);
+    p.block_rows = a.block_rows;
+    return a.dtype == ML_BF16 ? dispatch_nt<__nv_bfloat16, false, false, true>(nt, grid, smem, p, s, a.name)
+                              : dispatch_nt<float, false, false, true>(nt, grid, smem, p, s, a.name);
+  }
   if (a.dtype == ML_BF16) {
     if (a.out_f32) return dispatch_nt<__nv_bfloat16, true, false>(nt, grid, smem, p, s, a.name);
     return gate ? dispatch_nt<__nv_bfloat16, false, true>(nt, grid, smem, p, s, a.name)

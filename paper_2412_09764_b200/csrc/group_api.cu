@@ -418,6 +418,26 @@ struct LoopbackTransport : Transport {
     timing_mark("loopback_sendrecv", s);
     return ML_OK;
   }
+  // fused exchange: every "peer" region is a local buffer of its own (the
+  // stores cost the HBM bytes the NVLink stores would not), no barrier
+  bool peer_on = false;
+  std::vector<char*> regions;
+  size_t region_bytes = 0;
+  ~LoopbackTransport() override {
+    for (char* p : regions) cudaFree(p);
+  }
+  bool has_peer_mem() const override { return peer_on && G > 1; }
+  char* peer_region(int g) override { return regions[size_t(g)]; }
+  mlStatus peer_setup(size_t bytes, cudaStream_t s) override {
+    if (bytes <= region_bytes) return ML_OK;
+    ML_CUDA_TRY(cudaStreamSynchronize(s));
+    for (char* p : regions) cudaFree(p);
+    regions.assign(size_t(G), nullptr);
+    for (auto& p : regions) ML_CUDA_TRY(cudaMalloc(&p, bytes));
+    region_bytes = bytes;
+    return ML_OK;
+  }
+  mlStatus peer_barrier(cudaStream_t) override { return ML_OK; }
 };
 
 // ------------------------------------------------------------ layout kernels
@@ -562,12 +582,19 @@ mlStatus bag_blocks(mlGroup_* g, const mlBagShape& s, mlOutMode mode, const void
     ML_TRY(g->tr->peer_setup(kPeerFlagBytes + 2 * half_bytes, st));
     const size_t off = kPeerFlagBytes + size_t(g->p2p_steps & 1) * half_bytes;
     ++g->p2p_steps;
-    for (int i = 0; i < G; ++i) {
-      const int to = (r + 1 + i) % G;      // own block last
-      char* dst = g->tr->peer_region(to) + off + size_t(r) * blk_bytes;
-      ML_TRY((embbag_fwd(&bs, V_shard, idx_all + int64_t(to) * s.T * s.B,
-                         w_all + int64_t(to) * s.T * s.B, nullptr, dst, nullptr, st)));
-    }
+    // ONE bag launch over all G*T_loc tokens: token block `to` (rank `to`'s
+    // tokens) is stored into rank `to`'s region, slot `r`
+    void* blocks[kMaxOutBlocks];
+    if (G > kMaxOutBlocks) return fail(ML_ERR_CONFIG, "fused exchange: G <= 64");
+    for (int to = 0; to < G; ++to) blocks[to] = g->tr->peer_region(to) + off + size_t(r) * blk_bytes;
+    BagFwdArgs a;
+    a.V = V_shard; a.ldv = dvG; a.N = s.N;
+    a.idx = idx_all; a.w = w_all; a.B = s.B; a.nbags = G * s.T; a.dv = dvG;
+    a.out = blocks[0]; a.ldo = dvG; a.dtype = s.dtype;
+    a.out_blocks = blocks; a.block_rows = s.T;
+    a.name = "embbag_fwd";
+    timing_mark(nullptr, st);
+    ML_TRY(launch_bag_fwd(a, st));
     ML_TRY(g->tr->peer_barrier(st));
     *recv_out = g->tr->peer_region(r) + off;
     return ML_OK;
@@ -761,6 +788,7 @@ mlStatus ml_group_set_p2p(mlGroup g, int on) {
   if (!g) return fail(ML_ERR_ARG, "null group");
   if (auto* t = dynamic_cast<NcclTransport*>(g->tr)) t->peer_on = on != 0;
   else if (auto* h = dynamic_cast<HubTransport*>(g->tr)) h->peer_on = on != 0;
+  else if (auto* l = dynamic_cast<LoopbackTransport*>(g->tr)) l->peer_on = on != 0;
   return ML_OK;
   ML_API_END_X
 }

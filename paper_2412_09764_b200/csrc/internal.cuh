@@ -10,6 +10,7 @@ bool serial_mode();
 // ------------------------------------------------------------ bag forward
 // out[b, out_col0 + c] = sum_{j<B} w[b,j] * V[idx[b,j], c]   for c < dv
 // (optionally gated: out = y * silu(gate[b, c]); y_ungated gets y).
+constexpr int kMaxOutBlocks = 64;
 struct BagFwdArgs {
   const void* V = nullptr; int64_t ldv = 0; int64_t N = 0;
   const int32_t* idx = nullptr; const float* w = nullptr;
@@ -18,6 +19,9 @@ struct BagFwdArgs {
   const void* gate = nullptr; void* y_ungated = nullptr;
   mlDtype dtype = ML_BF16;
   const char* name = "bag_fwd";   // timing / profiling label
+  // blocked output (nullable host array of ceil(nbags / block_rows) bases):
+  // bag b -> out_blocks[b / block_rows] row b % block_rows
+  void* const* out_blocks = nullptr; int32_t block_rows = 0;
 };
 mlStatus check_cols(int32_t dv, mlDtype dt, const char* what);
 mlStatus launch_bag_fwd(const BagFwdArgs& a, cudaStream_t s);
