@@ -599,8 +599,23 @@ mlStatus bag_blocks(mlGroup_* g, const mlBagShape& s, mlOutMode mode, const void
     *recv_out = g->tr->peer_region(r) + off;
     return ML_OK;
   }
-  const bool p2p = mode == ML_OUT_ALLTOALL && g->tr->has_p2p();
+  // Mode P: one bag launch over all G*T_loc tokens, then one all-to-all --
+  // measured faster than the block pipeline (one launch per destination's
+  // T_loc tokens, each block sent while the next is gathered): a block fills
+  // less than half the GPU at C4/C5 (the launches cost 0.08-0.13 ms more per
+  // step than the NVLink transfer they would hide, 10-80 us at 700 GB/s).
+  // ML_GROUP_PIPELINE=1 restores the pipeline.
+  static const bool pipe_env = [] {
+    const char* e = std::getenv("ML_GROUP_PIPELINE");
+    return e && e[0] == '1';
+  }();
+  const bool p2p = mode == ML_OUT_ALLTOALL && g->tr->has_p2p() && pipe_env;
   const bool pipelined = p2p || mode == ML_OUT_ALLGATHER;
+  if (mode == ML_OUT_ALLTOALL && !pipelined) {
+    const mlBagShape all{s.N, dvG, G * s.T, s.B, s.dtype, ML_F32};
+    ML_TRY((embbag_fwd(&all, V_shard, idx_all, w_all, nullptr, b.y_part, nullptr, st)));
+    return g->tr->all_to_all(b.y_part, b.recv, blk_bytes, st);
+  }
   // measurement mode (ml_set_serial): the exchange runs on the caller's
   // stream, so each collective's timing event brackets it alone
   cudaStream_t cs = serial_mode() ? st : g->comm;
