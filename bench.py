@@ -185,7 +185,10 @@ def coll_bytes(cfg, G, T_loc, mode):
            "nccl_all_to_all": (G - 1) * blk,                      # dy slices
            "nccl_reduce_scatter": (G - 1) * T_loc * B * 4}        # partial dw
     if mode == "alltoall":
-        out["nccl_sendrecv"] = (G - 1) * blk                      # the forward's blocks
+        if os.environ.get("ML_GROUP_PIPELINE") == "1":
+            out["nccl_sendrecv"] = (G - 1) * blk                  # the forward's blocks (ring)
+        else:
+            out["nccl_all_to_all"] += (G - 1) * blk               # the forward's blocks
     else:
         out["nccl_all_gather"] += G * (G - 1) * blk               # every block to everyone
     return out
