@@ -40,7 +40,7 @@ int num_sms() {
 // events, so tensor-core GEMMs overlap the HBM-bound bag kernels.  One set
 // per caller stream (calls on different streams never share them).
 struct Aux {
-  cudaStream_t s[3];
+  cudaStream_t s[4];      // 3: the sparse key backward's dq gather (beside the dK sort)
   cudaEvent_t ev[8];
 };
 
@@ -97,6 +97,7 @@ static mlStatus aux_for(cudaStream_t caller, Aux** out) {
   ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[0], cudaStreamNonBlocking));
   ML_CUDA_TRY(cudaStreamCreateWithPriority(&a->s[1], cudaStreamNonBlocking, hi));
   ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[2], cudaStreamNonBlocking));
+  ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[3], cudaStreamNonBlocking));
   for (auto& e : a->ev) ML_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   m[caller] = a;
   *out = a;
@@ -329,9 +330,15 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
     // per distinct sub-key, the other slots get the sentinel key H*S)
     ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, nullptr, qn,
                               b.ds1w, b.ds2w, st));
-    // dq_half[t,h] = sum_a ds_half[a] K_half[h, a]   (one warp per (t, h))
-    float* dq_target = dq;
-    ML_TRY(launch_pkm_dq(s, b.key1, b.key2, b.ds1w, b.ds2w, K1, K2, dq_target, st));
+    // dq_half[t,h] = sum_a ds_half[a] K_half[h, a]   (one warp per (t, h)),
+    // on its own stream beside the dK sorts and segmented passes (both only
+    // read what softmax_bwd wrote; the gather is L2/HBM-bound, the sorts
+    // latency-bound)
+    Aux* aux = nullptr;
+    ML_TRY(aux_for(st, &aux));
+    cudaStream_t qs = aux->s[3];
+    ML_TRY(stream_dep(st, qs, aux->ev[6]));
+    ML_TRY(launch_pkm_dq(s, b.key1, b.key2, b.ds1w, b.ds2w, K1, K2, dq, qs));
     const int bits = ceil_log2(HS + 1);
     for (int half = 0; half < 2; ++half) {
       const int32_t* key = half ? b.key2 : b.key1;
@@ -350,6 +357,7 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
       g.name = "pkm_dK_segreduce";
       ML_TRY(launch_segreduce(g, st));
     }
+    ML_TRY(stream_dep(qs, st, aux->ev[7]));   // join the dq gather
   }
   if (s.qk_norm) {  // chain through x_hat = x / max(||x||, eps)
     ML_TRY(launch_qk_proj(q, int64_t(s.T) * s.H * 2, Dh, s.dtype, dq, dq, false, st));
