@@ -21,7 +21,7 @@ a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
-t = bench.make_inputs(cfg, dev, 1, 0, ops, torch)
+t = bench.make_inputs(cfg, dev, 1, 0, ops, torch, False)
 k = cfg["k"]
 dK1 = torch.zeros(t["K1"].shape, dtype=torch.float32, device=dev)
 dK2 = torch.zeros(t["K2"].shape, dtype=torch.float32, device=dev)
