@@ -45,12 +45,57 @@ __global__ void pack_kernel(const char* src, int G, int64_t T_loc, int64_t vs, c
   }
 }
 
+// pack straight into G destination buffers (block g -> dst.p[g]): the dy
+// slices of the backward stored into their owners' exchange regions
+struct DstBlocks { char* p[kMaxOutBlocks]; };
+__global__ void pack_peers_kernel(const char* src, int G, int64_t T_loc, int64_t vs,
+                                  const __grid_constant__ DstBlocks dst) {
+  const int64_t nvec = int64_t(G) * T_loc * vs;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t g = i / (T_loc * vs);
+    const int64_t r = i - g * (T_loc * vs);
+    const int64_t t = r / vs, c = r - t * vs;
+    stg_v4(dst.p[g] + r * 16, ldg_nc_v4(src + ((t * G + g) * vs + c) * 16));
+  }
+}
+
+// out[i] = sum over g = 0..G-1 (in rank order: deterministic) of slots[g][i]
+__global__ void sum_ranks_kernel(const float* slots, int G, int64_t n, float* out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    float t = 0.f;
+    for (int g = 0; g < G; ++g) t += slots[int64_t(g) * n + i];
+    out[i] = t;
+  }
+}
+
 unsigned grid_for(int64_t n) {
   const int64_t b = (n + 255) / 256;
   return unsigned(std::min<int64_t>(b, int64_t(num_sms()) * 16));
 }
 
 }  // namespace
+
+mlStatus launch_group_pack_peers(const void* src, int G, int64_t T_loc, int32_t dv_slice,
+                                 void* const* dst, mlDtype dt, cudaStream_t s) {
+  const int64_t vs = int64_t(dv_slice) * int64_t(dtype_size(dt)) / 16;
+  const int64_t n = int64_t(G) * T_loc * vs;
+  if (n <= 0) return ML_OK;
+  if (G > kMaxOutBlocks) return fail(ML_ERR_CONFIG, "group pack: G <= 64");
+  DstBlocks d{};
+  for (int g = 0; g < G; ++g) d.p[g] = static_cast<char*>(dst[g]);
+  pack_peers_kernel<<<grid_for(n), 256, 0, s>>>(static_cast<const char*>(src), G, T_loc, vs, d);
+  ML_LAUNCH_CHECK("group_pack");
+  return ML_OK;
+}
+
+mlStatus launch_sum_ranks(const float* slots, int G, int64_t n, float* out, cudaStream_t s) {
+  if (n <= 0) return ML_OK;
+  sum_ranks_kernel<<<grid_for(n), 256, 0, s>>>(slots, G, n, out);
+  ML_LAUNCH_CHECK("group_sum_ranks");
+  return ML_OK;
+}
 
 mlStatus launch_group_unpack(const void* recv, int G, int64_t T_loc, int32_t dv_slice,
                              const void* gate, void* y, void* z, mlDtype dt, cudaStream_t s) {

@@ -479,6 +479,7 @@ struct mlGroup_ {
   std::vector<cudaEvent_t> blk;     // per-block events of the pipelined forward
   cudaEvent_t state_ready = nullptr;
   uint64_t p2p_steps = 0;           // fused forward exchanges so far (double-buffer parity)
+  uint64_t p2p_bwd_steps = 0;       // fused backward exchanges so far
 };
 
 namespace ml {
@@ -531,6 +532,29 @@ mlBagShape shard_shape(const mlGroup_* g, const mlBagShape& s) {
   return b;
 }
 
+// The exchange region of the fused (peer-memory) form, identical on every
+// rank for a shape: epoch flags, then the forward's y blocks, the backward's
+// dy blocks and partial dw blocks -- each section double-buffered by the
+// parity of its exchange count (a half is rewritten two exchanges later,
+// after the barrier of the one in between, which its receiver passes only
+// after consuming it).
+struct PeerLayout { size_t y_off, y_half, dy_off, dy_half, dw_off, dw_half, dw_blk, total; };
+PeerLayout peer_layout(const mlGroup_* g, const mlBagShape& s) {
+  const int G = g->tr->G;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t blk = size_t(s.T) * (s.dv / G) * dtype_size(s.dtype);
+  PeerLayout L;
+  L.y_half = up(size_t(G) * blk);
+  L.dy_half = L.y_half;
+  L.dw_blk = size_t(s.T) * s.B * sizeof(float);
+  L.dw_half = up(size_t(G) * L.dw_blk);
+  L.y_off = kPeerFlagBytes;
+  L.dy_off = L.y_off + 2 * L.y_half;
+  L.dw_off = L.dy_off + 2 * L.dy_half;
+  L.total = L.dw_off + 2 * L.dw_half;
+  return L;
+}
+
 struct FwdBufs { int32_t* iw_send; int32_t* iw_recv; void* y_part; void* recv; };
 void fwd_carve(Carver& c, const mlGroup_* g, const mlBagShape& s, mlOutMode mode, FwdBufs& b) {
   const int G = g->tr->G;
@@ -578,9 +602,9 @@ mlStatus bag_blocks(mlGroup_* g, const mlBagShape& s, mlOutMode mode, const void
     // collective.  Regions are double-buffered by step parity: a writer
     // reuses a half only two steps later, after the barrier of the step in
     // between, which the receiver passes only after unpacking this one.
-    const size_t half_bytes = size_t(G) * blk_bytes;
-    ML_TRY(g->tr->peer_setup(kPeerFlagBytes + 2 * half_bytes, st));
-    const size_t off = kPeerFlagBytes + size_t(g->p2p_steps & 1) * half_bytes;
+    const PeerLayout L = peer_layout(g, s);
+    ML_TRY(g->tr->peer_setup(L.total, st));
+    const size_t off = L.y_off + size_t(g->p2p_steps & 1) * L.y_half;
     ++g->p2p_steps;
     // ONE bag launch over all G*T_loc tokens: token block `to` (rank `to`'s
     // tokens) is stored into rank `to`'s region, slot `r`
@@ -937,7 +961,24 @@ mlStatus embbag_bwd_group(mlGroup g, const mlBagShape* shape, const void* V_shar
     if (state_bytes < sb) return fail(ML_ERR_WORKSPACE, "embbag_bwd_group: state too small");
     ML_CUDA_TRY(cudaStreamWaitEvent(st, g->state_ready, 0));
   }
-  if (mode == ML_OUT_ALLTOALL) {
+  const bool fused = g->tr->has_peer_mem();
+  PeerLayout L{};
+  size_t par = 0;
+  const void* dy_slices = b.dy_recv;
+  if (fused) {   // fused exchange: stores straight into the owners' regions
+    L = peer_layout(g, *shape);
+    ML_TRY(g->tr->peer_setup(L.total, st));
+    par = size_t(g->p2p_bwd_steps++ & 1);
+  }
+  if (mode == ML_OUT_ALLTOALL && fused) {
+    // slice g of this rank's dy rows -> rank g's region, slot r
+    void* dst[kMaxOutBlocks];
+    const size_t blk = size_t(shape->T) * dvG * e;
+    for (int to = 0; to < G; ++to) dst[to] = g->tr->peer_region(to) + L.dy_off + par * L.dy_half + size_t(r) * blk;
+    ML_TRY(launch_group_pack_peers(dy, G, shape->T, dvG, dst, shape->dtype, st));
+    ML_TRY(g->tr->peer_barrier(st));
+    dy_slices = g->tr->peer_region(r) + L.dy_off + par * L.dy_half;
+  } else if (mode == ML_OUT_ALLTOALL) {
     // dy of this rank's tokens -> [G][T_loc][dv/G] -> slice g to rank g
     ML_TRY((ml_group_pack(dy, G, shape->T, shape->dv, b.dy_send, shape->dtype, st)));
     ML_TRY(g->tr->all_to_all(b.dy_send, b.dy_recv, size_t(shape->T) * dvG * e, st));
@@ -951,9 +992,18 @@ mlStatus embbag_bwd_group(mlGroup g, const mlBagShape* shape, const void* V_shar
     ML_TRY((embbag_bwd_prepare(&bs, idx_all, b.state, sb, st)));
     state = b.state;
   }
-  ML_TRY((embbag_bwd_state(&bs, V_shard, w_all, b.dy_recv, state, sb, rows, dV_shard, U,
+  ML_TRY((embbag_bwd_state(&bs, V_shard, w_all, dy_slices, state, sb, rows, dV_shard, U,
                                        b.dw_part, b.bag_ws, wb, st)));
   // partial dw (a dot over this rank's dv/G columns) summed over the shards
+  if (fused) {   // block g -> rank g's region slot r; the owner sums the G slots in rank order
+    const int64_t n = int64_t(shape->T) * shape->B;
+    for (int to = 0; to < G; ++to)
+      ML_CUDA_TRY(cudaMemcpyAsync(g->tr->peer_region(to) + L.dw_off + par * L.dw_half + size_t(r) * L.dw_blk,
+                                  b.dw_part + int64_t(to) * n, L.dw_blk, cudaMemcpyDeviceToDevice, st));
+    ML_TRY(g->tr->peer_barrier(st));
+    return launch_sum_ranks(reinterpret_cast<const float*>(g->tr->peer_region(r) + L.dw_off + par * L.dw_half),
+                            G, n, dw_local, st);
+  }
   return g->tr->reduce_scatter_f32(b.dw_part, dw_local, size_t(shape->T) * shape->B, st);
   ML_API_END_X
 }

@@ -216,6 +216,11 @@ mlStatus launch_sparse_adam(const int32_t* rows, const void* dV, mlDtype gdt, co
                             int32_t* steps, const mlAdamParams& hp, cudaStream_t s);
 
 // ------------------------------------------------------------ group layout
+// fused exchange (peer memory): pack block g straight into dst[g]; the
+// owner's deterministic sum of G rank slots
+mlStatus launch_group_pack_peers(const void* src, int G, int64_t T_loc, int32_t dv_slice,
+                                 void* const* dst, mlDtype dt, cudaStream_t s);
+mlStatus launch_sum_ranks(const float* slots, int G, int64_t n, float* out, cudaStream_t s);
 mlStatus launch_group_unpack(const void* recv, int G, int64_t T_loc, int32_t dv_slice,
                              const void* gate, void* y, void* z, mlDtype dt, cudaStream_t s);
 mlStatus launch_group_pack(const void* src, int G, int64_t T_loc, int32_t dv_slice, void* dst,

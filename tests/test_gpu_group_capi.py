@@ -258,12 +258,14 @@ def test_group_state_merge_bit_identical(G, T_loc, B, N):
         assert torch.equal(x, y), n
 
 
-@pytest.mark.parametrize("G", [2, 3, 4])
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
 def test_capi_group_p2p_equals_sendrecv(G):
-    """The fused peer-memory forward exchange produces exactly the point-to-
-    point path's results (same kernels, same arithmetic; only where the bag
-    kernel stores its rows differs), over three steps (both halves of the
-    double-buffered exchange region, reused)."""
+    """The fused peer-memory exchanges (forward y blocks stored by the bag
+    kernel into the owners' regions; backward dy slices stored by the pack
+    kernel, partial dw blocks copied into the owners' slots and summed there
+    in rank order) produce exactly the collective path's results (same
+    arithmetic, same summation order), over three steps (both halves of every
+    double-buffered section reused)."""
     from paper_2412_09764_b200 import ops
     T_loc, H, S, Dk, k, D = 64, 2, 64, 128, 8, 128
     # the full row and every rank's slice must pass the row-width rule
