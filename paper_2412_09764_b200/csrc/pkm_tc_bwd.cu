@@ -268,6 +268,222 @@ __global__ void __launch_bounds__(kThreadsB, 1)
   }
 }
 
+// ---- CTA-pair form (cta_group::2, M = 256): the two CTAs of a cluster take
+// two adjacent 128-row m-tiles of the same (h, half, n-tile); each loads its
+// own A rows and HALF of the B columns, the leader issues one M = 256 MMA per
+// k-step, each CTA accumulates its rows in its own TMEM.  Per CTA the B bytes
+// per stage halve (the key / query tile is shared across the pair), so the
+// TMA traffic that bounds the single-CTA kernel drops by a third.
+constexpr int kStagesP = 6;
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsB, 1)
+    pkm_bwd_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB1,
+                       const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmD,
+                       BwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t bytes_a = kBM * kBK * 2;                      // this CTA's 128 rows x 64 K
+  const uint32_t bytes_b = uint32_t(p.BN / 2) * kBK * 2;       // this CTA's half of the N columns
+  uint8_t* sA = base;
+  uint8_t* sB = base + kStagesP * bytes_a;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStagesP * bytes_b);
+  uint64_t* empty = full + kStagesP;
+  uint64_t* tfull = empty + kStagesP;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 1024);
+
+  const uint32_t rank = cluster_ctarank();
+  const int cl = int(blockIdx.x >> 1), ncl = int(gridDim.x >> 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStagesP; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 256);     // both CTAs' epilogue threads (leader's copy is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB1)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                      // peer barriers initialised, TMEM allocated in both
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nbh = p.BN / 128;          // 64-column B boxes per CTA per stage
+
+  // unit -> (problem pr = h*2 + half, m-tile pair mp, n-tile nt)
+  auto decode = [&](int u, int& pr, int& mp, int& nt) {
+    nt = u % p.n_tiles;
+    const int r = u / p.n_tiles;
+    mp = r % p.m_tiles;               // m_tiles holds the PAIR count here
+    pr = r / p.m_tiles;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs, each its own rows / columns)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cl; u < p.tiles; u += ncl) {
+        int pr, mp, nt;
+        decode(u, pr, mp, nt);
+        const int h = pr >> 1, half = pr & 1;
+        const int mt = 2 * mp + int(rank);
+        const CUtensorMap* tmB = half ? &tmB2 : &tmB1;
+        for (int kc = 0; kc < p.k_chunks; ++kc) {
+          mbar_wait_t<true>(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * (bytes_a + bytes_b));
+          const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
+          uint8_t* a = sA + stage * bytes_a;
+          uint8_t* b = sB + stage * bytes_b;
+          if constexpr (MODE == MODE_DQ) {
+            tma_load_2d_pair(a, &tmA, lbar, pr * p.S + kc * kBK, mt * kBM);
+            for (int j = 0; j < nbh; ++j)
+              tma_load_2d_pair(b + j * 8192, tmB, lbar, nt * p.BN + int(rank) * (p.BN / 2) + j * 64,
+                               h * p.S + kc * kBK);
+          } else {
+            for (int j = 0; j < 2; ++j)
+              tma_load_2d_pair(a + j * 8192, &tmA, lbar, pr * p.S + mt * kBM + j * 64, kc * kBK);
+            for (int j = 0; j < nbh; ++j)
+              tma_load_2d_pair(b + j * 8192, &tmB1, lbar,
+                               h * p.Dk + half * p.Dh + nt * p.BN + int(rank) * (p.BN / 2) + j * 64,
+                               kc * kBK);
+          }
+          if (++stage == kStagesP) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer: the leader only
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = cl; u < p.tiles; u += ncl) {
+        mbar_wait_t<true>(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + uint32_t(acc * p.BN);
+        for (int kc = 0; kc < p.k_chunks; ++kc) {
+          mbar_wait_t<true>(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * bytes_a), b0 = smem_u32(sB + stage * bytes_b);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = MODE == MODE_DQ ? desc_sw128(a0 + 32 * k, 16, 1024)
+                                                : desc_sw128(a0 + 2048 * k, 8192, 1024);
+            const uint64_t bd = desc_sw128(b0 + 2048 * k, 8192, 1024);
+            umma_f16_pair(dcol, ad, bd, p.idesc, (kc | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[stage]);
+          if (++stage == kStagesP) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue (both CTAs): own rows from own TMEM
+    const int q4 = warp & 3;
+    int sbuf = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = cl; u < p.tiles; u += ncl) {
+      int pr, mp, nt;
+      decode(u, pr, mp, nt);
+      const int h = pr >> 1, half = pr & 1;
+      const int mt = 2 * mp + int(rank);
+      const int row = mt * kBM + q4 * 32 + lane;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      float* dst;
+      bool valid;
+      if constexpr (MODE == MODE_DQ) {
+        valid = row < p.T;
+        dst = p.dq + int64_t(row) * p.H * p.Dk + h * p.Dk + half * p.Dh + nt * p.BN;
+      } else {
+        valid = true;
+        dst = (half ? p.dK2 : p.dK1) + (int64_t(h) * p.S + row) * p.Dh + nt * p.BN;
+      }
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
+        if constexpr (MODE == MODE_DQ) {
+          float* stg = stage_all + ((warp - 4) * 2 + (sbuf & 1)) * 1024;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            *reinterpret_cast<uint4*>(stg + lane * 32 + ((v ^ (lane & 7)) << 2)) =
+                make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmD)),
+                "r"(smem_u32(stg)), "r"(h * p.Dk + half * p.Dh + nt * p.BN + c0),
+                "r"(mt * kBM + q4 * 32)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          ++sbuf;
+          continue;
+        }
+        if (valid) {
+          float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            float4 x = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+            const float4 o = d4[v];
+            x.x += o.x; x.y += o.y; x.z += o.z; x.w += o.w;
+            d4[v] = x;
+          }
+        }
+      }
+      tc_fence_before();
+      if (rank == 0) mbar_arrive(&tempty[acc]);
+      else mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (MODE == MODE_DQ && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                      // both CTAs done before the pair's TMEM is freed
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(p.tmem_cols));
+  }
+}
+
 int bn_for(int Dh) { return Dh % 256 == 0 ? 256 : (Dh % 128 == 0 ? 128 : 64); }
 
 }  // namespace
@@ -314,6 +530,64 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
                       size_t(4) * 2 * 1024 * sizeof(float);
   static size_t configured[2] = {0, 0};
   const int grid_max = num_sms();
+  // CTA pairs (cta_group::2): 256-column n-tiles, whole 256-row key pairs for dK
+  static const bool pair_env = [] {
+    const char* e = std::getenv("ML_PKM_BWD_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  if (pair_env && !ds_lo && p.BN == 256 && sh.S % 256 == 0) {
+    const size_t smem2 = 1024 + size_t(kStagesP) * (kBM * kBK * 2 + size_t(p.BN / 2) * kBK * 2) + 1024 +
+                         size_t(4) * 2 * 1024 * sizeof(float);
+    static bool attr2 = false;
+    if (!attr2) {
+      ML_CUDA_TRY(cudaFuncSetAttribute(pkm_bwd_tc2_kernel<MODE_DQ>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+      ML_CUDA_TRY(cudaFuncSetAttribute(pkm_bwd_tc2_kernel<MODE_DK>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+      attr2 = true;
+    }
+    const uint32_t idesc2 = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(p.BN >> 3) << 17) |
+                            (uint32_t(256 >> 4) << 24);
+    const int ncl_max = grid_max / 2;
+    {   // dq
+      CUtensorMap ma, mb1, mb2, md;
+      ML_TRY(make_map(&ma, ds, uint64_t(HS2), uint64_t(sh.T), uint64_t(HS2) * 2, kBK, kBM));
+      ML_TRY(make_map(&mb1, K1, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, 64, kBK));
+      ML_TRY(make_map(&mb2, K2, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, 64, kBK));
+      EncodeFn f = encode_fn();
+      if (!f) return fail(ML_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+      cuuint64_t dims[2] = {uint64_t(sh.H) * sh.Dk, uint64_t(sh.T)};
+      cuuint64_t strides[1] = {uint64_t(sh.H) * sh.Dk * 4};
+      cuuint32_t box[2] = {32, 32};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult r = f(&md, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(ML_ERR_CUDA, "cuTensorMapEncodeTiled (dq) failed: " + std::to_string(int(r)));
+      BwdParams pq = p;
+      pq.m_tiles = ((sh.T + kBM - 1) / kBM + 1) / 2;      // 128-row m-tile PAIRS
+      pq.k_chunks = sh.S / kBK;
+      pq.tiles = sh.H * 2 * pq.m_tiles * pq.n_tiles;
+      pq.idesc = idesc2 | (1u << 16);
+      const int ncl = std::min(pq.tiles, ncl_max);
+      pkm_bwd_tc2_kernel<MODE_DQ><<<2 * ncl, kThreadsB, smem2, s>>>(ma, mb1, mb2, md, pq);
+      ML_LAUNCH_CHECK("pkm_dq_tc");
+    }
+    {   // dK
+      CUtensorMap ma, mb;
+      ML_TRY(make_map(&ma, ds, uint64_t(HS2), uint64_t(sh.T), uint64_t(HS2) * 2, 64, kBK));
+      ML_TRY(make_map(&mb, q, uint64_t(sh.H) * sh.Dk, uint64_t(sh.T), uint64_t(sh.H) * sh.Dk * 2, 64, kBK));
+      BwdParams pk = p;
+      pk.m_tiles = sh.S / 256;                             // 256-key pairs
+      pk.k_chunks = (sh.T + kBK - 1) / kBK;
+      pk.tiles = sh.H * 2 * pk.m_tiles * pk.n_tiles;
+      pk.idesc = idesc2 | (1u << 15) | (1u << 16);
+      const int ncl = std::min(pk.tiles, ncl_max);
+      pkm_bwd_tc2_kernel<MODE_DK><<<2 * ncl, kThreadsB, smem2, s>>>(ma, mb, mb, mb, pk);
+      ML_LAUNCH_CHECK("pkm_dK_tc");
+    }
+    return ML_OK;
+  }
   // ---- dq = ds K: A K-major (ds rows), B MN-major (key table)
   {
     CUtensorMap ma, mb1, mb2, mlo;
