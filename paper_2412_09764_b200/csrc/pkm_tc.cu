@@ -241,6 +241,190 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 
+// ---- CTA-pair scoring (cta_group::2, M = 256 tokens): the two CTAs of a
+// cluster take adjacent 128-token m-tiles of the same (h, half); each loads
+// its own query rows and HALF of every 256-key subtile, the leader issues one
+// M = 256 MMA per k-step, each CTA accumulates its rows in its own TMEM and
+// runs the same epilogue (scores by TMA store, chunk maxima).  Per CTA the
+// key bytes per stage halve.
+constexpr int kStagesP = 6;
+
+template <bool CHUNKS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    pkm_scores_tc2_kernel(const __grid_constant__ CUtensorMap tmQ,
+                          const __grid_constant__ CUtensorMap tmK1,
+                          const __grid_constant__ CUtensorMap tmK2,
+                          const __grid_constant__ CUtensorMap tmS, TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t bytes_a = kBM * kBK * 2;
+  const uint32_t bytes_b = uint32_t(p.BN / 2) * kBK * 2;
+  uint8_t* sA = base;
+  uint8_t* sB = base + kStagesP * bytes_a;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStagesP * bytes_b);
+  uint64_t* empty = full + kStagesP;
+  uint64_t* tfull = empty + kStagesP;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 1024);
+
+  const uint32_t rank = cluster_ctarank();
+  const int cl = int(blockIdx.x >> 1), ncl = int(gridDim.x >> 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStagesP; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK1)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmS)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  // unit -> (m-tile pair mp, hh = h*2 + half); p.m_tiles holds the pair count
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cl; u < p.tiles; u += ncl) {
+        const int mp = u % p.m_tiles, hh = u / p.m_tiles;
+        const int h = hh >> 1, half = hh & 1;
+        const int mt = 2 * mp + int(rank);
+        const CUtensorMap* tmK = half ? &tmK2 : &tmK1;
+        for (int n = 0; n < p.n_sub; ++n) {
+          for (int kc = 0; kc < p.k_chunks; ++kc) {
+            mbar_wait_t<true>(&empty[stage], phase ^ 1);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * (bytes_a + bytes_b));
+            const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
+            tma_load_2d_pair(sA + stage * bytes_a, &tmQ, lbar, h * p.Dk + half * p.Dh + kc * kBK,
+                             mt * kBM);
+            tma_load_2d_pair(sB + stage * bytes_b, tmK, lbar, kc * kBK,
+                             h * p.S + n * p.BN + int(rank) * (p.BN / 2));
+            if (++stage == kStagesP) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer: the leader
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = cl; u < p.tiles; u += ncl) {
+        for (int n = 0; n < p.n_sub; ++n) {
+          mbar_wait_t<true>(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t dcol = tmem_base + uint32_t(acc * p.BN);
+          for (int kc = 0; kc < p.k_chunks; ++kc) {
+            mbar_wait_t<true>(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t ad = sw128_desc(smem_u32(sA + stage * bytes_a));
+            const uint64_t bd = sw128_desc(smem_u32(sB + stage * bytes_b));
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_f16_pair(dcol, ad + 2 * k, bd + 2 * k, p.idesc, (kc | k) != 0 ? 1u : 0u);
+            umma_commit_pair(&empty[stage]);
+            if (++stage == kStagesP) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit_pair(&tfull[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue (both CTAs): own rows
+    const int q4 = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int it = 0;
+    float* stg0 = stage_all + (warp - 4) * 2 * kStageFloats;
+    for (int u = cl; u < p.tiles; u += ncl) {
+      const int mp = u % p.m_tiles, hh = u / p.m_tiles;
+      const int mt = 2 * mp + int(rank);
+      const int row0 = mt * kBM + q4 * 32;
+      for (int n = 0; n < p.n_sub; ++n) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        float cm[8];
+        for (int c0 = 0; c0 < p.BN; c0 += 32, ++it) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
+          if constexpr (CHUNKS) {
+            float m = __uint_as_float(r[0]);
+#pragma unroll
+            for (int j = 1; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]));
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j == (c0 >> 5)) cm[j] = m;
+          }
+          float* stg = stg0 + (it & 1) * kStageFloats;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            *reinterpret_cast<uint4*>(stg + lane * 32 + ((v ^ (lane & 7)) << 2)) =
+                make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmS, stg, n * p.BN + c0, hh, row0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+        tc_fence_before();
+        if (rank == 0) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));
+        if (CHUNKS && row0 + lane < p.T) {
+          float* dst = p.cmax + (int64_t(row0 + lane) * p.H * 2 + hh) * (p.S >> 5) + (n * p.BN >> 5);
+          reinterpret_cast<float4*>(dst)[0] = make_float4(cm[0], cm[1], cm[2], cm[3]);
+          reinterpret_cast<float4*>(dst)[1] = make_float4(cm[4], cm[5], cm[6], cm[7]);
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(p.tmem_cols));
+  }
+}
+
 // ============================================================================
 // Scoring fused with the half top-k filter (no score matrix in HBM; opt-in).
 //
@@ -593,6 +777,40 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
     ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(smem)));
     configured = smem;
+  }
+  // opt-in (ML_PKM_PAIR=1): measured equal to the single-CTA kernel (C2 0.168
+  // vs 0.163 ms, S = 4096 0.649 vs 0.644, S = 8192 0.714 vs 0.721) -- the
+  // score stores, not the key-tile loads the pair halves, bound it
+  static const bool pair_env = [] {
+    const char* e = std::getenv("ML_PKM_PAIR");
+    return e && e[0] == '1';
+  }();
+  if (pair_env && p.BN == 256) {
+    // CTA pairs: 128-key boxes of the key tables, m-tile pairs
+    CUtensorMap mh1, mh2;
+    ML_TRY(make_map(&mh1, K1, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN / 2));
+    ML_TRY(make_map(&mh2, K2, uint64_t(Dh), uint64_t(sh.H) * sh.S, uint64_t(Dh) * 2, kBK, p.BN / 2));
+    TcParams pp = p;
+    pp.m_tiles = (p.m_tiles + 1) / 2;
+    pp.tiles = pp.m_tiles * sh.H * 2;
+    pp.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(p.BN >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+    const size_t smem2 = 1024 + size_t(kStagesP) * (kBM * kBK * 2 + size_t(p.BN / 2) * kBK * 2) + 1024 +
+                         size_t(4) * 2 * kStageFloats * sizeof(float);
+    static bool attr2 = false;
+    if (!attr2) {
+      ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_tc2_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+      ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_tc2_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+      attr2 = true;
+    }
+    const int ncl = std::min(pp.tiles, num_sms() / 2);
+    if (cmax)
+      pkm_scores_tc2_kernel<true><<<2 * ncl, kThreads, smem2, s>>>(mq, mh1, mh2, ms, pp);
+    else
+      pkm_scores_tc2_kernel<false><<<2 * ncl, kThreads, smem2, s>>>(mq, mh1, mh2, ms, pp);
+    ML_LAUNCH_CHECK("pkm_scores_tc");
+    return ML_OK;
   }
   const int grid = std::min(p.tiles, num_sms());
   pkm_scores_tc_kernel<<<grid, kThreads, smem, s>>>(mq, mk1, mk2, ms, p);
