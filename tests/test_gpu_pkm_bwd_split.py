@@ -84,3 +84,42 @@ def test_split_ds_backward_meets_fp32_tolerance(T, H, S, Dk, k):
     print(f"max rel err dq: split {rel(dq, rdq):.2e}, bf16 ds {rel(sq, rdq):.2e}; "
           f"dK1: split {rel(dK1, rdK1):.2e}, bf16 ds {rel(sK1, rdK1):.2e}")
     assert rel(dq, rdq) < rel(sq, rdq) and rel(dK1, rdK1) < rel(sK1, rdK1)
+
+
+def _bwd_env(arrays, env):
+    with tempfile.TemporaryDirectory() as d:
+        for n, a in arrays.items():
+            np.save(os.path.join(d, n + ".npy"), a)
+        code = (
+            "import numpy as np, torch\n"
+            "from paper_2412_09764_b200 import ops\n"
+            f"d = {d!r}\n"
+            "L = lambda n: torch.from_numpy(np.load(d + '/' + n + '.npy')).cuda()\n"
+            "b = lambda n: L(n).to(torch.bfloat16)\n"
+            "dq, dK1, dK2 = ops.pkm_topk_bwd(b('q'), b('K1'), b('K2'), L('idx'), L('w'), L('dw'))\n"
+            "for n, t in (('dq', dq), ('dK1', dK1), ('dK2', dK2)):\n"
+            "    np.save(d + '/o_' + n + '.npy', t.float().cpu().numpy())\n")
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), cwd=root,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return [np.load(os.path.join(d, f"o_{n}.npy")) for n in ("dq", "dK1", "dK2")]
+
+
+@pytest.mark.parametrize("T,H,S,Dk,k", [(300, 2, 512, 512, 16), (130, 4, 1024, 1024, 32)])
+def test_cta_pair_backward_equals_single_cta(T, H, S, Dk, k):
+    """The CTA-pair (cta_group::2, M = 256) key/query backward GEMMs give
+    exactly the single-CTA kernels' dq / dK (same k-step order per element),
+    including a ragged token count whose last pair has an empty half."""
+    sc = gen.scale_for("K1", Dk=Dk)
+    q = gen.tensor(42, "q", (T, H, Dk), dtype="bf16")
+    K1 = gen.tensor(42, "K1", (H, S, Dk // 2), scale=sc, dtype="bf16")
+    K2 = gen.tensor(42, "K2", (H, S, Dk // 2), scale=sc, dtype="bf16")
+    ridx, _, rw = opkm.pkm_lookup(q.astype(np.float64), K1.astype(np.float64), K2.astype(np.float64), k)
+    dw = gen.tensor(42, "dout", (T, H, k), dtype="f32")
+    arrays = dict(q=q.astype(np.float32), K1=K1.astype(np.float32), K2=K2.astype(np.float32),
+                  idx=ridx.astype(np.int32), w=rw.astype(np.float32), dw=dw.astype(np.float32))
+    pair = _bwd_env(arrays, {"ML_PKM_BWD_PAIR": "1"})
+    single = _bwd_env(arrays, {"ML_PKM_BWD_PAIR": "0"})
+    for a, b in zip(pair, single):
+        assert np.array_equal(a, b)
