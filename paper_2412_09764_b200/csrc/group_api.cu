@@ -6,23 +6,27 @@
 // corresponding to its own portion of the indices."
 //
 // A group owns its transport: NCCL (ml_group_init; one process per GPU, the
-// 128-byte unique id broadcast by the caller) or an in-process hub whose G
+// 128-byte unique id broadcast by the caller), an in-process hub whose G
 // ranks are host threads on one device (ml_group_init_hub; the collectives
 // are host-synchronised copies, so no kernel ever waits on another -- the
-// single-GPU test harness of exactly this protocol code).
+// single-GPU test harness of exactly this protocol code), or a loopback (one
+// rank with the network removed: t_ref(G) of SURVEY §8(e) through this code
+// path, ml_group_init_loopback).
 //
-// Forward (mode P, the paper's): (idx, w) packed into one all-gather; the
-// bag forward over all group tokens on this rank's [N, dv/G] slice runs one
-// token block (one source rank's tokens) at a time and each finished block
-// is sent to its owner on a communication stream while the next block is
-// computed (point-to-point ring steps), so NVLink traffic overlaps the
-// HBM-bound gather; the owner interleaves the G slices (+ the silu gate).
-// Mode N (north-star wording): the blocks are all-gathered instead and every
-// rank holds every token's full row.
-// Backward (reading Q14): the dy slices travel back by one all-to-all, the
-// sorted segmented reduction runs on the local slice (dV never leaves the
-// rank), and the partial dw (a dot over dv/G columns) is reduce-scattered to
-// the token owners.
+// Forward (mode P, the paper's): (idx, w) packed into one all-gather; own
+// positions sorted for the backward's inverse map on a preparation stream
+// (the sorted lists all-gathered and merged later: the map is built once per
+// group); the bag forward over all group tokens on this rank's [N, dv/G]
+// slice as one launch, its G token blocks sent to their owners by one
+// all-to-all, and the owner interleaves the G slices (+ the silu gate).  Mode
+// N (north-star wording): the blocks are all-gathered instead and every rank
+// holds every token's full row.  With peer memory (ml_group_set_p2p) the bag
+// kernel stores every block straight into its owner's exchange region.
+// Backward (reading Q14): the dy slices travel back by one all-to-all (or are
+// stored into the owners' regions), the sorted segmented reduction runs on
+// the local slice (dV never leaves the rank), and the partial dw (a dot over
+// dv/G columns) is reduce-scattered to the token owners (or summed by them
+// from their regions in rank order).
 #include "internal.cuh"
 
 #include <dlfcn.h>
