@@ -187,10 +187,15 @@ __global__ void __launch_bounds__(256) sort_hist_kernel(SortPassParams p, bool f
 // then writes every digit's run contiguously (coalesced) at its global offset.
 // dynamic smem: s_cnt[kSortWarps][nbins], s_dstart[nbins], s_goff[nbins],
 //               s_key[kSortTile], s_val[kSortTile]
+// ML_SORT_MINB (build switch): blocks per SM of the scatter kernel; 3 spills
+// (80 registers) and measured 163 vs 143 us per 2-pass C2 sort
+#ifndef ML_SORT_MINB
+#define ML_SORT_MINB 2
+#endif
 // (A variant writing each key straight to its global slot, without the
 // shared-memory staging, measured 155 vs 144 us per 2-pass sort of 2.1M keys.)
 template <bool ONESWEEP, int ROUNDS = kSortRounds>
-__global__ void __launch_bounds__(256, 2) sort_scatter_kernel(SortPassParams p, bool first) {
+__global__ void __launch_bounds__(256, ML_SORT_MINB) sort_scatter_kernel(SortPassParams p, bool first) {
   constexpr int TILE = kSortWarps * ROUNDS * 32;
   extern __shared__ int s_dyn[];
   const int nbins = 1 << p.dbits;
