@@ -1,7 +1,7 @@
 """SASS evidence of the Blackwell-native paths (B200_PROFILING.md "What proves
 a Blackwell-native kernel"): counts of tcgen05 / TMA / TMEM / bulk-copy /
 mbarrier / FFMA2 / 256-bit store mnemonics per kernel of libmemlayer.so.
-    python scripts/sass_evidence.py > profiles/r01_sass_evidence.txt
+    python scripts/sass_evidence.py > profiles/r02_sass_evidence.txt
 """
 import collections
 import os
@@ -11,7 +11,8 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 so = os.path.join(ROOT, "paper_2412_09764_b200", "libmemlayer.so")
 sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
-keys = ["UTCHMMA", "UTCBAR", "LDTM", "UTMALDG", "UTMASTG", "UBLKCP", "SYNCS.ARRIVE",
+keys = ["UTCHMMA", "UTCHMMA.2CTA", "UTCBAR", "UTCBAR.2CTA", "LDTM", "UTMALDG", "UTMALDG.2D.2CTA",
+        "UTMASTG", "UBLKCP", "SYNCS.ARRIVE",
         "SYNCS.PHASECHK", "FFMA2", "STG.E.ENL2.256", "HMMA", "HGMMA", "LDGSTS"]
 cur, ev, arch = None, collections.defaultdict(collections.Counter), set()
 for line in sass.splitlines():
