@@ -79,7 +79,8 @@ def _run_hub(t, G, T_loc, dv, k, mode, p2p=False):
 @pytest.mark.parametrize("G,mode,p2p", [(1, "alltoall", False), (2, "alltoall", False),
                                          (4, "alltoall", False), (1, "allgather", False),
                                          (2, "allgather", False), (4, "allgather", False),
-                                         (2, "alltoall", True), (4, "alltoall", True)])
+                                         (2, "alltoall", True), (4, "alltoall", True),
+                                         (2, "allgather", True)])
 def test_capi_group_layer_vs_oracle(G, mode, p2p):
     """p2p: the fused forward exchange (ml_group_set_p2p), the bag kernel of
     every block storing straight into the owner's exchange region."""
