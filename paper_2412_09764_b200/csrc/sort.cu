@@ -583,6 +583,151 @@ __global__ void __launch_bounds__(kScanThreads) run_scan2_kernel(const int32_t* 
   if (tile == ntiles - 1 && threadIdx.x == kScanThreads - 1 && n_slots) *n_slots = e;
 }
 
+// ---------------------------------------------------------------- counting sort
+// For a key range no larger than twice the key count (the value-row sort of a
+// step with at least N/2 positions, e.g. C2: 2.1M positions over 2^20 rows):
+// one histogram, one scan and one atomic-cursor scatter place every pair in
+// its run; the scatter order inside a run is arbitrary, so each run's
+// positions are then sorted ascending -- exactly the order the stable radix
+// sort produces (the values of a run are distinct positions).  Clamped keys
+// are handled as in load_key.  Run lengths: <= kFixShort by one thread,
+// longer runs by one CTA (shared-memory bitonic chunks + merge passes).
+constexpr int kFixShort = 32;
+constexpr int kFixSmem = 8192;
+constexpr uint32_t kPosMask = 0x7fffffffu;   // strips kClampedPos for ordering
+
+__global__ void __launch_bounds__(256) csort_hist_kernel(const int32_t* __restrict__ keys, int64_t n,
+                                                         uint32_t limit, int32_t* __restrict__ cnt,
+                                                         int* flag) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t k = uint32_t(keys[i]);
+    if (k >= limit) {
+      atomicExch(flag, 1);
+      k = 0;
+    }
+    atomicAdd(cnt + k, 1);
+  }
+}
+
+// cur: exclusive run offsets on entry, run ends on exit
+__global__ void __launch_bounds__(256) csort_scatter_kernel(const int32_t* __restrict__ keys, int64_t n,
+                                                            uint32_t limit, int32_t* __restrict__ cur,
+                                                            int32_t* __restrict__ kout,
+                                                            int32_t* __restrict__ vout) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t k = uint32_t(keys[i]);
+    const bool clamped = k >= limit;
+    if (clamped) k = 0;
+    const int32_t o = atomicAdd(cur + k, 1);
+    kout[o] = int32_t(k);
+    vout[o] = int32_t(i) | (clamped ? kClampedPos : 0);
+  }
+}
+
+// one thread per run head: short runs sorted in place, long ones listed
+__global__ void __launch_bounds__(256) csort_fix_kernel(const int32_t* __restrict__ kout,
+                                                        int32_t* __restrict__ vout,
+                                                        const int32_t* __restrict__ end, int64_t n,
+                                                        int32_t* __restrict__ long_list,
+                                                        int32_t* __restrict__ n_long) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t k = kout[i];
+    if (i > 0 && kout[i - 1] == k) continue;
+    const int len = int(int64_t(end[k]) - i);
+    if (len <= 1) continue;
+    if (len > kFixShort) {
+      long_list[atomicAdd(n_long, 1)] = int32_t(i);
+      continue;
+    }
+    int32_t a[kFixShort];
+    for (int j = 0; j < len; ++j) a[j] = vout[i + j];
+    for (int j = 1; j < len; ++j) {      // insertion sort on the position
+      const int32_t x = a[j];
+      int t = j - 1;
+      while (t >= 0 && (uint32_t(a[t]) & kPosMask) > (uint32_t(x) & kPosMask)) {
+        a[t + 1] = a[t];
+        --t;
+      }
+      a[t + 1] = x;
+    }
+    for (int j = 0; j < len; ++j) vout[i + j] = a[j];
+  }
+}
+
+// one CTA per long run (grid-stride over the list); tmp: scratch of n values
+__global__ void __launch_bounds__(256) csort_long_kernel(const int32_t* __restrict__ kout,
+                                                         int32_t* __restrict__ vout,
+                                                         int32_t* __restrict__ tmp,
+                                                         const int32_t* __restrict__ end,
+                                                         const int32_t* __restrict__ long_list,
+                                                         const int32_t* __restrict__ n_long) {
+  __shared__ uint32_t s[kFixSmem];
+  const int nl = *n_long;
+  const int tid = threadIdx.x;
+  for (int r = blockIdx.x; r < nl; r += gridDim.x) {
+    const int64_t b = long_list[r];
+    const int64_t L = int64_t(end[kout[b]]) - b;
+    int32_t* v = vout + b;
+    for (int64_t c0 = 0; c0 < L; c0 += kFixSmem) {      // chunks sorted in shared memory
+      const int m = int(L - c0 < kFixSmem ? L - c0 : kFixSmem);
+      int p2 = 64;
+      while (p2 < m) p2 <<= 1;
+      for (int j = tid; j < p2; j += 256) s[j] = j < m ? uint32_t(v[c0 + j]) : 0xffffffffu;
+      __syncthreads();
+      for (int k = 2; k <= p2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int t = tid; t < p2 / 2; t += 256) {
+            const int i0 = (t / j) * 2 * j + (t & (j - 1)), i1 = i0 + j;
+            const uint32_t x = s[i0], y = s[i1];
+            if (((x & kPosMask) > (y & kPosMask)) == ((i0 & k) == 0)) {
+              s[i0] = y;
+              s[i1] = x;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int j = tid; j < m; j += 256) v[c0 + j] = int32_t(s[j]);
+      __syncthreads();
+    }
+    int32_t* src = v;
+    int32_t* dst = tmp + b;
+    for (int64_t w = kFixSmem; w < L; w <<= 1) {         // merge passes (merge path per thread)
+      for (int64_t s0 = 0; s0 < L; s0 += 2 * w) {
+        const int32_t* A = src + s0;
+        const int64_t na = L - s0 < w ? L - s0 : w;
+        const int32_t* B = A + na;
+        const int64_t nb = L - s0 - na < w ? L - s0 - na : w;
+        const int64_t m = na + nb;
+        const int64_t o0 = m * tid / 256, o1 = m * (tid + 1) / 256;
+        int64_t lo = o0 - nb > 0 ? o0 - nb : 0, hi = o0 < na ? o0 : na;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if ((uint32_t(A[mid]) & kPosMask) <= (uint32_t(B[o0 - mid - 1]) & kPosMask)) lo = mid + 1;
+          else hi = mid;
+        }
+        int64_t ia = lo, ib = o0 - lo;
+        for (int64_t o = o0; o < o1; ++o) {
+          const bool takeA = ib >= nb ||
+              (ia < na && (uint32_t(A[ia]) & kPosMask) <= (uint32_t(B[ib]) & kPosMask));
+          dst[s0 + o] = takeA ? A[ia++] : B[ib++];
+        }
+      }
+      __syncthreads();
+      int32_t* t = src;
+      src = dst;
+      dst = t;
+    }
+    if (src != v) {
+      for (int64_t j = tid; j < L; j += 256) v[j] = src[j];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ host side
@@ -607,15 +752,23 @@ mlStatus scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* tmp
 static int sort_nblocks(int64_t n) { return int((n + kSortTile - 1) / kSortTile); }
 
 
+// The counting sort (csort_*) needs one counter per key; it is used when the
+// key range 2^bits is at most twice the key count, and only then are the
+// counters sized for it.
+static bool counting_sort_fits(int64_t n, int bits) {
+  return bits >= 1 && bits <= 30 && (int64_t(1) << bits) <= 2 * n;
+}
+
 void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b) {
-  (void)bits;
   const int nb = sort_nblocks(n);
   b.k[0] = c.take<int32_t>(n);
   b.v[0] = c.take<int32_t>(n);
   b.k[1] = c.take<int32_t>(n);
   b.v[1] = c.take<int32_t>(n);
-  b.counts = c.take<int32_t>((int64_t(1) << kMaxDigitBits) * nb);
-  b.scan_tmp = c.take<int32_t>(scan_tmp_elems((int64_t(1) << kMaxDigitBits) * nb));
+  const int64_t ncnt = std::max<int64_t>((int64_t(1) << kMaxDigitBits) * nb,
+                                         counting_sort_fits(n, bits) ? int64_t(1) << bits : 0);
+  b.counts = c.take<int32_t>(ncnt);
+  b.scan_tmp = c.take<int32_t>(scan_tmp_elems(ncnt));
   b.ghist = c.take<int32_t>(3 * (int64_t(1) << kMaxDigitBits) + 8);
 }
 
@@ -647,6 +800,36 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
   const int dbits = (bits + passes - 1) / passes;
   const int nbins = 1 << dbits;
   const int nb = sort_nblocks(n);
+  static const bool counting = [] {
+    const char* e = std::getenv("ML_SORT_COUNTING");
+    return !(e && e[0] == '0');
+  }();
+  if (counting && passes >= 2 && key_limit > 0 && key_limit <= (int64_t(1) << bits) &&
+      counting_sort_fits(n, bits) && n < (int64_t(1) << 31) - 1) {
+    const int fin = (passes - 1) & 1;    // the buffers sorted_result names
+    int32_t* kout = b.k[fin];
+    int32_t* vout = b.v[fin];
+    int32_t* spare_k = b.k[fin ^ 1];
+    int32_t* spare_v = b.v[fin ^ 1];
+    const uint32_t lim = uint32_t(key_limit);
+    int32_t* n_long = b.ghist;
+    ML_CUDA_TRY(cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * size_t(lim), s));
+    ML_CUDA_TRY(cudaMemsetAsync(n_long, 0, sizeof(int32_t), s));
+    const unsigned g = unsigned(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+    csort_hist_kernel<<<g, 256, 0, s>>>(keys_in, n, lim, b.counts, index_flag_ptr());
+    ML_LAUNCH_CHECK("csort_hist");
+    ML_TRY(scan_exclusive(b.counts, b.counts, lim, b.scan_tmp, nullptr, s));
+    csort_scatter_kernel<<<g, 256, 0, s>>>(keys_in, n, lim, b.counts, kout, vout);
+    ML_LAUNCH_CHECK("csort_scatter");
+    csort_fix_kernel<<<g, 256, 0, s>>>(kout, vout, b.counts, n, spare_k, n_long);
+    ML_LAUNCH_CHECK("csort_fix");
+    csort_long_kernel<<<unsigned(num_sms()), 256, 0, s>>>(kout, vout, spare_v, b.counts, spare_k,
+                                                          n_long);
+    ML_LAUNCH_CHECK("csort_long");
+    *keys = kout;
+    *vals = vout;
+    return ML_OK;
+  }
   static bool attr = false;
   if (!attr) {
     const int max_smem = int(sizeof(int)) * ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile);

@@ -1,0 +1,76 @@
+"""The inverse index map's sort (§3.1.4: "preprocessing to
+inverse the token_id to embedding_id mapping") through the C ABI
+(embbag_bwd_group_sort_local at rank 0: the positions of idx sorted stably by
+row).  A stable sort has exactly one result, so the expectation is numpy's
+stable argsort of the clamped rows (an index outside [0, N) sorts as row 0
+with kClampedPos = bit 31 on its position; include/memlayer.h).
+
+Both device algorithms are covered: the counting sort (key range 2^ceil(log2
+N) <= 2 * positions and >= 2 radix passes, i.e. N > 2048) with its three run
+regimes (one thread <= 32, one CTA's shared memory <= 8192, CTA merge passes
+beyond), and the radix sort (larger key ranges)."""
+import numpy as np
+import pytest
+import torch
+
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2412_09764_b200 import ops  # noqa: F401  (fails loudly without the .so)
+    yield
+
+
+def _expected(idx, N):
+    k = idx.astype(np.int64).ravel()
+    clamped = (k < 0) | (k >= N)
+    k = np.where(clamped, 0, k)
+    order = np.argsort(k, kind="stable")
+    pos = order.astype(np.int64) | (clamped[order].astype(np.int64) << 31)
+    return k[order].astype(np.int32), pos.astype(np.uint32).view(np.int32)
+
+
+def _rows(seed, N, P, kind):
+    rng = np.random.default_rng([seed, N, P, len(kind)])
+    idx = rng.integers(0, N, P, dtype=np.int64)
+    if kind == "hot":             # one ~5k run (shared-memory chunk), many 33..200 runs
+        idx[rng.random(P) < 0.3] = 7
+        med = rng.integers(0, N, 60)
+        sel = rng.random(P) < 0.25
+        idx[sel] = med[rng.integers(0, 60, int(sel.sum()))]
+    elif kind == "one":           # a single run of every position (merge passes)
+        idx[:] = N - 1
+    elif kind == "two_big":       # two runs > 8192, interleaved
+        idx = np.where(rng.random(P) < 0.5, 3, N - 2)
+    elif kind == "clamped":       # out-of-range indices join row 0's run
+        bad = rng.random(P) < 0.05
+        idx[bad] = np.where(rng.random(int(bad.sum())) < 0.5, -1 - rng.integers(0, 9, int(bad.sum())),
+                            N + rng.integers(0, 9, int(bad.sum())))
+        idx[rng.random(P) < 0.02] = 0
+    return idx.astype(np.int32)
+
+
+@pytest.mark.parametrize("N,P,kind", [
+    (5000, 16384, "uniform"),       # counting sort, short runs
+    (5000, 16384 + 77, "hot"),      # ragged count; long runs in shared memory
+    (4097, 3 * 8192 + 5, "one"),    # one run of 24581: chunk sorts + 2 merge passes
+    (8000, 40000, "two_big"),
+    (6000, 9000, "clamped"),
+    (1 << 20, 1 << 21, "uniform"),  # the C2 value-row sort (2^20 rows, 2.1M positions)
+    (1 << 20, 1 << 18, "uniform"),  # key range > 2 * count: radix sort
+    (1 << 20, 1 << 18, "hot"),
+    (1000, 5000, "uniform"),        # one radix pass (bits <= 11)
+])
+def test_sort_local_is_the_stable_sort(N, P, kind):
+    from paper_2412_09764_b200 import ops
+    idx = _rows(11, N, P, kind)
+    lst = ops.group_sort_local(N, torch.from_numpy(idx).cuda().view(P, 1), 0)
+    torch.cuda.synchronize()
+    got = lst.cpu().numpy()
+    rows, pos = _expected(idx, N)
+    assert np.array_equal(got[0], rows), kind
+    assert np.array_equal(got[1], pos), kind
