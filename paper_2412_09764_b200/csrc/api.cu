@@ -41,7 +41,7 @@ int num_sms() {
 // per caller stream (calls on different streams never share them).
 struct Aux {
   cudaStream_t s[4];      // 3: the sparse key backward's dq gather (beside the dK sort)
-  cudaEvent_t ev[8];
+  cudaEvent_t ev[10];   // 8, 9: the fp16 key / query copies of the key backward
 };
 
 // Completion event of the backward state a forward built into a caller buffer
@@ -223,6 +223,7 @@ struct PkmBwdBufs {
   SortBufs sort; RunBufs runs; float* partial; int32_t* counters;
   __nv_bfloat16* ds_dense; __nv_bfloat16* ds_lo; void* gemm_ws;
   QkBufs qk; float* dK_tmp; float* ds1w; float* ds2w;
+  PkmBwdF16 f16; bool use_f16;   // fp16 operands of the tcgen05 key backward (pkm_bwd_f16)
 };
 static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
   const int64_t P = int64_t(s.T) * s.H * s.k;
@@ -232,12 +233,20 @@ static void pkm_bwd_carve(Carver& c, const mlPkmShape& s, PkmBwdBufs& b) {
   b.ds_dense = b.ds_lo = nullptr;
   b.gemm_ws = nullptr;
   b.dK_tmp = b.ds1w = b.ds2w = nullptr;
+  b.f16 = PkmBwdF16{nullptr, nullptr, nullptr, nullptr, nullptr};
+  b.use_f16 = false;
   qk_carve(c, s, b.qk);
   if (s.qk_norm) b.dK_tmp = c.take<float>(int64_t(2) * s.H * s.S * (s.Dk / 2));
   if (pkm_bwd_dense(s)) {
     b.ds_dense = c.take<__nv_bfloat16>(int64_t(s.T) * s.H * 2 * s.S);
     b.gemm_ws = c.take<char>(kGemmWs);
     if (pkm_bwd_split(s)) b.ds_lo = c.take<__nv_bfloat16>(int64_t(s.T) * s.H * 2 * s.S);
+    if (pkm_bwd_f16(s)) {
+      b.use_f16 = true;
+      b.f16.bound = c.take<float>(4);
+      b.f16.q16 = c.take<__half>(int64_t(s.T) * s.H * s.Dk);
+      b.f16.K16 = c.take<__half>(int64_t(2) * s.H * s.S * (s.Dk / 2));
+    }
     if (!c.base) {   // measuring: mark dense / split
       b.ds_dense = reinterpret_cast<__nv_bfloat16*>(1);
       if (b.ds_lo) b.ds_lo = b.ds_dense;
@@ -302,12 +311,30 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
       ML_CUDA_TRY(cudaMemsetAsync(b.ds_dense, 0, sizeof(__nv_bfloat16) * size_t(s.T) * s.H * 2 * s.S, st));
       timing_mark("memset", st);
     }
+    if (b.use_f16) {
+      // the fp16 query / key copies on aux 3 / aux 2, beside ds_bound and
+      // softmax_bwd (before the persistent contractions take every SM); the
+      // dq contraction waits for the keys (ev[8]), the dK contraction for q (ev[9])
+      Aux* aux = nullptr;
+      ML_TRY(aux_for(st, &aux));
+      ML_TRY(stream_dep(st, aux->s[3], aux->ev[6]));
+      ML_TRY(launch_pkm_bwd_f16_query(s, q, b.f16, aux->s[3]));
+      ML_CUDA_TRY(cudaEventRecord(aux->ev[9], aux->s[3]));
+      ML_TRY(stream_dep(st, aux->s[2], aux->ev[7]));
+      ML_TRY(launch_pkm_bwd_f16_keys(s, K1, K2, b.f16, aux->s[2]));
+      ML_CUDA_TRY(cudaEventRecord(aux->ev[8], aux->s[2]));
+      b.f16.keys_ready = aux->ev[8];
+      b.f16.q16_ready = aux->ev[9];
+      ML_TRY(launch_ds_bound(s, w, dw_part, ns, sstride, b.f16.bound, st));
+    }
     ML_TRY(launch_softmax_bwd(s, idx, w, dw_part, ns, sstride, b.ds, b.key1, b.key2, b.ds_dense, qn,
-                              nullptr, nullptr, st, b.ds_lo));
+                              nullptr, nullptr, st, b.ds_lo, b.use_f16 ? b.f16.bound : nullptr));
     if (pkm_bwd_tc_eligible(s)) {
       // hand-written tcgen05 contractions (pkm_tc_bwd.cu); with ds_lo the
-      // operand is the bf16 pair hi + lo (two MMAs per k-step)
-      ML_TRY(launch_pkm_bwd_tc(s, b.ds_dense, b.ds_lo, q, K1, K2, dq, dKo1, dKo2, st));
+      // operand is the bf16 pair hi + lo (two MMAs per k-step); with
+      // use_f16 all three operands are scaled fp16 copies
+      ML_TRY(launch_pkm_bwd_tc(s, b.ds_dense, b.ds_lo, q, K1, K2, dq, dKo1, dKo2, st,
+                               b.use_f16 ? &b.f16 : nullptr));
     } else {
     const int64_t lds = int64_t(s.H) * 2 * s.S;  // row pitch of ds_dense per token
     for (int half = 0; half < 2; ++half) {        // one strided-batched GEMM over heads each

@@ -157,10 +157,49 @@ bool pkm_bwd_tc_eligible(const mlPkmShape& sh);
 // opt-in (ML_PKM_BWD_SPLIT=1): ds carried as a bf16 hi/lo pair into the
 // tcgen05 key backward (needs the tcgen05 path and whole ds rows)
 bool pkm_bwd_split(const mlPkmShape& sh);
+// opt-in (ML_PKM_BWD_F16=1) for the tcgen05 key backward with whole ds rows
+// and no qk-norm: the three operands go to the tensor cores
+// as fp16 (11 significant bits; ds in bf16 would keep 8), each scaled by a
+// power of two 2^e from a bound on its magnitude so that it stays inside
+// fp16's range; the GEMM epilogues multiply by 2^-(e_ds + e_op) (exact).
+// bf16 q / keys convert exactly (8 <= 11 bits) inside fp16's normal range.
+bool pkm_bwd_f16(const mlPkmShape& sh);
+struct PkmBwdF16 {
+  float* bound;      // [4]: max|dw|, max|q|, max|K1|,|K2|, max|w|
+  __half* q16;       // [T, H, Dk]: fp16(q * 2^e_q)
+  __half* K16;       // [2][H, S, Dk/2]: fp16(K * 2^e_K)
+  cudaEvent_t keys_ready;  // nullable: the dq contraction waits for it (K16 made on another stream)
+  cudaEvent_t q16_ready;   // nullable: the dK contraction waits for it (q16 likewise)
+};
+// bound[0] = max |dw|, bound[3] = max |w| over the T*H*k positions (overwritten);
+// ds_f16_exp_ds turns them into a bound on every ds element
+mlStatus launch_ds_bound(const mlPkmShape& sh, const float* w, const float* dw_part, int nslices,
+                         int64_t slice_stride, float* bound, cudaStream_t s);
+// bound[2] + the fp16 copies of K1, K2 / bound[1] + the fp16 copy of q
+mlStatus launch_pkm_bwd_f16_keys(const mlPkmShape& sh, const void* K1, const void* K2,
+                                 const PkmBwdF16& f, cudaStream_t s);
+mlStatus launch_pkm_bwd_f16_query(const mlPkmShape& sh, const void* q, const PkmBwdF16& f,
+                                  cudaStream_t s);
+// the exponent e of an fp16 operand's scale: bound * 2^e < 2^14 (fp16 max 65504)
+__device__ __forceinline__ int ds_f16_exp(const float* bound) {
+  const float b = *bound;
+  if (!(b > 0.f) || !(b < 3.0e38f)) return 0;
+  int e;
+  frexpf(b, &e);                 // b < 2^e
+  e = 14 - e;
+  return e > 100 ? 100 : (e < -100 ? -100 : e);
+}
+// ds's exponent: ds_j = w_j (dw_j - sum_l w_l dw_l) gives |ds_j| <= W M (1 + k W)
+// (M = max|dw|, W = max|w|), and a sub-key's entry sums <= k of them
+__device__ __forceinline__ int ds_f16_exp_ds(const float* bound, int k) {
+  const float W = bound[3], kw = float(k) * W;
+  const float b = bound[0] * kw * (1.f + kw);
+  return ds_f16_exp(&b);
+}
 mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const __nv_bfloat16* ds_lo,
                            const void* q,
                            const void* K1, const void* K2, float* dq, float* dK1, float* dK2,
-                           cudaStream_t s);
+                           cudaStream_t s, const PkmBwdF16* f16 = nullptr);
 // dq from the deduplicated (key, ds) slots of softmax_bwd's sparse form
 mlStatus launch_pkm_dq(const mlPkmShape& sh, const int32_t* key1, const int32_t* key2,
                        const float* ds1, const float* ds2, const void* K1, const void* K2,
@@ -183,7 +222,7 @@ mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const floa
                             const float* dw_part, int nslices, int64_t slice_stride,
                             float* ds, int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,
                             const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s,
-                            __nv_bfloat16* ds_lo = nullptr);
+                            __nv_bfloat16* ds_lo = nullptr, const float* f16_bound = nullptr);
 
 // ------------------------------------------------------------ gate
 // z = y*silu(g); dy = dz*silu(g); dg = dz*y*silu'(g)   (elementwise, n elems)

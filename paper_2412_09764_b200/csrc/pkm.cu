@@ -904,6 +904,41 @@ __global__ void __launch_bounds__(32) cand_fallback_kernel(const __nv_bfloat16* 
   }
 }
 
+// bound[0] = max_o |dw_o| (dw = sum of the ns partials), bound[3] = max_o |w_o|
+// over the P = T*H*k positions (elementwise, coalesced; one atomic per block)
+__global__ void __launch_bounds__(256) ds_bound_kernel(const float* __restrict__ w,
+                                                       const float* __restrict__ dw_part, int ns,
+                                                       int64_t sstride, int64_t P, float* bound) {
+  float mdw = 0.f, mw = 0.f;
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < P;
+       o += int64_t(gridDim.x) * blockDim.x) {
+    float dwv = 0.f;
+    for (int s = 0; s < ns; ++s) dwv += dw_part[int64_t(s) * sstride + o];
+    mdw = fmaxf(mdw, fabsf(dwv));
+    mw = fmaxf(mw, fabsf(w[o]));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mdw = fmaxf(mdw, __shfl_xor_sync(FULL, mdw, off));
+    mw = fmaxf(mw, __shfl_xor_sync(FULL, mw, off));
+  }
+  __shared__ float s_m[2][8];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_m[0][wid] = mdw;
+    s_m[1][wid] = mw;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {      // values >= 0 order as ints
+    for (int i = 1; i < 8; ++i) {
+      mdw = fmaxf(mdw, s_m[0][i]);
+      mw = fmaxf(mw, s_m[1][i]);
+    }
+    atomicMax(reinterpret_cast<int*>(bound), __float_as_int(mdw));
+    atomicMax(reinterpret_cast<int*>(bound + 3), __float_as_int(mw));
+  }
+}
+
 // one warp per (t, h)
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, const float* w,
                                                           const float* dw_part, int ns,
@@ -911,7 +946,8 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
                                                           int S, int k, float* ds, int32_t* key1,
                                                           int32_t* key2, __nv_bfloat16* ds_dense,
                                                           QkNorm qn, float* ds1w, float* ds2w,
-                                                          int full_rows, __nv_bfloat16* ds_lo) {
+                                                          int full_rows, __nv_bfloat16* ds_lo,
+                                                          const float* f16_bound) {
   __shared__ int s_sub[8][2][32];
   __shared__ float s_ds[8][32];
   __shared__ float s_sc[8][2][32];
@@ -994,7 +1030,11 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const int32_t* idx, co
         }
       }
       if (leader) {
-        const __nv_bfloat16 hi = __float2bfloat16_rn(sum);
+        // fp16 form (f16_bound, full rows only): fp16(ds * 2^e) in the same
+        // 2-byte slots, read by the mixed-type MMA (pkm_tc_bwd.cu)
+        const __nv_bfloat16 hi = f16_bound
+            ? __ushort_as_bfloat16(__half_as_ushort(__float2half_rn(ldexpf(sum, ds_f16_exp_ds(f16_bound, k)))))
+            : __float2bfloat16_rn(sum);
         if (full_rows) {
           rows[half * S + a] = hi;
           if (ds_lo) rows_lo[half * S + a] = __float2bfloat16_rn(sum - __bfloat162float(hi));
@@ -1178,11 +1218,13 @@ mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const floa
                             const float* dw_part, int nslices, int64_t slice_stride, float* ds,
                             int32_t* key1, int32_t* key2, __nv_bfloat16* ds_dense,
                             const QkNorm& qn, float* ds1w, float* ds2w, cudaStream_t s,
-                            __nv_bfloat16* ds_lo) {
+                            __nv_bfloat16* ds_lo, const float* f16_bound) {
   const int64_t TH = int64_t(sh.T) * sh.H;
   if (TH <= 0) return ML_OK;
   const bool full = ds_dense && softmax_bwd_full_rows(sh);
   if (ds_lo && !full) return fail(ML_ERR_UNSUPPORTED, "softmax_bwd: the split ds needs full rows");
+  if (f16_bound && (!full || ds_lo || qn.qinv))
+    return fail(ML_ERR_UNSUPPORTED, "softmax_bwd: the fp16 ds needs full rows, no split, no qk-norm");
   const size_t smem = full ? size_t(ds_lo ? 16 : 8) * 2 * sh.S * sizeof(__nv_bfloat16) : 0;
   static bool attr = false;
   if (full && !attr) {
@@ -1192,8 +1234,20 @@ mlStatus launch_softmax_bwd(const mlPkmShape& sh, const int32_t* idx, const floa
   }
   softmax_bwd_kernel<<<unsigned((TH + 7) / 8), 256, smem, s>>>(
       idx, w, dw_part, nslices, slice_stride, TH, sh.H, sh.S, sh.k, ds, key1, key2, ds_dense, qn,
-      ds1w, ds2w, full ? 1 : 0, ds_lo);
+      ds1w, ds2w, full ? 1 : 0, ds_lo, f16_bound);
   ML_LAUNCH_CHECK("softmax_bwd");
+  return ML_OK;
+}
+
+mlStatus launch_ds_bound(const mlPkmShape& sh, const float* w, const float* dw_part, int nslices,
+                         int64_t slice_stride, float* bound, cudaStream_t s) {
+  const int64_t P = int64_t(sh.T) * sh.H * sh.k;
+  ML_CUDA_TRY(cudaMemsetAsync(bound, 0, sizeof(float), s));
+  ML_CUDA_TRY(cudaMemsetAsync(bound + 3, 0, sizeof(float), s));
+  if (P <= 0) return ML_OK;
+  const unsigned grid = unsigned(std::min<int64_t>((P + 255) / 256, int64_t(num_sms()) * 8));
+  ds_bound_kernel<<<grid, 256, 0, s>>>(w, dw_part, nslices, slice_stride, P, bound);
+  ML_LAUNCH_CHECK("ds_bound");
   return ML_OK;
 }
 

@@ -26,13 +26,24 @@ constexpr int kThreadsB = 256;
 
 enum Mode { MODE_DQ = 0, MODE_DK = 1 };
 
+// the exponent an fp16 operand copy was made with (to_f16_* kernels below):
+// 0 while max|x| is in [2^-2, 2^14), else ds_f16_exp
+__device__ __forceinline__ int op_f16_exp(const float* amax) {
+  const float m = *amax;
+  return (m >= 0.25f && m < 16384.f) ? 0 : ds_f16_exp(amax);
+}
+
 struct BwdParams {
-  int T, H, S, Dh, Dk;
+  int T, H, S, Dh, Dk, k;
   int BN, n_tiles, m_tiles, k_chunks, tiles;
   int split, stages;         // split: A = hi + lo (two bf16 tiles per stage)
   uint32_t idesc, tmem_cols;
   float* dq;                 // MODE_DQ: [T, H*Dk]
   float* dK1; float* dK2;    // MODE_DK: [H*S, Dh] each, accumulate
+  // fp16 operands (pkm_bwd_f16): ds scaled by 2^e_ds, the B operand by
+  // 2^e_op (ds_f16_exp of the bounds); the epilogue multiplies by 2^-(e_ds + e_op)
+  const float* ds_bound;
+  const float* op_bound;
 };
 
 // Smem descriptor of a 128-byte-swizzled tile.  K-major (an 8-row x 128-byte
@@ -189,6 +200,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     }
   } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> fp32 rows
     const int q4 = warp & 3;
+    const float ds_inv =
+        p.ds_bound ? ldexpf(1.f, -(ds_f16_exp_ds(p.ds_bound, p.k) + op_f16_exp(p.op_bound))) : 1.f;
     int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -211,6 +224,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * ds_inv);
         if constexpr (MODE == MODE_DQ) {
           // stage the 32x32 fp32 chunk (128-byte swizzle) and TMA-store it;
           // rows past T are clipped by the tensor map
@@ -406,6 +421,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsB, 1)
     }
   } else if (warp >= 4) {  // ---------------- epilogue (both CTAs): own rows from own TMEM
     const int q4 = warp & 3;
+    const float ds_inv =
+        p.ds_bound ? ldexpf(1.f, -(ds_f16_exp_ds(p.ds_bound, p.k) + op_f16_exp(p.op_bound))) : 1.f;
     int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -429,6 +446,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsB, 1)
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * ds_inv);
         if constexpr (MODE == MODE_DQ) {
           float* stg = stage_all + ((warp - 4) * 2 + (sbuf & 1)) * 1024;
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -484,6 +503,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsB, 1)
   }
 }
 
+// fp16 copies of the bf16 q / key operands.  One pass converts at scale 1
+// (exact for |x| in [2^-14, 65504]) and records max|x| (one atomic per
+// block); a second launch redoes the conversion at 2^e (ds_f16_exp) only when
+// that max leaves [2^-2, 2^14) (overflow risk, or a tensor so small that fp16
+// subnormals would cost precision) and otherwise exits at once.  The epilogue
+// reads the exponent the copy was made with from op_f16_exp.
+__global__ void __launch_bounds__(256) to_f16_pass1_kernel(const __nv_bfloat16* __restrict__ x, int64_t n,
+                                                           float* amax, __half* __restrict__ y) {
+  float m = 0.f;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  const int64_t n8 = vec ? n / 8 : 0;
+  for (int64_t i = t0; i < n8; i += stride) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(x) + i);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    uint4 o;
+    __half2* oh = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h[j]);
+      m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
+      oh[j] = __floats2half2_rn(f.x, f.y);
+    }
+    reinterpret_cast<uint4*>(y)[i] = o;
+  }
+  for (int64_t i = n8 * 8 + t0; i < n; i += stride) {
+    const float f = __bfloat162float(x[i]);
+    m = fmaxf(m, fabsf(f));
+    y[i] = __float2half_rn(f);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  __shared__ float s_m[8];
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {      // one atomic per block (same-address atomics serialise)
+    for (int i = 1; i < 8; ++i) m = fmaxf(m, s_m[i]);
+    atomicMax(reinterpret_cast<int*>(amax), __float_as_int(m));   // values >= 0
+  }
+}
+
+__global__ void __launch_bounds__(256) to_f16_redo_kernel(const __nv_bfloat16* __restrict__ x, int64_t n,
+                                                          const float* amax, __half* __restrict__ y) {
+  const int e = op_f16_exp(amax);
+  if (e == 0) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = __float2half_rn(ldexpf(__bfloat162float(x[i]), e));
+}
+
 int bn_for(int Dh) { return Dh % 256 == 0 ? 256 : (Dh % 128 == 0 ? 128 : 64); }
 
 }  // namespace
@@ -507,24 +576,76 @@ bool pkm_bwd_split(const mlPkmShape& sh) {
   return on && pkm_bwd_tc_eligible(sh) && softmax_bwd_full_rows(sh);
 }
 
+bool pkm_bwd_f16(const mlPkmShape& sh) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("ML_PKM_BWD_F16");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on && !sh.qk_norm && pkm_bwd_tc_eligible(sh) && softmax_bwd_full_rows(sh) && !pkm_bwd_split(sh);
+}
+
+static unsigned f16_grid(int64_t n) {
+  return unsigned(std::min<int64_t>((n / 8 + 255) / 256 + 1, int64_t(num_sms()) * 8));
+}
+
+mlStatus launch_pkm_bwd_f16_keys(const mlPkmShape& sh, const void* K1, const void* K2,
+                                 const PkmBwdF16& f, cudaStream_t s) {
+  const int64_t nk = int64_t(sh.H) * sh.S * (sh.Dk / 2);
+  const auto* k1 = static_cast<const __nv_bfloat16*>(K1);
+  const auto* k2 = static_cast<const __nv_bfloat16*>(K2);
+  ML_CUDA_TRY(cudaMemsetAsync(f.bound + 2, 0, sizeof(float), s));
+  to_f16_pass1_kernel<<<f16_grid(nk), 256, 0, s>>>(k1, nk, f.bound + 2, f.K16);
+  ML_LAUNCH_CHECK("pkm_bwd_f16_convert");
+  to_f16_pass1_kernel<<<f16_grid(nk), 256, 0, s>>>(k2, nk, f.bound + 2, f.K16 + nk);
+  ML_LAUNCH_CHECK("pkm_bwd_f16_convert");
+  to_f16_redo_kernel<<<unsigned(num_sms()), 256, 0, s>>>(k1, nk, f.bound + 2, f.K16);
+  ML_LAUNCH_CHECK("pkm_bwd_f16_redo");
+  to_f16_redo_kernel<<<unsigned(num_sms()), 256, 0, s>>>(k2, nk, f.bound + 2, f.K16 + nk);
+  ML_LAUNCH_CHECK("pkm_bwd_f16_redo");
+  return ML_OK;
+}
+
+mlStatus launch_pkm_bwd_f16_query(const mlPkmShape& sh, const void* q, const PkmBwdF16& f,
+                                  cudaStream_t s) {
+  const int64_t nq = int64_t(sh.T) * sh.H * sh.Dk;
+  const auto* qb = static_cast<const __nv_bfloat16*>(q);
+  ML_CUDA_TRY(cudaMemsetAsync(f.bound + 1, 0, sizeof(float), s));
+  to_f16_pass1_kernel<<<f16_grid(nq), 256, 0, s>>>(qb, nq, f.bound + 1, f.q16);
+  ML_LAUNCH_CHECK("pkm_bwd_f16_convert");
+  to_f16_redo_kernel<<<unsigned(num_sms()), 256, 0, s>>>(qb, nq, f.bound + 1, f.q16);
+  ML_LAUNCH_CHECK("pkm_bwd_f16_redo");
+  return ML_OK;
+}
+
 // dq (overwrite) and dK1/dK2 (accumulate) from ds [T, H, 2, S] bf16
 // (ds + ds_lo when ds_lo != NULL)
 mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const __nv_bfloat16* ds_lo,
                            const void* q,
                            const void* K1, const void* K2, float* dq, float* dK1, float* dK2,
-                           cudaStream_t s) {
+                           cudaStream_t s, const PkmBwdF16* f16) {
+  if (f16 && ds_lo) return fail(ML_ERR_UNSUPPORTED, "pkm_bwd_tc: fp16 operands and the split are exclusive");
+  if (f16) {          // the fp16 copies replace the bf16 operands
+    q = f16->q16;
+    K1 = f16->K16;
+    K2 = f16->K16 + int64_t(sh.H) * sh.S * (sh.Dk / 2);
+  }
   const int Dh = sh.Dk / 2;
   const int64_t HS2 = int64_t(sh.H) * 2 * sh.S;
   BwdParams p;
-  p.T = sh.T; p.H = sh.H; p.S = sh.S; p.Dh = Dh; p.Dk = sh.Dk;
+  p.T = sh.T; p.H = sh.H; p.S = sh.S; p.Dh = Dh; p.Dk = sh.Dk; p.k = sh.k;
   p.BN = bn_for(Dh);
   p.n_tiles = Dh / p.BN;
   p.tmem_cols = 32;
   while (p.tmem_cols < uint32_t(2 * p.BN)) p.tmem_cols <<= 1;
   p.dq = dq; p.dK1 = dK1; p.dK2 = dK2;
+  p.ds_bound = f16 ? f16->bound : nullptr;
+  p.op_bound = nullptr;
+  // A (atype, bits 7-9) and B (btype, bits 10-12): both bf16 (1) or both fp16 (0)
+  const uint32_t atype = f16 ? 0u : ((1u << 7) | (1u << 10));
   p.split = ds_lo ? 1 : 0;
   p.stages = ds_lo ? 3 : kStagesB;
-  const uint32_t base_idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(p.BN >> 3) << 17) |
+  const uint32_t base_idesc = (1u << 4) | atype | (uint32_t(p.BN >> 3) << 17) |
                               (uint32_t(kBM >> 4) << 24);
   const size_t smem = 1024 + size_t(p.stages) * ((kBM * kBK * 2 << p.split) + size_t(p.BN) * kBK * 2) + 1024 +
                       size_t(4) * 2 * 1024 * sizeof(float);
@@ -546,7 +667,7 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
       attr2 = true;
     }
-    const uint32_t idesc2 = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(p.BN >> 3) << 17) |
+    const uint32_t idesc2 = (1u << 4) | atype | (uint32_t(p.BN >> 3) << 17) |
                             (uint32_t(256 >> 4) << 24);
     const int ncl_max = grid_max / 2;
     {   // dq
@@ -569,7 +690,9 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
       pq.k_chunks = sh.S / kBK;
       pq.tiles = sh.H * 2 * pq.m_tiles * pq.n_tiles;
       pq.idesc = idesc2 | (1u << 16);
+      if (f16) pq.op_bound = f16->bound + 2;
       const int ncl = std::min(pq.tiles, ncl_max);
+      if (f16 && f16->keys_ready) ML_CUDA_TRY(cudaStreamWaitEvent(s, f16->keys_ready, 0));
       pkm_bwd_tc2_kernel<MODE_DQ><<<2 * ncl, kThreadsB, smem2, s>>>(ma, mb1, mb2, md, pq);
       ML_LAUNCH_CHECK("pkm_dq_tc");
     }
@@ -582,7 +705,9 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
       pk.k_chunks = (sh.T + kBK - 1) / kBK;
       pk.tiles = sh.H * 2 * pk.m_tiles * pk.n_tiles;
       pk.idesc = idesc2 | (1u << 15) | (1u << 16);
+      if (f16) pk.op_bound = f16->bound + 1;
       const int ncl = std::min(pk.tiles, ncl_max);
+      if (f16 && f16->q16_ready) ML_CUDA_TRY(cudaStreamWaitEvent(s, f16->q16_ready, 0));
       pkm_bwd_tc2_kernel<MODE_DK><<<2 * ncl, kThreadsB, smem2, s>>>(ma, mb, mb, mb, pk);
       ML_LAUNCH_CHECK("pkm_dK_tc");
     }
@@ -601,6 +726,7 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
     pq.k_chunks = sh.S / kBK;
     pq.tiles = sh.H * 2 * pq.m_tiles * pq.n_tiles;
     pq.idesc = base_idesc | (1u << 16);          // B MN-major
+    if (f16) pq.op_bound = f16->bound + 2;
     if (smem > configured[0]) {
       ML_CUDA_TRY(cudaFuncSetAttribute(pkm_bwd_tc_kernel<MODE_DQ>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -619,6 +745,7 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return fail(ML_ERR_CUDA, "cuTensorMapEncodeTiled (dq) failed: " + std::to_string(int(r)));
     }
+    if (f16 && f16->keys_ready) ML_CUDA_TRY(cudaStreamWaitEvent(s, f16->keys_ready, 0));
     pkm_bwd_tc_kernel<MODE_DQ><<<std::min(pq.tiles, grid_max), kThreadsB, smem, s>>>(ma, mb1, mb2, md, mlo, pq);
     ML_LAUNCH_CHECK("pkm_dq_tc");
   }
@@ -634,11 +761,13 @@ mlStatus launch_pkm_bwd_tc(const mlPkmShape& sh, const __nv_bfloat16* ds, const 
     pk.k_chunks = (sh.T + kBK - 1) / kBK;
     pk.tiles = sh.H * 2 * pk.m_tiles * pk.n_tiles;
     pk.idesc = base_idesc | (1u << 15) | (1u << 16);   // A and B MN-major
+    if (f16) pk.op_bound = f16->bound + 1;
     if (smem > configured[1]) {
       ML_CUDA_TRY(cudaFuncSetAttribute(pkm_bwd_tc_kernel<MODE_DK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       configured[1] = smem;
     }
+    if (f16 && f16->q16_ready) ML_CUDA_TRY(cudaStreamWaitEvent(s, f16->q16_ready, 0));
     pkm_bwd_tc_kernel<MODE_DK><<<std::min(pk.tiles, grid_max), kThreadsB, smem, s>>>(ma, mb, mb, mb, mlo, pk);
     ML_LAUNCH_CHECK("pkm_dK_tc");
   }

@@ -123,3 +123,49 @@ def test_cta_pair_backward_equals_single_cta(T, H, S, Dk, k):
     single = _bwd_env(arrays, {"ML_PKM_BWD_PAIR": "0"})
     for a, b in zip(pair, single):
         assert np.array_equal(a, b)
+
+
+def _case(seed, T, H, S, Dk, k, dw_scale=1.0, q_scale=1.0, k_scale=1.0):
+    # q_scale / k_scale: powers of two (the bf16 values stay exact)
+    sc = gen.scale_for("K1", Dk=Dk)
+    q = gen.tensor(seed, "q", (T, H, Dk), dtype="bf16") * q_scale
+    K1 = gen.tensor(seed, "K1", (H, S, Dk // 2), scale=sc, dtype="bf16") * k_scale
+    K2 = gen.tensor(seed, "K2", (H, S, Dk // 2), scale=sc, dtype="bf16") * k_scale
+    q64, K164, K264 = (a.astype(np.float64) for a in (q, K1, K2))
+    ridx, _, rw = opkm.pkm_lookup(q64, K164, K264, k)
+    dw = gen.tensor(seed, "dout", (T, H, k), dtype="f32").astype(np.float64) * dw_scale
+    dw = dw.astype(np.float32)
+    ref = opkm.pkm_bwd(q64, K164, K264, ridx, rw, dw.astype(np.float64))[:3]
+    arrays = dict(q=q.astype(np.float32), K1=K1.astype(np.float32), K2=K2.astype(np.float32),
+                  idx=ridx.astype(np.int32), w=rw.astype(np.float32), dw=dw)
+    return arrays, ref, key_magnitudes(q64, K164, K264, ridx, rw, dw.astype(np.float64))
+
+
+@pytest.mark.parametrize("T,H,S,Dk,k,dw_scale,q_scale,k_scale", [
+    (300, 4, 1024, 1024, 32, 1.0, 1.0, 1.0),    # C2 per-head shapes (CTA-pair kernels)
+    (150, 2, 512, 128, 8, 1.0, 1.0, 1.0),       # single-CTA kernels (BN = 64)
+    (130, 4, 1024, 1024, 32, 1e-30, 1.0, 1.0),  # the 2^e scale keeps tiny gradients normal in fp16
+    (130, 2, 1024, 512, 16, 1e25, 1.0, 1.0),    # ... and huge ones finite
+    (130, 2, 1024, 512, 16, 1.0, 2.0 ** 20, 2.0 ** -12),   # q beyond fp16's range, tiny keys:
+    (130, 2, 512, 256, 16, 1.0, 2.0 ** -24, 2.0 ** 18),    # the rescaling second pass
+])
+def test_fp16_ds_backward_meets_1e3(T, H, S, Dk, k, dw_scale, q_scale, k_scale):
+    """The opt-in fp16 form (ML_PKM_BWD_F16=1) of the tcgen05 key/query
+    backward runs on fp16 operands, each
+    scaled by a power of two from a bound on its magnitude: ds (11
+    significant bits instead of bf16's 8) and exact copies of the bf16 q /
+    keys; the epilogue unscales: dq, dK1, dK2 within 1e-3 of the fp64 oracle
+    (max error / max |ref|), elementwise within the rounding model at
+    u = 2^-11; the bf16 ds (ML_PKM_BWD_F16=0) is strictly worse."""
+    arrays, (rdq, rdK1, rdK2), (mdq, mdK1, mdK2) = _case(43, T, H, S, Dk, k, dw_scale, q_scale, k_scale)
+    got = _bwd_env(arrays, {"ML_PKM_BWD_F16": "1"})
+    rel = lambda a, r: float(np.max(np.abs(a - r)) / np.max(np.abs(r)))
+    for g, r, m, n in zip(got, (rdq, rdK1, rdK2), (mdq, mdK1, mdK2), ("dq", "dK1", "dK2")):
+        assert np.all(np.isfinite(g)), n
+        assert rel(g, r) <= 1e-3, (n, rel(g, r))
+        assert_close(g, r, 1e-3, n, mag=m, u=2.0 ** -11)
+    if dw_scale == 1.0 and q_scale == 1.0:
+        old = _bwd_env(arrays, {"ML_PKM_BWD_F16": "0"})
+        print("max rel err fp16 ds / bf16 ds:",
+              [f"{rel(g, r):.2e} / {rel(o, r):.2e}" for g, o, r in zip(got, old, (rdq, rdK1, rdK2))])
+        assert all(rel(g, r) < rel(o, r) for g, o, r in zip(got, old, (rdq, rdK1, rdK2)))
