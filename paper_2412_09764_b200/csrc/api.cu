@@ -40,7 +40,9 @@ int num_sms() {
 // events, so tensor-core GEMMs overlap the HBM-bound bag kernels.  One set
 // per caller stream (calls on different streams never share them).
 struct Aux {
-  cudaStream_t s[4];      // 3: the sparse key backward's dq gather (beside the dK sort)
+  // 3: the sparse key backward's dq gather (beside the dK sort); 4 (normal
+  // priority): the layer backward's gate weight-gradient GEMMs
+  cudaStream_t s[5];
   cudaEvent_t ev[10];   // 8, 9: the fp16 key / query copies of the key backward
 };
 
@@ -98,10 +100,22 @@ static mlStatus aux_for(cudaStream_t caller, Aux** out) {
   ML_CUDA_TRY(cudaStreamCreateWithPriority(&a->s[1], cudaStreamNonBlocking, hi));
   ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[2], cudaStreamNonBlocking));
   ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[3], cudaStreamNonBlocking));
+  ML_CUDA_TRY(cudaStreamCreateWithFlags(&a->s[4], cudaStreamNonBlocking));
   for (auto& e : a->ev) ML_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   m[caller] = a;
   *out = a;
   return ML_OK;
+}
+// The layer backward's gate weight-gradient GEMMs: aux 4 (normal priority),
+// so the value-row state build (the forward's aux 2, which the segmented pass
+// waits for) is not starved of SMs by them; ML_BWD_GEMM_STREAM=1 puts them on
+// the high-priority aux 1 (the earlier layout, for A/B runs)
+static cudaStream_t bwd_gemm_stream(const Aux* a) {
+  static const int gs = [] {
+    const char* e = std::getenv("ML_BWD_GEMM_STREAM");
+    return (e && e[0] == '1') ? 1 : 4;
+  }();
+  return a->s[gs];
 }
 // make `to` wait for all work enqueued so far on `from`
 static mlStatus stream_dep(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
@@ -950,6 +964,8 @@ mlStatus memory_layer_fwd_state(const mlLayerShape* shape, const void* x, const 
     int32_t *sk = nullptr, *sp = nullptr;
     cudaEvent_t done;
     ML_TRY(state_event(state, &done));
+    // (on the high-priority aux 1 it finished during the bag forward but
+    // slowed it by 0.11 ms: step 5.21 vs 5.15 ms, scripts/state_stream_ab.sh)
     ML_TRY(stream_dep(st, aux->s[2], aux->ev[4]));
     ML_TRY(bag_bwd_prepare(bag_of(s), idx_saved, ps.rows, ps.U, pb, &sk, &sp, aux->s[2]));
     ML_CUDA_TRY(cudaEventRecord(done, aux->s[2]));
@@ -1062,14 +1078,15 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
     ML_TRY(gemm_rm(false, true, T, s.dv, s.D, dout, s.D, W2, s.D, b.dz, s.dv, dt, false, b.gemm_ws,
                    kGemmWs, st));
     ML_TRY(launch_gate_bwd(b.dz, g_saved, y_saved, b.z, b.dy, b.dg, int64_t(T) * s.dv, dt, st));
-    // aux 1: dW2 = z^T dout ; dW1 = x^T dg ; dx = dg W1^T  (overlap the bag backward)
-    ML_TRY(stream_dep(st, aux->s[1], aux->ev[1]));
+    // aux 4: dW2 = z^T dout ; dW1 = x^T dg ; dx = dg W1^T  (overlap the bag backward)
+    cudaStream_t gst = bwd_gemm_stream(aux);
+    ML_TRY(stream_dep(st, gst, aux->ev[1]));
     ML_TRY(gemm_rm(true, false, s.dv, s.D, T, b.z, s.dv, dout, s.D, dW2, s.D, dt, true, b.gemm_ws2,
-                   kGemmWs, aux->s[1]));
+                   kGemmWs, gst));
     ML_TRY(gemm_rm(true, false, s.D, s.dv, T, x, s.D, b.dg, s.dv, dW1, s.dv, dt, true, b.gemm_ws2,
-                   kGemmWs, aux->s[1]));
+                   kGemmWs, gst));
     ML_TRY(gemm_rm(false, true, T, s.D, s.dv, b.dg, s.dv, W1, s.dv, dx, s.D, dt, false, b.gemm_ws2,
-                   kGemmWs, aux->s[1]));
+                   kGemmWs, gst));
     dy = b.dy;
   }
   ML_TRY(stream_dep(aux->s[0], st, aux->ev[2]));     // sorted runs ready
@@ -1094,7 +1111,7 @@ mlStatus memory_layer_bwd_state(const mlLayerShape* shape, const void* dout, con
   const int64_t P = int64_t(T) * bs.B;
   ML_TRY(pkm_bwd_core(s.pkm, q, K1, K2, idx_saved, w_saved, b.bag.dw_part, ns, P, dq, dK1, dK2,
                       b.pkm, st));
-  if (s.gated) ML_TRY(stream_dep(aux->s[1], st, aux->ev[3]));   // join the gate GEMMs
+  if (s.gated) ML_TRY(stream_dep(bwd_gemm_stream(aux), st, aux->ev[3]));   // join the gate GEMMs
   if (dw_out) ML_TRY(launch_sum_slices(b.bag.dw_part, ns, P, dw_out, st));
   return check_index_flag(st);
   ML_API_END
