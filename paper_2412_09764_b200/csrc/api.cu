@@ -416,9 +416,7 @@ static mlStatus bag_bwd_prepare(const mlBagShape& s, const int32_t* idx, int32_t
     ML_CUDA_TRY(cudaMemsetAsync(U, 0, sizeof(int32_t), st));
     return ML_OK;
   }
-  ML_TRY(sort_pairs(idx, P, ceil_log2(s.N), b.sort, skey, spos, st, s.N));
-  ML_TRY(find_runs(*skey, P, b.runs, rows, U, st));
-  return ML_OK;
+  return sort_pairs_runs(idx, P, ceil_log2(s.N), s.N, b.sort, b.runs, rows, U, skey, spos, st);
 }
 
 // *nsw (nullable): number of dw partial slices written to b.dw_part

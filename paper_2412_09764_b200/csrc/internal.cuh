@@ -88,6 +88,12 @@ mlStatus merge_sorted_lists(const int32_t* lists, int G, int64_t n_each, int32_t
                             int32_t* out_p, int32_t* scratch_k, int32_t* scratch_p, cudaStream_t s);
 mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out,
                    int32_t* U, cudaStream_t s);
+// sort_pairs + find_runs in one; opt-in ML_RUNS_ROWSCAN=1: where the
+// counting sort applies, the runs come from its per-row counts (no pass over
+// the sorted positions)
+mlStatus sort_pairs_runs(const int32_t* keys_in, int64_t n, int bits, int64_t key_limit,
+                         SortBufs& b, RunBufs& r, int32_t* rows_out, int32_t* U, int32_t** keys,
+                         int32_t** vals, cudaStream_t s);
 
 // ------------------------------------------------ segmented reduction
 // For every run of equal sorted keys (one output row per run):

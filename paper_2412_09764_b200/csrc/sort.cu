@@ -610,11 +610,14 @@ __global__ void __launch_bounds__(256) csort_hist_kernel(const int32_t* __restri
   }
 }
 
-// cur: exclusive run offsets on entry, run ends on exit
+// cur: exclusive run offsets on entry, run ends on exit; uid (nullable):
+// run id of every row, written to rid per position
 __global__ void __launch_bounds__(256) csort_scatter_kernel(const int32_t* __restrict__ keys, int64_t n,
                                                             uint32_t limit, int32_t* __restrict__ cur,
                                                             int32_t* __restrict__ kout,
-                                                            int32_t* __restrict__ vout) {
+                                                            int32_t* __restrict__ vout,
+                                                            const int32_t* __restrict__ uid,
+                                                            int32_t* __restrict__ rid) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     uint32_t k = uint32_t(keys[i]);
@@ -623,6 +626,79 @@ __global__ void __launch_bounds__(256) csort_scatter_kernel(const int32_t* __res
     const int32_t o = atomicAdd(cur + k, 1);
     kout[o] = int32_t(k);
     vout[o] = int32_t(i) | (clamped ? kClampedPos : 0);
+    if (uid) rid[o] = uid[k];
+  }
+}
+
+// The runs of the counting sort straight from the per-row counts (replaces
+// find_runs' two passes over the sorted positions): one scan over the N rows
+// of (count, row touched, pieces of a run longer than kPieceLen) gives every
+// touched row its first position, run id and piece base.  tmp: [3][nt + 1].
+__device__ __forceinline__ void row_triple(const int32_t* cnt, int64_t N, int64_t r, int& c, int& u, int& pc) {
+  c = r < N ? cnt[r] : 0;
+  u = c > 0 ? 1 : 0;
+  pc = c > kPieceLen ? (c + kPieceLen - 1) / kPieceLen : 0;
+}
+
+__global__ void __launch_bounds__(kScanThreads) rowscan_reduce_kernel(const int32_t* __restrict__ cnt,
+                                                                      int64_t N, int32_t* tmp,
+                                                                      int64_t tstride) {
+  __shared__ int s_warp[32];
+  const int64_t base = int64_t(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  int sc = 0, su = 0, sp = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int c, u, pc;
+    row_triple(cnt, N, base + i, c, u, pc);
+    sc += c; su += u; sp += pc;
+  }
+  int tc, tu, tp;
+  block_excl_scan(sc, s_warp, &tc);
+  block_excl_scan(su, s_warp, &tu);
+  block_excl_scan(sp, s_warp, &tp);
+  if (threadIdx.x == 0) {
+    tmp[blockIdx.x] = tc;
+    tmp[tstride + blockIdx.x] = tu;
+    tmp[2 * tstride + blockIdx.x] = tp;
+  }
+}
+
+// cnt: counts in, exclusive offsets out (the scatter's cursors); tot: the
+// three totals (n, U, pieces) from the top-level scans
+__global__ void __launch_bounds__(kScanThreads) rowscan_down_kernel(
+    int32_t* __restrict__ cnt, int64_t N, int64_t n, const int32_t* __restrict__ tmp, int64_t tstride,
+    const int32_t* __restrict__ tot, int32_t* __restrict__ uid, int32_t* __restrict__ run_begin,
+    int32_t* __restrict__ rows_out, int32_t* __restrict__ piece_base, int32_t* U, int32_t* n_slots) {
+  __shared__ int s_warp[32];
+  const int64_t base = int64_t(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  int c[kScanItems], u[kScanItems], pc[kScanItems], sc = 0, su = 0, sp = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    row_triple(cnt, N, base + i, c[i], u[i], pc[i]);
+    sc += c[i]; su += u[i]; sp += pc[i];
+  }
+  int t;
+  int ec = block_excl_scan(sc, s_warp, &t) + tmp[blockIdx.x];
+  int eu = block_excl_scan(su, s_warp, &t) + tmp[tstride + blockIdx.x];
+  int ep = block_excl_scan(sp, s_warp, &t) + tmp[2 * tstride + blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t r = base + i;
+    if (r < N) {
+      cnt[r] = ec;
+      uid[r] = eu;
+      if (c[i] > 0) {
+        run_begin[eu] = ec;
+        if (rows_out) rows_out[eu] = int32_t(r);
+        if (pc[i]) piece_base[ec] = ep;
+      }
+    }
+    ec += c[i]; eu += u[i]; ep += pc[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *U = tot[1];
+    *n_slots = tot[2];
+    run_begin[tot[1]] = int32_t(n);
   }
 }
 
@@ -640,6 +716,21 @@ __global__ void __launch_bounds__(256) csort_fix_kernel(const int32_t* __restric
     if (len <= 1) continue;
     if (len > kFixShort) {
       long_list[atomicAdd(n_long, 1)] = int32_t(i);
+      continue;
+    }
+    if (len <= 4) {           // most runs (C2: mean 2.3): a sorting network in registers
+      const uint32_t M = kPosMask;
+      int32_t x0 = vout[i], x1 = vout[i + 1];
+      int32_t x2 = len > 2 ? vout[i + 2] : int32_t(0x7fffffff);
+      int32_t x3 = len > 3 ? vout[i + 3] : int32_t(0x7fffffff);
+      auto cs = [M](int32_t& p, int32_t& q) {
+        if ((uint32_t(p) & M) > (uint32_t(q) & M)) { const int32_t t = p; p = q; q = t; }
+      };
+      cs(x0, x1); cs(x2, x3); cs(x0, x2); cs(x1, x3); cs(x1, x2);
+      vout[i] = x0;
+      vout[i + 1] = x1;
+      if (len > 2) vout[i + 2] = x2;
+      if (len > 3) vout[i + 3] = x3;
       continue;
     }
     int32_t a[kFixShort];
@@ -765,14 +856,77 @@ void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b) {
   b.v[0] = c.take<int32_t>(n);
   b.k[1] = c.take<int32_t>(n);
   b.v[1] = c.take<int32_t>(n);
+  // counting sort: [2^bits] counters + [2^bits] run ids of the rows; scan
+  // scratch for three row scans
+  const bool cf = counting_sort_fits(n, bits);
   const int64_t ncnt = std::max<int64_t>((int64_t(1) << kMaxDigitBits) * nb,
-                                         counting_sort_fits(n, bits) ? int64_t(1) << bits : 0);
+                                         cf ? int64_t(2) << bits : 0);
   b.counts = c.take<int32_t>(ncnt);
-  b.scan_tmp = c.take<int32_t>(scan_tmp_elems(ncnt));
+  b.scan_tmp = c.take<int32_t>(std::max<int64_t>(scan_tmp_elems(ncnt),
+                                                 cf ? 3 * scan_tmp_elems(int64_t(1) << bits) : 0));
   b.ghist = c.take<int32_t>(3 * (int64_t(1) << kMaxDigitBits) + 8);
 }
 
 static int sort_passes(int bits) { return (bits + kMaxDigitBits - 1) / kMaxDigitBits; }
+
+static bool counting_applies(int64_t n, int bits, int64_t key_limit) {
+  static const bool on = [] {
+    const char* e = std::getenv("ML_SORT_COUNTING");
+    return !(e && e[0] == '0');
+  }();
+  if (bits < 1) bits = 1;
+  return on && sort_passes(bits) >= 2 && key_limit > 0 && key_limit <= (int64_t(1) << bits) &&
+         counting_sort_fits(n, bits) && n < (int64_t(1) << 31) - 1;
+}
+
+// The counting sort (csort_* kernels), output where sorted_result names it.
+// r != nullptr: also the runs (find_runs' outputs) from the row scan.
+static mlStatus counting_sort(const int32_t* keys_in, int64_t n, int bits, int64_t key_limit,
+                              SortBufs& b, RunBufs* r, int32_t* rows_out, int32_t* U,
+                              int32_t** keys, int32_t** vals, cudaStream_t s) {
+  const int fin = (sort_passes(bits) - 1) & 1;
+  int32_t* kout = b.k[fin];
+  int32_t* vout = b.v[fin];
+  int32_t* spare_k = b.k[fin ^ 1];
+  int32_t* spare_v = b.v[fin ^ 1];
+  const uint32_t lim = uint32_t(key_limit);
+  int32_t* n_long = b.ghist;
+  ML_CUDA_TRY(cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * size_t(lim), s));
+  ML_CUDA_TRY(cudaMemsetAsync(n_long, 0, sizeof(int32_t), s));
+  const unsigned g = unsigned(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+  csort_hist_kernel<<<g, 256, 0, s>>>(keys_in, n, lim, b.counts, index_flag_ptr());
+  ML_LAUNCH_CHECK("csort_hist");
+  int32_t* uid = nullptr;
+  if (r) {
+    uid = b.counts + (int64_t(1) << bits);
+    const int64_t nt = (int64_t(lim) + kScanTile - 1) / kScanTile;
+    const int64_t ts = nt + 1;
+    int32_t* tot = b.ghist + 4;
+    rowscan_reduce_kernel<<<unsigned(nt), kScanThreads, 0, s>>>(b.counts, lim, b.scan_tmp, ts);
+    ML_LAUNCH_CHECK("csort_rowscan");
+    for (int j = 0; j < 3; ++j) {
+      scan_blocks_kernel<<<1, 1024, 0, s>>>(b.scan_tmp + j * ts, nt, tot + j);
+      ML_LAUNCH_CHECK("csort_rowscan");
+    }
+    rowscan_down_kernel<<<unsigned(nt), kScanThreads, 0, s>>>(
+        b.counts, lim, n, b.scan_tmp, ts, tot, uid, r->run_begin, rows_out, r->piece_base,
+        U ? U : r->lb, r->n_slots);
+    ML_LAUNCH_CHECK("csort_rowscan");
+  } else {
+    ML_TRY(scan_exclusive(b.counts, b.counts, lim, b.scan_tmp, nullptr, s));
+  }
+  csort_scatter_kernel<<<g, 256, 0, s>>>(keys_in, n, lim, b.counts, kout, vout, uid,
+                                         r ? r->rid : nullptr);
+  ML_LAUNCH_CHECK("csort_scatter");
+  csort_fix_kernel<<<g, 256, 0, s>>>(kout, vout, b.counts, n, spare_k, n_long);
+  ML_LAUNCH_CHECK("csort_fix");
+  csort_long_kernel<<<unsigned(num_sms()), 256, 0, s>>>(kout, vout, spare_v, b.counts, spare_k,
+                                                        n_long);
+  ML_LAUNCH_CHECK("csort_long");
+  *keys = kout;
+  *vals = vout;
+  return ML_OK;
+}
 
 mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t** vals) {
   if (n <= 0) {
@@ -800,36 +954,8 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
   const int dbits = (bits + passes - 1) / passes;
   const int nbins = 1 << dbits;
   const int nb = sort_nblocks(n);
-  static const bool counting = [] {
-    const char* e = std::getenv("ML_SORT_COUNTING");
-    return !(e && e[0] == '0');
-  }();
-  if (counting && passes >= 2 && key_limit > 0 && key_limit <= (int64_t(1) << bits) &&
-      counting_sort_fits(n, bits) && n < (int64_t(1) << 31) - 1) {
-    const int fin = (passes - 1) & 1;    // the buffers sorted_result names
-    int32_t* kout = b.k[fin];
-    int32_t* vout = b.v[fin];
-    int32_t* spare_k = b.k[fin ^ 1];
-    int32_t* spare_v = b.v[fin ^ 1];
-    const uint32_t lim = uint32_t(key_limit);
-    int32_t* n_long = b.ghist;
-    ML_CUDA_TRY(cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * size_t(lim), s));
-    ML_CUDA_TRY(cudaMemsetAsync(n_long, 0, sizeof(int32_t), s));
-    const unsigned g = unsigned(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
-    csort_hist_kernel<<<g, 256, 0, s>>>(keys_in, n, lim, b.counts, index_flag_ptr());
-    ML_LAUNCH_CHECK("csort_hist");
-    ML_TRY(scan_exclusive(b.counts, b.counts, lim, b.scan_tmp, nullptr, s));
-    csort_scatter_kernel<<<g, 256, 0, s>>>(keys_in, n, lim, b.counts, kout, vout);
-    ML_LAUNCH_CHECK("csort_scatter");
-    csort_fix_kernel<<<g, 256, 0, s>>>(kout, vout, b.counts, n, spare_k, n_long);
-    ML_LAUNCH_CHECK("csort_fix");
-    csort_long_kernel<<<unsigned(num_sms()), 256, 0, s>>>(kout, vout, spare_v, b.counts, spare_k,
-                                                          n_long);
-    ML_LAUNCH_CHECK("csort_long");
-    *keys = kout;
-    *vals = vout;
-    return ML_OK;
-  }
+  if (counting_applies(n, bits, key_limit))
+    return counting_sort(keys_in, n, bits, key_limit, b, nullptr, nullptr, nullptr, keys, vals, s);
   static bool attr = false;
   if (!attr) {
     const int max_smem = int(sizeof(int)) * ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile);
@@ -943,6 +1069,22 @@ mlStatus find_runs(const int32_t* skey, int64_t n, RunBufs& r, int32_t* rows_out
                                                          int(nt), st2, tickets + 1);
   ML_LAUNCH_CHECK("run_pieces");
   return ML_OK;
+}
+
+mlStatus sort_pairs_runs(const int32_t* keys_in, int64_t n, int bits, int64_t key_limit,
+                         SortBufs& b, RunBufs& r, int32_t* rows_out, int32_t* U, int32_t** keys,
+                         int32_t** vals, cudaStream_t s) {
+  // opt-in (ML_RUNS_ROWSCAN=1): bit-identical, and the state is ready ~0.1 ms
+  // sooner at C2, but the gate GEMMs that filled the segmented pass's wait
+  // then land after it: step 5.178 vs 5.143 ms (scripts/rowscan_check.sh)
+  static const bool rowscan = [] {
+    const char* e = std::getenv("ML_RUNS_ROWSCAN");
+    return e && e[0] == '1';
+  }();
+  if (n > 0 && rowscan && counting_applies(n, bits, key_limit))
+    return counting_sort(keys_in, n, bits < 1 ? 1 : bits, key_limit, b, &r, rows_out, U, keys, vals, s);
+  ML_TRY(sort_pairs(keys_in, n, bits, b, keys, vals, s, key_limit));
+  return find_runs(*keys, n, r, rows_out, U, s);
 }
 
 }  // namespace ml

@@ -74,3 +74,50 @@ def test_sort_local_is_the_stable_sort(N, P, kind):
     rows, pos = _expected(idx, N)
     assert np.array_equal(got[0], rows), kind
     assert np.array_equal(got[1], pos), kind
+
+
+def _bag_bwd_in_subprocess(arrays, env):
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        for n, a in arrays.items():
+            np.save(os.path.join(d, n + ".npy"), a)
+        code = (
+            "import numpy as np, torch\n"
+            "from paper_2412_09764_b200 import ops\n"
+            f"d = {d!r}\n"
+            "L = lambda n: torch.from_numpy(np.load(d + '/' + n + '.npy')).cuda()\n"
+            "rows, dV, dw = ops.embbag_bwd(L('V').to(torch.bfloat16), L('idx'), L('w'),\n"
+            "                              L('dy').to(torch.bfloat16))\n"
+            "for n, t in (('rows', rows), ('dV', dV), ('dw', dw)):\n"
+            "    np.save(d + '/o_' + n + '.npy', t.cpu().numpy())\n")
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), cwd=root,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return [np.load(os.path.join(d, f"o_{n}.npy")) for n in ("rows", "dV", "dw")]
+
+
+@pytest.mark.parametrize("N,T,B,kind,dv", [
+    (1 << 16, 1024, 128, "uniform", 1024),   # C2-like: 2 positions per row; the pipelined pass
+    (5000, 300, 64, "hot", 64),              # runs > 32 positions (pieces), one of ~5.8k
+    (6000, 160, 64, "clamped", 64),
+])
+def test_runs_from_counting_sort_bit_identical(N, T, B, kind, dv):
+    """The runs of the counting sort taken from its per-row counts (row scan,
+    ML_RUNS_ROWSCAN=1) give the segmented backward exactly the inputs the pass
+    over the sorted positions (find_runs, the default) and the radix sort
+    (ML_SORT_COUNTING=0) give: rows, dV and dw bit for bit."""
+    P = T * B
+    idx = _rows(12, N, P, kind).reshape(T, B)
+    rng = np.random.default_rng(5)
+    arrays = dict(V=rng.standard_normal((N, dv)).astype(np.float32), idx=idx,
+                  w=rng.random((T, B)).astype(np.float32),
+                  dy=rng.standard_normal((T, dv)).astype(np.float32))
+    base = _bag_bwd_in_subprocess(arrays, {"ML_RUNS_ROWSCAN": "1", "ML_SORT_COUNTING": "1"})
+    for env in ({"ML_RUNS_ROWSCAN": "0", "ML_SORT_COUNTING": "1"}, {"ML_SORT_COUNTING": "0"}):
+        other = _bag_bwd_in_subprocess(arrays, env)
+        for a, b, n in zip(base, other, ("rows", "dV", "dw")):
+            assert a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8)), (env, n)
