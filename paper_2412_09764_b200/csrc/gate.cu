@@ -3,6 +3,8 @@
 // cuBLASLt with fp32 accumulation), plus the compact->dense dV scatter.
 #include "internal.cuh"
 
+#include <cstdio>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -102,6 +104,11 @@ mlStatus launch_scatter_rows(const int32_t* rows, const void* dV, mlDtype gdt, c
   return ML_OK;
 }
 
+static bool tune_log() {
+  static const bool v = [] { const char* e = std::getenv("ML_GEMM_TUNE_LOG"); return e && e[0] == '1'; }();
+  return v;
+}
+
 mlStatus gemm_rm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const void* A,
                  int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, mlDtype ab,
                  bool c_f32, void* ws, size_t ws_bytes, cudaStream_t s, float beta) {
@@ -178,11 +185,13 @@ mlStatus gemm_rm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t
       // overwriting GEMMs (beta = 0) the top candidates are timed once, on the
       // first call of each problem signature, and the fastest is cached
       static const bool tune = [] { const char* e = std::getenv("ML_GEMM_TUNE"); return !(e && e[0] == '0'); }();
-      constexpr int kCand = 4;
+      constexpr int kCand = 8;
       cublasLtMatmulHeuristicResult_t all[kCand] = {};
       ck(cublasLtMatmulAlgoGetHeuristic(h, desc, l1, l2, lc, lc, pref, kCand, all, &nres), "heuristic");
       if (nres > 0) heur = all[0];
-      if (st == ML_OK && tune && nres > 1 && beta == 0.f) {
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      ML_CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+      if (st == ML_OK && tune && nres > 1 && beta == 0.f && cap == cudaStreamCaptureStatusNone) {
         // per host thread: concurrent callers (one thread per rank of a hub
         // group) must not record into each other's timing events
         thread_local cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -190,11 +199,16 @@ mlStatus gemm_rm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t
           ML_CUDA_TRY(cudaEventCreate(&e0));
           ML_CUDA_TRY(cudaEventCreate(&e1));
         }
+        // time the candidates on an idle device: work still running on the
+        // library's other streams (the state sort, the other gate GEMMs) made
+        // the choice vary from run to run (C2: 6 GEMMs 0.52 vs 0.60 ms)
+        ML_CUDA_TRY(cudaStreamSynchronize(s));
+        ML_CUDA_TRY(cudaDeviceSynchronize());
         const float alpha = 1.f;
         float best = 1e30f;
         for (int c = 0; c < nres && st == ML_OK; ++c) {
           float t = 1e30f;
-          for (int rep = 0; rep < 2 && st == ML_OK; ++rep) {
+          for (int rep = 0; rep < 5 && st == ML_OK; ++rep) {
             ML_CUDA_TRY(cudaEventRecord(e0, s));
             ck(cublasLtMatmul(h, desc, &alpha, B, l1, A, l2, &beta, C, lc, C, lc, &all[c].algo, ws,
                               ws_bytes, s), "matmul (tuning)");
@@ -208,6 +222,9 @@ mlStatus gemm_rm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t
             best = t;
             heur = all[c];
           }
+          if (tune_log())
+            std::fprintf(stderr, "gemm tune M=%lld N=%lld K=%lld tA=%d tB=%d cand %d: %.1f us\n",
+                         (long long)M, (long long)N, (long long)K, int(transA), int(transB), c, t * 1e3f);
         }
       }
       if (st == ML_OK && nres == 0) st = fail(ML_ERR_CUDA, "cublasLt: no algorithm");
