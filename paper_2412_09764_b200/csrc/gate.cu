@@ -199,11 +199,10 @@ mlStatus gemm_rm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t
           ML_CUDA_TRY(cudaEventCreate(&e0));
           ML_CUDA_TRY(cudaEventCreate(&e1));
         }
-        // time the candidates on an idle device: work still running on the
-        // library's other streams (the state sort, the other gate GEMMs) made
-        // the choice vary from run to run (C2: 6 GEMMs 0.52 vs 0.60 ms)
-        ML_CUDA_TRY(cudaStreamSynchronize(s));
-        ML_CUDA_TRY(cudaDeviceSynchronize());
+        // 8 candidates, best of 5 runs each (with 4, C2's fastest kernel for
+        // the 16384 x 2048 x 2048 GEMMs, the 6th candidate, was never timed).
+        // No device-wide sync: a rank thread of a hub group would wait on
+        // streams that wait on the other ranks' host threads
         const float alpha = 1.f;
         float best = 1e30f;
         for (int c = 0; c < nres && st == ML_OK; ++c) {
