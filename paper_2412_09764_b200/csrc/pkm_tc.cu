@@ -33,7 +33,13 @@ constexpr int kBM = 128;     // tokens per tile (UMMA_M)
 constexpr int kBK = 64;      // K elements per stage = one 128-byte swizzle atom of bf16
 constexpr int kStages = 4;
 constexpr int kStageFloats = 32 * 32;  // one epilogue staging tile: 32 token rows x 32 scores
-constexpr int kStageBufs = kStages > 3 ? 1 : 2;   // staging tiles per epilogue warp
+#ifndef ML_SCORE_STAGE_BUFS
+#define ML_SCORE_STAGE_BUFS 1
+#endif
+// staging tiles per epilogue warp (build switch; 2 tiles with the 4 stages
+// fit in 226 KiB and measured equal at C2: 0.166-0.175 ms either way,
+// scripts/gpu_ab_so_scores.sh)
+constexpr int kStageBufs = ML_SCORE_STAGE_BUFS;
 constexpr int kThreads = 256;
 
 struct TcParams {
