@@ -385,9 +385,10 @@ static mlStatus pkm_bwd_core(const mlPkmShape& s, const void* q, const void* K1,
       const int32_t* key = half ? b.key2 : b.key1;
       const float* wts = half ? b.ds2w : b.ds1w;
       // dK_half[h, a] += sum ds * q_half[t,h]  (sorted segments, dense
-      // accumulate; the sentinel slots sort last and are skipped)
+      // accumulate; the sentinel slots sort last and are skipped, so their
+      // order is free: order_limit = H*S)
       int32_t *skey, *spos;
-      ML_TRY(sort_pairs(key, P, bits, b.sort, &skey, &spos, st));
+      ML_TRY(sort_pairs(key, P, bits, b.sort, &skey, &spos, st, HS + 1, HS));
       ML_TRY(find_runs(skey, P, b.runs, nullptr, nullptr, st));
       SegArgs g;
       g.skey = skey; g.spos = spos; g.P = P; g.runs = &b.runs; g.w = wts;

@@ -61,8 +61,11 @@ void sort_carve(Carver& c, int64_t n, int bits, SortBufs& b);
 // as 0 and its position carries kClampedPos (the segmented pass gives it
 // weight 0).
 constexpr int32_t kClampedPos = int32_t(0x80000000u);
+// order_limit (>= 0): positions of keys >= order_limit may come in any order
+// (the caller skips them; the counting sort then leaves such runs unsorted)
 mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b,
-                    int32_t** keys, int32_t** vals, cudaStream_t s, int64_t key_limit = -1);
+                    int32_t** keys, int32_t** vals, cudaStream_t s, int64_t key_limit = -1,
+                    int64_t order_limit = -1);
 // Where sort_pairs(n, bits) leaves its result inside b (without sorting).
 mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t** vals);
 

@@ -599,14 +599,23 @@ constexpr uint32_t kPosMask = 0x7fffffffu;   // strips kClampedPos for ordering
 __global__ void __launch_bounds__(256) csort_hist_kernel(const int32_t* __restrict__ keys, int64_t n,
                                                          uint32_t limit, int32_t* __restrict__ cnt,
                                                          int* flag) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    uint32_t k = uint32_t(keys[i]);
-    if (k >= limit) {
-      atomicExch(flag, 1);
-      k = 0;
+  // warp-aggregated: one atomic per distinct key of a warp's 32 keys (a
+  // key shared by many positions -- the sparse key backward's sentinel --
+  // would otherwise serialise on one counter)
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t b0 = blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31); b0 < n; b0 += stride) {
+    const int64_t i = b0 + lane;
+    uint32_t k = 0xFFFFFFE0u | uint32_t(lane);    // distinct per lane when i >= n
+    if (i < n) {
+      k = uint32_t(keys[i]);
+      if (k >= limit) {
+        atomicExch(flag, 1);
+        k = 0;
+      }
     }
-    atomicAdd(cnt + k, 1);
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    if (i < n && lane == __ffs(peers) - 1) atomicAdd(cnt + k, __popc(peers));
   }
 }
 
@@ -618,15 +627,30 @@ __global__ void __launch_bounds__(256) csort_scatter_kernel(const int32_t* __res
                                                             int32_t* __restrict__ vout,
                                                             const int32_t* __restrict__ uid,
                                                             int32_t* __restrict__ rid) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    uint32_t k = uint32_t(keys[i]);
-    const bool clamped = k >= limit;
-    if (clamped) k = 0;
-    const int32_t o = atomicAdd(cur + k, 1);
-    kout[o] = int32_t(k);
-    vout[o] = int32_t(i) | (clamped ? kClampedPos : 0);
-    if (uid) rid[o] = uid[k];
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t b0 = blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31); b0 < n; b0 += stride) {
+    const int64_t i = b0 + lane;
+    uint32_t k = 0xFFFFFFE0u | uint32_t(lane);    // distinct per lane when i >= n
+    bool clamped = false;
+    if (i < n) {
+      k = uint32_t(keys[i]);
+      clamped = k >= limit;
+      if (clamped) k = 0;
+    }
+    // warp-aggregated cursor: the group's leader reserves popc slots, lanes
+    // take them in lane (= position) order
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const int leader = __ffs(peers) - 1;
+    int32_t o0 = 0;
+    if (i < n && lane == leader) o0 = atomicAdd(cur + k, __popc(peers));
+    o0 = __shfl_sync(0xffffffffu, o0, leader);
+    if (i < n) {
+      const int32_t o = o0 + __popc(peers & ((1u << lane) - 1u));
+      kout[o] = int32_t(k);
+      vout[o] = int32_t(i) | (clamped ? kClampedPos : 0);
+      if (uid) rid[o] = uid[k];
+    }
   }
 }
 
@@ -703,15 +727,19 @@ __global__ void __launch_bounds__(kScanThreads) rowscan_down_kernel(
 }
 
 // one thread per run head: short runs sorted in place, long ones listed
+// (runs of keys >= order_limit keep the scatter's order: their positions'
+// order is irrelevant to the caller)
 __global__ void __launch_bounds__(256) csort_fix_kernel(const int32_t* __restrict__ kout,
                                                         int32_t* __restrict__ vout,
                                                         const int32_t* __restrict__ end, int64_t n,
                                                         int32_t* __restrict__ long_list,
-                                                        int32_t* __restrict__ n_long) {
+                                                        int32_t* __restrict__ n_long,
+                                                        uint32_t order_limit) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t k = kout[i];
     if (i > 0 && kout[i - 1] == k) continue;
+    if (uint32_t(k) >= order_limit) continue;
     const int len = int(int64_t(end[k]) - i);
     if (len <= 1) continue;
     if (len > kFixShort) {
@@ -875,15 +903,19 @@ static bool counting_applies(int64_t n, int bits, int64_t key_limit) {
     return !(e && e[0] == '0');
   }();
   if (bits < 1) bits = 1;
+  // n <= 8 * key_limit: short runs on average.  The fixup sorts a run longer
+  // than 32 positions with one CTA; with ~128 positions per key (C3's sparse
+  // key backward) that cost 0.92 ms against the radix sort's 0.43
   return on && sort_passes(bits) >= 2 && key_limit > 0 && key_limit <= (int64_t(1) << bits) &&
-         counting_sort_fits(n, bits) && n < (int64_t(1) << 31) - 1;
+         counting_sort_fits(n, bits) && n <= 8 * key_limit && n < (int64_t(1) << 31) - 1;
 }
 
 // The counting sort (csort_* kernels), output where sorted_result names it.
 // r != nullptr: also the runs (find_runs' outputs) from the row scan.
 static mlStatus counting_sort(const int32_t* keys_in, int64_t n, int bits, int64_t key_limit,
                               SortBufs& b, RunBufs* r, int32_t* rows_out, int32_t* U,
-                              int32_t** keys, int32_t** vals, cudaStream_t s) {
+                              int32_t** keys, int32_t** vals, cudaStream_t s,
+                              int64_t order_limit = -1) {
   const int fin = (sort_passes(bits) - 1) & 1;
   int32_t* kout = b.k[fin];
   int32_t* vout = b.v[fin];
@@ -918,7 +950,8 @@ static mlStatus counting_sort(const int32_t* keys_in, int64_t n, int bits, int64
   csort_scatter_kernel<<<g, 256, 0, s>>>(keys_in, n, lim, b.counts, kout, vout, uid,
                                          r ? r->rid : nullptr);
   ML_LAUNCH_CHECK("csort_scatter");
-  csort_fix_kernel<<<g, 256, 0, s>>>(kout, vout, b.counts, n, spare_k, n_long);
+  const uint32_t ol = (order_limit >= 0 && order_limit < int64_t(lim)) ? uint32_t(order_limit) : lim;
+  csort_fix_kernel<<<g, 256, 0, s>>>(kout, vout, b.counts, n, spare_k, n_long, ol);
   ML_LAUNCH_CHECK("csort_fix");
   csort_long_kernel<<<unsigned(num_sms()), 256, 0, s>>>(kout, vout, spare_v, b.counts, spare_k,
                                                         n_long);
@@ -942,7 +975,7 @@ mlStatus sorted_result(int64_t n, int bits, SortBufs& b, int32_t** keys, int32_t
 }
 
 mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, int32_t** keys,
-                    int32_t** vals, cudaStream_t s, int64_t key_limit) {
+                    int32_t** vals, cudaStream_t s, int64_t key_limit, int64_t order_limit) {
   if (n <= 0) {
     *keys = b.k[0];
     *vals = b.v[0];
@@ -955,7 +988,8 @@ mlStatus sort_pairs(const int32_t* keys_in, int64_t n, int bits, SortBufs& b, in
   const int nbins = 1 << dbits;
   const int nb = sort_nblocks(n);
   if (counting_applies(n, bits, key_limit))
-    return counting_sort(keys_in, n, bits, key_limit, b, nullptr, nullptr, nullptr, keys, vals, s);
+    return counting_sort(keys_in, n, bits, key_limit, b, nullptr, nullptr, nullptr, keys, vals, s,
+                         order_limit);
   static bool attr = false;
   if (!attr) {
     const int max_smem = int(sizeof(int)) * ((kSortWarps + 2) * (1 << kMaxDigitBits) + 2 * kSortTile);

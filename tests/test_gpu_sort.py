@@ -121,3 +121,50 @@ def test_runs_from_counting_sort_bit_identical(N, T, B, kind, dv):
         other = _bag_bwd_in_subprocess(arrays, env)
         for a, b, n in zip(base, other, ("rows", "dV", "dw")):
             assert a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8)), (env, n)
+
+
+def _pkm_bwd_in_subprocess(arrays, env):
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        for n, a in arrays.items():
+            np.save(os.path.join(d, n + ".npy"), a)
+        code = (
+            "import numpy as np, torch\n"
+            "from paper_2412_09764_b200 import ops\n"
+            f"d = {d!r}\n"
+            "L = lambda n: torch.from_numpy(np.load(d + '/' + n + '.npy')).cuda()\n"
+            "b = lambda n: L(n).to(torch.bfloat16)\n"
+            "dq, dK1, dK2 = ops.pkm_topk_bwd(b('q'), b('K1'), b('K2'), L('idx'), L('w'), L('dw'))\n"
+            "for n, t in (('dq', dq), ('dK1', dK1), ('dK2', dK2)):\n"
+            "    np.save(d + '/o_' + n + '.npy', t.float().cpu().numpy())\n")
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), cwd=root,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return [np.load(os.path.join(d, f"o_{n}.npy")) for n in ("dq", "dK1", "dK2")]
+
+
+@pytest.mark.parametrize("T,H,S,Dk,k", [(512, 4, 4096, 256, 32), (1500, 2, 4096, 128, 16)])
+def test_sparse_key_backward_counting_sort_bit_identical(T, H, S, Dk, k):
+    """The sparse key backward (S > 2048) sorts its half-key slots with the
+    counting sort when the key range 2^ceil(log2(H*S + 1)) is at most twice
+    the slot count and the slots at most 8 per key (both cases here);
+    the deduplication sentinel's run (most slots) stays unordered, which the
+    segmented pass skips: dq, dK1, dK2 equal the radix path's bit for bit."""
+    from oracle import pkm as opkm
+    from synthetic import gen
+    sc = gen.scale_for("K1", Dk=Dk)
+    q = gen.tensor(44, "q", (T, H, Dk), dtype="bf16")
+    K1 = gen.tensor(44, "K1", (H, S, Dk // 2), scale=sc, dtype="bf16")
+    K2 = gen.tensor(44, "K2", (H, S, Dk // 2), scale=sc, dtype="bf16")
+    ridx, _, rw = opkm.pkm_lookup(q.astype(np.float64), K1.astype(np.float64), K2.astype(np.float64), k)
+    dw = gen.tensor(44, "dout", (T, H, k), dtype="f32")
+    arrays = dict(q=q.astype(np.float32), K1=K1.astype(np.float32), K2=K2.astype(np.float32),
+                  idx=ridx.astype(np.int32), w=rw.astype(np.float32), dw=dw.astype(np.float32))
+    a = _pkm_bwd_in_subprocess(arrays, {"ML_SORT_COUNTING": "1"})
+    b = _pkm_bwd_in_subprocess(arrays, {"ML_SORT_COUNTING": "0"})
+    for x, y, n in zip(a, b, ("dq", "dK1", "dK2")):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), n
