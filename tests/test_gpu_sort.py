@@ -46,6 +46,8 @@ def _rows(seed, N, P, kind):
         idx[:] = N - 1
     elif kind == "two_big":       # two runs > 8192, interleaved
         idx = np.where(rng.random(P) < 0.5, 3, N - 2)
+    elif kind == "all_clamped":   # every index out of range: one run of row 0
+        idx = np.where(rng.random(P) < 0.5, -7, N + 3)
     elif kind == "clamped":       # out-of-range indices join row 0's run
         bad = rng.random(P) < 0.05
         idx[bad] = np.where(rng.random(int(bad.sum())) < 0.5, -1 - rng.integers(0, 9, int(bad.sum())),
@@ -60,6 +62,8 @@ def _rows(seed, N, P, kind):
     (4097, 3 * 8192 + 5, "one"),    # one run of 24581: chunk sorts + 2 merge passes
     (8000, 40000, "two_big"),
     (6000, 9000, "clamped"),
+    (4500, 4096, "all_clamped"),    # a single 4096-position run of clamped positions
+    (2049, 2048 * 3 + 1, "uniform"),  # smallest counting-sort key range (2 passes), ragged
     (1 << 20, 1 << 21, "uniform"),  # the C2 value-row sort (2^20 rows, 2.1M positions)
     (1 << 20, 1 << 18, "uniform"),  # key range > 2 * count: radix sort
     (1 << 20, 1 << 18, "hot"),
