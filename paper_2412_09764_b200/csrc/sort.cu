@@ -593,6 +593,7 @@ __global__ void __launch_bounds__(kScanThreads) run_scan2_kernel(const int32_t* 
 // are handled as in load_key.  Run lengths: <= kFixShort by one thread,
 // longer runs by one CTA (shared-memory bitonic chunks + merge passes).
 constexpr int kFixShort = 32;
+constexpr int kFixMed = 256;       // runs of 33..256 positions: one warp each
 constexpr int kFixSmem = 8192;
 constexpr uint32_t kPosMask = 0x7fffffffu;   // strips kClampedPos for ordering
 
@@ -734,7 +735,7 @@ __global__ void __launch_bounds__(256) csort_fix_kernel(const int32_t* __restric
                                                         const int32_t* __restrict__ end, int64_t n,
                                                         int32_t* __restrict__ long_list,
                                                         int32_t* __restrict__ n_long,
-                                                        uint32_t order_limit) {
+                                                        uint32_t order_limit, int64_t med_off) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int32_t k = kout[i];
@@ -742,8 +743,11 @@ __global__ void __launch_bounds__(256) csort_fix_kernel(const int32_t* __restric
     if (uint32_t(k) >= order_limit) continue;
     const int len = int(int64_t(end[k]) - i);
     if (len <= 1) continue;
-    if (len > kFixShort) {
-      long_list[atomicAdd(n_long, 1)] = int32_t(i);
+    if (len > kFixShort) {     // n_long[0]: CTA runs (list from the front), n_long[1]:
+      if (len > kFixMed)       // warp runs (list from long_list + med_off)
+        long_list[atomicAdd(n_long, 1)] = int32_t(i);
+      else
+        long_list[med_off + atomicAdd(n_long + 1, 1)] = int32_t(i);
       continue;
     }
     if (len <= 4) {           // most runs (C2: mean 2.3): a sorting network in registers
@@ -773,6 +777,42 @@ __global__ void __launch_bounds__(256) csort_fix_kernel(const int32_t* __restric
       a[t + 1] = x;
     }
     for (int j = 0; j < len; ++j) vout[i + j] = a[j];
+  }
+}
+
+// one warp per medium run (33..kFixMed positions): a bitonic sort of the run
+// (padded to a power of two) in the warp's shared-memory slice
+__global__ void __launch_bounds__(256) csort_med_kernel(const int32_t* __restrict__ kout,
+                                                       int32_t* __restrict__ vout,
+                                                       const int32_t* __restrict__ end,
+                                                       const int32_t* __restrict__ med_list,
+                                                       const int32_t* __restrict__ n_med) {
+  __shared__ uint32_t s_all[8][kFixMed];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* sw = s_all[wid];
+  const int nm = *n_med;
+  for (int r = blockIdx.x * 8 + wid; r < nm; r += gridDim.x * 8) {
+    const int64_t b = med_list[r];
+    const int len = int(int64_t(end[kout[b]]) - b);
+    int p2 = 64;
+    while (p2 < len) p2 <<= 1;
+    for (int j = lane; j < p2; j += 32) sw[j] = j < len ? uint32_t(vout[b + j]) : 0xffffffffu;
+    __syncwarp();
+    for (int k = 2; k <= p2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = lane; t < p2 / 2; t += 32) {
+          const int i0 = (t / j) * 2 * j + (t & (j - 1)), i1 = i0 + j;
+          const uint32_t x = sw[i0], y = sw[i1];
+          if (((x & kPosMask) > (y & kPosMask)) == ((i0 & k) == 0)) {
+            sw[i0] = y;
+            sw[i1] = x;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    for (int j = lane; j < len; j += 32) vout[b + j] = int32_t(sw[j]);
+    __syncwarp();
   }
 }
 
@@ -903,11 +943,20 @@ static bool counting_applies(int64_t n, int bits, int64_t key_limit) {
     return !(e && e[0] == '0');
   }();
   if (bits < 1) bits = 1;
-  // n <= 8 * key_limit: short runs on average.  The fixup sorts a run longer
-  // than 32 positions with one CTA; with ~128 positions per key (C3's sparse
-  // key backward) that cost 0.92 ms against the radix sort's 0.43
+  // n <= 8 * key_limit (ML_SORT_COUNTING_MAX_PER_KEY): short runs on
+  // average.  The fixup sorts runs of 33..256 positions with one warp, longer
+  // ones with one CTA.  Measured: with every long run on a CTA, ~128
+  // positions per key (C3's sparse key backward) cost 0.92 ms against the
+  // radix sort's 0.43; at 32 per key (C5 per rank, 70 % of them one
+  // sentinel key whose atomics serialise) the counting sort only broke even
+  // (10.93-10.99 vs 10.87-10.91 ms); at 8 per key (C4 per rank) it wins
+  // (1.66 vs 1.695 ms), at 2 (C2) too (5.05-5.10 vs 5.13)
+  static const int64_t per_key = [] {
+    const char* e = std::getenv("ML_SORT_COUNTING_MAX_PER_KEY");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(8);
+  }();
   return on && sort_passes(bits) >= 2 && key_limit > 0 && key_limit <= (int64_t(1) << bits) &&
-         counting_sort_fits(n, bits) && n <= 8 * key_limit && n < (int64_t(1) << 31) - 1;
+         counting_sort_fits(n, bits) && n <= per_key * key_limit && n < (int64_t(1) << 31) - 1;
 }
 
 // The counting sort (csort_* kernels), output where sorted_result names it.
@@ -924,7 +973,7 @@ static mlStatus counting_sort(const int32_t* keys_in, int64_t n, int bits, int64
   const uint32_t lim = uint32_t(key_limit);
   int32_t* n_long = b.ghist;
   ML_CUDA_TRY(cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * size_t(lim), s));
-  ML_CUDA_TRY(cudaMemsetAsync(n_long, 0, sizeof(int32_t), s));
+  ML_CUDA_TRY(cudaMemsetAsync(n_long, 0, 2 * sizeof(int32_t), s));   // CTA runs, warp runs
   const unsigned g = unsigned(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
   csort_hist_kernel<<<g, 256, 0, s>>>(keys_in, n, lim, b.counts, index_flag_ptr());
   ML_LAUNCH_CHECK("csort_hist");
@@ -951,8 +1000,13 @@ static mlStatus counting_sort(const int32_t* keys_in, int64_t n, int bits, int64
                                          r ? r->rid : nullptr);
   ML_LAUNCH_CHECK("csort_scatter");
   const uint32_t ol = (order_limit >= 0 && order_limit < int64_t(lim)) ? uint32_t(order_limit) : lim;
-  csort_fix_kernel<<<g, 256, 0, s>>>(kout, vout, b.counts, n, spare_k, n_long, ol);
+  // the run lists share spare_k: runs > kFixShort number at most n / 33 each
+  const int64_t med_off = n / 2;
+  csort_fix_kernel<<<g, 256, 0, s>>>(kout, vout, b.counts, n, spare_k, n_long, ol, med_off);
   ML_LAUNCH_CHECK("csort_fix");
+  csort_med_kernel<<<unsigned(num_sms()) * 2, 256, 0, s>>>(kout, vout, b.counts, spare_k + med_off,
+                                                           n_long + 1);
+  ML_LAUNCH_CHECK("csort_med");
   csort_long_kernel<<<unsigned(num_sms()), 256, 0, s>>>(kout, vout, spare_v, b.counts, spare_k,
                                                         n_long);
   ML_LAUNCH_CHECK("csort_long");

@@ -151,11 +151,13 @@ def _pkm_bwd_in_subprocess(arrays, env):
         return [np.load(os.path.join(d, f"o_{n}.npy")) for n in ("dq", "dK1", "dK2")]
 
 
-@pytest.mark.parametrize("T,H,S,Dk,k", [(512, 4, 4096, 256, 32), (1500, 2, 4096, 128, 16)])
+@pytest.mark.parametrize("T,H,S,Dk,k", [(512, 4, 4096, 256, 32), (1500, 2, 4096, 128, 16),
+                                       (2048, 4, 4096, 256, 32)])   # 16 slots per key: warp-sorted runs
 def test_sparse_key_backward_counting_sort_bit_identical(T, H, S, Dk, k):
     """The sparse key backward (S > 2048) sorts its half-key slots with the
     counting sort when the key range 2^ceil(log2(H*S + 1)) is at most twice
-    the slot count and the slots at most 8 per key (both cases here);
+    the slot count and the slots at most ML_SORT_COUNTING_MAX_PER_KEY per key
+    (default 8; 64 here, so the third case's runs go through the warp sort);
     the deduplication sentinel's run (most slots) stays unordered, which the
     segmented pass skips: dq, dK1, dK2 equal the radix path's bit for bit."""
     from oracle import pkm as opkm
@@ -168,7 +170,7 @@ def test_sparse_key_backward_counting_sort_bit_identical(T, H, S, Dk, k):
     dw = gen.tensor(44, "dout", (T, H, k), dtype="f32")
     arrays = dict(q=q.astype(np.float32), K1=K1.astype(np.float32), K2=K2.astype(np.float32),
                   idx=ridx.astype(np.int32), w=rw.astype(np.float32), dw=dw.astype(np.float32))
-    a = _pkm_bwd_in_subprocess(arrays, {"ML_SORT_COUNTING": "1"})
+    a = _pkm_bwd_in_subprocess(arrays, {"ML_SORT_COUNTING": "1", "ML_SORT_COUNTING_MAX_PER_KEY": "64"})
     b = _pkm_bwd_in_subprocess(arrays, {"ML_SORT_COUNTING": "0"})
     for x, y, n in zip(a, b, ("dq", "dK1", "dK2")):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), n
