@@ -3,5 +3,5 @@
 bash scripts/r2_sweep_final.sh
 bash scripts/gpu_profiles_r2.sh
 CMD4="python bench.py --config c4 --per-rank 8 --steps 2 --warmup 3 --no-cpu-baseline --no-variants"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3200 --csv \
   --log-file gpurun_out/r2p_c4_launches.csv $CMD4 > gpurun_out/r2p_c4_ncu.log 2>&1; echo c4_launch_exit=$?
