@@ -26,8 +26,11 @@ class MemoryLayerFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, q, K1, K2, V, W1, W2, k, qk_norm=False, dense_value_grad=False):
         x, q = x.contiguous(), q.contiguous()
-        out, saved = ops.memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True, qk_norm=qk_norm,
-                                          keep_state=True)
+        # the library launches on the current device's current stream: make
+        # the inputs' device current (a layer on cuda:1 without set_device)
+        with torch.cuda.device(x.device):
+            out, saved = ops.memory_layer_fwd(x, q, K1, K2, V, W1, W2, k, gated=True,
+                                              qk_norm=qk_norm, keep_state=True)
         ctx.saved = saved
         ctx.dense_value_grad = dense_value_grad
         ctx.save_for_backward(x, q, K1, K2, V, W1, W2)
@@ -36,7 +39,9 @@ class MemoryLayerFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dout):
         x, q, K1, K2, V, W1, W2 = ctx.saved_tensors
-        g = ops.memory_layer_bwd(dout.contiguous().to(V.dtype), x, q, K1, K2, V, W1, W2, ctx.saved)
+        with torch.cuda.device(x.device):
+            g = ops.memory_layer_bwd(dout.contiguous().to(V.dtype), x, q, K1, K2, V, W1, W2,
+                                     ctx.saved)
         U = int(g.U.item())
         rows = g.rows[:U].long()
         if ctx.dense_value_grad:
