@@ -750,19 +750,34 @@ __global__ void __launch_bounds__(256) csort_fix_kernel(const int32_t* __restric
         long_list[med_off + atomicAdd(n_long + 1, 1)] = int32_t(i);
       continue;
     }
+    const uint32_t M = kPosMask;
+    auto cs = [M](int32_t& p, int32_t& q) {
+      if ((uint32_t(p) & M) > (uint32_t(q) & M)) { const int32_t t = p; p = q; q = t; }
+    };
     if (len <= 4) {           // most runs (C2: mean 2.3): a sorting network in registers
-      const uint32_t M = kPosMask;
       int32_t x0 = vout[i], x1 = vout[i + 1];
       int32_t x2 = len > 2 ? vout[i + 2] : int32_t(0x7fffffff);
       int32_t x3 = len > 3 ? vout[i + 3] : int32_t(0x7fffffff);
-      auto cs = [M](int32_t& p, int32_t& q) {
-        if ((uint32_t(p) & M) > (uint32_t(q) & M)) { const int32_t t = p; p = q; q = t; }
-      };
       cs(x0, x1); cs(x2, x3); cs(x0, x2); cs(x1, x3); cs(x1, x2);
       vout[i] = x0;
       vout[i + 1] = x1;
       if (len > 2) vout[i + 2] = x2;
       if (len > 3) vout[i + 3] = x3;
+      continue;
+    }
+    if (len <= 8) {           // Batcher's odd-even merge network for 8 (19 exchanges)
+      int32_t x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = j < len ? vout[i + j] : int32_t(0x7fffffff);
+      cs(x[0], x[1]); cs(x[2], x[3]); cs(x[4], x[5]); cs(x[6], x[7]);
+      cs(x[0], x[2]); cs(x[1], x[3]); cs(x[4], x[6]); cs(x[5], x[7]);
+      cs(x[1], x[2]); cs(x[5], x[6]);
+      cs(x[0], x[4]); cs(x[1], x[5]); cs(x[2], x[6]); cs(x[3], x[7]);
+      cs(x[2], x[4]); cs(x[3], x[5]);
+      cs(x[1], x[2]); cs(x[3], x[4]); cs(x[5], x[6]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < len) vout[i + j] = x[j];
       continue;
     }
     int32_t a[kFixShort];
