@@ -41,6 +41,14 @@ constexpr int kStageFloats = 32 * 32;  // one epilogue staging tile: 32 token ro
 // scripts/gpu_ab_so_scores.sh)
 constexpr int kStageBufs = ML_SCORE_STAGE_BUFS;
 constexpr int kThreads = 256;
+// epilogue warps of the single-CTA scoring kernel (build switch): 8 = two
+// warps per TMEM lane quarter, each draining half of a subtile's columns
+// (C2: 0.166-0.168 vs 0.170 ms with 4, scripts/gpu_ab_so_scores.sh)
+#ifndef ML_SCORE_EPI_WARPS
+#define ML_SCORE_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = ML_SCORE_EPI_WARPS;
+constexpr int kThreadsS = 128 + 32 * kEpiWarps;
 
 struct TcParams {
   float* scores;
@@ -118,7 +126,7 @@ __device__ __forceinline__ void tc_mma(uint8_t* sA, uint8_t* sB, uint64_t* full,
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsS, 1)
     pkm_scores_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                          const __grid_constant__ CUtensorMap tmK1,
                          const __grid_constant__ CUtensorMap tmK2,
@@ -146,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 32 * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -173,6 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) tc_mma<kStages>(sA, sB, full, empty, tfull, tempty, bytes_a, bytes_b, tmem_base, p);
   } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> fp32 scores
     const int q4 = warp & 3;
+    // column part of each subtile this warp drains (kEpiWarps / 4 parts)
+    const int nparts = min(kEpiWarps / 4, p.BN / 32), part = (warp - 4) >> 2;
+    const int cw = part < nparts ? p.BN / nparts : 0, cbeg = part * (p.BN / nparts);
     int acc = 0;
     uint32_t acc_phase = 0;
     int it = 0;
@@ -184,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         float cm[8];          // this row's chunk maxima of the subtile (BN / 32 <= 8)
-        for (int c0 = 0; c0 < p.BN; c0 += 32, ++it) {
+        for (int c0 = cbeg; c0 < cbeg + cw; c0 += 32, ++it) {
           uint32_t r[32];
           tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * p.BN + c0), r);
           if (p.cmax) {
@@ -217,9 +228,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
-        if (p.cmax && row0 + lane < p.T) {    // 32 contiguous bytes per row (BN = 256)
+        if (p.cmax && row0 + lane < p.T && part < nparts) {
           float* dst = p.cmax + (int64_t(row0 + lane) * p.H * 2 + hh) * (p.S >> 5) + (n * p.BN >> 5);
-          if (p.BN == 256) {
+          if (nparts > 1) {   // this warp's chunks only
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j >= (cbeg >> 5) && j < ((cbeg + cw) >> 5)) dst[j] = cm[j];
+          } else if (p.BN == 256) {   // 32 contiguous bytes per row
             reinterpret_cast<float4*>(dst)[0] = make_float4(cm[0], cm[1], cm[2], cm[3]);
             reinterpret_cast<float4*>(dst)[1] = make_float4(cm[4], cm[5], cm[6], cm[7]);
           } else {
@@ -777,7 +792,7 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
     if (r != CUDA_SUCCESS) return fail(ML_ERR_CUDA, "cuTensorMapEncodeTiled (scores) failed: " + std::to_string(int(r)));
   }
   const size_t smem = 1024 + size_t(kStages) * (kBM * kBK * 2 + size_t(p.BN) * kBK * 2) + 1024 +
-                      size_t(4) * kStageBufs * kStageFloats * sizeof(float);
+                      size_t(kEpiWarps) * kStageBufs * kStageFloats * sizeof(float);
   static size_t configured = 0;
   if (smem > configured) {
     ML_CUDA_TRY(cudaFuncSetAttribute(pkm_scores_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -819,7 +834,7 @@ mlStatus launch_pkm_scores_tc(const mlPkmShape& sh, const void* q, const void* K
     return ML_OK;
   }
   const int grid = std::min(p.tiles, num_sms());
-  pkm_scores_tc_kernel<<<grid, kThreads, smem, s>>>(mq, mk1, mk2, ms, p);
+  pkm_scores_tc_kernel<<<grid, kThreadsS, smem, s>>>(mq, mk1, mk2, ms, p);
   ML_LAUNCH_CHECK("pkm_scores_tc");
   return ML_OK;
 }
