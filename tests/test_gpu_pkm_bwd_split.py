@@ -29,6 +29,12 @@ def _cuda():
     yield
 
 
+# the key-backward form under test is set explicitly, whatever the outer
+# environment selects (the suite is also run under these switches)
+_FORM = {"ML_PKM_BWD_SPARSE": "0", "ML_PKM_BWD_SPLIT": "0", "ML_PKM_BWD_F16": "0",
+         "ML_PKM_BWD_TC": "1"}
+
+
 def _bwd_in_subprocess(arrays, split):
     with tempfile.TemporaryDirectory() as d:
         for n, a in arrays.items():
@@ -42,7 +48,7 @@ def _bwd_in_subprocess(arrays, split):
             "dq, dK1, dK2 = ops.pkm_topk_bwd(b('q'), b('K1'), b('K2'), L('idx'), L('w'), L('dw'))\n"
             "for n, t in (('dq', dq), ('dK1', dK1), ('dK2', dK2)):\n"
             "    np.save(d + '/o_' + n + '.npy', t.float().cpu().numpy())\n")
-        env = dict(os.environ, ML_PKM_BWD_SPLIT="1" if split else "0")
+        env = {**os.environ, **_FORM, "ML_PKM_BWD_SPLIT": "1" if split else "0"}
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                            text=True, timeout=600)
@@ -100,8 +106,8 @@ def _bwd_env(arrays, env):
             "for n, t in (('dq', dq), ('dK1', dK1), ('dK2', dK2)):\n"
             "    np.save(d + '/o_' + n + '.npy', t.float().cpu().numpy())\n")
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), cwd=root,
-                           capture_output=True, text=True, timeout=600)
+        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **_FORM, **env},
+                           cwd=root, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
         return [np.load(os.path.join(d, f"o_{n}.npy")) for n in ("dq", "dK1", "dK2")]
 
